@@ -1,0 +1,6 @@
+"""`fpx.bounds` -> paper_2501_12349_b200.bounds (drop-in alias of the reference module name)."""
+import sys as _sys
+
+from paper_2501_12349_b200 import bounds as _impl
+
+_sys.modules[__name__] = _impl

@@ -1,0 +1,182 @@
+/* fpx.h -- C ABI of libfpx_sm100.so, the B200 (sm_100a) findpts hot path.
+ *
+ * Drop-in boundary for the reference package `fpx` (arXiv 2501.12349).  The
+ * reference ships only Python (basis.py, bounds.py) and specifies the rest in
+ * SPEC.md; each entry point below names the reference interface it replaces.
+ * A host binding (ctypes, see paper_2501_12349_b200/_C.py and INTEGRATION.md)
+ * passes plain device pointers and sizes; no torch types cross this ABI.
+ *
+ * Conventions
+ *   - every pointer argument is a caller-owned DEVICE pointer unless the name
+ *     ends in _host;
+ *   - every call takes a cudaStream_t (as void*) and is stream-ordered and
+ *     asynchronous unless documented as synchronising;
+ *   - return 0 on success, a negative FPX_E* code otherwise; the message is in
+ *     the thread-local fpx_last_error().  Per-point outcomes are codes in the
+ *     outputs, never errors;
+ *   - all coordinates are FP64, element / point indices int32 (int64 counts).
+ *
+ * Layouts (bounds.py:58-94)
+ *   basis     packed per-order constants, see FPX_BASIS_* offsets
+ *   nodes     [E][d][N^dr]   lexicographic, first reference axis fastest
+ *   aabb      [E][2][d]      lo, hi (expanded)
+ *   obb_c     [E][d]         OBB centre
+ *   obb_inv   [E][d][d]      OBB inverse transform (unit cube frame)
+ *   frame     [E][d + d*d]   element centre x_c and J_c^{-1} (best-first order)
+ *   hbox      [E][2][d]      hash box = AABB  intersect  OBB enclosure (D5)
+ *   grid      [9]            lo[3], hi[3], h[3] of the local hash grid
+ *   x         [n][d]         query points
+ *   r         [n][dr]        reference coordinates
+ *   field     [E][C][Nf^dr]  nodal field blocks
+ */
+#ifndef FPX_H
+#define FPX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FPX_ABI_VERSION 1
+
+/* error codes */
+#define FPX_OK 0
+#define FPX_EINVAL -1     /* bad argument */
+#define FPX_ECUDA -2      /* CUDA runtime error */
+#define FPX_ECAPACITY -3  /* output capacity too small; *needed set */
+#define FPX_EUNSUPPORTED -4 /* order / dimension not compiled in */
+
+/* record codes (decision D10: gslib convention) */
+#define FPX_INTERIOR 0
+#define FPX_BORDER 1
+#define FPX_NOT_FOUND 2
+
+/* packed basis constants: offsets in doubles for order p, N = p+1, M */
+#define FPX_BASIS_NODES(N, M) 0
+#define FPX_BASIS_SCALE(N, M) (N)
+#define FPX_BASIS_PROJ0(N, M) (2 * (N))
+#define FPX_BASIS_PROJ1(N, M) (3 * (N))
+#define FPX_BASIS_ETA(N, M) (4 * (N))
+#define FPX_BASIS_LO(N, M) (4 * (N) + (M))
+#define FPX_BASIS_HI(N, M) (4 * (N) + (M) + (N) * (M))
+#define FPX_BASIS_SIZE(N, M) (4 * (N) + (M) + 2 * (N) * (M))
+
+/* Device-resident setup of one rank's mesh (engine.EngineSetup).
+ * POD of device pointers owned by the caller (torch tensors in EngineSetup). */
+typedef struct fpx_mesh_t {
+  int32_t d, dr, N, M;          /* phys dim, ref dim, nodes/axis, interval pts */
+  int64_t E;                    /* elements on this rank */
+  const double* basis;          /* packed constants (FPX_BASIS_*) */
+  const double* nodes;
+  const double* aabb;
+  const double* obb_c;
+  const double* obb_inv;
+  const uint8_t* obb_ok;
+  const double* frame;
+  const double* grid;
+  int32_t ncell;                /* cells per axis of the local map */
+  int32_t max_list;             /* longest CSR list (capacity planning) */
+  const int32_t* offsets;       /* [ncell^d + 1] */
+  const int32_t* elems;         /* CSR element ids, ascending per cell */
+  /* Newton settings (invmap.NewtonSettings) */
+  int32_t max_iters;
+  double tol, grow, keep, accept, shrink, alpha0;
+  /* surface classification eps_d: abs >= 0 wins, else rel*diag */
+  double eps_d_abs, eps_d_rel;
+} fpx_mesh_t;
+
+/* Diagnostic counters written by fpx_find (device int64[FPX_STATS_LEN]). */
+#define FPX_STAT_POINTS 0        /* points processed */
+#define FPX_STAT_BOXTESTS 1      /* candidate box tests (hash-list entries) */
+#define FPX_STAT_NEWTON 2        /* Newton-ed (point, element) candidates */
+#define FPX_STAT_ITERS 3         /* Newton iterations over all candidates */
+#define FPX_STAT_ROUND2_POINTS 4 /* points needing the exhaustive round */
+#define FPX_STAT_ROUND2_PAIRS 5  /* (point, element) pairs in round 2 */
+#define FPX_STAT_OVERFLOW 6      /* pairs dropped for lack of workspace (>0: rerun) */
+#define FPX_STAT_EVALS 7         /* fused field evaluations */
+#define FPX_STATS_LEN 8
+
+int fpx_abi_version(void);
+const char* fpx_last_error(void);
+/* 1 if order N (nodes/axis) is compiled in for (d, dr) */
+int fpx_supported(int d, int dr, int N);
+
+/* Per-element bounds: element_aabb + element_obb batched over E elements
+ * (replaces bounds.py:292-297 and bounds.py:366-384, built on
+ * bound_function_1d/2d bounds.py:155-201), plus the D5 hash box and the
+ * centre frame.  status[e]: 0 ok, 1 degenerate (bounds.py:244, setup error),
+ * 2 OBB unusable (bounds.py:349,361 SingularTransformError -> AABB only,
+ * SPEC.md:191).  Bit-identical to the oracle for identical basis constants
+ * (no FMA contraction). */
+int fpx_setup_bounds(int d, int dr, int N, int M, int64_t E, const double* basis,
+                     const double* nodes, double expansion, double* aabb, double* obb_c,
+                     double* obb_inv, double* hbox, double* frame, uint8_t* obb_ok,
+                     int32_t* status, void* stream);
+
+/* bound_function_1d (dr=1, values [nf][N] -> lower/upper [nf][M]) and
+ * bound_function_2d (dr=2, values [nf][N*N] with i fastest -> [nf][M][M]),
+ * replacing bounds.py:155-171 and bounds.py:174-201. */
+int fpx_bound_function(int dr, int N, int M, int64_t nf, const double* basis,
+                       const double* values, double* lower, double* upper, void* stream);
+
+/* build_local_map over boxes [E][2][d]: grid over the union
+ * of the boxes, CSR cell -> ascending element ids.
+ * Synchronising.  Pass elems == NULL (or cap too small) to get
+ * offsets/grid and *needed_host; then call again with cap >= needed.
+ * ws: FPX workspace of fpx_hash_workspace_bytes(). */
+size_t fpx_hash_workspace_bytes(int d, int64_t E, int ncell);
+int fpx_hash_build(int d, int64_t E, const double* box, int ncell, double* grid,
+                   int32_t* offsets, int32_t* elems, int64_t cap, int64_t* needed_host,
+                   int32_t* max_list_host, void* ws, size_t ws_bytes, void* stream);
+
+/* lookup_local's addressing: cell_of per point, -1 outside. */
+int fpx_cell_of(const fpx_mesh_t* m, int64_t n, const double* x, int64_t* cell, void* stream);
+
+/* engine.find Phase A on this rank:
+ * hash lookup, AABB then OBB filter, trust-region Newton (invmap.invert_point
+ * SPEC.md:298-307) per candidate, classify, winner rule D6.  Writes
+ * code/elem/r/dist per point (NOT_FOUND: elem -1, r = dist = NaN).
+ * If field != NULL, also evaluates the field at the winning (elem, r)
+ * (engine.find_and_interpolate) into values [n][C]
+ * (NaN for NOT_FOUND).  iters (optional) = Newton iterations per point.
+ * stats: device int64[FPX_STATS_LEN] (zeroed by the call).
+ * ws: fpx_find_workspace_bytes(m->E, n, pair_cap). */
+size_t fpx_find_workspace_bytes(int64_t E, int64_t n, int64_t pair_cap);
+int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int32_t* elem,
+             double* r, double* dist, int32_t* iters, const double* field, int C,
+             double* values, int64_t* stats, int64_t pair_cap, void* ws, size_t ws_bytes,
+             void* stream);
+
+/* engine.interpolate local part (basis.py:285-303 contraction):
+ * values [n][C] at records (code, elem, r); NOT_FOUND -> NaN (D12).
+ * fbasis: packed constants of the field order (Nf may differ from N). */
+size_t fpx_eval_workspace_bytes(int64_t E, int64_t n);
+int fpx_findpts_eval(int dr, int Nf, const double* fbasis, int C, int64_t E,
+                     const double* field, int64_t n, const int32_t* code, const int32_t* elem,
+                     const double* r, double* values, void* ws, size_t ws_bytes, void* stream);
+
+/* invmap.invert_point batched over explicit (point, element) pairs
+ * (SPEC.md:298-307): r [npairs][dr], dist, iters, converged. */
+int fpx_invert_pairs(const fpx_mesh_t* m, int64_t npairs, const double* x, const int32_t* elem,
+                     double* r, double* dist, int32_t* iters, int32_t* converged, void* stream);
+
+/* invmap.forward_map batched: x [n][d], G [n][d][dr],
+ * H2 [n][d][6] (optional; symmetric order rr,ss,tt,rs,rt,st). */
+int fpx_forward_map(const fpx_mesh_t* m, int64_t n, const int32_t* elem, const double* r,
+                    double* x, double* G, double* H2, void* stream);
+
+/* Multi-rank routing helpers (engine Phase B):
+ * global-grid cell owner of each point and the destination counts for an
+ * all-to-allv: dest[n] in [-1, nranks), counts [nranks] (device int64). */
+int fpx_route_count(int64_t n, const int32_t* dest, int nranks, int64_t* counts, void* stream);
+/* Stable pack by destination: perm[n] = position of point i in the send buffer
+ * (-1 for dest < 0); offsets [nranks] = exclusive scan of counts. */
+int fpx_route_pack(int64_t n, const int32_t* dest, int nranks, const int64_t* offsets,
+                   int64_t* perm, void* ws, size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FPX_H */

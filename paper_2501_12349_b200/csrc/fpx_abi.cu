@@ -1,0 +1,456 @@
+// fpx_abi.cu -- extern "C" entry points of libfpx_sm100.so (include/fpx.h).
+//
+// Host-side orchestration of the kernels: argument checks, workspace
+// carving, CUB scans, stream-ordered launches.  No exceptions cross the ABI;
+// failures return FPX_E* with a thread-local message.
+#include <cub/device/device_scan.cuh>
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "../../include/fpx.h"
+#include "fpx_common.cuh"
+#include "fpx_kernels.cuh"
+
+namespace fpx {
+cudaError_t launch_invert_pairs_grouped(const fpx_mesh_t& m, const double* x,
+                                        const int32_t* sorted, const Item* items,
+                                        const int64_t* nitems_dev, int64_t items_cap, double* r,
+                                        double* dist, int32_t* iters, int32_t* conv,
+                                        cudaStream_t st);
+}
+
+using fpx::Item;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define FPX_CK(expr)                                                                   \
+  do {                                                                                 \
+    cudaError_t e_ = (expr);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(FPX_ECUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                                 \
+  } while (0)
+
+// Bump allocator over a caller-provided workspace (256-byte aligned slices).
+struct Carver {
+  char* base;
+  size_t cap, off;
+  explicit Carver(void* b, size_t c) : base((char*)b), cap(c), off(0) {}
+  template <typename T>
+  T* take(size_t count) {
+    size_t a = (off + 255) & ~size_t(255);
+    off = a + count * sizeof(T);
+    if (!base) return nullptr;
+    return reinterpret_cast<T*>(base + a);
+  }
+  bool ok() const { return off <= cap; }
+};
+
+size_t scan_temp_u64(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, (uint64_t*)nullptr, (uint64_t*)nullptr, (int)n);
+  return bytes;
+}
+size_t scan_temp_i64(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, (int64_t*)nullptr, (int64_t*)nullptr, (int)n);
+  return bytes;
+}
+size_t scan_temp_i32(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, (int32_t*)nullptr, (int32_t*)nullptr, (int)n);
+  return bytes;
+}
+
+int64_t items_cap_of(int64_t E, int64_t units) { return E + units / FPX_ITEM + 2; }
+
+// Grouping buffers for up to `units` units over E elements.
+struct Group {
+  int32_t* count;
+  int32_t* cursor;
+  uint64_t* packed;
+  uint64_t* packed_off;
+  Item* items;
+  int64_t* nitems;
+  int32_t* sorted;
+  void* temp;
+  size_t temp_bytes;
+  int64_t items_cap;
+  void carve(Carver& c, int64_t E, int64_t units) {
+    count = c.take<int32_t>(E);
+    cursor = c.take<int32_t>(E);
+    packed = c.take<uint64_t>(E + 1);
+    packed_off = c.take<uint64_t>(E + 1);
+    items_cap = items_cap_of(E, units);
+    items = c.take<Item>(items_cap);
+    nitems = c.take<int64_t>(1);
+    sorted = c.take<int32_t>(units > 0 ? units : 1);
+    temp_bytes = scan_temp_u64(E + 1);
+    temp = c.take<char>(temp_bytes);
+  }
+  // counts must be filled; builds items and scatters units.
+  cudaError_t build(int64_t E, int64_t units_cap, const int64_t* units_dev,
+                    const int32_t* unit_elem, const int32_t* unit_ids, cudaStream_t st) {
+    cudaError_t e;
+    if ((e = fpx::launch_pack_counts(E, count, packed, st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(packed + E, 0, sizeof(uint64_t), st)) != cudaSuccess) return e;
+    size_t tb = temp_bytes;
+    if ((e = cub::DeviceScan::ExclusiveSum(temp, tb, packed, packed_off, (int)(E + 1), st)) !=
+        cudaSuccess)
+      return e;
+    if ((e = fpx::launch_make_items(E, count, packed_off, items, nitems, st)) != cudaSuccess)
+      return e;
+    if ((e = cudaMemsetAsync(cursor, 0, sizeof(int32_t) * E, st)) != cudaSuccess) return e;
+    return fpx::launch_scatter_units(units_cap, units_dev, unit_elem, unit_ids, packed_off,
+                                     cursor, sorted, st);
+  }
+};
+
+struct FindWs {
+  int32_t *best, *npass, *upts;
+  int64_t *upair_cnt, *pair_off, *nun, *npairs;
+  int32_t *pair_pt, *pair_elem, *pcode, *piters;
+  double *pr, *pdist;
+  Group g1, g2;
+  void* scan2_temp;
+  size_t scan2_bytes;
+  void carve(Carver& c, int64_t E, int64_t n, int64_t cap) {
+    best = c.take<int32_t>(n);
+    npass = c.take<int32_t>(n);
+    upts = c.take<int32_t>(n);
+    upair_cnt = c.take<int64_t>(n + 1);
+    pair_off = c.take<int64_t>(n + 1);
+    nun = c.take<int64_t>(1);
+    npairs = c.take<int64_t>(1);
+    pair_pt = c.take<int32_t>(cap);
+    pair_elem = c.take<int32_t>(cap);
+    pcode = c.take<int32_t>(cap);
+    piters = c.take<int32_t>(cap);
+    pr = c.take<double>(3 * cap);
+    pdist = c.take<double>(cap);
+    g1.carve(c, E, n);
+    g2.carve(c, E, cap);
+    scan2_bytes = scan_temp_i64(n + 1);
+    scan2_temp = c.take<char>(scan2_bytes);
+  }
+};
+
+__global__ void k_pairs_total(const int64_t* __restrict__ pair_off, const int64_t* __restrict__ nun,
+                              int64_t cap, int64_t* npairs, int64_t* stats, int64_t n) {
+  const int64_t t = pair_off[*nun];
+  *npairs = t < cap ? t : cap;
+  stats[FPX_STAT_POINTS] = n;
+  stats[FPX_STAT_ROUND2_POINTS] = *nun;
+  stats[FPX_STAT_ROUND2_PAIRS] = t;
+}
+
+__global__ void k_count_elems(int64_t n, const int32_t* __restrict__ elem, int32_t* count) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&count[elem[k]], 1);
+}
+
+__global__ void k_route_count(int64_t n, const int32_t* __restrict__ dest, int nranks,
+                              int64_t* counts) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int d = dest[k];
+    if (d >= 0 && d < nranks) atomicAdd((unsigned long long*)&counts[d], 1ull);
+  }
+}
+
+__global__ void k_route_flags(int64_t n, const int32_t* __restrict__ dest, int rank,
+                              int64_t* flags) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x)
+    flags[k] = dest[k] == rank ? 1 : 0;
+}
+
+__global__ void k_route_place(int64_t n, const int32_t* __restrict__ dest, int rank,
+                              const int64_t* __restrict__ pos, const int64_t* __restrict__ offsets,
+                              int64_t* perm) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int d = dest[k];
+    if (d == rank) perm[k] = offsets[rank] + pos[k];
+    else if (d < 0 && rank == 0) perm[k] = -1;
+  }
+}
+
+unsigned grid1(int64_t n, int threads = 256) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b > 148 * 32) b = 148 * 32;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int check_mesh(const fpx_mesh_t* m) {
+  if (!m) return fail(FPX_EINVAL, "mesh is NULL");
+  if (!(m->d == 2 || m->d == 3) || m->dr < 1 || m->dr > m->d)
+    return fail(FPX_EINVAL, "bad dimensions d=%d dr=%d", m->d, m->dr);
+  if (!fpx::newton_supported(m->d, m->dr, m->N))
+    return fail(FPX_EUNSUPPORTED, "order N=%d not compiled for d=%d dr=%d", m->N, m->d, m->dr);
+  if (m->E < 1 || m->E > INT32_MAX) return fail(FPX_EINVAL, "bad element count %lld", (long long)m->E);
+  return FPX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fpx_abi_version(void) { return FPX_ABI_VERSION; }
+
+const char* fpx_last_error(void) { return g_err.c_str(); }
+
+int fpx_supported(int d, int dr, int N) { return fpx::newton_supported(d, dr, N) ? 1 : 0; }
+
+int fpx_setup_bounds(int d, int dr, int N, int M, int64_t E, const double* basis,
+                     const double* nodes, double expansion, double* aabb, double* obb_c,
+                     double* obb_inv, double* hbox, double* frame, uint8_t* obb_ok,
+                     int32_t* status, void* stream) {
+  if (!(d == 2 || d == 3) || dr < 1 || dr > d) return fail(FPX_EINVAL, "bad d/dr %d/%d", d, dr);
+  if (N < 2 || N > FPX_SETUP_MAXN) return fail(FPX_EUNSUPPORTED, "setup supports 2 <= N <= %d", FPX_SETUP_MAXN);
+  if (M < N || M > 4 * FPX_SETUP_MAXN) return fail(FPX_EINVAL, "bad interval count M=%d", M);
+  if (E < 0) return fail(FPX_EINVAL, "negative element count");
+  if (E == 0) return FPX_OK;
+  FPX_CK(fpx::launch_setup_bounds(d, dr, N, M, E, basis, nodes, expansion, aabb, obb_c, obb_inv,
+                                  hbox, frame, obb_ok, status, S(stream)));
+  return FPX_OK;
+}
+
+int fpx_bound_function(int dr, int N, int M, int64_t nf, const double* basis,
+                       const double* values, double* lower, double* upper, void* stream) {
+  if (dr != 1 && dr != 2) return fail(FPX_EINVAL, "bound_function: dr must be 1 or 2");
+  if (N < 2 || N > FPX_SETUP_MAXN || M < N || M > 4 * FPX_SETUP_MAXN)
+    return fail(FPX_EINVAL, "bound_function: bad N=%d M=%d", N, M);
+  if (nf <= 0) return FPX_OK;
+  FPX_CK(fpx::launch_bound_function(dr, N, M, nf, basis, values, lower, upper, S(stream)));
+  return FPX_OK;
+}
+
+size_t fpx_hash_workspace_bytes(int d, int64_t E, int ncell) {
+  (void)E;
+  int64_t nc = 1;
+  for (int c = 0; c < d; ++c) nc *= ncell;
+  Carver c(nullptr, 0);
+  c.take<int32_t>(nc + 1);
+  c.take<int32_t>(nc + 1);
+  c.take<int32_t>(1);
+  c.take<char>(scan_temp_i32(nc + 1));
+  return c.off + 256;
+}
+
+int fpx_hash_build(int d, int64_t E, const double* box, int ncell, double* grid,
+                   int32_t* offsets, int32_t* elems, int64_t cap, int64_t* needed_host,
+                   int32_t* max_list_host, void* ws, size_t ws_bytes, void* stream) {
+  if (!(d == 2 || d == 3)) return fail(FPX_EINVAL, "hash: bad d=%d", d);
+  if (E < 1) return fail(FPX_EINVAL, "build_local_map: empty element list (SPEC.md:234)");
+  if (ncell < 1 || ncell > 1024) return fail(FPX_EINVAL, "hash: cells per axis %d", ncell);
+  int64_t nc = 1;
+  for (int c = 0; c < d; ++c) nc *= ncell;
+  if (nc > (int64_t)1 << 30) return fail(FPX_EINVAL, "hash: too many cells (%lld)", (long long)nc);
+  Carver cv(ws, ws_bytes);
+  int32_t* cnt = cv.take<int32_t>(nc + 1);
+  int32_t* cursor = cv.take<int32_t>(nc + 1);
+  int32_t* maxl = cv.take<int32_t>(1);
+  size_t tb = scan_temp_i32(nc + 1);
+  void* temp = cv.take<char>(tb);
+  if (!cv.ok()) return fail(FPX_EINVAL, "hash workspace too small (%zu < %zu)", ws_bytes, cv.off);
+  cudaStream_t st = S(stream);
+  FPX_CK(fpx::launch_hash_grid(d, E, box, ncell, grid, st));
+  FPX_CK(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (nc + 1), st));
+  FPX_CK(fpx::launch_hash_count(d, E, box, grid, ncell, cnt, st));
+  FPX_CK(cub::DeviceScan::ExclusiveSum(temp, tb, cnt, offsets, (int)(nc + 1), st));
+  int32_t total = 0;
+  FPX_CK(cudaMemcpyAsync(&total, offsets + nc, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  FPX_CK(cudaStreamSynchronize(st));
+  if (total < 0) return fail(FPX_EINVAL, "hash: entry count overflow");
+  if (needed_host) *needed_host = total;
+  if (!elems || cap < total) return FPX_OK;
+  FPX_CK(cudaMemsetAsync(cursor, 0, sizeof(int32_t) * (nc + 1), st));
+  FPX_CK(cudaMemsetAsync(maxl, 0, sizeof(int32_t), st));
+  FPX_CK(fpx::launch_hash_fill(d, E, box, grid, ncell, offsets, cursor, elems, st));
+  FPX_CK(fpx::launch_hash_sort(nc, offsets, elems, maxl, st));
+  int32_t ml = 0;
+  FPX_CK(cudaMemcpyAsync(&ml, maxl, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  FPX_CK(cudaStreamSynchronize(st));
+  if (max_list_host) *max_list_host = ml;
+  return FPX_OK;
+}
+
+int fpx_cell_of(const fpx_mesh_t* m, int64_t n, const double* x, int64_t* cell, void* stream) {
+  if (!m) return fail(FPX_EINVAL, "mesh is NULL");
+  if (n <= 0) return FPX_OK;
+  FPX_CK(fpx::launch_cell_of(m->d, m->grid, m->ncell, n, x, cell, S(stream)));
+  return FPX_OK;
+}
+
+size_t fpx_find_workspace_bytes(int64_t E, int64_t n, int64_t pair_cap) {
+  Carver c(nullptr, 0);
+  FindWs w;
+  w.carve(c, E, n > 0 ? n : 1, pair_cap > 0 ? pair_cap : 1);
+  return c.off + 256;
+}
+
+int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int32_t* elem,
+             double* r, double* dist, int32_t* iters, const double* field, int C,
+             double* values, int64_t* stats, int64_t pair_cap, void* ws, size_t ws_bytes,
+             void* stream) {
+  int rc = check_mesh(m);
+  if (rc) return rc;
+  if (n < 0 || n > INT32_MAX) return fail(FPX_EINVAL, "bad point count %lld", (long long)n);
+  if (!stats) return fail(FPX_EINVAL, "stats buffer required");
+  if (field && (C < 1 || !values)) return fail(FPX_EINVAL, "field given without C/values");
+  if (pair_cap < 1) pair_cap = 1;
+  cudaStream_t st = S(stream);
+  FPX_CK(cudaMemsetAsync(stats, 0, sizeof(int64_t) * FPX_STATS_LEN, st));
+  if (n == 0) return FPX_OK;
+  const int64_t E = m->E;
+  Carver cv(ws, ws_bytes);
+  FindWs w;
+  w.carve(cv, E, n, pair_cap);
+  if (!cv.ok()) return fail(FPX_EINVAL, "find workspace too small (%zu < %zu)", ws_bytes, cv.off);
+  const fpx_mesh_t& M = *m;
+  // --- prefilter: hash lookup + AABB/OBB filter + best-first candidate
+  FPX_CK(cudaMemsetAsync(w.g1.count, 0, sizeof(int32_t) * E, st));
+  FPX_CK(fpx::launch_find_prefilter(M, n, x, w.best, w.npass, code, elem, r, dist, iters,
+                                    field ? values : nullptr, C, w.g1.count, stats, st));
+  // --- round 1: group by best-first element, Newton, fused eval
+  FPX_CK(w.g1.build(E, n, nullptr, w.best, nullptr, st));
+  FPX_CK(cudaMemsetAsync(w.upair_cnt, 0, sizeof(int64_t) * (n + 1), st));
+  FPX_CK(cudaMemsetAsync(w.nun, 0, sizeof(int64_t), st));
+  FPX_CK(fpx::launch_newton_round1(M, n, x, w.g1.sorted, w.g1.items, w.g1.nitems, w.g1.items_cap,
+                                   w.npass, code, elem, r, dist, iters, field, C, values, w.upts,
+                                   w.upair_cnt, w.nun, stats, st));
+  // --- round 2: every other passing candidate of the unresolved points
+  size_t tb = w.scan2_bytes;
+  FPX_CK(cub::DeviceScan::ExclusiveSum(w.scan2_temp, tb, w.upair_cnt, w.pair_off, (int)(n + 1), st));
+  FPX_CK(cudaMemsetAsync(w.g2.count, 0, sizeof(int32_t) * E, st));
+  FPX_CK(fpx::launch_round2_emit(M, n, w.nun, w.upts, x, w.best, w.pair_off, pair_cap, w.pair_pt,
+                                 w.pair_elem, w.g2.count, stats, st));
+  k_pairs_total<<<1, 1, 0, st>>>(w.pair_off, w.nun, pair_cap, w.npairs, stats, n);
+  FPX_CK(cudaGetLastError());
+  FPX_CK(w.g2.build(E, pair_cap, w.npairs, w.pair_elem, nullptr, st));
+  FPX_CK(fpx::launch_newton_pairs(M, x, w.pair_pt, w.g2.sorted, w.g2.items, w.g2.nitems,
+                                  w.g2.items_cap, w.pcode, w.pr, w.pdist, w.piters, stats, st));
+  FPX_CK(fpx::launch_round2_finalize(M, n, w.nun, w.upts, w.pair_off, pair_cap, w.pair_elem,
+                                     w.pcode, w.pr, w.pdist, w.piters, code, elem, r, dist, iters,
+                                     field, C, values, stats, st));
+  return FPX_OK;
+}
+
+size_t fpx_eval_workspace_bytes(int64_t E, int64_t n) {
+  Carver c(nullptr, 0);
+  c.take<int32_t>(n > 0 ? n : 1);
+  Group g;
+  g.carve(c, E, n > 0 ? n : 1);
+  return c.off + 256;
+}
+
+int fpx_findpts_eval(int dr, int Nf, const double* fbasis, int C, int64_t E,
+                     const double* field, int64_t n, const int32_t* code, const int32_t* elem,
+                     const double* r, double* values, void* ws, size_t ws_bytes, void* stream) {
+  if (dr < 1 || dr > 3) return fail(FPX_EINVAL, "eval: bad dr=%d", dr);
+  if (!fpx::newton_supported(dr == 3 ? 3 : (dr == 2 ? 2 : 2), dr, Nf))
+    return fail(FPX_EUNSUPPORTED, "eval: field order N=%d not compiled for dr=%d", Nf, dr);
+  if (C < 1) return fail(FPX_EINVAL, "eval: components must be >= 1");
+  if (E < 1 || n < 0) return fail(FPX_EINVAL, "eval: bad sizes");
+  if (n == 0) return FPX_OK;
+  cudaStream_t st = S(stream);
+  Carver cv(ws, ws_bytes);
+  int32_t* unit_elem = cv.take<int32_t>(n);
+  Group g;
+  g.carve(cv, E, n);
+  if (!cv.ok()) return fail(FPX_EINVAL, "eval workspace too small (%zu < %zu)", ws_bytes, cv.off);
+  FPX_CK(cudaMemsetAsync(g.count, 0, sizeof(int32_t) * E, st));
+  FPX_CK(fpx::launch_eval_mark(n, C, code, elem, values, unit_elem, g.count, st));
+  FPX_CK(g.build(E, n, nullptr, unit_elem, nullptr, st));
+  FPX_CK(fpx::launch_eval_items(dr, Nf, fbasis, C, field, r, g.sorted, g.items, g.nitems,
+                                g.items_cap, values, st));
+  return FPX_OK;
+}
+
+int fpx_invert_pairs(const fpx_mesh_t* m, int64_t npairs, const double* x, const int32_t* elem,
+                     double* r, double* dist, int32_t* iters, int32_t* converged, void* stream) {
+  int rc = check_mesh(m);
+  if (rc) return rc;
+  if (npairs <= 0) return FPX_OK;
+  cudaStream_t st = S(stream);
+  Carver probe(nullptr, 0);
+  Group g;
+  g.carve(probe, m->E, npairs);
+  void* ws = nullptr;
+  FPX_CK(cudaMallocAsync(&ws, probe.off + 256, st));
+  Carver cv(ws, probe.off + 256);
+  g.carve(cv, m->E, npairs);
+  FPX_CK(cudaMemsetAsync(g.count, 0, sizeof(int32_t) * m->E, st));
+  k_count_elems<<<grid1(npairs), 256, 0, st>>>(npairs, elem, g.count);
+  FPX_CK(cudaGetLastError());
+  FPX_CK(g.build(m->E, npairs, nullptr, elem, nullptr, st));
+  FPX_CK(fpx::launch_invert_pairs_grouped(*m, x, g.sorted, g.items, g.nitems, g.items_cap, r, dist,
+                                          iters, converged, st));
+  FPX_CK(cudaFreeAsync(ws, st));
+  return FPX_OK;
+}
+
+int fpx_forward_map(const fpx_mesh_t* m, int64_t n, const int32_t* elem, const double* r,
+                    double* x, double* G, double* H2, void* stream) {
+  int rc = check_mesh(m);
+  if (rc) return rc;
+  if (n <= 0) return FPX_OK;
+  FPX_CK(fpx::launch_forward_map(*m, n, elem, r, x, G, H2, S(stream)));
+  return FPX_OK;
+}
+
+int fpx_route_count(int64_t n, const int32_t* dest, int nranks, int64_t* counts, void* stream) {
+  if (nranks < 1) return fail(FPX_EINVAL, "route: nranks < 1");
+  cudaStream_t st = S(stream);
+  FPX_CK(cudaMemsetAsync(counts, 0, sizeof(int64_t) * nranks, st));
+  if (n <= 0) return FPX_OK;
+  k_route_count<<<grid1(n), 256, 0, st>>>(n, dest, nranks, counts);
+  FPX_CK(cudaGetLastError());
+  return FPX_OK;
+}
+
+int fpx_route_pack(int64_t n, const int32_t* dest, int nranks, const int64_t* offsets,
+                   int64_t* perm, void* ws, size_t ws_bytes, void* stream) {
+  if (nranks < 1) return fail(FPX_EINVAL, "route: nranks < 1");
+  if (n <= 0) return FPX_OK;
+  cudaStream_t st = S(stream);
+  Carver cv(ws, ws_bytes);
+  int64_t* flags = cv.take<int64_t>(n);
+  int64_t* pos = cv.take<int64_t>(n);
+  size_t tb = scan_temp_i64(n);
+  void* temp = cv.take<char>(tb);
+  if (!ws) return fail(FPX_EINVAL, "route: workspace required (%zu bytes)", cv.off + 256);
+  if (!cv.ok()) return fail(FPX_EINVAL, "route workspace too small (%zu < %zu)", ws_bytes, cv.off);
+  for (int rk = 0; rk < nranks; ++rk) {
+    k_route_flags<<<grid1(n), 256, 0, st>>>(n, dest, rk, flags);
+    FPX_CK(cudaGetLastError());
+    size_t t2 = tb;
+    FPX_CK(cub::DeviceScan::ExclusiveSum(temp, t2, flags, pos, (int)n, st));
+    k_route_place<<<grid1(n), 256, 0, st>>>(n, dest, rk, pos, offsets, perm);
+    FPX_CK(cudaGetLastError());
+  }
+  return FPX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,86 @@
+// fpx_group.cu -- element grouping of find/eval work units.
+//
+// Units (points or (point, element) pairs) keyed by element id are bucketed
+// with a counting sort: per-element counts, one exclusive scan of the packed
+// (items << 32 | count) words, then a scatter.  A work item is one element
+// and up to FPX_ITEM units; one warp processes one item.  Order within an
+// element is irrelevant: every unit's result depends only on its own inputs.
+#include "fpx_common.cuh"
+#include "fpx_kernels.cuh"
+
+namespace fpx {
+
+static unsigned grid_of(int64_t n, int threads) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b > 148 * 32) b = 148 * 32;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+__global__ void k_pack_counts(int64_t E, const int32_t* __restrict__ count, uint64_t* packed) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t c = (uint32_t)count[e];
+    const uint64_t it = (c + FPX_ITEM - 1) / FPX_ITEM;
+    packed[e] = (it << 32) | c;
+  }
+}
+
+// packed_off = exclusive scan of packed (E + 1 entries: last = totals).
+__global__ void k_make_items(int64_t E, const int32_t* __restrict__ count,
+                             const uint64_t* __restrict__ packed_off, Item* items,
+                             int64_t* nitems_dev) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int c = count[e];
+    const uint64_t o = packed_off[e];
+    const int64_t item0 = (int64_t)(o >> 32);
+    const int64_t unit0 = (int64_t)(o & 0xffffffffull);
+    for (int q = 0; q * FPX_ITEM < c; ++q) {
+      Item it;
+      it.elem = (int32_t)e;
+      it.start = (int32_t)(unit0 + q * FPX_ITEM);
+      it.count = c - q * FPX_ITEM < FPX_ITEM ? c - q * FPX_ITEM : FPX_ITEM;
+      items[item0 + q] = it;
+    }
+    if (e == E - 1) *nitems_dev = (int64_t)(packed_off[E] >> 32);
+  }
+}
+
+__global__ void k_scatter_units(int64_t cap, const int64_t* __restrict__ n_dev,
+                                const int32_t* __restrict__ unit_elem,
+                                const int32_t* __restrict__ unit_ids,
+                                const uint64_t* __restrict__ packed_off, int32_t* cursor,
+                                int32_t* sorted) {
+  const int64_t n = n_dev ? *n_dev : cap;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const int e = unit_elem[u];
+    if (e < 0) continue;
+    const int slot = atomicAdd(&cursor[e], 1);
+    sorted[(int64_t)(packed_off[e] & 0xffffffffull) + slot] = unit_ids ? unit_ids[u] : (int32_t)u;
+  }
+}
+
+cudaError_t launch_pack_counts(int64_t E, const int32_t* count, uint64_t* packed,
+                               cudaStream_t st) {
+  k_pack_counts<<<grid_of(E, 256), 256, 0, st>>>(E, count, packed);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_make_items(int64_t E, const int32_t* count, const uint64_t* packed_off,
+                              Item* items, int64_t* nitems_dev, cudaStream_t st) {
+  k_make_items<<<grid_of(E, 256), 256, 0, st>>>(E, count, packed_off, items, nitems_dev);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scatter_units(int64_t nunits_cap, const int64_t* nunits_dev,
+                                 const int32_t* unit_elem, const int32_t* unit_ids,
+                                 const uint64_t* packed_off, int32_t* cursor, int32_t* sorted,
+                                 cudaStream_t st) {
+  k_scatter_units<<<grid_of(nunits_cap, 256), 256, 0, st>>>(nunits_cap, nunits_dev, unit_elem,
+                                                            unit_ids, packed_off, cursor, sorted);
+  return cudaGetLastError();
+}
+
+}  // namespace fpx

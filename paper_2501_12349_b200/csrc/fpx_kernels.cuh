@@ -1,0 +1,93 @@
+// fpx_kernels.cuh -- host launchers shared between the kernel TUs and the ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/fpx.h"
+
+#define FPX_SETUP_MAXN 16  // setup kernels: nodes per axis <= 16 (p <= 15)
+#define FPX_ITEM 32        // (point|pair) slots per warp work item
+
+namespace fpx {
+
+// Work item of the element-major kernels: one warp, one element, <= 32 units.
+struct Item {
+  int32_t elem;
+  int32_t start;  // offset into the element-sorted unit array
+  int32_t count;
+};
+
+cudaError_t launch_setup_bounds(int d, int dr, int N, int M, int64_t E, const double* basis,
+                                const double* nodes, double expansion, double* aabb, double* obb_c,
+                                double* obb_inv, double* hbox, double* frame, uint8_t* obb_ok,
+                                int32_t* status, cudaStream_t st);
+cudaError_t launch_bound_function(int dr, int N, int M, int64_t nf, const double* basis,
+                                  const double* values, double* lower, double* upper,
+                                  cudaStream_t st);
+cudaError_t launch_hash_grid(int d, int64_t E, const double* box, int ncell, double* grid,
+                             cudaStream_t st);
+cudaError_t launch_hash_count(int d, int64_t E, const double* box, const double* grid, int n,
+                              int32_t* cnt, cudaStream_t st);
+cudaError_t launch_hash_fill(int d, int64_t E, const double* box, const double* grid, int n,
+                             const int32_t* offsets, int32_t* cursor, int32_t* elems,
+                             cudaStream_t st);
+cudaError_t launch_hash_sort(int64_t ncells, const int32_t* offsets, int32_t* elems,
+                             int32_t* max_list, cudaStream_t st);
+cudaError_t launch_cell_of(int d, const double* grid, int n, int64_t npts, const double* x,
+                           int64_t* cell, cudaStream_t st);
+cudaError_t launch_find_prefilter(const fpx_mesh_t& m, int64_t n, const double* x, int32_t* best,
+                                  int32_t* npass, int32_t* code, int32_t* elem, double* r,
+                                  double* dist, int32_t* iters, double* values, int C,
+                                  int32_t* elem_count, int64_t* stats, cudaStream_t st);
+cudaError_t launch_round2_emit(const fpx_mesh_t& m, int64_t nun_cap, const int64_t* nun_dev,
+                               const int32_t* upts, const double* x, const int32_t* best,
+                               const int64_t* pair_off, int64_t pair_cap, int32_t* pair_pt,
+                               int32_t* pair_elem, int32_t* elem_count, int64_t* stats,
+                               cudaStream_t st);
+
+// Element grouping (fpx_group.cu): count -> packed scan -> items + scatter.
+cudaError_t launch_make_items(int64_t E, const int32_t* count, const uint64_t* packed_off,
+                              Item* items, int64_t* nitems_dev, cudaStream_t st);
+cudaError_t launch_pack_counts(int64_t E, const int32_t* count, uint64_t* packed,
+                               cudaStream_t st);
+cudaError_t launch_scatter_units(int64_t nunits_cap, const int64_t* nunits_dev,
+                                 const int32_t* unit_elem, const int32_t* unit_ids,
+                                 const uint64_t* packed_off, int32_t* cursor, int32_t* sorted,
+                                 cudaStream_t st);
+
+// Newton / eval (fpx_newton.cu, FMA allowed).
+bool newton_supported(int d, int dr, int N);
+cudaError_t launch_newton_round1(const fpx_mesh_t& m, int64_t n, const double* x,
+                                 const int32_t* sorted_pts, const Item* items,
+                                 const int64_t* nitems_dev, int64_t items_cap,
+                                 const int32_t* npass, int32_t* code, int32_t* elem, double* r,
+                                 double* dist, int32_t* iters, const double* field, int C,
+                                 double* values, int32_t* upts, int64_t* upair_cnt,
+                                 int64_t* nun_dev, int64_t* stats, cudaStream_t st);
+cudaError_t launch_newton_pairs(const fpx_mesh_t& m, const double* x, const int32_t* pair_pt,
+                                const int32_t* sorted_pairs, const Item* items,
+                                const int64_t* nitems_dev, int64_t items_cap, int32_t* pcode,
+                                double* pr, double* pdist, int32_t* piters, int64_t* stats,
+                                cudaStream_t st);
+cudaError_t launch_round2_finalize(const fpx_mesh_t& m, int64_t nun_cap, const int64_t* nun_dev,
+                                   const int32_t* upts, const int64_t* pair_off,
+                                   int64_t pair_cap, const int32_t* pair_elem,
+                                   const int32_t* pcode, const double* pr, const double* pdist,
+                                   const int32_t* piters, int32_t* code, int32_t* elem, double* r,
+                                   double* dist, int32_t* iters, const double* field, int C,
+                                   double* values, int64_t* stats, cudaStream_t st);
+cudaError_t launch_eval_items(int dr, int Nf, const double* fbasis, int C, const double* field,
+                              const double* r, const int32_t* sorted_pts, const Item* items,
+                              const int64_t* nitems_dev, int64_t items_cap, double* values,
+                              cudaStream_t st);
+cudaError_t launch_eval_mark(int64_t n, int C, const int32_t* code, const int32_t* elem,
+                             double* values, int32_t* unit_elem, int32_t* count,
+                             cudaStream_t st);
+cudaError_t launch_invert_pairs(const fpx_mesh_t& m, int64_t npairs, const double* x,
+                                const int32_t* elem, double* r, double* dist, int32_t* iters,
+                                int32_t* conv, cudaStream_t st);
+cudaError_t launch_forward_map(const fpx_mesh_t& m, int64_t n, const int32_t* elem,
+                               const double* r, double* x, double* G, double* H2,
+                               cudaStream_t st);
+
+}  // namespace fpx

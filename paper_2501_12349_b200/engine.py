@@ -1,0 +1,324 @@
+"""Setup / Find / Interpolate (drop-in for SPEC.md:381-447 `engine`).
+
+Everything per point runs in the CUDA kernels of libfpx_sm100.so:
+setup -> `fpx_setup_bounds` + `fpx_hash_build`; find -> `fpx_find`
+(prefilter, element-grouped Newton, round 2, fused eval); interpolate ->
+`fpx_findpts_eval`.  Multi-rank Phase B routes points and
+records between ranks with torch.distributed all-to-alls (NCCL over NVLink on
+GPUs) around those kernels.
+
+Batched SoA interface:
+  setup(nodes f64[E, d, N**dr], order, ref_dim, options=..., group=...)
+  find(S, x f64[n, d]) -> FindRecords(code, rank, elem, r, dist)
+  interpolate(S, field f64[E, C, Nf**dr] | Field, records) -> f64[n, C]
+  find_and_interpolate(S, field, x) -> (values, records)
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field as dfield
+
+import numpy as np
+import torch
+
+from . import _C, transport
+from .basis import ReferenceBasis, build_basis_envelope
+from .bounds import DegenerateElementError, GeometryError, device_basis, element_boxes
+from .invmap import BORDER, INTERIOR, NOT_FOUND, NewtonSettings
+from .spatial_hash import CartesianGrid, GlobalMapShard, build_global_map, n_cells
+
+__all__ = ["EngineOptions", "EngineSetup", "Field", "FindRecord", "FindRecords", "setup",
+           "find", "interpolate", "find_and_interpolate", "INTERIOR", "BORDER", "NOT_FOUND"]
+
+
+@dataclass
+class EngineOptions:
+    """Setup options."""
+
+    expansion: float = 0.10
+    interval_count: int | None = None
+    cells_local: int | None = None
+    cells_global: int | None = None
+    newton: NewtonSettings = dfield(default_factory=NewtonSettings)
+    eps_d: float | None = None        # absolute surface threshold; None -> relative
+    eps_d_rel: float = 1e-10
+    pair_capacity: float = 2.0        # round-2 pair workspace, x n (grows on demand)
+
+
+@dataclass
+class Field:
+    """Per-element coefficient blocks u^e [E, C, Nf**dr] of order `order`
+    (SPEC.md:394-397)."""
+
+    blocks: torch.Tensor
+    order: int
+
+    @property
+    def components(self) -> int:
+        return int(self.blocks.shape[1])
+
+
+@dataclass
+class FindRecord:
+    """q* = {m*, e*, r*, d*, c*} of one point."""
+
+    code: int
+    rank: int
+    elem: int
+    r: np.ndarray
+    dist: float
+
+
+@dataclass
+class FindRecords:
+    """Batched records (device tensors).  NOT_FOUND: rank = elem = -1,
+    r = dist = NaN (decision D10)."""
+
+    code: torch.Tensor
+    rank: torch.Tensor
+    elem: torch.Tensor
+    r: torch.Tensor
+    dist: torch.Tensor
+    iters: torch.Tensor | None = None
+    stats: dict | None = None
+
+    def __len__(self) -> int:
+        return int(self.code.shape[0])
+
+    def __getitem__(self, i: int) -> FindRecord:
+        return FindRecord(int(self.code[i]), int(self.rank[i]), int(self.elem[i]),
+                          self.r[i].cpu().numpy(), float(self.dist[i]))
+
+    def counts(self) -> dict:
+        c = torch.bincount(self.code.long(), minlength=3).tolist()
+        return {"INTERIOR": c[0], "BORDER": c[1], "NOT_FOUND": c[2]}
+
+
+class EngineSetup:
+    """Device-resident setup of this rank's mesh partition;
+    immutable after construction."""
+
+    def __init__(self):
+        self.workspace = None
+        self.stats_host = None
+
+    @property
+    def num_elements(self) -> int:
+        return self.E
+
+    def local_map_entries(self) -> int:
+        return int(self.elems.numel())
+
+
+def _as_device_nodes(nodes, dev) -> torch.Tensor:
+    if hasattr(nodes, "nodes") and hasattr(nodes, "order"):   # toolkit.MeshData
+        nodes = nodes.nodes
+    t = torch.as_tensor(nodes, dtype=torch.float64)
+    return t.to(dev).contiguous()
+
+
+def setup(nodes, order: int | None = None, ref_dim: int | None = None, *,
+          options: EngineOptions | None = None, group: transport.RankGroup | None = None,
+          elem_offset: int = 0) -> EngineSetup:
+    """Build envelopes, per-element AABB/OBB, the local map Psi_L and, for
+    several ranks, the global map Psi_G.  `nodes` holds this
+    rank's elements f64[E, d, N**dr] (or a toolkit.MeshData)."""
+    opt = options or EngineOptions()
+    dev = _C.require_cuda()
+    if hasattr(nodes, "order") and order is None:
+        order, ref_dim = nodes.order, nodes.ref_dim
+    X = _as_device_nodes(nodes, dev)
+    if X.ndim != 3:
+        raise GeometryError(f"nodes must be [E, d, N**dr], got {tuple(X.shape)}")
+    E, d, K = X.shape
+    if order is None:
+        raise GeometryError("order required")
+    N = order + 1
+    if ref_dim is None:
+        ref_dim = {N: 1, N * N: 2, N * N * N: 3}.get(K)
+    if ref_dim is None or N ** ref_dim != K or not (1 <= ref_dim <= d) or d not in (2, 3):
+        raise GeometryError(f"nodes shape {tuple(X.shape)} inconsistent with order {order}")
+    if E < 1:
+        raise GeometryError("setup needs at least one element")
+    if not bool(torch.isfinite(X).all()):
+        raise GeometryError("non-finite nodal coordinates")
+    if not _C.lib().fpx_supported(d, ref_dim, N):
+        raise _C.FpxNativeError(f"order {order} (d={d}, dr={ref_dim}) not compiled in")
+    basis = ReferenceBasis(order, opt.interval_count)
+    env = build_basis_envelope(basis)
+    bdev = device_basis(env, dev)
+    bx = element_boxes(X, d, ref_dim, env, opt.expansion, bdev)
+    status = bx["status"]
+    if bool((status == 1).any()):
+        bad = int(torch.nonzero(status == 1)[0, 0])
+        raise DegenerateElementError(f"element {bad} has zero extent on every axis")
+    S = EngineSetup()
+    S.device, S.phys_dim, S.ref_dim, S.order, S.E = dev, d, ref_dim, order, E
+    S.basis, S.envelope, S.basis_dev, S.options = basis, env, bdev, opt
+    S.nodes = X
+    S.aabb, S.obb_c, S.obb_inv = bx["aabb"], bx["obb_c"], bx["obb_inv"]
+    S.obb_ok, S.frame, S.hbox = bx["obb_ok"], bx["frame"], bx["hbox"]
+    # Psi_L over the hash boxes (decision D5)
+    from .spatial_hash import build_local_map
+    lmap = build_local_map(S.hbox, opt.cells_local or n_cells(E, d))
+    S.local_map = lmap
+    S.grid_dev, S.offsets, S.elems, S.ncell, S.max_list = \
+        lmap.grid_dev, lmap.offsets, lmap.elems if lmap.entries else \
+        torch.zeros(1, dtype=torch.int32, device=dev), lmap.grid.cells, lmap.max_list
+    m = _C.MeshT()
+    m.d, m.dr, m.N, m.M, m.E = d, ref_dim, N, env.interval_points.size, E
+    m.basis, m.nodes = bdev.data_ptr(), X.data_ptr()
+    m.aabb, m.obb_c, m.obb_inv = S.aabb.data_ptr(), S.obb_c.data_ptr(), S.obb_inv.data_ptr()
+    m.obb_ok, m.frame, m.grid = S.obb_ok.data_ptr(), S.frame.data_ptr(), S.grid_dev.data_ptr()
+    m.ncell, m.max_list = S.ncell, S.max_list
+    m.offsets, m.elems = S.offsets.data_ptr(), S.elems.data_ptr()
+    opt.newton.apply(m)
+    m.eps_d_abs = -1.0 if opt.eps_d is None else float(opt.eps_d)
+    m.eps_d_rel = float(opt.eps_d_rel)
+    S.mesh_t = m
+    # multi-rank: global map Psi_G over the union of all ranks' boxes
+    S.group = group or transport.RankGroup()
+    S.elem_offset = elem_offset
+    S.global_map = None
+    if not S.group.single:
+        lo = S.hbox[:, 0].amin(0).cpu()
+        hi = S.hbox[:, 1].amax(0).cpu()
+        glo, ghi = transport.reduce_domain_bbox(S.group, lo, hi)
+        etot = sum(transport.allgather_counts(S.group, E))
+        ng = opt.cells_global or n_cells(etot, d)
+        S.global_map = build_global_map(S.group, S.hbox, glo.numpy(), ghi.numpy(), ng)
+    return S
+
+
+# ---------------------------------------------------------------- find
+def _workspace(S: EngineSetup, n: int, pair_cap: int) -> torch.Tensor:
+    need = _C.lib().fpx_find_workspace_bytes(S.E, n, pair_cap)
+    if S.workspace is None or S.workspace.numel() < need:
+        S.workspace = torch.empty(need, dtype=torch.uint8, device=S.device)
+    return S.workspace
+
+
+def _stats_dict(st: np.ndarray) -> dict:
+    return {k: int(v) for k, v in zip(_C.STAT_NAMES, st)}
+
+
+def _find_local(S: EngineSetup, x: torch.Tensor, field: Field | None = None,
+                want_iters: bool = False):
+    """Phase A on this rank: the fpx_find kernel pipeline.  Returns a dict of
+    device tensors (code, elem [local ids], r, dist, values?, iters?) and the
+    kernel counters."""
+    n = int(x.shape[0])
+    dev = S.device
+    dr = S.ref_dim
+    out = dict(code=torch.empty(n, dtype=torch.int32, device=dev),
+               elem=torch.empty(n, dtype=torch.int32, device=dev),
+               r=torch.empty((n, dr), dtype=torch.float64, device=dev),
+               dist=torch.empty(n, dtype=torch.float64, device=dev))
+    out["iters"] = torch.empty(n, dtype=torch.int32, device=dev) if want_iters else None
+    blocks, C = None, 0
+    if field is not None:
+        blocks = field.blocks
+        C = int(blocks.shape[1])
+        out["values"] = torch.empty((n, C), dtype=torch.float64, device=dev)
+    stats = torch.zeros(_C.STATS_LEN, dtype=torch.int64, device=dev)
+    if n == 0:
+        return out, _stats_dict(np.zeros(_C.STATS_LEN, np.int64))
+    cap = max(1024, int(S.options.pair_capacity * n))
+    while True:
+        ws = _workspace(S, n, cap)
+        _C.check(_C.lib().fpx_find(
+            S.mesh_t, n, _C.ptr(x), _C.ptr(out["code"]), _C.ptr(out["elem"]), _C.ptr(out["r"]),
+            _C.ptr(out["dist"]), _C.ptr(out["iters"]), _C.ptr(blocks), C,
+            _C.ptr(out.get("values")), _C.ptr(stats), cap, _C.ptr(ws), ws.numel(),
+            _C.stream_handle()), "fpx_find")
+        st = stats.cpu().numpy()   # synchronises: records are complete here
+        if st[_C.STAT_NAMES.index("overflow")] == 0:
+            return out, _stats_dict(st)
+        cap = int(st[_C.STAT_NAMES.index("round2_pairs")]) + 1024   # rerun, exact size
+
+
+def _prep_points(S: EngineSetup, x) -> torch.Tensor:
+    t = torch.as_tensor(x, dtype=torch.float64)
+    if t.ndim != 2 or t.shape[1] != S.phys_dim:
+        raise ValueError(f"points must be [n, {S.phys_dim}], got {tuple(t.shape)}")
+    return t.to(S.device, non_blocking=True).contiguous()
+
+
+def _field_of(S: EngineSetup, field) -> Field:
+    if isinstance(field, Field):
+        f = field
+    else:
+        f = Field(torch.as_tensor(field, dtype=torch.float64), S.order)
+    b = f.blocks.to(S.device).contiguous()
+    if b.ndim != 3 or b.shape[0] != S.E or b.shape[2] != (f.order + 1) ** S.ref_dim:
+        raise ValueError(f"field blocks {tuple(b.shape)} do not match the mesh "
+                         f"(E={S.E}, Nf**dr with order {f.order})")
+    return Field(b, f.order)
+
+
+def find(S: EngineSetup, x, *, want_iters: bool = False) -> FindRecords:
+    """Computational coordinates of every point."""
+    xt = _prep_points(S, x)
+    loc, stats = _find_local(S, xt, None, want_iters)
+    if S.group.single:
+        return _records_single(S, loc, stats)
+    from .routing import phase_b
+    return phase_b(S, xt, loc, stats, None)
+
+
+def _records_single(S: EngineSetup, loc, stats, values_key=False) -> FindRecords:
+    code, elem = loc["code"], loc["elem"]
+    found = code != NOT_FOUND
+    rank = torch.where(found, torch.zeros_like(elem), torch.full_like(elem, -1))
+    if S.elem_offset:
+        elem = torch.where(found, elem + S.elem_offset, elem)
+    return FindRecords(code, rank, elem, loc["r"], loc["dist"], loc.get("iters"), stats)
+
+
+def interpolate(S: EngineSetup, field, records: FindRecords) -> torch.Tensor:
+    """Field values at found points; NaN for NOT_FOUND."""
+    f = _field_of(S, field)
+    if S.group.single:
+        return _eval_local(S, f, records.code, records.elem - S.elem_offset, records.r)
+    from .routing import interpolate_routed
+    return interpolate_routed(S, f, records)
+
+
+def _eval_local(S: EngineSetup, f: Field, code, elem, r) -> torch.Tensor:
+    n = int(code.shape[0])
+    C = f.components
+    out = torch.empty((n, C), dtype=torch.float64, device=S.device)
+    if n == 0:
+        return out
+    if f.order == S.order:
+        fb, Nf = S.basis_dev, S.order + 1
+    else:
+        fenv = build_basis_envelope(ReferenceBasis(f.order))
+        fb, Nf = device_basis(fenv, S.device), f.order + 1
+    L = _C.lib()
+    wsb = L.fpx_eval_workspace_bytes(S.E, n)
+    ws = torch.empty(wsb, dtype=torch.uint8, device=S.device)
+    code = code.to(torch.int32).contiguous()
+    elem = elem.to(torch.int32).contiguous()
+    r = r.contiguous()
+    _C.check(L.fpx_findpts_eval(S.ref_dim, Nf, _C.ptr(fb), C, S.E, _C.ptr(f.blocks), n,
+                                _C.ptr(code), _C.ptr(elem), _C.ptr(r), _C.ptr(out), _C.ptr(ws),
+                                wsb, _C.stream_handle()), "fpx_findpts_eval")
+    return out
+
+
+def find_and_interpolate(S: EngineSetup, field, x, *, want_iters: bool = False):
+    """find + interpolate with one record set.  For an
+    isoparametric field the evaluation is fused into the find kernels."""
+    f = _field_of(S, field)
+    xt = _prep_points(S, x)
+    fused = f.order == S.order
+    loc, stats = _find_local(S, xt, f if fused else None, want_iters)
+    if S.group.single:
+        rec = _records_single(S, loc, stats)
+        vals = loc["values"] if fused else _eval_local(S, f, loc["code"], loc["elem"], loc["r"])
+        return vals, rec
+    from .routing import phase_b
+    rec = phase_b(S, xt, loc, stats, f if fused else None)
+    if fused:
+        return rec.values, rec
+    return interpolate(S, f, rec), rec

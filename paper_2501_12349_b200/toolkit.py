@@ -1,0 +1,253 @@
+"""Synthetic meshes, fields and query points (`toolkit`).
+
+The reference ships no generators; the definitions here are
+frozen so the oracle, the tests and bench.py all see identical inputs:
+
+* ``kershaw``   -- CEED Kershaw map of [0,1]^3 with a
+  quintic smoothstep, eps_y = eps_z = 0.3: the cfg-2/cfg-3 headline meshes.
+* ``box``       -- "cartesian-deformed" box in 2D/3D: x_c + a*s_c*prod_b
+  sin(2 pi x_b), s = (+1, -1, +1) (cfg-1 with a = 0.02).
+* ``spiral``    -- one thick planar spiral element.
+* ``sphere`` / ``torus`` -- quad surface meshes embedded in 3D (cfg-4).
+
+Every mesh is a `MeshData`: nodes f64[E, d, N**dr], lexicographic node order
+with the first reference axis fastest (bounds.py:58-94).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .basis import gll_nodes
+
+__all__ = ["MeshData", "MeshSpec", "generate_mesh", "kershaw_mesh", "box_mesh",
+           "spiral_mesh", "sphere_mesh", "torus_mesh", "analytic_field", "uniform_points",
+           "surface_points", "partition_blocks"]
+
+
+@dataclass
+class MeshData:
+    nodes: np.ndarray      # (E, d, N**dr)
+    phys_dim: int
+    ref_dim: int
+    order: int
+
+    @property
+    def num_elements(self) -> int:
+        return self.nodes.shape[0]
+
+
+@dataclass
+class MeshSpec:
+    generator: str = "kershaw"
+    dims: int = 3
+    order: int = 4
+    elements: int = 8          # per axis
+    amplitude: float = 0.3     # kershaw eps / box deformation amplitude
+    refinement: int = 0
+
+
+def _ref_grid(p: int, dr: int) -> list[np.ndarray]:
+    """Reference GLL coordinates of the N**dr element nodes, axis 0 fastest."""
+    z = gll_nodes(p)
+    axes = np.meshgrid(*([z] * dr), indexing="ij")
+    return [a.transpose(tuple(range(dr))[::-1]).reshape(-1) for a in axes]
+
+
+def _unit_cells(n: int, p: int, d: int) -> np.ndarray:
+    """Nodes of an n^d Cartesian grid of [0,1]^d: (E, d, N^d), element index
+    lexicographic (x fastest)."""
+    ref = _ref_grid(p, d)
+    idx = np.meshgrid(*([np.arange(n)] * d), indexing="ij")
+    idx = [a.transpose(tuple(range(d))[::-1]).reshape(-1) for a in idx]
+    E = n ** d
+    out = np.empty((E, d, ref[0].size))
+    for c in range(d):
+        out[:, c, :] = (idx[c][:, None] + 0.5 * (ref[c][None, :] + 1.0)) / n
+    return out
+
+
+def _smoothstep(t):
+    t = np.clip(t, 0.0, 1.0)
+    return t * t * t * (t * (6.0 * t - 15.0) + 10.0)
+
+
+def _right(e, x):
+    return np.where(x <= 0.5, (2.0 - e) * x, 1.0 + e * (x - 1.0))
+
+
+def _left(e, x):
+    return 1.0 - _right(e, 1.0 - x)
+
+
+def _kershaw_1d(x, y, e):
+    layer = np.minimum(np.floor(6.0 * x), 5.0)
+    lam = 6.0 * x - layer
+    L, R = _left(e, y), _right(e, y)
+
+    def step(a, b, t):
+        return a + (b - a) * _smoothstep(t)
+
+    out = np.select(
+        [layer == 0, (layer == 1) | (layer == 4), layer == 2, layer == 3],
+        [L, step(L, R, lam), step(R, L, lam / 2.0), step(R, L, (1.0 + lam) / 2.0)],
+        default=R)
+    return out
+
+
+def kershaw_mesh(n: int, p: int, eps: float = 0.3) -> MeshData:
+    """n^3 hexes of order p on [0,1]^3 under the Kershaw map (eps_y=eps_z)."""
+    X = _unit_cells(n, p, 3)
+    x, y, z = X[:, 0], X[:, 1], X[:, 2]
+    out = np.stack([x, _kershaw_1d(x, y, eps), _kershaw_1d(x, z, eps)], axis=1)
+    return MeshData(np.ascontiguousarray(out), 3, 3, p)
+
+
+def box_mesh(d: int, n: int, p: int, amp: float = 0.02) -> MeshData:
+    """Cartesian-deformed n^d box of [0,1]^d (cfg-1: d=2, n=16, p=3)."""
+    X = _unit_cells(n, p, d)
+    bump = np.prod(np.sin(2.0 * np.pi * X), axis=1)
+    sgn = np.array([1.0, -1.0, 1.0])[:d]
+    out = X + amp * sgn[None, :, None] * bump[:, None, :]
+    return MeshData(np.ascontiguousarray(out), d, d, p)
+
+
+def spiral_mesh(p: int = 9, turns: float = 0.75, r0: float = 0.5, r1: float = 1.5,
+                thickness: float = 0.25) -> MeshData:
+    """A single thick 2D spiral element of order p: reference
+    r runs along the spiral arm, s across its thickness."""
+    ref = _ref_grid(p, 2)
+    r, s = ref
+    t = 0.5 * (r + 1.0)
+    theta = 2.0 * np.pi * turns * t
+    rad = r0 + (r1 - r0) * t + 0.5 * thickness * s
+    nodes = np.stack([rad * np.cos(theta), rad * np.sin(theta)])
+    return MeshData(nodes[None].copy(), 2, 2, p)
+
+
+def sphere_mesh(n: int, p: int, radius: float = 1.0) -> MeshData:
+    """Cubed-sphere surface: 6 n^2 quads of order p (gnomonic face grid)."""
+    ref = _ref_grid(p, 2)
+    elems = []
+    for face in range(6):
+        for j in range(n):
+            for i in range(n):
+                a = np.pi / 4.0 * (-1.0 + 2.0 * (i + 0.5 * (ref[0] + 1.0)) / n)
+                b = np.pi / 4.0 * (-1.0 + 2.0 * (j + 0.5 * (ref[1] + 1.0)) / n)
+                u, v = np.tan(a), np.tan(b)
+                one = np.ones_like(u)
+                axis, sgn = face // 2, 1.0 if face % 2 == 0 else -1.0
+                cube = [None, None, None]
+                cube[axis] = sgn * one
+                others = [k for k in range(3) if k != axis]
+                cube[others[0]] = u * sgn
+                cube[others[1]] = v
+                P = np.stack(cube)
+                P = radius * P / np.linalg.norm(P, axis=0, keepdims=True)
+                elems.append(P)
+    return MeshData(np.ascontiguousarray(np.stack(elems)), 3, 2, p)
+
+
+def torus_mesh(n_major: int, n_minor: int, p: int, R: float = 1.0, r: float = 0.3) -> MeshData:
+    """Torus surface (theta, phi) tensor grid of quads of order p."""
+    ref = _ref_grid(p, 2)
+    elems = []
+    for j in range(n_minor):
+        for i in range(n_major):
+            th = 2.0 * np.pi * (i + 0.5 * (ref[0] + 1.0)) / n_major
+            ph = 2.0 * np.pi * (j + 0.5 * (ref[1] + 1.0)) / n_minor
+            rho = R + r * np.cos(ph)
+            elems.append(np.stack([rho * np.cos(th), rho * np.sin(th), r * np.sin(ph)]))
+    return MeshData(np.ascontiguousarray(np.stack(elems)), 3, 2, p)
+
+
+def generate_mesh(spec: MeshSpec) -> MeshData:
+    """SPEC.md:464-467 `generate_mesh`; refinement is applied by increasing the
+    per-axis element count 2**refinement (oct-refinement of a box)."""
+    n = spec.elements * (2 ** spec.refinement)
+    if spec.generator == "kershaw":
+        return kershaw_mesh(n, spec.order, spec.amplitude)
+    if spec.generator in ("box", "cartesian-deformed", "refined-box"):
+        return box_mesh(spec.dims, n, spec.order, spec.amplitude)
+    if spec.generator == "spiral":
+        return spiral_mesh(spec.order)
+    if spec.generator == "sphere":
+        return sphere_mesh(n, spec.order)
+    if spec.generator == "torus":
+        return torus_mesh(2 * n, n, spec.order)
+    raise ValueError(f"unknown generator {spec.generator!r}")
+
+
+def analytic_field(name: str, mesh: MeshData, order: int | None = None, **kw) -> np.ndarray:
+    """Nodal field f64[E, C, Nf**dr] by sampling at the mesh's own nodes
+    (isoparametric: field order = geometry order)."""
+    X = mesh.nodes
+    if order is not None and order != mesh.order:
+        raise ValueError("only isoparametric fields are generated here")
+    d = mesh.phys_dim
+    if name == "constant":
+        return np.full((X.shape[0], 1, X.shape[2]), kw.get("value", 1.0))
+    if name == "coordinates":
+        return X.copy()
+    if name == "polynomial":
+        deg = kw.get("degree", mesh.order)
+        # sum_c (c+1) x_c^deg (+ x0*x1 for deg >= 2): total degree <= deg;
+        # reproduced exactly by interpolation only on affine elements
+        s = sum((c + 1.0) * X[:, c] ** deg for c in range(d))
+        if deg >= 2:
+            s = s + X[:, 0] * X[:, 1]
+        return s[:, None, :]
+    if name == "smooth":
+        x = X[:, 0]
+        y = X[:, 1]
+        z = X[:, 2] if d == 3 else 0.0
+        return (np.sin(np.pi * x) * np.cos(np.pi * y) * np.exp(z))[:, None, :]
+    if name == "wavefront":
+        a = kw.get("alpha", 200.0)
+        xc, yc, r = kw.get("xc", -0.05), kw.get("yc", -0.05), kw.get("r", 0.7)
+        rr = np.sqrt((X[:, 0] - xc) ** 2 + (X[:, 1] - yc) ** 2)
+        return np.arctan(a * (rr - r))[:, None, :]
+    raise ValueError(f"unknown field {name!r}")
+
+
+def uniform_points(n: int, d: int, seed: int = 1, lo=0.0, hi=1.0) -> np.ndarray:
+    """n uniform points in [lo, hi]^d (seeded numpy Generator)."""
+    rng = np.random.default_rng(seed)
+    return rng.uniform(lo, hi, size=(n, d))
+
+
+def surface_points(mesh: MeshData, n: int, seed: int = 1, offset_frac: float = 0.3,
+                   max_offset: float = 1e-5):
+    """cfg-4 query points: random (element, r) mapped to x(r); a fraction
+    gets a normal offset |t| <= max_offset.  Returns
+    (points, element, r, offset)."""
+    from .basis import ReferenceBasis, lagrange_eval
+    rng = np.random.default_rng(seed)
+    rb = ReferenceBasis(mesh.order)
+    E = mesh.num_elements
+    e = rng.integers(0, E, size=n)
+    r = rng.uniform(-1, 1, size=(n, 2))
+    vr, dr_, _ = lagrange_eval(rb, r[:, 0])
+    vs, ds, _ = lagrange_eval(rb, r[:, 1])
+    N = mesh.order + 1
+    Xe = mesh.nodes[e].reshape(n, 3, N, N)          # (n, d, s, r)
+    x = np.einsum("ncji,ni,nj->nc", Xe, vr, vs)
+    tr = np.einsum("ncji,ni,nj->nc", Xe, dr_, vs)
+    ts = np.einsum("ncji,ni,nj->nc", Xe, vr, ds)
+    nrm = np.cross(tr, ts)
+    nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+    off = np.where(rng.uniform(size=n) < offset_frac,
+                   rng.uniform(-max_offset, max_offset, size=n), 0.0)
+    return x + off[:, None] * nrm, e, r, off
+
+
+def partition_blocks(E: int, nranks: int) -> list[tuple[int, int]]:
+    """Contiguous block partition of element ids over ranks."""
+    base, extra = divmod(E, nranks)
+    out, start = [], 0
+    for k in range(nranks):
+        cnt = base + (1 if k < extra else 0)
+        out.append((start, start + cnt))
+        start += cnt
+    return out
