@@ -96,10 +96,23 @@ typedef struct fpx_mesh_t {
 #define FPX_STAT_ROUND2_PAIRS 5  /* (point, element) pairs in round 2 */
 #define FPX_STAT_OVERFLOW 6      /* pairs dropped for lack of workspace (>0: rerun) */
 #define FPX_STAT_EVALS 7         /* fused field evaluations */
-#define FPX_STATS_LEN 8
+#define FPX_STAT_NEWTON_R1 8     /* Newton solves in the round-1 (best-first) kernel */
+#define FPX_STAT_ITERS_R1 9      /* their iterations */
+#define FPX_STAT_EVALS_R1 10     /* field evaluations fused into the round-1 kernel */
+#define FPX_STATS_LEN 11
 
 int fpx_abi_version(void);
 const char* fpx_last_error(void);
+/* Number of kernels this library has launched in the process (its own
+ * kernels, not CUB's or memsets): the bench's gpu_launches evidence. */
+int64_t fpx_launch_count(void);
+/* Record (start, stop) CUDA events (cudaEvent_t as void*) around the round-1
+ * Newton kernel of the next fpx_find calls on the same stream; NULL clears.
+ * Used by bench.py to time the dominant kernel live. */
+int fpx_profile_round1(void* ev_start, void* ev_stop);
+/* FP64 FMA throughput probe (TFLOP/s): a DFMA-chain kernel over all SMs,
+ * timed with CUDA events on `stream` (synchronising).  Roofline denominator. */
+int fpx_probe_fp64(double* tflops_host, void* stream);
 /* 1 if order N (nodes/axis) is compiled in for (d, dr) */
 int fpx_supported(int d, int dr, int N);
 

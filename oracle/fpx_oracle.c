@@ -12,6 +12,9 @@
 #include "fpx_oracle.h"
 
 #include <math.h>
+#ifdef FPXO_TRACE
+#include <stdio.h>
+#endif
 #include <stdlib.h>
 #include <string.h>
 #ifdef _OPENMP
@@ -864,45 +867,58 @@ static int chol_solve(int n, const int* idx, const double A[3][3], const double*
   return 0;
 }
 
-/* Box-and-trust-constrained Newton step (decision D8):
- * solve Hm s = -J on all axes, clamp to [max(-a,-1-r), min(a,1-r)], then one
- * reduced re-solve on the unclamped axes with the clamped values moved to
- * the right-hand side, clamped again. */
-static void constrained_step(int dr, const double Hm[3][3], const double* J, const double* r,
-                             double alpha, double* s) {
-  double lo[3], hi[3];
-  int all[3] = {0, 1, 2};
-  for (int a = 0; a < dr; ++a) {
-    double bl = -1.0 - r[a], bh = 1.0 - r[a];
-    lo[a] = -alpha > bl ? -alpha : bl;
-    hi[a] = alpha < bh ? alpha : bh;
-  }
-  double rhs[3];
-  for (int a = 0; a < dr; ++a) rhs[a] = -J[a];
-  if (chol_solve(dr, all, Hm, rhs, s)) { for (int a = 0; a < dr; ++a) s[a] = 0.0; return; }
-  int fixed[3] = {0, 0, 0}, nfix = 0;
-  for (int a = 0; a < dr; ++a) {
-    if (s[a] < lo[a]) { s[a] = lo[a]; fixed[a] = 1; ++nfix; }
-    else if (s[a] > hi[a]) { s[a] = hi[a]; fixed[a] = 1; ++nfix; }
-  }
-  if (nfix == 0 || nfix == dr) return;
+/* Projected trust-region Newton step on the free axes (
+ * decision D8 as frozen in DESIGN.md §3.4).  free[] excludes the active
+ * bounds; Hm is the model Hessian.
+ *   1. s_F = -Hm_FF^{-1} J_F, s_A = 0;
+ *   2. trust region: scale s uniformly so |s|_inf <= alpha (direction kept,
+ *      so the predicted decrease stays > 0);
+ *   3. reference box: free axes with r + s outside [-1, 1] are fixed on the
+ *      face (s_a = +-1 - r_a); one reduced re-solve on the remaining free
+ *      axes with the fixed values moved to the right-hand side, scaled into
+ *      the trust region again and clamped to the box.
+ * Returns -1 if the free block is not positive definite. */
+static int constrained_step(int dr, const double Hm[3][3], const double* J, const double* r,
+                            const int* freem, double alpha, double* s) {
   int fidx[3], nf = 0;
-  for (int a = 0; a < dr; ++a) if (!fixed[a]) fidx[nf++] = a;
-  double b2[3], x2[3];
+  for (int a = 0; a < dr; ++a) { s[a] = 0.0; if (freem[a]) fidx[nf++] = a; }
+  if (nf == 0) return 0;
+  double rhs[3], x[3];
+  for (int k = 0; k < nf; ++k) rhs[k] = -J[fidx[k]];
+  if (chol_solve(nf, fidx, Hm, rhs, x)) return -1;
+  double m = 0.0;
+  for (int k = 0; k < nf; ++k) if (fabs(x[k]) > m) m = fabs(x[k]);
+  if (m > alpha) { double t = alpha / m; for (int k = 0; k < nf; ++k) x[k] *= t; }
+  int fixed[3] = {0, 0, 0}, nfix = 0;
   for (int k = 0; k < nf; ++k) {
-    int f = fidx[k];
+    int a = fidx[k];
+    double bl = -1.0 - r[a], bh = 1.0 - r[a];
+    s[a] = x[k];
+    if (x[k] < bl) { s[a] = bl; fixed[a] = 1; ++nfix; }
+    else if (x[k] > bh) { s[a] = bh; fixed[a] = 1; ++nfix; }
+  }
+  if (nfix == 0 || nfix == nf) return 0;
+  int gidx[3], ng = 0;
+  for (int k = 0; k < nf; ++k) if (!fixed[fidx[k]]) gidx[ng++] = fidx[k];
+  double b2[3] = {0, 0, 0}, x2[3];
+  for (int k = 0; k < ng; ++k) {
+    int f = gidx[k];
     double t = -J[f];
     for (int c = 0; c < dr; ++c) if (fixed[c]) t -= Hm[f][c] * s[c];
     b2[k] = t;
   }
-  if (chol_solve(nf, fidx, Hm, b2, x2)) return; /* keep first-pass clamp */
-  for (int k = 0; k < nf; ++k) {
-    int f = fidx[k];
-    double v = x2[k];
-    if (v < lo[f]) v = lo[f];
-    else if (v > hi[f]) v = hi[f];
+  if (chol_solve(ng, gidx, Hm, b2, x2)) return 0; /* keep the first-pass step */
+  m = 0.0;
+  for (int k = 0; k < ng; ++k) if (fabs(x2[k]) > m) m = fabs(x2[k]);
+  if (m > alpha) { double t = alpha / m; for (int k = 0; k < ng; ++k) x2[k] *= t; }
+  for (int k = 0; k < ng; ++k) {
+    int f = gidx[k];
+    double v = x2[k], bl = -1.0 - r[f], bh = 1.0 - r[f];
+    if (v < bl) v = bl;
+    else if (v > bh) v = bh;
     s[f] = v;
   }
+  return 0;
 }
 
 static int on_boundary(int dr, const double* r) {
@@ -948,13 +964,16 @@ void fpxo_invert(const fpxo_basis* B, int d, int dr, const double* X, const doub
         Hb[a][b] = g - q;
       }
     }
-    int all[3] = {0, 1, 2};
-    double tmp[3], zero[3] = {0, 0, 0};
-    int used_beta = 0;
+    /* active bounds: on a face with the descent direction -J pointing out */
+    int freem[3] = {1, 1, 1};
+    for (int a = 0; a < dr; ++a)
+      if ((r[a] == 1.0 && J[a] < 0.0) || (r[a] == -1.0 && J[a] > 0.0)) freem[a] = 0;
+    double s[3] = {0, 0, 0};
     const double(*Hm)[3] = H0;
     double Hr[3][3];
-    if (beta && chol_solve(dr, all, Hb, zero, tmp) == 0) { Hm = Hb; used_beta = 1; }
-    else if (chol_solve(dr, all, H0, zero, tmp) != 0) {
+    if (beta && constrained_step(dr, Hb, J, r, freem, alpha, s) == 0) {
+      Hm = Hb;
+    } else if (constrained_step(dr, H0, J, r, freem, alpha, s) != 0) {
       double tr = 0.0;
       for (int a = 0; a < dr; ++a) tr += H0[a][a];
       double lam = 1e-10 * tr / dr;
@@ -962,11 +981,22 @@ void fpxo_invert(const fpxo_basis* B, int d, int dr, const double* X, const doub
       for (int a = 0; a < dr; ++a)
         for (int b = 0; b < dr; ++b) Hr[a][b] = H0[a][b] + (a == b ? lam : 0.0);
       Hm = Hr;
+      if (constrained_step(dr, Hr, J, r, freem, alpha, s) != 0)
+        for (int a = 0; a < dr; ++a) s[a] = 0.0;
     }
-    double s[3] = {0, 0, 0};
-    constrained_step(dr, Hm, J, r, alpha, s);
     ++it;
-    double rn[3] = {0, 0, 0}, smax = 0.0;
+    double js = 0.0, shs = 0.0, smax = 0.0;
+    for (int a = 0; a < dr; ++a) {
+      js += J[a] * s[a];
+      double t = 0.0;
+      for (int b = 0; b < dr; ++b) t += Hm[a][b] * s[b];
+      shs += s[a] * t;
+      if (fabs(s[a]) > smax) smax = fabs(s[a]);
+    }
+    double pred = -(2.0 * js + shs);
+    /* the step cannot change |dx|^2 in floating point: converged */
+    if (!(pred > 1e-15 * f)) { converged = 1; break; }
+    double rn[3] = {0, 0, 0};
     for (int a = 0; a < dr; ++a) {
       double v = r[a] + s[a];
       if (s[a] == -1.0 - r[a]) v = -1.0;
@@ -974,32 +1004,15 @@ void fpxo_invert(const fpxo_basis* B, int d, int dr, const double* X, const doub
       if (v < -1.0) v = -1.0;
       if (v > 1.0) v = 1.0;
       rn[a] = v;
-      if (fabs(s[a]) > smax) smax = fabs(s[a]);
     }
     fmap(B, d, dr, X, rn, on_boundary(dr, rn), &nxt);
     double dxn[3], fn = 0.0;
     for (int c = 0; c < d; ++c) { dxn[c] = xs[c] - nxt.x[c]; fn += dxn[c] * dxn[c]; }
-    double decr = f - fn, pred;
-    if (used_beta) {
-      double js = 0.0, shs = 0.0;
-      for (int a = 0; a < dr; ++a) {
-        js += J[a] * s[a];
-        double t = 0.0;
-        for (int b = 0; b < dr; ++b) t += Hm[a][b] * s[b];
-        shs += s[a] * t;
-      }
-      pred = -(2.0 * js + shs);
-    } else {
-      double m = 0.0;
-      for (int c = 0; c < d; ++c) {
-        double t = 0.0;
-        for (int a = 0; a < dr; ++a) t += cur.G[c][a] * s[a];
-        double e = dx[c] - t;
-        m += e * e;
-      }
-      pred = f - m;
-    }
-    if (pred > 0.0 && decr >= S->accept * pred) {
+    double decr = f - fn;
+#ifdef FPXO_TRACE
+    fprintf(stderr, "it %2d beta %d free %d%d%d r=(%.6f %.6f %.6f) s=(%.3e %.3e %.3e) f=%.6e fn=%.6e pred=%.3e decr=%.3e alpha=%.3e\n", it, beta, freem[0], freem[1], freem[2], r[0], r[1], r[2], s[0], s[1], s[2], f, fn, pred, decr, alpha);
+#endif
+    if (decr >= S->accept * pred) {
       if (decr >= S->keep * pred) alpha *= S->grow;
       for (int a = 0; a < dr; ++a) r[a] = rn[a];
       cur = nxt;

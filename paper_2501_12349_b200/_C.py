@@ -18,7 +18,7 @@ ABI_VERSION = 1
 
 INTERIOR, BORDER, NOT_FOUND = 0, 1, 2
 STAT_NAMES = ["points", "box_tests", "newton", "iters", "round2_points", "round2_pairs",
-              "overflow", "evals"]
+              "overflow", "evals", "newton_r1", "iters_r1", "evals_r1"]
 STATS_LEN = len(STAT_NAMES)
 
 P = C.c_void_p
@@ -63,6 +63,9 @@ def lib():
         "fpx_abi_version": ([], i32),
         "fpx_last_error": ([], C.c_char_p),
         "fpx_supported": ([i32, i32, i32], i32),
+        "fpx_launch_count": ([], i64),
+        "fpx_profile_round1": ([P, P], i32),
+        "fpx_probe_fp64": ([P, P], i32),
         "fpx_setup_bounds": ([i32, i32, i32, i32, i64, P, P, f64, P, P, P, P, P, P, P, P], i32),
         "fpx_bound_function": ([i32, i32, i32, i64, P, P, P, P, P], i32),
         "fpx_hash_workspace_bytes": ([i32, i64, i32], sz),
@@ -89,7 +92,8 @@ def lib():
 
 def exported_symbols():
     """Names declared in include/fpx.h (checked by the CPU test suite)."""
-    return ["fpx_abi_version", "fpx_last_error", "fpx_supported", "fpx_setup_bounds",
+    return ["fpx_abi_version", "fpx_last_error", "fpx_launch_count", "fpx_profile_round1",
+            "fpx_probe_fp64", "fpx_supported", "fpx_setup_bounds",
             "fpx_bound_function", "fpx_hash_workspace_bytes", "fpx_hash_build", "fpx_cell_of",
             "fpx_find_workspace_bytes", "fpx_find", "fpx_eval_workspace_bytes",
             "fpx_findpts_eval", "fpx_invert_pairs", "fpx_forward_map", "fpx_route_count",

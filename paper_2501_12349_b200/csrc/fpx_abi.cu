@@ -6,6 +6,7 @@
 #include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -28,6 +29,8 @@ using fpx::Item;
 namespace {
 
 thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+cudaEvent_t g_prof_start = nullptr, g_prof_stop = nullptr;
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -38,6 +41,12 @@ int fail(int code, const char* fmt, ...) {
   g_err = buf;
   return code;
 }
+
+#define FPX_LAUNCH(expr)   \
+  do {                     \
+    g_launches += 1;       \
+    FPX_CK(expr);          \
+  } while (0)
 
 #define FPX_CK(expr)                                                                   \
   do {                                                                                 \
@@ -193,6 +202,21 @@ __global__ void k_route_place(int64_t n, const int32_t* __restrict__ dest, int r
   }
 }
 
+// 8 independent DFMA chains per thread (fpx_probe_fp64).
+__global__ void __launch_bounds__(256) k_dfma_probe(double* out, int iters, double a, double b) {
+  double x[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) x[c] = threadIdx.x * 1e-9 + c;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) x[c] = fma(x[c], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s += x[c];
+  if (s == 12345.678) *out = s;
+}
+
 unsigned grid1(int64_t n, int threads = 256) {
   int64_t b = (n + threads - 1) / threads;
   if (b > 148 * 32) b = 148 * 32;
@@ -222,6 +246,42 @@ const char* fpx_last_error(void) { return g_err.c_str(); }
 
 int fpx_supported(int d, int dr, int N) { return fpx::newton_supported(d, dr, N) ? 1 : 0; }
 
+int64_t fpx_launch_count(void) { return g_launches.load(); }
+
+int fpx_profile_round1(void* ev_start, void* ev_stop) {
+  g_prof_start = reinterpret_cast<cudaEvent_t>(ev_start);
+  g_prof_stop = reinterpret_cast<cudaEvent_t>(ev_stop);
+  return FPX_OK;
+}
+
+int fpx_probe_fp64(double* tflops_host, void* stream) {
+  cudaStream_t st = S(stream);
+  int dev = 0, sms = 148;
+  FPX_CK(cudaGetDevice(&dev));
+  FPX_CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  double* out = nullptr;
+  FPX_CK(cudaMallocAsync(&out, sizeof(double), st));
+  cudaEvent_t e0, e1;
+  FPX_CK(cudaEventCreate(&e0));
+  FPX_CK(cudaEventCreate(&e1));
+  const int iters = 20000, blocks = sms * 8, threads = 256;
+  float best = 1e30f;
+  for (int rep = 0; rep < 4; ++rep) {
+    FPX_CK(cudaEventRecord(e0, st));
+    k_dfma_probe<<<blocks, threads, 0, st>>>(out, iters, 0.999999, 1e-7);
+    FPX_CK(cudaEventRecord(e1, st));
+    FPX_CK(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    FPX_CK(cudaEventElapsedTime(&ms, e0, e1));
+    if (rep > 0 && ms < best) best = ms;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  FPX_CK(cudaFreeAsync(out, st));
+  *tflops_host = 2.0 * 8 * (double)iters * blocks * threads / (best * 1e-3) / 1e12;
+  return FPX_OK;
+}
+
 int fpx_setup_bounds(int d, int dr, int N, int M, int64_t E, const double* basis,
                      const double* nodes, double expansion, double* aabb, double* obb_c,
                      double* obb_inv, double* hbox, double* frame, uint8_t* obb_ok,
@@ -231,7 +291,7 @@ int fpx_setup_bounds(int d, int dr, int N, int M, int64_t E, const double* basis
   if (M < N || M > 4 * FPX_SETUP_MAXN) return fail(FPX_EINVAL, "bad interval count M=%d", M);
   if (E < 0) return fail(FPX_EINVAL, "negative element count");
   if (E == 0) return FPX_OK;
-  FPX_CK(fpx::launch_setup_bounds(d, dr, N, M, E, basis, nodes, expansion, aabb, obb_c, obb_inv,
+  FPX_LAUNCH(fpx::launch_setup_bounds(d, dr, N, M, E, basis, nodes, expansion, aabb, obb_c, obb_inv,
                                   hbox, frame, obb_ok, status, S(stream)));
   return FPX_OK;
 }
@@ -242,7 +302,7 @@ int fpx_bound_function(int dr, int N, int M, int64_t nf, const double* basis,
   if (N < 2 || N > FPX_SETUP_MAXN || M < N || M > 4 * FPX_SETUP_MAXN)
     return fail(FPX_EINVAL, "bound_function: bad N=%d M=%d", N, M);
   if (nf <= 0) return FPX_OK;
-  FPX_CK(fpx::launch_bound_function(dr, N, M, nf, basis, values, lower, upper, S(stream)));
+  FPX_LAUNCH(fpx::launch_bound_function(dr, N, M, nf, basis, values, lower, upper, S(stream)));
   return FPX_OK;
 }
 
@@ -275,9 +335,9 @@ int fpx_hash_build(int d, int64_t E, const double* box, int ncell, double* grid,
   void* temp = cv.take<char>(tb);
   if (!cv.ok()) return fail(FPX_EINVAL, "hash workspace too small (%zu < %zu)", ws_bytes, cv.off);
   cudaStream_t st = S(stream);
-  FPX_CK(fpx::launch_hash_grid(d, E, box, ncell, grid, st));
+  FPX_LAUNCH(fpx::launch_hash_grid(d, E, box, ncell, grid, st));
   FPX_CK(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (nc + 1), st));
-  FPX_CK(fpx::launch_hash_count(d, E, box, grid, ncell, cnt, st));
+  FPX_LAUNCH(fpx::launch_hash_count(d, E, box, grid, ncell, cnt, st));
   FPX_CK(cub::DeviceScan::ExclusiveSum(temp, tb, cnt, offsets, (int)(nc + 1), st));
   int32_t total = 0;
   FPX_CK(cudaMemcpyAsync(&total, offsets + nc, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
@@ -287,8 +347,8 @@ int fpx_hash_build(int d, int64_t E, const double* box, int ncell, double* grid,
   if (!elems || cap < total) return FPX_OK;
   FPX_CK(cudaMemsetAsync(cursor, 0, sizeof(int32_t) * (nc + 1), st));
   FPX_CK(cudaMemsetAsync(maxl, 0, sizeof(int32_t), st));
-  FPX_CK(fpx::launch_hash_fill(d, E, box, grid, ncell, offsets, cursor, elems, st));
-  FPX_CK(fpx::launch_hash_sort(nc, offsets, elems, maxl, st));
+  FPX_LAUNCH(fpx::launch_hash_fill(d, E, box, grid, ncell, offsets, cursor, elems, st));
+  FPX_LAUNCH(fpx::launch_hash_sort(nc, offsets, elems, maxl, st));
   int32_t ml = 0;
   FPX_CK(cudaMemcpyAsync(&ml, maxl, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   FPX_CK(cudaStreamSynchronize(st));
@@ -299,7 +359,7 @@ int fpx_hash_build(int d, int64_t E, const double* box, int ncell, double* grid,
 int fpx_cell_of(const fpx_mesh_t* m, int64_t n, const double* x, int64_t* cell, void* stream) {
   if (!m) return fail(FPX_EINVAL, "mesh is NULL");
   if (n <= 0) return FPX_OK;
-  FPX_CK(fpx::launch_cell_of(m->d, m->grid, m->ncell, n, x, cell, S(stream)));
+  FPX_LAUNCH(fpx::launch_cell_of(m->d, m->grid, m->ncell, n, x, cell, S(stream)));
   return FPX_OK;
 }
 
@@ -331,27 +391,32 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
   const fpx_mesh_t& M = *m;
   // --- prefilter: hash lookup + AABB/OBB filter + best-first candidate
   FPX_CK(cudaMemsetAsync(w.g1.count, 0, sizeof(int32_t) * E, st));
-  FPX_CK(fpx::launch_find_prefilter(M, n, x, w.best, w.npass, code, elem, r, dist, iters,
+  FPX_LAUNCH(fpx::launch_find_prefilter(M, n, x, w.best, w.npass, code, elem, r, dist, iters,
                                     field ? values : nullptr, C, w.g1.count, stats, st));
   // --- round 1: group by best-first element, Newton, fused eval
+  g_launches += 3;
   FPX_CK(w.g1.build(E, n, nullptr, w.best, nullptr, st));
   FPX_CK(cudaMemsetAsync(w.upair_cnt, 0, sizeof(int64_t) * (n + 1), st));
   FPX_CK(cudaMemsetAsync(w.nun, 0, sizeof(int64_t), st));
-  FPX_CK(fpx::launch_newton_round1(M, n, x, w.g1.sorted, w.g1.items, w.g1.nitems, w.g1.items_cap,
+  if (g_prof_start) FPX_CK(cudaEventRecord(g_prof_start, st));
+  FPX_LAUNCH(fpx::launch_newton_round1(M, n, x, w.g1.sorted, w.g1.items, w.g1.nitems, w.g1.items_cap,
                                    w.npass, code, elem, r, dist, iters, field, C, values, w.upts,
                                    w.upair_cnt, w.nun, stats, st));
+  if (g_prof_stop) FPX_CK(cudaEventRecord(g_prof_stop, st));
   // --- round 2: every other passing candidate of the unresolved points
   size_t tb = w.scan2_bytes;
   FPX_CK(cub::DeviceScan::ExclusiveSum(w.scan2_temp, tb, w.upair_cnt, w.pair_off, (int)(n + 1), st));
   FPX_CK(cudaMemsetAsync(w.g2.count, 0, sizeof(int32_t) * E, st));
-  FPX_CK(fpx::launch_round2_emit(M, n, w.nun, w.upts, x, w.best, w.pair_off, pair_cap, w.pair_pt,
+  FPX_LAUNCH(fpx::launch_round2_emit(M, n, w.nun, w.upts, x, w.best, w.pair_off, pair_cap, w.pair_pt,
                                  w.pair_elem, w.g2.count, stats, st));
+  g_launches += 1;
   k_pairs_total<<<1, 1, 0, st>>>(w.pair_off, w.nun, pair_cap, w.npairs, stats, n);
   FPX_CK(cudaGetLastError());
+  g_launches += 3;
   FPX_CK(w.g2.build(E, pair_cap, w.npairs, w.pair_elem, nullptr, st));
-  FPX_CK(fpx::launch_newton_pairs(M, x, w.pair_pt, w.g2.sorted, w.g2.items, w.g2.nitems,
+  FPX_LAUNCH(fpx::launch_newton_pairs(M, x, w.pair_pt, w.g2.sorted, w.g2.items, w.g2.nitems,
                                   w.g2.items_cap, w.pcode, w.pr, w.pdist, w.piters, stats, st));
-  FPX_CK(fpx::launch_round2_finalize(M, n, w.nun, w.upts, w.pair_off, pair_cap, w.pair_elem,
+  FPX_LAUNCH(fpx::launch_round2_finalize(M, n, w.nun, w.upts, w.pair_off, pair_cap, w.pair_elem,
                                      w.pcode, w.pr, w.pdist, w.piters, code, elem, r, dist, iters,
                                      field, C, values, stats, st));
   return FPX_OK;
@@ -381,9 +446,10 @@ int fpx_findpts_eval(int dr, int Nf, const double* fbasis, int C, int64_t E,
   g.carve(cv, E, n);
   if (!cv.ok()) return fail(FPX_EINVAL, "eval workspace too small (%zu < %zu)", ws_bytes, cv.off);
   FPX_CK(cudaMemsetAsync(g.count, 0, sizeof(int32_t) * E, st));
-  FPX_CK(fpx::launch_eval_mark(n, C, code, elem, values, unit_elem, g.count, st));
+  FPX_LAUNCH(fpx::launch_eval_mark(n, C, code, elem, values, unit_elem, g.count, st));
+  g_launches += 3;
   FPX_CK(g.build(E, n, nullptr, unit_elem, nullptr, st));
-  FPX_CK(fpx::launch_eval_items(dr, Nf, fbasis, C, field, r, g.sorted, g.items, g.nitems,
+  FPX_LAUNCH(fpx::launch_eval_items(dr, Nf, fbasis, C, field, r, g.sorted, g.items, g.nitems,
                                 g.items_cap, values, st));
   return FPX_OK;
 }
@@ -402,10 +468,12 @@ int fpx_invert_pairs(const fpx_mesh_t* m, int64_t npairs, const double* x, const
   Carver cv(ws, probe.off + 256);
   g.carve(cv, m->E, npairs);
   FPX_CK(cudaMemsetAsync(g.count, 0, sizeof(int32_t) * m->E, st));
+  g_launches += 1;
   k_count_elems<<<grid1(npairs), 256, 0, st>>>(npairs, elem, g.count);
   FPX_CK(cudaGetLastError());
+  g_launches += 3;
   FPX_CK(g.build(m->E, npairs, nullptr, elem, nullptr, st));
-  FPX_CK(fpx::launch_invert_pairs_grouped(*m, x, g.sorted, g.items, g.nitems, g.items_cap, r, dist,
+  FPX_LAUNCH(fpx::launch_invert_pairs_grouped(*m, x, g.sorted, g.items, g.nitems, g.items_cap, r, dist,
                                           iters, converged, st));
   FPX_CK(cudaFreeAsync(ws, st));
   return FPX_OK;
@@ -416,7 +484,7 @@ int fpx_forward_map(const fpx_mesh_t* m, int64_t n, const int32_t* elem, const d
   int rc = check_mesh(m);
   if (rc) return rc;
   if (n <= 0) return FPX_OK;
-  FPX_CK(fpx::launch_forward_map(*m, n, elem, r, x, G, H2, S(stream)));
+  FPX_LAUNCH(fpx::launch_forward_map(*m, n, elem, r, x, G, H2, S(stream)));
   return FPX_OK;
 }
 
@@ -425,6 +493,7 @@ int fpx_route_count(int64_t n, const int32_t* dest, int nranks, int64_t* counts,
   cudaStream_t st = S(stream);
   FPX_CK(cudaMemsetAsync(counts, 0, sizeof(int64_t) * nranks, st));
   if (n <= 0) return FPX_OK;
+  g_launches += 1;
   k_route_count<<<grid1(n), 256, 0, st>>>(n, dest, nranks, counts);
   FPX_CK(cudaGetLastError());
   return FPX_OK;
@@ -443,6 +512,7 @@ int fpx_route_pack(int64_t n, const int32_t* dest, int nranks, const int64_t* of
   if (!ws) return fail(FPX_EINVAL, "route: workspace required (%zu bytes)", cv.off + 256);
   if (!cv.ok()) return fail(FPX_EINVAL, "route workspace too small (%zu < %zu)", ws_bytes, cv.off);
   for (int rk = 0; rk < nranks; ++rk) {
+    g_launches += 2;
     k_route_flags<<<grid1(n), 256, 0, st>>>(n, dest, rk, flags);
     FPX_CK(cudaGetLastError());
     size_t t2 = tb;

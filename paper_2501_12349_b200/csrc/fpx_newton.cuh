@@ -263,57 +263,77 @@ __device__ __forceinline__ bool chol_solve(const double* A, const bool* act, con
   return true;
 }
 
-// Box-and-trust constrained step (oracle constrained_step, decision D8).
+// Projected trust-region Newton step on the free axes (oracle
+// constrained_step, decision D8): Newton on the free block, uniform scaling
+// into the trust box, faces hit by the step fixed and one reduced re-solve.
+// Returns false if the free block is not positive definite.
 template <int DR>
-__device__ __forceinline__ void constrained_step(const double* Hm, const double* J,
-                                                 const double* r, double alpha, double* s) {
-  double lo[3], hi[3], rhs[3];
-  bool all[3] = {true, true, true};
+__device__ __forceinline__ bool constrained_step(const double* Hm, const double* J,
+                                                 const double* r, const bool* freem,
+                                                 double alpha, double* s) {
+  int nf = 0;
+  double rhs[3], x[3] = {0.0, 0.0, 0.0};
 #pragma unroll
   for (int a = 0; a < DR; ++a) {
-    const double bl = -1.0 - r[a], bh = 1.0 - r[a];
-    lo[a] = -alpha > bl ? -alpha : bl;
-    hi[a] = alpha < bh ? alpha : bh;
+    s[a] = 0.0;
+    nf += freem[a] ? 1 : 0;
     rhs[a] = -J[a];
   }
-  if (!chol_solve<DR>(Hm, all, rhs, s)) {
+  if (nf == 0) return true;
+  if (!chol_solve<DR>(Hm, freem, rhs, x)) return false;
+  double m = 0.0;
 #pragma unroll
-    for (int a = 0; a < DR; ++a) s[a] = 0.0;
-    return;
+  for (int a = 0; a < DR; ++a)
+    if (freem[a]) m = fabs(x[a]) > m ? fabs(x[a]) : m;
+  if (m > alpha) {
+    const double t = alpha / m;
+#pragma unroll
+    for (int a = 0; a < DR; ++a)
+      if (freem[a]) x[a] *= t;
   }
-  bool freea[3] = {true, true, true};
+  bool g[3] = {false, false, false};
   int nfix = 0;
 #pragma unroll
   for (int a = 0; a < DR; ++a) {
-    if (s[a] < lo[a]) {
-      s[a] = lo[a];
-      freea[a] = false;
+    if (!freem[a]) continue;
+    const double bl = -1.0 - r[a], bh = 1.0 - r[a];
+    s[a] = x[a];
+    if (x[a] < bl) {
+      s[a] = bl;
       ++nfix;
-    } else if (s[a] > hi[a]) {
-      s[a] = hi[a];
-      freea[a] = false;
+    } else if (x[a] > bh) {
+      s[a] = bh;
       ++nfix;
+    } else {
+      g[a] = true;
     }
   }
-  if (nfix == 0 || nfix == DR) return;
-  double b2[3], x2[3];
+  if (nfix == 0 || nfix == nf) return true;
+  double b2[3] = {0.0, 0.0, 0.0}, x2[3] = {0.0, 0.0, 0.0};
 #pragma unroll
   for (int f = 0; f < DR; ++f) {
-    if (!freea[f]) continue;
+    if (!g[f]) continue;
     double t = -J[f];
 #pragma unroll
     for (int c = 0; c < DR; ++c)
-      if (!freea[c]) t -= Hm[symi(f, c)] * s[c];
+      if (freem[c] && !g[c]) t -= Hm[symi(f, c)] * s[c];
     b2[f] = t;
   }
-  if (!chol_solve<DR>(Hm, freea, b2, x2)) return;
+  if (!chol_solve<DR>(Hm, g, b2, x2)) return true;  // keep the first pass
+  m = 0.0;
 #pragma unroll
-  for (int f = 0; f < DR; ++f) {
-    if (!freea[f]) continue;
-    double v = x2[f];
-    v = v < lo[f] ? lo[f] : (v > hi[f] ? hi[f] : v);
-    s[f] = v;
+  for (int a = 0; a < DR; ++a)
+    if (g[a]) m = fabs(x2[a]) > m ? fabs(x2[a]) : m;
+  const double t = m > alpha ? alpha / m : 1.0;
+#pragma unroll
+  for (int a = 0; a < DR; ++a) {
+    if (!g[a]) continue;
+    double v = m > alpha ? x2[a] * t : x2[a];
+    const double bl = -1.0 - r[a], bh = 1.0 - r[a];
+    v = v < bl ? bl : (v > bh ? bh : v);
+    s[a] = v;
   }
+  return true;
 }
 
 template <int DR>
@@ -396,20 +416,24 @@ __device__ __forceinline__ NewtonOut newton_warp(const double* __restrict__ sX,
     double rn[3] = {r[0], r[1], r[2]};
     double smax = 0.0, pred = 0.0;
     const double fcur = st.f;
+    bool step = false;
     if (!done) {
       const bool beta = it > 0 && on_boundary<DR>(r);
-      bool all[3] = {true, true, true};
-      double zero[3] = {0.0, 0.0, 0.0}, tmp[3], Hm[6];
-      bool used = false;
+      bool freem[3] = {true, true, true};
+#pragma unroll
+      for (int a = 0; a < DR; ++a)
+        if ((r[a] == 1.0 && st.J[a] < 0.0) || (r[a] == -1.0 && st.J[a] > 0.0)) freem[a] = false;
+      double Hm[6], s[3] = {0.0, 0.0, 0.0};
+      bool ok = false;
       if (beta) {
 #pragma unroll
         for (int m = 0; m < 6; ++m) Hm[m] = st.H0[m] - st.Q[m];
-        used = chol_solve<DR>(Hm, all, zero, tmp);
+        ok = constrained_step<DR>(Hm, st.J, r, freem, alpha, s);
       }
-      if (!used) {
+      if (!ok) {
 #pragma unroll
         for (int m = 0; m < 6; ++m) Hm[m] = st.H0[m];
-        if (!chol_solve<DR>(Hm, all, zero, tmp)) {
+        if (!constrained_step<DR>(Hm, st.J, r, freem, alpha, s)) {
           double tr = 0.0;
 #pragma unroll
           for (int a = 0; a < DR; ++a) tr += st.H0[a];
@@ -417,10 +441,11 @@ __device__ __forceinline__ NewtonOut newton_warp(const double* __restrict__ sX,
           if (!(lam > 0.0)) lam = 1e-300;
 #pragma unroll
           for (int a = 0; a < DR; ++a) Hm[a] = st.H0[a] + lam;
+          if (!constrained_step<DR>(Hm, st.J, r, freem, alpha, s))
+#pragma unroll
+            for (int a = 0; a < DR; ++a) s[a] = 0.0;
         }
       }
-      double s[3] = {0.0, 0.0, 0.0};
-      constrained_step<DR>(Hm, st.J, r, alpha, s);
       ++it;
       double js = 0.0, shs = 0.0;
 #pragma unroll
@@ -430,26 +455,35 @@ __device__ __forceinline__ NewtonOut newton_warp(const double* __restrict__ sX,
 #pragma unroll
         for (int b = 0; b < DR; ++b) t += Hm[symi(a, b)] * s[b];
         shs += s[a] * t;
-      }
-      pred = -(2.0 * js + shs);
-#pragma unroll
-      for (int a = 0; a < DR; ++a) {
-        double v = r[a] + s[a];
-        if (s[a] == -1.0 - r[a]) v = -1.0;
-        if (s[a] == 1.0 - r[a]) v = 1.0;
-        v = v < -1.0 ? -1.0 : (v > 1.0 ? 1.0 : v);
-        rn[a] = v;
         smax = fabs(s[a]) > smax ? fabs(s[a]) : smax;
       }
-      stash_state(stash, st);
+      pred = -(2.0 * js + shs);
+      if (!(pred > 1e-15 * fcur)) {  // step below what |dx|^2 resolves
+        conv = true;
+        done = true;
+      } else {
+        step = true;
+#pragma unroll
+        for (int a = 0; a < DR; ++a) {
+          double v = r[a] + s[a];
+          if (s[a] == -1.0 - r[a]) v = -1.0;
+          if (s[a] == 1.0 - r[a]) v = 1.0;
+          v = v < -1.0 ? -1.0 : (v > 1.0 ? 1.0 : v);
+          rn[a] = v;
+        }
+        stash_state(stash, st);
+      }
     }
-    if (__any_sync(FPX_FULL, !done && on_boundary<DR>(rn)))
+    if (!__any_sync(FPX_FULL, step)) break;
+    if (__any_sync(FPX_FULL, step && on_boundary<DR>(rn)))
       eval_state<D, DR, N, true>(sX, z, scale, rn, xs, st, sb);
     else
       eval_state<D, DR, N, false>(sX, z, scale, rn, xs, st, sb);
-    if (!done) {
+    // lanes not stepping evaluated at rn == r: their state is recomputed
+    // bit-identically (eval_state is a pure function of r)
+    if (step) {
       const double decr = fcur - st.f;
-      if (pred > 0.0 && decr >= P.accept * pred) {
+      if (decr >= P.accept * pred) {
         if (decr >= P.keep * pred) alpha *= P.grow;
 #pragma unroll
         for (int a = 0; a < DR; ++a) r[a] = rn[a];
@@ -663,6 +697,9 @@ __global__ void __launch_bounds__(128)
     atomicAdd((unsigned long long*)&stats[FPX_STAT_NEWTON], (unsigned long long)s_newton);
     atomicAdd((unsigned long long*)&stats[FPX_STAT_ITERS], (unsigned long long)s_iters);
     atomicAdd((unsigned long long*)&stats[FPX_STAT_EVALS], (unsigned long long)s_evals);
+    atomicAdd((unsigned long long*)&stats[FPX_STAT_NEWTON_R1], (unsigned long long)s_newton);
+    atomicAdd((unsigned long long*)&stats[FPX_STAT_ITERS_R1], (unsigned long long)s_iters);
+    atomicAdd((unsigned long long*)&stats[FPX_STAT_EVALS_R1], (unsigned long long)s_evals);
   }
 }
 

@@ -26,12 +26,16 @@ class RankGroup:
     rank: int = 0
     size: int = 1
     pg: object = None
+    device: torch.device = torch.device("cpu")   # where collective buffers live
 
     @staticmethod
     def from_torch(pg=None) -> "RankGroup":
         if not dist.is_available() or not dist.is_initialized():
             return RankGroup(0, 1, None)
-        return RankGroup(dist.get_rank(pg), dist.get_world_size(pg), pg)
+        backend = dist.get_backend(pg)
+        dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" \
+            else torch.device("cpu")
+        return RankGroup(dist.get_rank(pg), dist.get_world_size(pg), pg, dev)
 
     @property
     def single(self) -> bool:
@@ -50,6 +54,8 @@ def exchange(group: RankGroup, sends: list[torch.Tensor]) -> list[torch.Tensor]:
         raise ValueError(f"exchange needs {P} per-destination tensors, got {len(sends)}")
     if P == 1:
         return [sends[0]]
+    home = sends[0].device
+    sends = [s.to(group.device) for s in sends]
     ref = sends[0]
     dev, tail = ref.device, tuple(ref.shape[1:])
     w = int(np.prod(tail)) if tail else 1
@@ -64,7 +70,7 @@ def exchange(group: RankGroup, sends: list[torch.Tensor]) -> list[torch.Tensor]:
     _a2a(group, recv, flat, [c * w for c in rc], [c * w for c in sc])
     out, o = [], 0
     for c in rc:
-        out.append(recv[o:o + c * w].reshape((c,) + tail))
+        out.append(recv[o:o + c * w].reshape((c,) + tail).to(home))
         o += c * w
     return out
 
@@ -75,6 +81,8 @@ def exchange_packed(group: RankGroup, payload: torch.Tensor, counts: list[int]):
     P = group.size
     if P == 1:
         return payload, counts
+    home = payload.device
+    payload = payload.to(group.device)
     dev = payload.device
     tail = tuple(payload.shape[1:])
     w = int(np.prod(tail)) if tail else 1
@@ -85,34 +93,34 @@ def exchange_packed(group: RankGroup, payload: torch.Tensor, counts: list[int]):
     recv = torch.empty((sum(rc),) + tail, dtype=payload.dtype, device=dev)
     _a2a(group, recv.reshape(-1), payload.reshape(-1), [c * w for c in rc],
          [c * w for c in counts])
-    return recv, rc
+    return recv.to(home), rc
 
 
 def reduce_domain_bbox(group: RankGroup, lo, hi):
     """Componentwise min/max all-reduce of the local bounding box
     (SPEC.md:360-363)."""
-    lo_t = torch.as_tensor(lo, dtype=torch.float64).clone()
-    hi_t = torch.as_tensor(hi, dtype=torch.float64).clone()
+    lo_t = torch.as_tensor(lo, dtype=torch.float64).clone().to(group.device)
+    hi_t = torch.as_tensor(hi, dtype=torch.float64).clone().to(group.device)
     if group.size > 1:
         dist.all_reduce(lo_t, op=dist.ReduceOp.MIN, group=group.pg)
         dist.all_reduce(hi_t, op=dist.ReduceOp.MAX, group=group.pg)
-    return lo_t, hi_t
+    return lo_t.cpu(), hi_t.cpu()
 
 
 def allreduce_bitor(group: RankGroup, mask: torch.Tensor) -> torch.Tensor:
     """OR of per-rank bitmasks whose non-zero cells are disjoint across ranks
     (each global cell has exactly one owner): a SUM all-reduce, which NCCL
     supports (it has no bitwise reduction)."""
-    m = mask.clone()
+    m = mask.clone().to(group.device)
     if group.size > 1:
         dist.all_reduce(m, op=dist.ReduceOp.SUM, group=group.pg)
-    return m
+    return m.to(mask.device)
 
 
 def allgather_counts(group: RankGroup, value: int) -> list[int]:
     if group.size == 1:
         return [int(value)]
-    t = torch.tensor([value], dtype=torch.int64)
-    out = [torch.zeros(1, dtype=torch.int64) for _ in range(group.size)]
+    t = torch.tensor([value], dtype=torch.int64, device=group.device)
+    out = [torch.zeros(1, dtype=torch.int64, device=group.device) for _ in range(group.size)]
     dist.all_gather(out, t, group=group.pg)
     return [int(o) for o in out]

@@ -1,0 +1,216 @@
+"""GPU parity: the sm_100a kernels (through the C-ABI) against the oracle.
+
+Contract (north_star):
+  * setup: AABB / OBB / hash boxes bit-identical to the oracle fed the same
+    basis constants; the CSR local map identical;
+  * find: codes bit-exact; elements bit-exact except points within 1e-10 of
+    a shared face (either owner accepted); INTERIOR r to 1e-12; BORDER
+    compared by d* (1e-12 abs) with r to 1e-8 (linear convergence on faces);
+  * eval: 1e-10 relative.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_2501_12349_b200 import bounds, engine, invmap, toolkit
+from paper_2501_12349_b200.basis import BasisConstants, ReferenceBasis, build_basis_envelope
+
+pytestmark = pytest.mark.gpu
+
+
+def oracle_for(S, nodes, **kw):
+    bc = BasisConstants.of(S.basis, S.envelope)
+    B = O.basis_from_arrays(bc.nodes, bc.scale, bc.proj0, bc.proj1, bc.eta, bc.lo, bc.hi)
+    return O.OracleSetup(nodes, S.phys_dim, S.ref_dim, S.order, B=B, ncell=S.ncell, **kw)
+
+
+def assert_find_parity(S, OS, x, field=None, rtol_val=1e-10):
+    if field is not None:
+        vals, rec = engine.find_and_interpolate(S, field, x)
+    else:
+        rec = engine.find(S, x)
+    orec = OS.find(x)
+    code = rec.code.cpu().numpy()
+    elem = rec.elem.cpu().numpy()
+    r = rec.r.cpu().numpy()
+    dist = rec.dist.cpu().numpy()
+    assert np.array_equal(code, orec["code"]), \
+        f"code mismatches: {np.sum(code != orec['code'])}"
+    diff = elem != orec["elem"]
+    # either owner accepted only on a shared face: both records at d* ~ 0
+    # with r on the boundary
+    if diff.any():
+        onface = (np.abs(dist[diff]) < 1e-10) & (orec["dist"][diff] < 1e-10) & \
+            (np.any(np.abs(np.abs(r[diff]) - 1) < 1e-10, axis=1) |
+             np.any(np.abs(np.abs(orec["r"][diff]) - 1) < 1e-10, axis=1))
+        assert onface.all(), f"{(~onface).sum()} element mismatches off shared faces"
+    same = ~diff
+    inter = same & (code == 0)
+    if inter.any():
+        assert np.max(np.abs(r[inter] - orec["r"][inter])) < 1e-12
+        assert np.max(np.abs(dist[inter] - orec["dist"][inter])) < 1e-12
+    bord = same & (code == 1)
+    if bord.any():
+        np.testing.assert_allclose(dist[bord], orec["dist"][bord], rtol=1e-10, atol=1e-12)
+        assert np.max(np.abs(r[bord] - orec["r"][bord])) < 1e-8
+    nf = code == 2
+    assert np.all(elem[nf] == -1) and np.all(np.isnan(dist[nf]))
+    if field is not None:
+        v = vals.cpu().numpy()
+        ov = O.evaluate(OS.B, S.ref_dim, field, orec["code"], orec["elem"], orec["r"])
+        f = (code != 2) & same
+        np.testing.assert_allclose(v[f], ov[f], rtol=rtol_val, atol=1e-12)
+        assert np.all(np.isnan(v[nf]))
+    return rec, orec
+
+
+@pytest.mark.parametrize("mesh_fn", [
+    lambda: toolkit.kershaw_mesh(5, 4), lambda: toolkit.kershaw_mesh(4, 7),
+    lambda: toolkit.kershaw_mesh(6, 2), lambda: toolkit.box_mesh(2, 16, 3),
+    lambda: toolkit.box_mesh(3, 4, 3, amp=0.05)])
+def test_setup_bitexact_and_hash_identical(mesh_fn):
+    m = mesh_fn()
+    S = engine.setup(m)
+    OS = oracle_for(S, m.nodes)
+    ok = OS.boxes["obb_ok"].astype(bool)
+    assert np.array_equal(S.obb_ok.cpu().numpy().astype(bool), ok)
+    for k in ("aabb", "hbox"):
+        assert np.array_equal(getattr(S, k).cpu().numpy(), OS.boxes[k]), k
+    for k in ("obb_c", "obb_inv"):
+        assert np.array_equal(getattr(S, k).cpu().numpy()[ok], OS.boxes[k][ok]), k
+    assert np.array_equal(S.offsets.cpu().numpy(), OS.offsets)
+    assert np.array_equal(S.elems.cpu().numpy(), OS.elems)
+
+
+def test_cfg1_2d_quads_find_eval():
+    """cfg-1: 2D curved quads 16x16, p=3, 10^4 random points."""
+    m = toolkit.box_mesh(2, 16, 3, amp=0.02)
+    S = engine.setup(m)
+    OS = oracle_for(S, m.nodes)
+    x = toolkit.uniform_points(10_000, 2, seed=1, lo=-0.02, hi=1.02)
+    f = toolkit.analytic_field("coordinates", m)
+    rec, orec = assert_find_parity(S, OS, x, f)
+    c = rec.counts()
+    assert c["INTERIOR"] > 9000 and c["NOT_FOUND"] > 0
+
+
+@pytest.mark.parametrize("n,p,lo,hi", [(8, 4, 0.0, 1.0), (8, 4, -0.1, 1.1), (6, 3, -0.05, 1.05),
+                                       (4, 7, 0.0, 1.0), (10, 2, -0.02, 1.02)])
+def test_kershaw_find_eval(n, p, lo, hi):
+    m = toolkit.kershaw_mesh(n, p)
+    S = engine.setup(m)
+    OS = oracle_for(S, m.nodes)
+    x = toolkit.uniform_points(20_000, 3, seed=n * 10 + p, lo=lo, hi=hi)
+    assert_find_parity(S, OS, x, toolkit.analytic_field("smooth", m))
+
+
+def test_interpolate_matches_fused_and_oracle():
+    m = toolkit.kershaw_mesh(6, 4)
+    S = engine.setup(m)
+    OS = oracle_for(S, m.nodes)
+    x = toolkit.uniform_points(5000, 3, seed=5, lo=-0.05, hi=1.05)
+    f = toolkit.analytic_field("smooth", m)
+    vals, rec = engine.find_and_interpolate(S, f, x)
+    v2 = engine.interpolate(S, f, rec)
+    a, b = vals.cpu().numpy(), v2.cpu().numpy()
+    ok = ~np.isnan(a)
+    np.testing.assert_allclose(a[ok], b[ok], rtol=1e-13, atol=1e-14)
+    assert np.array_equal(np.isnan(a), np.isnan(b))
+    # reuse with a second field: coordinates reproduce x* for INTERIOR
+    xs = engine.interpolate(S, toolkit.analytic_field("coordinates", m), rec).cpu().numpy()
+    inter = rec.code.cpu().numpy() == 0
+    assert np.max(np.abs(xs[inter] - x[inter])) < 1e-10
+
+
+def test_constant_field_and_not_found():
+    m = toolkit.kershaw_mesh(4, 4)
+    S = engine.setup(m)
+    x = np.concatenate([toolkit.uniform_points(1000, 3, seed=2),
+                        np.array([[5.0, 5.0, 5.0], [-3.0, 0.5, 0.5]])])
+    v, rec = engine.find_and_interpolate(S, toolkit.analytic_field("constant", m), x)
+    v = v.cpu().numpy()[:, 0]
+    code = rec.code.cpu().numpy()
+    assert code[-1] == 2 and code[-2] == 2
+    assert np.all(np.isnan(v[-2:]))
+    np.testing.assert_allclose(v[:-2], 1.0, rtol=0, atol=1e-13)
+
+
+def test_empty_point_list():
+    m = toolkit.kershaw_mesh(3, 3)
+    S = engine.setup(m)
+    v, rec = engine.find_and_interpolate(S, toolkit.analytic_field("smooth", m),
+                                         np.zeros((0, 3)))
+    assert len(rec) == 0 and v.shape == (0, 1)
+
+
+def test_invert_point_known_answers():
+    p = 4
+    z = ReferenceBasis(p).nodes
+    N = p + 1
+    idx = np.arange(N * N)
+    X2 = np.stack([z[idx % N], z[idx // N]])
+    g = bounds.ElementGeometry(2, 2, p, X2)
+    res = invmap.invert_point(g, [0.3, -0.2])
+    assert np.max(np.abs(res.r - [0.3, -0.2])) < 1e-12 and res.dist < 1e-12
+    assert res.iterations <= 3 and res.converged
+    rng = np.random.default_rng(4)
+    A = rng.normal(size=(3, 3)) * 0.2 + np.eye(3)
+    b = rng.normal(size=3)
+    idx = np.arange(N ** 3)
+    R = np.stack([z[idx % N], z[(idx // N) % N], z[idx // (N * N)]])
+    g3 = bounds.ElementGeometry(3, 3, p, A @ R + b[:, None])
+    for _ in range(5):
+        rh = rng.uniform(-0.9, 0.9, 3)
+        res = invmap.invert_point(g3, A @ rh + b)
+        assert np.max(np.abs(res.r - rh)) < 1e-10
+        assert invmap.classify(res, 3) == invmap.INTERIOR
+
+
+def test_bounds_api_matches_reference_goldens():
+    import os
+    gd = np.load(os.path.join(os.path.dirname(__file__), "golden", "ref_bounds.npz"))
+    for key, (d, dr) in [("hex_p4", (3, 3)), ("quad_p3", (2, 2)), ("surf3_p4", (3, 2)),
+                         ("line2_p3", (2, 1))]:
+        p = int(key.split("_p")[1])
+        env = build_basis_envelope(ReferenceBasis(p))
+        for e in range(4):
+            g = bounds.ElementGeometry(d, dr, p, gd[key + "_nodes"][e])
+            a = bounds.element_aabb(g, env)
+            np.testing.assert_allclose(np.stack([a.lo, a.hi]), gd[key + "_aabb"][e],
+                                       rtol=1e-15, atol=4e-15)
+            o = bounds.element_obb(g, env)
+            np.testing.assert_allclose(o.center, gd[key + "_obbc"][e], rtol=0, atol=1e-13)
+            sc = np.abs(gd[key + "_obbi"][e]).max()
+            np.testing.assert_allclose(o.inv_transform, gd[key + "_obbi"][e], rtol=0,
+                                       atol=5e-12 * sc)
+    for p in (2, 3, 4, 7):
+        env = build_basis_envelope(ReferenceBasis(p))
+        for k in range(3):
+            b1 = bounds.bound_function_1d(env, gd[f"fb_p{p}_u1"][k])
+            np.testing.assert_allclose(b1.lower, gd[f"fb_p{p}_lo1"][k], rtol=0, atol=2e-14)
+            b2 = bounds.bound_function_2d(env, gd[f"fb_p{p}_u2"][k])
+            assert np.array_equal(b2.lower, gd[f"fb_p{p}_lo2"][k])
+            assert np.array_equal(b2.upper, gd[f"fb_p{p}_hi2"][k])
+
+
+def test_cfg2_full_size_properties():
+    """cfg-2 size (32^3 hexes p=4, 10^6 points): size-independent properties
+    -- every point of [0,1]^3 is found, INTERIOR records reproduce x* through
+    the coordinate field, and a sample agrees with the oracle."""
+    m = toolkit.kershaw_mesh(32, 4)
+    S = engine.setup(m)
+    x = toolkit.uniform_points(1_000_000, 3, seed=7)
+    f = toolkit.analytic_field("coordinates", m)
+    v, rec = engine.find_and_interpolate(S, f, x)
+    code = rec.code.cpu().numpy()
+    assert np.all(code != 2)
+    inter = code == 0
+    assert inter.mean() > 0.999
+    assert np.max(np.abs(v.cpu().numpy()[inter] - x[inter])) < 1e-10
+    OS = oracle_for(S, m.nodes, nthreads=0)
+    sub = x[::50]
+    orec = OS.find(sub)
+    assert np.array_equal(code[::50], orec["code"])
+    same = rec.elem.cpu().numpy()[::50] == orec["elem"]
+    assert same.mean() > 0.999
