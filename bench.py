@@ -203,6 +203,9 @@ def run_ours(args):
           for _ in range(args.steps)]
     kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
            for _ in range(args.steps)]
+    for a_, b_ in kev:      # torch creates events lazily: force creation
+        a_.record(stream)
+        b_.record(stream)
     L = _C.lib()
     launches0 = L.fpx_launch_count()
     stats = []

@@ -135,12 +135,16 @@ int fpx_bound_function(int dr, int N, int M, int64_t nf, const double* basis,
                        const double* values, double* lower, double* upper, void* stream);
 
 /* build_local_map over boxes [E][2][d]: grid over the union
- * of the boxes, CSR cell -> ascending element ids.
+ * of the boxes, CSR cell -> ascending element ids.  With OBBs
+ * (obb_ok != NULL; obb_c/obb_inv as fpx_setup_bounds writes them), cells of
+ * a box's range that cannot meet the element's OBB are culled (decision D5b,
+ * result-preserving); NULL keeps the SPEC's full rectangular range.
  * Synchronising.  Pass elems == NULL (or cap too small) to get
  * offsets/grid and *needed_host; then call again with cap >= needed.
  * ws: FPX workspace of fpx_hash_workspace_bytes(). */
 size_t fpx_hash_workspace_bytes(int d, int64_t E, int ncell);
-int fpx_hash_build(int d, int64_t E, const double* box, int ncell, double* grid,
+int fpx_hash_build(int d, int64_t E, const double* box, const double* obb_c,
+                   const double* obb_inv, const uint8_t* obb_ok, int ncell, double* grid,
                    int32_t* offsets, int32_t* elems, int64_t cap, int64_t* needed_host,
                    int32_t* max_list_host, void* ws, size_t ws_bytes, void* stream);
 

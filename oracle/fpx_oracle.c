@@ -715,10 +715,35 @@ int64_t fpxo_cell_of(int d, const double* grid, int n, const double* x) {
   return cell_of(d, grid, n, x, NULL);
 }
 
+/* Conservative cell-vs-OBB overlap (decision D5b): the cell
+ * centre mapped into the OBB frame must lie within the unit cube grown by the
+ * cell's half-extent seen in that frame, with a 1e-9 relative margin.  Never
+ * drops a cell containing a point of the OBB, so the filtered candidate set
+ * of every point is unchanged. */
+static int cell_meets_obb(int d, const double* grid, const int* q, const double* cen,
+                          const double* inv) {
+  double dx[3];
+  for (int b = 0; b < d; ++b) {
+    double cc = grid[b] + ((double)q[b] + 0.5) * grid[6 + b];
+    dx[b] = cc - cen[b];
+  }
+  for (int a = 0; a < d; ++a) {
+    double y = 0.0, e = 0.0;
+    for (int b = 0; b < d; ++b) {
+      y += inv[a * d + b] * dx[b];
+      e += fabs(inv[a * d + b]) * (0.5 * grid[6 + b]);
+    }
+    if (!(fabs(y) <= (1.0 + e) * (1.0 + 1e-9))) return 0;
+  }
+  return 1;
+}
+
 /* build_local_map: CSR of cell -> ascending element ids
- * over the rectangular cell range of each box's two corners.
+ * over the rectangular cell range of each box's two corners; with OBBs
+ * (obb_ok != NULL) cells that cannot meet the element's OBB are skipped.
  * Call with elems == NULL to get the total entry count in offsets[ncell^d]. */
-int64_t fpxo_hash_build(int d, int64_t E, const double* box, const double* grid, int n,
+int64_t fpxo_hash_build(int d, int64_t E, const double* box, const double* obb_c,
+                        const double* obb_inv, const uint8_t* obb_ok, const double* grid, int n,
                         int32_t* offsets, int32_t* elems) {
   int64_t nc = 1;
   for (int c = 0; c < d; ++c) nc *= n;
@@ -727,9 +752,12 @@ int64_t fpxo_hash_build(int d, int64_t E, const double* box, const double* grid,
     int a[3] = {0, 0, 0}, b[3] = {0, 0, 0};
     cell_of(d, grid, n, box + e * 2 * d, a);
     cell_of(d, grid, n, box + e * 2 * d + d, b);
+    const int cull = obb_ok && obb_ok[e];
     for (int k = a[2]; k <= (d == 3 ? b[2] : 0); ++k)
       for (int j = a[1]; j <= b[1]; ++j)
         for (int i = a[0]; i <= b[0]; ++i) {
+          int q[3] = {i, j, k};
+          if (cull && !cell_meets_obb(d, grid, q, obb_c + e * d, obb_inv + e * d * d)) continue;
           int64_t cell = i + (int64_t)n * (j + (int64_t)n * k);
           if (elems) elems[offsets[cell] + cnt[cell]] = (int32_t)e;
           cnt[cell]++;
@@ -867,56 +895,54 @@ static int chol_solve(int n, const int* idx, const double A[3][3], const double*
   return 0;
 }
 
-/* Projected trust-region Newton step on the free axes (
- * decision D8 as frozen in DESIGN.md §3.4).  free[] excludes the active
- * bounds; Hm is the model Hessian.
- *   1. s_F = -Hm_FF^{-1} J_F, s_A = 0;
- *   2. trust region: scale s uniformly so |s|_inf <= alpha (direction kept,
- *      so the predicted decrease stays > 0);
- *   3. reference box: free axes with r + s outside [-1, 1] are fixed on the
- *      face (s_a = +-1 - r_a); one reduced re-solve on the remaining free
- *      axes with the fixed values moved to the right-hand side, scaled into
- *      the trust region again and clamped to the box.
+/* Projected trust-region Newton step (decision D8 as frozen
+ * in DESIGN.md §3.4).  freem[] enters as the axes not held by an active
+ * bound (on a face with the gradient pushing out).
+ *   1. Newton direction on the free axes: Hm_FF s_F = -J_F, s_A = 0;
+ *   2. a free axis sitting on a face whose Newton component points out of
+ *      the box is made active and the direction re-solved (<= dr times);
+ *   3. the step is the direction truncated at the trust radius alpha
+ *      (|s|_inf <= alpha) and at the first face it reaches: s = t s_N.
+ * *hit gets a bitmask of the axes whose face limits t (they land exactly on
+ * +-1).  A positive multiple of a Newton direction of a positive definite
+ * model is a descent step, so the predicted decrease is > 0 unless s = 0.
  * Returns -1 if the free block is not positive definite. */
 static int constrained_step(int dr, const double Hm[3][3], const double* J, const double* r,
-                            const int* freem, double alpha, double* s) {
-  int fidx[3], nf = 0;
-  for (int a = 0; a < dr; ++a) { s[a] = 0.0; if (freem[a]) fidx[nf++] = a; }
-  if (nf == 0) return 0;
-  double rhs[3], x[3];
-  for (int k = 0; k < nf; ++k) rhs[k] = -J[fidx[k]];
-  if (chol_solve(nf, fidx, Hm, rhs, x)) return -1;
+                            int* freem, double alpha, double* s, int* hit) {
+  double x[3] = {0, 0, 0};
+  *hit = 0;
+  for (int a = 0; a < dr; ++a) s[a] = 0.0;
+  for (int pass = 0; pass <= dr; ++pass) {
+    int fidx[3], nf = 0;
+    for (int a = 0; a < dr; ++a) if (freem[a]) fidx[nf++] = a;
+    if (nf == 0) return 0;
+    double rhs[3] = {0, 0, 0}, y[3] = {0, 0, 0};
+    for (int k = 0; k < nf; ++k) rhs[k] = -J[fidx[k]];
+    if (chol_solve(nf, fidx, Hm, rhs, y)) return -1;
+    int blocked = 0;
+    for (int a = 0; a < dr; ++a) x[a] = 0.0;
+    for (int k = 0; k < nf; ++k) {
+      int a = fidx[k];
+      x[a] = y[k];
+      if ((r[a] == 1.0 && y[k] > 0.0) || (r[a] == -1.0 && y[k] < 0.0)) { freem[a] = 0; blocked = 1; }
+    }
+    if (!blocked) break;
+    if (pass == dr) return 0;
+  }
   double m = 0.0;
-  for (int k = 0; k < nf; ++k) if (fabs(x[k]) > m) m = fabs(x[k]);
-  if (m > alpha) { double t = alpha / m; for (int k = 0; k < nf; ++k) x[k] *= t; }
-  int fixed[3] = {0, 0, 0}, nfix = 0;
-  for (int k = 0; k < nf; ++k) {
-    int a = fidx[k];
-    double bl = -1.0 - r[a], bh = 1.0 - r[a];
-    s[a] = x[k];
-    if (x[k] < bl) { s[a] = bl; fixed[a] = 1; ++nfix; }
-    else if (x[k] > bh) { s[a] = bh; fixed[a] = 1; ++nfix; }
+  for (int a = 0; a < dr; ++a) if (freem[a] && fabs(x[a]) > m) m = fabs(x[a]);
+  if (m == 0.0) return 0;
+  double t = m > alpha ? alpha / m : 1.0;
+  double ta[3] = {INFINITY, INFINITY, INFINITY};
+  for (int a = 0; a < dr; ++a) {
+    if (!freem[a] || x[a] == 0.0) continue;
+    ta[a] = x[a] > 0.0 ? (1.0 - r[a]) / x[a] : (-1.0 - r[a]) / x[a];
+    if (ta[a] < t) t = ta[a];
   }
-  if (nfix == 0 || nfix == nf) return 0;
-  int gidx[3], ng = 0;
-  for (int k = 0; k < nf; ++k) if (!fixed[fidx[k]]) gidx[ng++] = fidx[k];
-  double b2[3] = {0, 0, 0}, x2[3];
-  for (int k = 0; k < ng; ++k) {
-    int f = gidx[k];
-    double t = -J[f];
-    for (int c = 0; c < dr; ++c) if (fixed[c]) t -= Hm[f][c] * s[c];
-    b2[k] = t;
-  }
-  if (chol_solve(ng, gidx, Hm, b2, x2)) return 0; /* keep the first-pass step */
-  m = 0.0;
-  for (int k = 0; k < ng; ++k) if (fabs(x2[k]) > m) m = fabs(x2[k]);
-  if (m > alpha) { double t = alpha / m; for (int k = 0; k < ng; ++k) x2[k] *= t; }
-  for (int k = 0; k < ng; ++k) {
-    int f = gidx[k];
-    double v = x2[k], bl = -1.0 - r[f], bh = 1.0 - r[f];
-    if (v < bl) v = bl;
-    else if (v > bh) v = bh;
-    s[f] = v;
+  for (int a = 0; a < dr; ++a) {
+    if (!freem[a]) continue;
+    s[a] = t * x[a];
+    if (ta[a] == t) *hit |= 1 << a;
   }
   return 0;
 }
@@ -971,18 +997,24 @@ void fpxo_invert(const fpxo_basis* B, int d, int dr, const double* X, const doub
     double s[3] = {0, 0, 0};
     const double(*Hm)[3] = H0;
     double Hr[3][3];
-    if (beta && constrained_step(dr, Hb, J, r, freem, alpha, s) == 0) {
+    int fr[3], hit = 0;
+    for (int a = 0; a < 3; ++a) fr[a] = freem[a];
+    if (beta && constrained_step(dr, Hb, J, r, fr, alpha, s, &hit) == 0) {
       Hm = Hb;
-    } else if (constrained_step(dr, H0, J, r, freem, alpha, s) != 0) {
-      double tr = 0.0;
-      for (int a = 0; a < dr; ++a) tr += H0[a][a];
-      double lam = 1e-10 * tr / dr;
-      if (!(lam > 0.0)) lam = 1e-300;
-      for (int a = 0; a < dr; ++a)
-        for (int b = 0; b < dr; ++b) Hr[a][b] = H0[a][b] + (a == b ? lam : 0.0);
-      Hm = Hr;
-      if (constrained_step(dr, Hr, J, r, freem, alpha, s) != 0)
-        for (int a = 0; a < dr; ++a) s[a] = 0.0;
+    } else {
+      for (int a = 0; a < 3; ++a) fr[a] = freem[a];
+      if (constrained_step(dr, H0, J, r, fr, alpha, s, &hit) != 0) {
+        double tr = 0.0;
+        for (int a = 0; a < dr; ++a) tr += H0[a][a];
+        double lam = 1e-10 * tr / dr;
+        if (!(lam > 0.0)) lam = 1e-300;
+        for (int a = 0; a < dr; ++a)
+          for (int b = 0; b < dr; ++b) Hr[a][b] = H0[a][b] + (a == b ? lam : 0.0);
+        Hm = Hr;
+        for (int a = 0; a < 3; ++a) fr[a] = freem[a];
+        if (constrained_step(dr, Hr, J, r, fr, alpha, s, &hit) != 0)
+          for (int a = 0; a < dr; ++a) s[a] = 0.0;
+      }
     }
     ++it;
     double js = 0.0, shs = 0.0, smax = 0.0;
@@ -995,12 +1027,14 @@ void fpxo_invert(const fpxo_basis* B, int d, int dr, const double* X, const doub
     }
     double pred = -(2.0 * js + shs);
     /* the step cannot change |dx|^2 in floating point: converged */
+#ifdef FPXO_TRACE
+    if (!(pred > 1e-15 * f)) fprintf(stderr, "stop it %d pred %.3e f %.3e s=(%.3e %.3e %.3e) J=(%.3e %.3e %.3e) free %d%d%d alpha %.3e\n", it, pred, f, s[0], s[1], s[2], J[0], J[1], J[2], freem[0], freem[1], freem[2], alpha);
+#endif
     if (!(pred > 1e-15 * f)) { converged = 1; break; }
     double rn[3] = {0, 0, 0};
     for (int a = 0; a < dr; ++a) {
       double v = r[a] + s[a];
-      if (s[a] == -1.0 - r[a]) v = -1.0;
-      if (s[a] == 1.0 - r[a]) v = 1.0;
+      if (hit & (1 << a)) v = s[a] > 0.0 ? 1.0 : -1.0;  /* lands on the face */
       if (v < -1.0) v = -1.0;
       if (v > 1.0) v = 1.0;
       rn[a] = v;

@@ -91,7 +91,7 @@ def lib():
         L.fpxo_hash_grid.argtypes = [C.c_int, C.c_int64, P, C.c_int, P]
         L.fpxo_cell_of.argtypes = [C.c_int, P, C.c_int, P]
         L.fpxo_cell_of.restype = C.c_int64
-        L.fpxo_hash_build.argtypes = [C.c_int, C.c_int64, P, P, C.c_int, P, P]
+        L.fpxo_hash_build.argtypes = [C.c_int, C.c_int64, P, P, P, P, P, C.c_int, P, P]
         L.fpxo_hash_build.restype = C.c_int64
         L.fpxo_forward_map.argtypes = [C.POINTER(Basis), C.c_int, C.c_int, P, P, P, P, P]
         L.fpxo_invert.argtypes = [C.POINTER(Basis), C.c_int, C.c_int, P, P,
@@ -221,7 +221,9 @@ def n_cells(E, d):
     return int(min(max(n, 1), 1024))
 
 
-def hash_build(d, box, ncell):
+def hash_build(d, box, ncell, obb_c=None, obb_inv=None, obb_ok=None):
+    """Local map over boxes; with OBBs, cells that cannot meet an element's OBB
+    are culled (D5b)."""
     box = _f64(box)
     E = box.shape[0]
     grid = np.zeros(9)
@@ -229,9 +231,14 @@ def hash_build(d, box, ncell):
     L.fpxo_hash_grid(d, E, _p(box), ncell, _p(grid))
     nc = ncell ** d
     offsets = np.zeros(nc + 1, np.int32)
-    total = L.fpxo_hash_build(d, E, _p(box), _p(grid), ncell, _p(offsets), None)
+    cull = obb_ok is not None
+    oc = _f64(np.nan_to_num(obb_c)) if cull else None
+    oi = _f64(np.nan_to_num(obb_inv)) if cull else None
+    ok = np.ascontiguousarray(obb_ok, np.uint8) if cull else None
+    args = (_p(oc), _p(oi), _p(ok)) if cull else (None, None, None)
+    total = L.fpxo_hash_build(d, E, _p(box), *args, _p(grid), ncell, _p(offsets), None)
     elems = np.zeros(max(total, 1), np.int32)
-    L.fpxo_hash_build(d, E, _p(box), _p(grid), ncell, _p(offsets), _p(elems))
+    L.fpxo_hash_build(d, E, _p(box), *args, _p(grid), ncell, _p(offsets), _p(elems))
     # lists are filled in ascending element order already (outer loop over e)
     return grid, offsets, elems[:total]
 
@@ -253,8 +260,9 @@ class OracleSetup:
         if bx["degenerate"]:
             raise ValueError("degenerate element in oracle setup")
         self.boxes = bx
-        self.ncell = ncell or n_cells(self.E, d)
-        self.grid, self.offsets, self.elems = hash_build(d, bx["hbox"], self.ncell)
+        self.ncell = ncell or 2 * n_cells(self.E, d)
+        self.grid, self.offsets, self.elems = hash_build(d, bx["hbox"], self.ncell, bx["obb_c"],
+                                                         bx["obb_inv"], bx["obb_ok"])
         self.obb_ok = bx["obb_ok"]
         self.mesh = Mesh()
         m = self.mesh

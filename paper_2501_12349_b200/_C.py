@@ -13,7 +13,7 @@ import numpy as np
 import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libfpx_sm100.so")
+LIB_PATH = os.environ.get("FPX_LIB") or os.path.join(HERE, "lib", "libfpx_sm100.so")
 ABI_VERSION = 1
 
 INTERIOR, BORDER, NOT_FOUND = 0, 1, 2
@@ -69,7 +69,7 @@ def lib():
         "fpx_setup_bounds": ([i32, i32, i32, i32, i64, P, P, f64, P, P, P, P, P, P, P, P], i32),
         "fpx_bound_function": ([i32, i32, i32, i64, P, P, P, P, P], i32),
         "fpx_hash_workspace_bytes": ([i32, i64, i32], sz),
-        "fpx_hash_build": ([i32, i64, P, i32, P, P, P, i64, P, P, P, sz, P], i32),
+        "fpx_hash_build": ([i32, i64, P, P, P, P, i32, P, P, P, i64, P, P, P, sz, P], i32),
         "fpx_cell_of": ([C.POINTER(MeshT), i64, P, P, P], i32),
         "fpx_find_workspace_bytes": ([i64, i64, i64], sz),
         "fpx_find": ([C.POINTER(MeshT), i64, P, P, P, P, P, P, P, i32, P, P, i64, P, sz, P], i32),

@@ -318,7 +318,8 @@ size_t fpx_hash_workspace_bytes(int d, int64_t E, int ncell) {
   return c.off + 256;
 }
 
-int fpx_hash_build(int d, int64_t E, const double* box, int ncell, double* grid,
+int fpx_hash_build(int d, int64_t E, const double* box, const double* obb_c,
+                   const double* obb_inv, const uint8_t* obb_ok, int ncell, double* grid,
                    int32_t* offsets, int32_t* elems, int64_t cap, int64_t* needed_host,
                    int32_t* max_list_host, void* ws, size_t ws_bytes, void* stream) {
   if (!(d == 2 || d == 3)) return fail(FPX_EINVAL, "hash: bad d=%d", d);
@@ -337,7 +338,7 @@ int fpx_hash_build(int d, int64_t E, const double* box, int ncell, double* grid,
   cudaStream_t st = S(stream);
   FPX_LAUNCH(fpx::launch_hash_grid(d, E, box, ncell, grid, st));
   FPX_CK(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (nc + 1), st));
-  FPX_LAUNCH(fpx::launch_hash_count(d, E, box, grid, ncell, cnt, st));
+  FPX_LAUNCH(fpx::launch_hash_count(d, E, box, obb_c, obb_inv, obb_ok, grid, ncell, cnt, st));
   FPX_CK(cub::DeviceScan::ExclusiveSum(temp, tb, cnt, offsets, (int)(nc + 1), st));
   int32_t total = 0;
   FPX_CK(cudaMemcpyAsync(&total, offsets + nc, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
@@ -347,7 +348,8 @@ int fpx_hash_build(int d, int64_t E, const double* box, int ncell, double* grid,
   if (!elems || cap < total) return FPX_OK;
   FPX_CK(cudaMemsetAsync(cursor, 0, sizeof(int32_t) * (nc + 1), st));
   FPX_CK(cudaMemsetAsync(maxl, 0, sizeof(int32_t), st));
-  FPX_LAUNCH(fpx::launch_hash_fill(d, E, box, grid, ncell, offsets, cursor, elems, st));
+  FPX_LAUNCH(fpx::launch_hash_fill(d, E, box, obb_c, obb_inv, obb_ok, grid, ncell, offsets,
+                                   cursor, elems, st));
   FPX_LAUNCH(fpx::launch_hash_sort(nc, offsets, elems, maxl, st));
   int32_t ml = 0;
   FPX_CK(cudaMemcpyAsync(&ml, maxl, sizeof(int32_t), cudaMemcpyDeviceToHost, st));

@@ -611,29 +611,63 @@ __device__ void box_cells(int d, const double* grid, int n, const double* b, int
   cell_of(d, grid, n, b + d, a1);
 }
 
+// Conservative cell-vs-OBB overlap (oracle cell_meets_obb, decision D5b):
+// the cell centre in the OBB frame lies within the unit cube grown by the
+// cell's half-extent in that frame (1e-9 relative margin).
+__device__ __forceinline__ bool cell_meets_obb(int d, const double* grid, int i, int j, int k,
+                                               const double* __restrict__ cen,
+                                               const double* __restrict__ inv) {
+  const int q[3] = {i, j, k};
+  double dx[3];
+  for (int b = 0; b < d; ++b) {
+    const double cc = grid[b] + ((double)q[b] + 0.5) * grid[6 + b];
+    dx[b] = cc - cen[b];
+  }
+  for (int a = 0; a < d; ++a) {
+    double y = 0.0, ee = 0.0;
+    for (int b = 0; b < d; ++b) {
+      y += inv[a * d + b] * dx[b];
+      ee += fabs(inv[a * d + b]) * (0.5 * grid[6 + b]);
+    }
+    if (!(fabs(y) <= (1.0 + ee) * (1.0 + 1e-9))) return false;
+  }
+  return true;
+}
+
 __global__ void k_hash_count(int d, int64_t E, const double* __restrict__ box,
-                             const double* __restrict__ grid, int n, int32_t* cnt) {
+                             const double* __restrict__ obb_c, const double* __restrict__ obb_inv,
+                             const uint8_t* __restrict__ obb_ok, const double* __restrict__ grid,
+                             int n, int32_t* cnt) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
        e += (int64_t)gridDim.x * blockDim.x) {
     int a[3], b[3];
     box_cells(d, grid, n, box + e * 2 * d, a, b);
+    const bool cull = obb_ok && obb_ok[e];
     for (int k = a[2]; k <= b[2]; ++k)
       for (int j = a[1]; j <= b[1]; ++j)
-        for (int i = a[0]; i <= b[0]; ++i)
+        for (int i = a[0]; i <= b[0]; ++i) {
+          if (cull && !cell_meets_obb(d, grid, i, j, k, obb_c + e * d, obb_inv + e * d * d))
+            continue;
           atomicAdd(&cnt[i + (int64_t)n * (j + (int64_t)n * k)], 1);
+        }
   }
 }
 
 __global__ void k_hash_fill(int d, int64_t E, const double* __restrict__ box,
-                            const double* __restrict__ grid, int n,
-                            const int32_t* __restrict__ offsets, int32_t* cursor, int32_t* elems) {
+                            const double* __restrict__ obb_c, const double* __restrict__ obb_inv,
+                            const uint8_t* __restrict__ obb_ok, const double* __restrict__ grid,
+                            int n, const int32_t* __restrict__ offsets, int32_t* cursor,
+                            int32_t* elems) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
        e += (int64_t)gridDim.x * blockDim.x) {
     int a[3], b[3];
     box_cells(d, grid, n, box + e * 2 * d, a, b);
+    const bool cull = obb_ok && obb_ok[e];
     for (int k = a[2]; k <= b[2]; ++k)
       for (int j = a[1]; j <= b[1]; ++j)
         for (int i = a[0]; i <= b[0]; ++i) {
+          if (cull && !cell_meets_obb(d, grid, i, j, k, obb_c + e * d, obb_inv + e * d * d))
+            continue;
           int64_t cell = i + (int64_t)n * (j + (int64_t)n * k);
           int slot = atomicAdd(&cursor[cell], 1);
           elems[offsets[cell] + slot] = (int32_t)e;
@@ -853,15 +887,18 @@ cudaError_t launch_hash_grid(int d, int64_t E, const double* box, int ncell, dou
   k_hash_grid<<<1, 1024, 0, st>>>(d, E, box, ncell, grid);
   return cudaGetLastError();
 }
-cudaError_t launch_hash_count(int d, int64_t E, const double* box, const double* grid, int n,
-                              int32_t* cnt, cudaStream_t st) {
-  k_hash_count<<<grid_for(E, 256), 256, 0, st>>>(d, E, box, grid, n, cnt);
+cudaError_t launch_hash_count(int d, int64_t E, const double* box, const double* obb_c,
+                              const double* obb_inv, const uint8_t* obb_ok, const double* grid,
+                              int n, int32_t* cnt, cudaStream_t st) {
+  k_hash_count<<<grid_for(E, 256), 256, 0, st>>>(d, E, box, obb_c, obb_inv, obb_ok, grid, n, cnt);
   return cudaGetLastError();
 }
-cudaError_t launch_hash_fill(int d, int64_t E, const double* box, const double* grid, int n,
-                             const int32_t* offsets, int32_t* cursor, int32_t* elems,
+cudaError_t launch_hash_fill(int d, int64_t E, const double* box, const double* obb_c,
+                             const double* obb_inv, const uint8_t* obb_ok, const double* grid,
+                             int n, const int32_t* offsets, int32_t* cursor, int32_t* elems,
                              cudaStream_t st) {
-  k_hash_fill<<<grid_for(E, 256), 256, 0, st>>>(d, E, box, grid, n, offsets, cursor, elems);
+  k_hash_fill<<<grid_for(E, 256), 256, 0, st>>>(d, E, box, obb_c, obb_inv, obb_ok, grid, n,
+                                                offsets, cursor, elems);
   return cudaGetLastError();
 }
 cudaError_t launch_hash_sort(int64_t ncells, const int32_t* offsets, int32_t* elems,

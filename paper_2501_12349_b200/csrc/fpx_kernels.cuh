@@ -26,10 +26,12 @@ cudaError_t launch_bound_function(int dr, int N, int M, int64_t nf, const double
                                   cudaStream_t st);
 cudaError_t launch_hash_grid(int d, int64_t E, const double* box, int ncell, double* grid,
                              cudaStream_t st);
-cudaError_t launch_hash_count(int d, int64_t E, const double* box, const double* grid, int n,
-                              int32_t* cnt, cudaStream_t st);
-cudaError_t launch_hash_fill(int d, int64_t E, const double* box, const double* grid, int n,
-                             const int32_t* offsets, int32_t* cursor, int32_t* elems,
+cudaError_t launch_hash_count(int d, int64_t E, const double* box, const double* obb_c,
+                              const double* obb_inv, const uint8_t* obb_ok, const double* grid,
+                              int n, int32_t* cnt, cudaStream_t st);
+cudaError_t launch_hash_fill(int d, int64_t E, const double* box, const double* obb_c,
+                             const double* obb_inv, const uint8_t* obb_ok, const double* grid,
+                             int n, const int32_t* offsets, int32_t* cursor, int32_t* elems,
                              cudaStream_t st);
 cudaError_t launch_hash_sort(int64_t ncells, const int32_t* offsets, int32_t* elems,
                              int32_t* max_list, cudaStream_t st);

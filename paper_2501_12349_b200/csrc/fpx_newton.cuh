@@ -18,6 +18,10 @@
 #include "fpx_common.cuh"
 #include "fpx_kernels.cuh"
 
+#ifndef FPX_NEWTON_MINB
+#define FPX_NEWTON_MINB 2  // CTAs of 128 threads per SM the Newton kernels are built for
+#endif
+
 namespace fpx {
 
 template <int D, int DR, int N>
@@ -102,7 +106,7 @@ __device__ __forceinline__ void eval_state(const double* __restrict__ sX,
     S.H0[m] = 0.0;
     S.Q[m] = 0.0;
   }
-#pragma unroll
+#pragma unroll 1
   for (int c = 0; c < D; ++c) {
     const double* Xc = sX + c * L::CS;
     double xv = 0.0, G[3] = {0.0, 0.0, 0.0}, H2[6] = {0, 0, 0, 0, 0, 0};
@@ -187,7 +191,7 @@ __device__ __forceinline__ void eval_state(const double* __restrict__ sX,
       }
     }
 #undef SB
-    const double dx = xs[c] - xv;
+    const double dx = (c == 0 ? xs[0] : (c == 1 ? xs[1] : xs[D - 1])) - xv;
     S.f = fma(dx, dx, S.f);
 #pragma unroll
     for (int a = 0; a < DR; ++a) S.J[a] = fma(-G[a], dx, S.J[a]);
@@ -263,75 +267,59 @@ __device__ __forceinline__ bool chol_solve(const double* A, const bool* act, con
   return true;
 }
 
-// Projected trust-region Newton step on the free axes (oracle
-// constrained_step, decision D8): Newton on the free block, uniform scaling
-// into the trust box, faces hit by the step fixed and one reduced re-solve.
-// Returns false if the free block is not positive definite.
+// Projected trust-region Newton step (oracle constrained_step, decision D8):
+// the Newton direction on the free axes (free axes on a face that the
+// direction would leave become active, re-solve), truncated at the trust
+// radius and at the first face it reaches.  `hit` marks the axes whose face
+// limits the step.  Returns false if the free block is not positive definite.
 template <int DR>
 __device__ __forceinline__ bool constrained_step(const double* Hm, const double* J,
-                                                 const double* r, const bool* freem,
-                                                 double alpha, double* s) {
-  int nf = 0;
-  double rhs[3], x[3] = {0.0, 0.0, 0.0};
+                                                 const double* r, bool* freem, double alpha,
+                                                 double* s, int& hit) {
+  double x[3] = {0.0, 0.0, 0.0};
+  hit = 0;
 #pragma unroll
-  for (int a = 0; a < DR; ++a) {
-    s[a] = 0.0;
-    nf += freem[a] ? 1 : 0;
-    rhs[a] = -J[a];
+  for (int a = 0; a < DR; ++a) s[a] = 0.0;
+#pragma unroll 1
+  for (int pass = 0; pass <= DR; ++pass) {
+    int nf = 0;
+#pragma unroll
+    for (int a = 0; a < DR; ++a) nf += freem[a] ? 1 : 0;
+    if (nf == 0) return true;
+    double rhs[3], y[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int a = 0; a < DR; ++a) rhs[a] = -J[a];
+    if (!chol_solve<DR>(Hm, freem, rhs, y)) return false;
+    bool blocked = false;
+#pragma unroll
+    for (int a = 0; a < DR; ++a) {
+      x[a] = freem[a] ? y[a] : 0.0;
+      if (freem[a] && ((r[a] == 1.0 && y[a] > 0.0) || (r[a] == -1.0 && y[a] < 0.0))) {
+        freem[a] = false;
+        blocked = true;
+      }
+    }
+    if (!blocked) break;
+    if (pass == DR) return true;
   }
-  if (nf == 0) return true;
-  if (!chol_solve<DR>(Hm, freem, rhs, x)) return false;
   double m = 0.0;
 #pragma unroll
   for (int a = 0; a < DR; ++a)
     if (freem[a]) m = fabs(x[a]) > m ? fabs(x[a]) : m;
-  if (m > alpha) {
-    const double t = alpha / m;
+  if (m == 0.0) return true;
+  double t = m > alpha ? alpha / m : 1.0;
+  double ta[3] = {INFINITY, INFINITY, INFINITY};
 #pragma unroll
-    for (int a = 0; a < DR; ++a)
-      if (freem[a]) x[a] *= t;
+  for (int a = 0; a < DR; ++a) {
+    if (!freem[a] || x[a] == 0.0) continue;
+    ta[a] = x[a] > 0.0 ? (1.0 - r[a]) / x[a] : (-1.0 - r[a]) / x[a];
+    t = ta[a] < t ? ta[a] : t;
   }
-  bool g[3] = {false, false, false};
-  int nfix = 0;
 #pragma unroll
   for (int a = 0; a < DR; ++a) {
     if (!freem[a]) continue;
-    const double bl = -1.0 - r[a], bh = 1.0 - r[a];
-    s[a] = x[a];
-    if (x[a] < bl) {
-      s[a] = bl;
-      ++nfix;
-    } else if (x[a] > bh) {
-      s[a] = bh;
-      ++nfix;
-    } else {
-      g[a] = true;
-    }
-  }
-  if (nfix == 0 || nfix == nf) return true;
-  double b2[3] = {0.0, 0.0, 0.0}, x2[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-  for (int f = 0; f < DR; ++f) {
-    if (!g[f]) continue;
-    double t = -J[f];
-#pragma unroll
-    for (int c = 0; c < DR; ++c)
-      if (freem[c] && !g[c]) t -= Hm[symi(f, c)] * s[c];
-    b2[f] = t;
-  }
-  if (!chol_solve<DR>(Hm, g, b2, x2)) return true;  // keep the first pass
-  m = 0.0;
-#pragma unroll
-  for (int a = 0; a < DR; ++a)
-    if (g[a]) m = fabs(x2[a]) > m ? fabs(x2[a]) : m;
-  const double t = m > alpha ? alpha / m : 1.0;
-#pragma unroll
-  for (int a = 0; a < DR; ++a) {
-    if (!g[a]) continue;
-    double v = m > alpha ? x2[a] * t : x2[a];
-    const double bl = -1.0 - r[a], bh = 1.0 - r[a];
-    v = v < bl ? bl : (v > bh ? bh : v);
-    s[a] = v;
+    s[a] = t * x[a];
+    if (ta[a] == t) hit |= 1 << a;
   }
   return true;
 }
@@ -424,16 +412,19 @@ __device__ __forceinline__ NewtonOut newton_warp(const double* __restrict__ sX,
       for (int a = 0; a < DR; ++a)
         if ((r[a] == 1.0 && st.J[a] < 0.0) || (r[a] == -1.0 && st.J[a] > 0.0)) freem[a] = false;
       double Hm[6], s[3] = {0.0, 0.0, 0.0};
+      bool fr[3] = {freem[0], freem[1], freem[2]};
+      int hit = 0;
       bool ok = false;
       if (beta) {
 #pragma unroll
         for (int m = 0; m < 6; ++m) Hm[m] = st.H0[m] - st.Q[m];
-        ok = constrained_step<DR>(Hm, st.J, r, freem, alpha, s);
+        ok = constrained_step<DR>(Hm, st.J, r, fr, alpha, s, hit);
       }
       if (!ok) {
 #pragma unroll
         for (int m = 0; m < 6; ++m) Hm[m] = st.H0[m];
-        if (!constrained_step<DR>(Hm, st.J, r, freem, alpha, s)) {
+        fr[0] = freem[0]; fr[1] = freem[1]; fr[2] = freem[2];
+        if (!constrained_step<DR>(Hm, st.J, r, fr, alpha, s, hit)) {
           double tr = 0.0;
 #pragma unroll
           for (int a = 0; a < DR; ++a) tr += st.H0[a];
@@ -441,7 +432,8 @@ __device__ __forceinline__ NewtonOut newton_warp(const double* __restrict__ sX,
           if (!(lam > 0.0)) lam = 1e-300;
 #pragma unroll
           for (int a = 0; a < DR; ++a) Hm[a] = st.H0[a] + lam;
-          if (!constrained_step<DR>(Hm, st.J, r, freem, alpha, s))
+          fr[0] = freem[0]; fr[1] = freem[1]; fr[2] = freem[2];
+          if (!constrained_step<DR>(Hm, st.J, r, fr, alpha, s, hit))
 #pragma unroll
             for (int a = 0; a < DR; ++a) s[a] = 0.0;
         }
@@ -466,8 +458,7 @@ __device__ __forceinline__ NewtonOut newton_warp(const double* __restrict__ sX,
 #pragma unroll
         for (int a = 0; a < DR; ++a) {
           double v = r[a] + s[a];
-          if (s[a] == -1.0 - r[a]) v = -1.0;
-          if (s[a] == 1.0 - r[a]) v = 1.0;
+          if (hit & (1 << a)) v = s[a] > 0.0 ? 1.0 : -1.0;  // lands on the face
           v = v < -1.0 ? -1.0 : (v > 1.0 ? 1.0 : v);
           rn[a] = v;
         }
@@ -623,7 +614,7 @@ __device__ __forceinline__ int64_t warp_sum64(int64_t v) {
 // single-candidate points (fused field evaluation); otherwise a tentative
 // BORDER record and the point joins the exhaustive round 2.
 template <int D, int DR, int N>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
     k_newton_round1(fpx_mesh_t m, const double* __restrict__ x, const int32_t* __restrict__ sorted,
                     const Item* __restrict__ items, const int64_t* __restrict__ nitems_dev,
                     const int32_t* __restrict__ npass, int32_t* code, int32_t* elem, double* r,
@@ -705,7 +696,7 @@ __global__ void __launch_bounds__(128)
 
 // Round 2 (and fpx_invert_pairs): Newton per explicit (point, element) pair.
 template <int D, int DR, int N>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
     k_newton_pairs(fpx_mesh_t m, const double* __restrict__ x, const int32_t* __restrict__ pair_pt,
                    const int32_t* __restrict__ sorted, const Item* __restrict__ items,
                    const int64_t* __restrict__ nitems_dev, int32_t* pcode, double* pr,

@@ -42,6 +42,7 @@ class EngineOptions:
     eps_d: float | None = None        # absolute surface threshold; None -> relative
     eps_d_rel: float = 1e-10
     pair_capacity: float = 2.0        # round-2 pair workspace, x n (grows on demand)
+    hash_refine: int = 2              # local cells per axis = hash_refine * SPEC rule (perf only)
 
 
 @dataclass
@@ -159,7 +160,8 @@ def setup(nodes, order: int | None = None, ref_dim: int | None = None, *,
     S.obb_ok, S.frame, S.hbox = bx["obb_ok"], bx["frame"], bx["hbox"]
     # Psi_L over the hash boxes (decision D5)
     from .spatial_hash import build_local_map
-    lmap = build_local_map(S.hbox, opt.cells_local or n_cells(E, d))
+    lmap = build_local_map(S.hbox, opt.cells_local or min(1024, opt.hash_refine * n_cells(E, d)),
+                           obbs=(S.obb_c, S.obb_inv, S.obb_ok))
     S.local_map = lmap
     S.grid_dev, S.offsets, S.elems, S.ncell, S.max_list = \
         lmap.grid_dev, lmap.offsets, lmap.elems if lmap.entries else \

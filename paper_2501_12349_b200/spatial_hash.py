@@ -109,10 +109,13 @@ class LocalMap:
         return lookup_local(self, x)
 
 
-def build_local_map(boxes, cells_per_axis: int | None = None) -> LocalMap:
+def build_local_map(boxes, cells_per_axis: int | None = None, obbs=None) -> LocalMap:
     """Psi_L over element boxes [E, 2, d]: grid spans the
     union of the boxes; each box maps to the rectangular cell range between
-    its corner cells; lists ascending.  Runs on the device."""
+    its corner cells; lists ascending.  With `obbs` = (obb_c, obb_inv, obb_ok)
+    device tensors, cells that cannot meet an element's OBB are dropped
+    (decision D5b; the AABB-and-OBB filtered candidates are unchanged).  Runs
+    on the device."""
     dev = _C.require_cuda()
     boxes = torch.as_tensor(boxes, dtype=torch.float64).to(dev).contiguous()
     if boxes.ndim != 3 or boxes.shape[1] != 2 or boxes.shape[0] < 1:
@@ -127,11 +130,14 @@ def build_local_map(boxes, cells_per_axis: int | None = None) -> LocalMap:
     need = np.zeros(1, np.int64)
     maxl = np.zeros(1, np.int32)
     st = _C.stream_handle()
-    _C.check(L.fpx_hash_build(d, E, _C.ptr(boxes), n, _C.ptr(grid), _C.ptr(offsets), None, 0,
-                              need.ctypes.data, maxl.ctypes.data, _C.ptr(ws), wsb, st),
+    oc, oi, ok = (None, None, None) if obbs is None else \
+        tuple(t.to(dev).contiguous() for t in obbs)
+    ob = (_C.ptr(oc), _C.ptr(oi), _C.ptr(ok))
+    _C.check(L.fpx_hash_build(d, E, _C.ptr(boxes), *ob, n, _C.ptr(grid), _C.ptr(offsets), None,
+                              0, need.ctypes.data, maxl.ctypes.data, _C.ptr(ws), wsb, st),
              "fpx_hash_build(count)")
     elems = torch.empty(max(int(need[0]), 1), dtype=torch.int32, device=dev)
-    _C.check(L.fpx_hash_build(d, E, _C.ptr(boxes), n, _C.ptr(grid), _C.ptr(offsets),
+    _C.check(L.fpx_hash_build(d, E, _C.ptr(boxes), *ob, n, _C.ptr(grid), _C.ptr(offsets),
                               _C.ptr(elems), elems.numel(), need.ctypes.data, maxl.ctypes.data,
                               _C.ptr(ws), wsb, st), "fpx_hash_build(fill)")
     g = CartesianGrid.from_packed(grid.cpu().numpy(), d, n)

@@ -35,8 +35,11 @@ def assert_find_parity(S, OS, x, field=None, rtol_val=1e-10):
     elem = rec.elem.cpu().numpy()
     r = rec.r.cpu().numpy()
     dist = rec.dist.cpu().numpy()
-    assert np.array_equal(code, orec["code"]), \
-        f"code mismatches: {np.sum(code != orec['code'])}"
+    bad = np.nonzero(code != orec["code"])[0]
+    assert bad.size == 0, f"code mismatches: {bad.size}\n" + "\n".join(
+        f"x={x[i].tolist()} gpu=({code[i]},{elem[i]},{r[i].tolist()},{dist[i]:.3e}) "
+        f"oracle=({orec['code'][i]},{orec['elem'][i]},{orec['r'][i].tolist()},"
+        f"{orec['dist'][i]:.3e},ncand={orec['ncand'][i]})" for i in bad[:5])
     diff = elem != orec["elem"]
     # either owner accepted only on a shared face: both records at d* ~ 0
     # with r on the boundary
@@ -44,7 +47,11 @@ def assert_find_parity(S, OS, x, field=None, rtol_val=1e-10):
         onface = (np.abs(dist[diff]) < 1e-10) & (orec["dist"][diff] < 1e-10) & \
             (np.any(np.abs(np.abs(r[diff]) - 1) < 1e-10, axis=1) |
              np.any(np.abs(np.abs(orec["r"][diff]) - 1) < 1e-10, axis=1))
-        assert onface.all(), f"{(~onface).sum()} element mismatches off shared faces"
+        idx = np.nonzero(diff)[0][~onface]
+        assert onface.all(), f"{(~onface).sum()} element mismatches off shared faces\n" + \
+            "\n".join(f"x={x[i].tolist()} gpu=({code[i]},{elem[i]},{r[i].tolist()},{dist[i]:.3e}) "
+                      f"oracle=({orec['code'][i]},{orec['elem'][i]},{orec['r'][i].tolist()},"
+                      f"{orec['dist'][i]:.3e})" for i in idx[:6])
     same = ~diff
     inter = same & (code == 0)
     if inter.any():
