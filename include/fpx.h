@@ -92,14 +92,15 @@ typedef struct fpx_mesh_t {
 #define FPX_STAT_BOXTESTS 1      /* candidate box tests (hash-list entries) */
 #define FPX_STAT_NEWTON 2        /* Newton-ed (point, element) candidates */
 #define FPX_STAT_ITERS 3         /* Newton iterations over all candidates */
-#define FPX_STAT_ROUND2_POINTS 4 /* points needing the exhaustive round */
-#define FPX_STAT_ROUND2_PAIRS 5  /* (point, element) pairs in round 2 */
+#define FPX_STAT_ROUND2_POINTS 4 /* points unresolved after round 1 (next-best round 2) */
+#define FPX_STAT_ROUND2_PAIRS 5  /* (point, element) pairs in rounds 2 and 3 */
 #define FPX_STAT_OVERFLOW 6      /* pairs dropped for lack of workspace (>0: rerun) */
 #define FPX_STAT_EVALS 7         /* fused field evaluations */
 #define FPX_STAT_NEWTON_R1 8     /* Newton solves in the round-1 (best-first) kernel */
 #define FPX_STAT_ITERS_R1 9      /* their iterations */
 #define FPX_STAT_EVALS_R1 10     /* field evaluations fused into the round-1 kernel */
-#define FPX_STATS_LEN 11
+#define FPX_STAT_ROUND3_POINTS 11 /* points needing the exhaustive round 3 */
+#define FPX_STATS_LEN 12
 
 int fpx_abi_version(void);
 const char* fpx_last_error(void);
@@ -160,7 +161,7 @@ int fpx_cell_of(const fpx_mesh_t* m, int64_t n, const double* x, int64_t* cell, 
  * (NaN for NOT_FOUND).  iters (optional) = Newton iterations per point.
  * stats: device int64[FPX_STATS_LEN] (zeroed by the call).
  * ws: fpx_find_workspace_bytes(m->E, n, pair_cap). */
-size_t fpx_find_workspace_bytes(int64_t E, int64_t n, int64_t pair_cap);
+size_t fpx_find_workspace_bytes(const fpx_mesh_t* m, int64_t n, int64_t pair_cap);
 int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int32_t* elem,
              double* r, double* dist, int32_t* iters, const double* field, int C,
              double* values, int64_t* stats, int64_t pair_cap, void* ws, size_t ws_bytes,

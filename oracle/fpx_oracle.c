@@ -867,7 +867,7 @@ static const int SYM[3][3] = {{0, 3, 4}, {3, 1, 5}, {4, 5, 2}};
 /* Cholesky solve of the principal submatrix A[idx][idx] (n <= 3), pivot
  * test p > 1e-14 |trace| (decision D8: non-positive pivot -> not PD). */
 static int chol_solve(int n, const int* idx, const double A[3][3], const double* b, double* x) {
-  double L[3][3] = {{0}}, y[3];
+  double L[3][3] = {{0}}, y[3], iL[3];
   double tr = 0.0;
   for (int k = 0; k < n; ++k) tr += A[idx[k]][idx[k]];
   double thr = 1e-14 * fabs(tr);
@@ -876,21 +876,22 @@ static int chol_solve(int n, const int* idx, const double A[3][3], const double*
     for (int m = 0; m < k; ++m) s -= L[k][m] * L[k][m];
     if (!(s > thr)) return -1;
     L[k][k] = sqrt(s);
+    iL[k] = 1.0 / L[k][k];
     for (int i = k + 1; i < n; ++i) {
       double t = A[idx[i]][idx[k]];
       for (int m = 0; m < k; ++m) t -= L[i][m] * L[k][m];
-      L[i][k] = t / L[k][k];
+      L[i][k] = t * iL[k];
     }
   }
   for (int k = 0; k < n; ++k) {
     double t = b[k];
     for (int m = 0; m < k; ++m) t -= L[k][m] * y[m];
-    y[k] = t / L[k][k];
+    y[k] = t * iL[k];
   }
   for (int k = n - 1; k >= 0; --k) {
     double t = y[k];
     for (int m = k + 1; m < n; ++m) t -= L[m][k] * x[m];
-    x[k] = t / L[k][k];
+    x[k] = t * iL[k];
   }
   return 0;
 }
@@ -963,7 +964,7 @@ void fpxo_invert(const fpxo_basis* B, int d, int dr, const double* X, const doub
   int bi = 0;
   for (int n = 0; n < K; ++n) {
     double dd = 0.0;
-    for (int c = 0; c < d; ++c) { double t = xs[c] - X[c * K + n]; dd += t * t; }
+    for (int c = 0; c < d; ++c) { double t = xs[c] - X[c * K + n]; dd = fma(t, t, dd); }
     if (dd < best) { best = dd; bi = n; }
   }
   double r[3] = {0, 0, 0};

@@ -18,7 +18,7 @@ ABI_VERSION = 1
 
 INTERIOR, BORDER, NOT_FOUND = 0, 1, 2
 STAT_NAMES = ["points", "box_tests", "newton", "iters", "round2_points", "round2_pairs",
-              "overflow", "evals", "newton_r1", "iters_r1", "evals_r1"]
+              "overflow", "evals", "newton_r1", "iters_r1", "evals_r1", "round3_points"]
 STATS_LEN = len(STAT_NAMES)
 
 P = C.c_void_p
@@ -71,7 +71,7 @@ def lib():
         "fpx_hash_workspace_bytes": ([i32, i64, i32], sz),
         "fpx_hash_build": ([i32, i64, P, P, P, P, i32, P, P, P, i64, P, P, P, sz, P], i32),
         "fpx_cell_of": ([C.POINTER(MeshT), i64, P, P, P], i32),
-        "fpx_find_workspace_bytes": ([i64, i64, i64], sz),
+        "fpx_find_workspace_bytes": ([C.POINTER(MeshT), i64, i64], sz),
         "fpx_find": ([C.POINTER(MeshT), i64, P, P, P, P, P, P, P, i32, P, P, i64, P, sz, P], i32),
         "fpx_eval_workspace_bytes": ([i64, i64], sz),
         "fpx_findpts_eval": ([i32, i32, P, i32, i64, P, i64, P, P, P, P, P, sz, P], i32),

@@ -132,21 +132,40 @@ struct Group {
 };
 
 struct FindWs {
-  int32_t *best, *npass, *upts;
-  int64_t *upair_cnt, *pair_off, *nun, *npairs;
+  int32_t *best, *npass, *upts, *upts3, *tried2;
+  int64_t *upair_cnt, *pair_off, *nun, *nun3, *npairs;
   int32_t *pair_pt, *pair_elem, *pcode, *piters;
   double *pr, *pdist;
   Group g1, g2;
   void* scan2_temp;
   size_t scan2_bytes;
+  // point ordering by hash cell
+  int32_t *cellid, *cell_count, *cell_off, *cell_cursor, *order;
+  void* scan3_temp;
+  size_t scan3_bytes;
+  int64_t ncells;
+  void carve_cells(Carver& c, int64_t n, int64_t nc) {
+    ncells = nc;
+    cellid = c.take<int32_t>(n);
+    cell_count = c.take<int32_t>(nc + 2);
+    cell_off = c.take<int32_t>(nc + 2);
+    cell_cursor = c.take<int32_t>(nc + 2);
+    order = c.take<int32_t>(n);
+    scan3_bytes = scan_temp_i32(nc + 2);
+    scan3_temp = c.take<char>(scan3_bytes);
+  }
   void carve(Carver& c, int64_t E, int64_t n, int64_t cap) {
     best = c.take<int32_t>(n);
     npass = c.take<int32_t>(n);
     upts = c.take<int32_t>(n);
+    upts3 = c.take<int32_t>(n);
+    tried2 = c.take<int32_t>(n);
     upair_cnt = c.take<int64_t>(n + 1);
     pair_off = c.take<int64_t>(n + 1);
     nun = c.take<int64_t>(1);
+    nun3 = c.take<int64_t>(1);
     npairs = c.take<int64_t>(1);
+    if (cap < n) cap = n;   // the next-best round needs one pair per point
     pair_pt = c.take<int32_t>(cap);
     pair_elem = c.take<int32_t>(cap);
     pcode = c.take<int32_t>(cap);
@@ -161,12 +180,14 @@ struct FindWs {
 };
 
 __global__ void k_pairs_total(const int64_t* __restrict__ pair_off, const int64_t* __restrict__ nun,
-                              int64_t cap, int64_t* npairs, int64_t* stats, int64_t n) {
-  const int64_t t = pair_off[*nun];
+                              const int64_t* __restrict__ nun3, int64_t cap, int64_t* npairs,
+                              int64_t* stats, int64_t n) {
+  const int64_t t = pair_off[*nun3];
   *npairs = t < cap ? t : cap;
   stats[FPX_STAT_POINTS] = n;
-  stats[FPX_STAT_ROUND2_POINTS] = *nun;
-  stats[FPX_STAT_ROUND2_PAIRS] = t;
+  stats[FPX_STAT_ROUND2_POINTS] = *nun;    // after round 1
+  stats[FPX_STAT_ROUND3_POINTS] = *nun3;   // after round 2
+  stats[FPX_STAT_ROUND2_PAIRS] = t + *nun; // next-best pairs + exhaustive pairs
 }
 
 __global__ void k_count_elems(int64_t n, const int32_t* __restrict__ elem, int32_t* count) {
@@ -365,10 +386,17 @@ int fpx_cell_of(const fpx_mesh_t* m, int64_t n, const double* x, int64_t* cell, 
   return FPX_OK;
 }
 
-size_t fpx_find_workspace_bytes(int64_t E, int64_t n, int64_t pair_cap) {
+static int64_t cells_of(const fpx_mesh_t* m) {
+  int64_t nc = 1;
+  for (int c = 0; c < m->d; ++c) nc *= m->ncell;
+  return nc;
+}
+
+size_t fpx_find_workspace_bytes(const fpx_mesh_t* m, int64_t n, int64_t pair_cap) {
   Carver c(nullptr, 0);
   FindWs w;
-  w.carve(c, E, n > 0 ? n : 1, pair_cap > 0 ? pair_cap : 1);
+  w.carve(c, m->E, n > 0 ? n : 1, pair_cap > 0 ? pair_cap : 1);
+  w.carve_cells(c, n > 0 ? n : 1, cells_of(m));
   return c.off + 256;
 }
 
@@ -381,6 +409,7 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
   if (n < 0 || n > INT32_MAX) return fail(FPX_EINVAL, "bad point count %lld", (long long)n);
   if (!stats) return fail(FPX_EINVAL, "stats buffer required");
   if (field && (C < 1 || !values)) return fail(FPX_EINVAL, "field given without C/values");
+  if (pair_cap < n) pair_cap = n;   // matches FindWs::carve
   if (pair_cap < 1) pair_cap = 1;
   cudaStream_t st = S(stream);
   FPX_CK(cudaMemsetAsync(stats, 0, sizeof(int64_t) * FPX_STATS_LEN, st));
@@ -389,11 +418,24 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
   Carver cv(ws, ws_bytes);
   FindWs w;
   w.carve(cv, E, n, pair_cap);
+  w.carve_cells(cv, n, cells_of(m));
   if (!cv.ok()) return fail(FPX_EINVAL, "find workspace too small (%zu < %zu)", ws_bytes, cv.off);
   const fpx_mesh_t& M = *m;
+  // --- order the points by hash cell (counting sort)
+  const int64_t nc = w.ncells;
+  FPX_CK(cudaMemsetAsync(w.cell_count, 0, sizeof(int32_t) * (nc + 2), st));
+  FPX_LAUNCH(fpx::launch_point_cells(M, n, x, w.cellid, w.cell_count, st));
+  {
+    size_t tb3 = w.scan3_bytes;
+    FPX_CK(cub::DeviceScan::ExclusiveSum(w.scan3_temp, tb3, w.cell_count, w.cell_off,
+                                         (int)(nc + 2), st));
+  }
+  FPX_CK(cudaMemsetAsync(w.cell_cursor, 0, sizeof(int32_t) * (nc + 2), st));
+  FPX_LAUNCH(fpx::launch_point_scatter(n, w.cellid, w.cell_off, w.cell_cursor, w.order, st));
   // --- prefilter: hash lookup + AABB/OBB filter + best-first candidate
   FPX_CK(cudaMemsetAsync(w.g1.count, 0, sizeof(int32_t) * E, st));
-  FPX_LAUNCH(fpx::launch_find_prefilter(M, n, x, w.best, w.npass, code, elem, r, dist, iters,
+  FPX_LAUNCH(fpx::launch_find_prefilter(M, n, x, w.order, w.cellid, w.best, w.npass, code, elem,
+                                        r, dist, iters,
                                     field ? values : nullptr, C, w.g1.count, stats, st));
   // --- round 1: group by best-first element, Newton, fused eval
   g_launches += 3;
@@ -405,22 +447,37 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
                                    w.npass, code, elem, r, dist, iters, field, C, values, w.upts,
                                    w.upair_cnt, w.nun, stats, st));
   if (g_prof_stop) FPX_CK(cudaEventRecord(g_prof_stop, st));
-  // --- round 2: every other passing candidate of the unresolved points
+  // --- round 2: the next best-first candidate of every unresolved point
+  FPX_CK(cudaMemsetAsync(w.g2.count, 0, sizeof(int32_t) * E, st));
+  FPX_LAUNCH(fpx::launch_round_next_emit(M, n, w.nun, w.upts, x, w.best, w.tried2, w.pair_pt,
+                                         w.pair_elem, w.g2.count, st));
+  g_launches += 3;
+  FPX_CK(w.g2.build(E, n, w.nun, w.pair_elem, nullptr, st));
+  FPX_LAUNCH(fpx::launch_newton_pairs(M, x, w.pair_pt, w.g2.sorted, w.g2.items, w.g2.nitems,
+                                      w.g2.items_cap, w.pcode, w.pr, w.pdist, w.piters, stats, st));
+  FPX_CK(cudaMemsetAsync(w.upair_cnt, 0, sizeof(int64_t) * (n + 1), st));
+  FPX_CK(cudaMemsetAsync(w.nun3, 0, sizeof(int64_t), st));
+  FPX_LAUNCH(fpx::launch_round2_finalize(M, n, w.nun, w.upts, nullptr, pair_cap, w.pair_elem,
+                                         w.pcode, w.pr, w.pdist, w.piters, code, elem, r, dist,
+                                         iters, field, C, values, w.npass, 2, w.upts3,
+                                         w.upair_cnt, w.nun3, stats, st));
+  // --- round 3: every remaining passing candidate of the still unresolved
   size_t tb = w.scan2_bytes;
   FPX_CK(cub::DeviceScan::ExclusiveSum(w.scan2_temp, tb, w.upair_cnt, w.pair_off, (int)(n + 1), st));
   FPX_CK(cudaMemsetAsync(w.g2.count, 0, sizeof(int32_t) * E, st));
-  FPX_LAUNCH(fpx::launch_round2_emit(M, n, w.nun, w.upts, x, w.best, w.pair_off, pair_cap, w.pair_pt,
-                                 w.pair_elem, w.g2.count, stats, st));
+  FPX_LAUNCH(fpx::launch_round2_emit(M, n, w.nun3, w.upts3, x, w.best, w.tried2, w.pair_off,
+                                     pair_cap, w.pair_pt, w.pair_elem, w.g2.count, stats, st));
   g_launches += 1;
-  k_pairs_total<<<1, 1, 0, st>>>(w.pair_off, w.nun, pair_cap, w.npairs, stats, n);
+  k_pairs_total<<<1, 1, 0, st>>>(w.pair_off, w.nun, w.nun3, pair_cap, w.npairs, stats, n);
   FPX_CK(cudaGetLastError());
   g_launches += 3;
   FPX_CK(w.g2.build(E, pair_cap, w.npairs, w.pair_elem, nullptr, st));
   FPX_LAUNCH(fpx::launch_newton_pairs(M, x, w.pair_pt, w.g2.sorted, w.g2.items, w.g2.nitems,
-                                  w.g2.items_cap, w.pcode, w.pr, w.pdist, w.piters, stats, st));
-  FPX_LAUNCH(fpx::launch_round2_finalize(M, n, w.nun, w.upts, w.pair_off, pair_cap, w.pair_elem,
-                                     w.pcode, w.pr, w.pdist, w.piters, code, elem, r, dist, iters,
-                                     field, C, values, stats, st));
+                                      w.g2.items_cap, w.pcode, w.pr, w.pdist, w.piters, stats, st));
+  FPX_LAUNCH(fpx::launch_round2_finalize(M, n, w.nun3, w.upts3, w.pair_off, pair_cap, w.pair_elem,
+                                         w.pcode, w.pr, w.pdist, w.piters, code, elem, r, dist,
+                                         iters, field, C, values, w.npass, 0, nullptr, nullptr,
+                                         nullptr, stats, st));
   return FPX_OK;
 }
 

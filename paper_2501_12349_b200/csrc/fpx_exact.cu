@@ -726,23 +726,79 @@ __device__ __forceinline__ bool obb_in(int d, const double* __restrict__ cen,
   return true;
 }
 
-// Candidate loop of engine.find Phase A up to the Newton solve: for each
-// point, the hash list (ascending ids), the AABB then OBB filter.  Emits the
-// best-first candidate (smallest |J_c^{-1}(x - x_c)|_inf, ties -> lower id)
-// and the number of candidates that passed.  Points with none are final
-// NOT_FOUND.
-__global__ void k_find_prefilter(fpx_mesh_t m, int64_t n, const double* __restrict__ x,
-                                 int32_t* best, int32_t* npass, int32_t* code, int32_t* elem,
-                                 double* r, double* dist, int32_t* iters, double* values, int C,
-                                 int32_t* elem_count, int64_t* stats) {
-  const int d = m.d, dr = m.dr;
-  int64_t boxtests = 0;
+// Best-first value of candidate e at x: |J_c^{-1}(x - x_c)|_inf.
+__device__ __forceinline__ double bestfirst_value(int d, const double* __restrict__ fr,
+                                                  const double* x) {
+  double dx[3];
+  for (int c = 0; c < d; ++c) dx[c] = x[c] - fr[c];
+  double v = 0.0;
+  for (int c = 0; c < d; ++c) {
+    double y = 0.0;
+    for (int b = 0; b < d; ++b) y += fr[d + c * d + b] * dx[b];
+    v = fabs(y) > v ? fabs(y) : v;
+  }
+  return v;
+}
+
+// Point ordering by hash cell (counting sort): adjacent lanes of the
+// prefilter then walk the same candidate lists and read the same element
+// records.  Points outside the grid go to the extra bucket `ncells`.
+__global__ void k_point_cells(fpx_mesh_t m, int64_t n, const double* __restrict__ x,
+                              int32_t* cellid, int32_t* cell_count) {
+  const int d = m.d;
+  int64_t nc = 1;
+  for (int c = 0; c < d; ++c) nc *= m.ncell;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * blockDim.x) {
     double xx[3] = {0, 0, 0};
     for (int c = 0; c < d; ++c) xx[c] = x[k * d + c];
     int ax[3];
     int64_t cell = cell_of(d, m.grid, m.ncell, xx, ax);
+    if (cell < 0) cell = nc;
+    cellid[k] = (int32_t)cell;
+    atomicAdd(&cell_count[cell], 1);
+  }
+}
+
+__global__ void k_point_scatter(int64_t n, const int32_t* __restrict__ cellid,
+                                const int32_t* __restrict__ cell_off, int32_t* cursor,
+                                int32_t* order) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int c = cellid[k];
+    const int slot = atomicAdd(&cursor[c], 1);
+    order[cell_off[c] + slot] = (int32_t)k;
+  }
+}
+
+// Candidate loop of engine.find Phase A up to the Newton solve: for each
+// point, the hash list (ascending ids), the AABB then OBB filter.  Emits the
+// best-first candidate (smallest |J_c^{-1}(x - x_c)|_inf, ties -> lower id)
+// and the number of candidates that passed.  Points with none are final
+// NOT_FOUND.
+__global__ void k_find_prefilter(fpx_mesh_t m, int64_t n, const double* __restrict__ x,
+                                 const int32_t* __restrict__ order,
+                                 const int32_t* __restrict__ cellid, int32_t* best,
+                                 int32_t* npass, int32_t* code, int32_t* elem, double* r,
+                                 double* dist, int32_t* iters, double* values, int C,
+                                 int32_t* elem_count, int64_t* stats) {
+  const int d = m.d, dr = m.dr;
+  int64_t nc = 1;
+  for (int c = 0; c < d; ++c) nc *= m.ncell;
+  int64_t boxtests = 0;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = order ? order[t] : t;
+    double xx[3] = {0, 0, 0};
+    for (int c = 0; c < d; ++c) xx[c] = x[k * d + c];
+    int ax[3];
+    int64_t cell;
+    if (cellid) {
+      cell = cellid[k];
+      if (cell == nc) cell = -1;
+    } else {
+      cell = cell_of(d, m.grid, m.ncell, xx, ax);
+    }
     int cnt = 0, bst = -1;
     double bval = INFINITY;
     if (cell >= 0) {
@@ -754,15 +810,7 @@ __global__ void k_find_prefilter(fpx_mesh_t m, int64_t n, const double* __restri
         if (m.obb_ok[e] && !obb_in(d, m.obb_c + (int64_t)e * d, m.obb_inv + (int64_t)e * d * d, xx))
           continue;
         ++cnt;
-        const double* fr = m.frame + (int64_t)e * (d + d * d);
-        double dx[3];
-        for (int c = 0; c < d; ++c) dx[c] = xx[c] - fr[c];
-        double v = 0.0;
-        for (int c = 0; c < d; ++c) {
-          double y = 0.0;
-          for (int b = 0; b < d; ++b) y += fr[d + c * d + b] * dx[b];
-          v = fabs(y) > v ? fabs(y) : v;
-        }
+        const double v = bestfirst_value(d, m.frame + (int64_t)e * (d + d * d), xx);
         if (v < bval) {  // strict: ties keep the lower (earlier) id
           bval = v;
           bst = e;
@@ -792,9 +840,52 @@ __global__ void k_find_prefilter(fpx_mesh_t m, int64_t n, const double* __restri
 // Round 2 emit: for every unresolved point, the passing candidates other
 // than its round-1 element, written contiguously at pair_off (point order),
 // and counted per element.
+// Round 2 emit: the next best-first candidate (smallest value, ties -> lower
+// id) of every unresolved point other than its round-1 element; one pair per
+// point at index u.
+__global__ void k_round_next_emit(fpx_mesh_t m, const int64_t* __restrict__ nun_dev,
+                                  const int32_t* __restrict__ upts, const double* __restrict__ x,
+                                  const int32_t* __restrict__ best, int32_t* tried2,
+                                  int32_t* pair_pt, int32_t* pair_elem, int32_t* elem_count) {
+  const int d = m.d;
+  const int64_t nun = *nun_dev;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < nun;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const int k = upts[u];
+    double xx[3] = {0, 0, 0};
+    for (int c = 0; c < d; ++c) xx[c] = x[(int64_t)k * d + c];
+    int ax[3];
+    const int64_t cell = cell_of(d, m.grid, m.ncell, xx, ax);
+    const int skip = best[k];
+    int bst = -1;
+    double bval = INFINITY;
+    const int s = m.offsets[cell], t = m.offsets[cell + 1];
+    for (int q = s; q < t; ++q) {
+      const int e = m.elems[q];
+      if (e == skip) continue;
+      if (!aabb_in(d, m.aabb + (int64_t)e * 2 * d, xx)) continue;
+      if (m.obb_ok[e] && !obb_in(d, m.obb_c + (int64_t)e * d, m.obb_inv + (int64_t)e * d * d, xx))
+        continue;
+      const double v = bestfirst_value(d, m.frame + (int64_t)e * (d + d * d), xx);
+      if (v < bval) {
+        bval = v;
+        bst = e;
+      }
+    }
+    tried2[k] = bst;
+    pair_pt[u] = k;
+    pair_elem[u] = bst;
+    if (bst >= 0) atomicAdd(&elem_count[bst], 1);
+  }
+}
+
+// Round 3 emit: every remaining passing candidate (not the round-1 or
+// round-2 element) of the points still unresolved, written contiguously at
+// pair_off (point order) and counted per element.
 __global__ void k_round2_emit(fpx_mesh_t m, const int64_t* __restrict__ nun_dev,
                               const int32_t* __restrict__ upts,
                               const double* __restrict__ x, const int32_t* __restrict__ best,
+                              const int32_t* __restrict__ skip2,
                               const int64_t* __restrict__ pair_off, int64_t pair_cap,
                               int32_t* pair_pt, int32_t* pair_elem, int32_t* elem_count,
                               int64_t* stats) {
@@ -810,10 +901,11 @@ __global__ void k_round2_emit(fpx_mesh_t m, const int64_t* __restrict__ nun_dev,
     int64_t cell = cell_of(d, m.grid, m.ncell, xx, ax);
     int64_t o = pair_off[u];
     const int skip = best[k];
+    const int skipb = skip2 ? skip2[k] : -1;
     const int s = m.offsets[cell], t = m.offsets[cell + 1];
     for (int q = s; q < t; ++q) {
       const int e = m.elems[q];
-      if (e == skip) continue;
+      if (e == skip || e == skipb) continue;
       if (!aabb_in(d, m.aabb + (int64_t)e * 2 * d, xx)) continue;
       if (m.obb_ok[e] && !obb_in(d, m.obb_c + (int64_t)e * d, m.obb_inv + (int64_t)e * d * d, xx))
         continue;
@@ -911,22 +1003,43 @@ cudaError_t launch_cell_of(int d, const double* grid, int n, int64_t npts, const
   k_cell_of<<<grid_for(npts, 256), 256, 0, st>>>(d, grid, n, npts, x, cell);
   return cudaGetLastError();
 }
-cudaError_t launch_find_prefilter(const fpx_mesh_t& m, int64_t n, const double* x, int32_t* best,
+cudaError_t launch_find_prefilter(const fpx_mesh_t& m, int64_t n, const double* x,
+                                  const int32_t* order, const int32_t* cellid, int32_t* best,
                                   int32_t* npass, int32_t* code, int32_t* elem, double* r,
                                   double* dist, int32_t* iters, double* values, int C,
                                   int32_t* elem_count, int64_t* stats, cudaStream_t st) {
-  k_find_prefilter<<<grid_for(n, 256), 256, 0, st>>>(m, n, x, best, npass, code, elem, r, dist,
-                                                     iters, values, C, elem_count, stats);
+  k_find_prefilter<<<grid_for(n, 256), 256, 0, st>>>(m, n, x, order, cellid, best, npass, code,
+                                                     elem, r, dist, iters, values, C, elem_count,
+                                                     stats);
+  return cudaGetLastError();
+}
+cudaError_t launch_point_cells(const fpx_mesh_t& m, int64_t n, const double* x, int32_t* cellid,
+                               int32_t* cell_count, cudaStream_t st) {
+  k_point_cells<<<grid_for(n, 256), 256, 0, st>>>(m, n, x, cellid, cell_count);
+  return cudaGetLastError();
+}
+cudaError_t launch_point_scatter(int64_t n, const int32_t* cellid, const int32_t* cell_off,
+                                 int32_t* cursor, int32_t* order, cudaStream_t st) {
+  k_point_scatter<<<grid_for(n, 256), 256, 0, st>>>(n, cellid, cell_off, cursor, order);
   return cudaGetLastError();
 }
 cudaError_t launch_round2_emit(const fpx_mesh_t& m, int64_t nun_cap, const int64_t* nun_dev,
                                const int32_t* upts, const double* x, const int32_t* best,
-                               const int64_t* pair_off, int64_t pair_cap, int32_t* pair_pt,
-                               int32_t* pair_elem, int32_t* elem_count, int64_t* stats,
-                               cudaStream_t st) {
-  k_round2_emit<<<grid_for(nun_cap, 128), 128, 0, st>>>(m, nun_dev, upts, x, best, pair_off,
-                                                        pair_cap, pair_pt, pair_elem, elem_count,
-                                                        stats);
+                               const int32_t* skip2, const int64_t* pair_off, int64_t pair_cap,
+                               int32_t* pair_pt, int32_t* pair_elem, int32_t* elem_count,
+                               int64_t* stats, cudaStream_t st) {
+  k_round2_emit<<<grid_for(nun_cap, 128), 128, 0, st>>>(m, nun_dev, upts, x, best, skip2,
+                                                        pair_off, pair_cap, pair_pt, pair_elem,
+                                                        elem_count, stats);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_round_next_emit(const fpx_mesh_t& m, int64_t nun_cap, const int64_t* nun_dev,
+                                   const int32_t* upts, const double* x, const int32_t* best,
+                                   int32_t* tried2, int32_t* pair_pt, int32_t* pair_elem,
+                                   int32_t* elem_count, cudaStream_t st) {
+  k_round_next_emit<<<grid_for(nun_cap, 128), 128, 0, st>>>(m, nun_dev, upts, x, best, tried2,
+                                                            pair_pt, pair_elem, elem_count);
   return cudaGetLastError();
 }
 

@@ -72,10 +72,13 @@ cudaError_t launch_round2_finalize(const fpx_mesh_t& m, int64_t nun_cap, const i
                                    const int32_t* pcode, const double* pr, const double* pdist,
                                    const int32_t* piters, int32_t* code, int32_t* elem, double* r,
                                    double* dist, int32_t* iters, const double* field, int C,
-                                   double* values, int64_t* stats, cudaStream_t st) {
+                                   double* values, const int32_t* npass, int min_pass,
+                                   int32_t* next_upts, int64_t* next_cnt, int64_t* nnext,
+                                   int64_t* stats, cudaStream_t st) {
   return dispatch<Finalize>(m.d, m.dr, m.N, m, nun_cap, nun_dev, upts, pair_off, pair_cap,
                             pair_elem, pcode, pr, pdist, piters, code, elem, r, dist, iters,
-                            field, C, values, stats, st);
+                            field, C, values, npass, min_pass, next_upts, next_cnt, nnext, stats,
+                            st);
 }
 
 cudaError_t launch_forward_map(const fpx_mesh_t& m, int64_t n, const int32_t* elem,

@@ -221,7 +221,7 @@ __device__ __forceinline__ int symi(int a, int b) {
 template <int DR>
 __device__ __forceinline__ bool chol_solve(const double* A, const bool* act, const double* b,
                                            double* x) {
-  double L[3][3], y[3];
+  double L[3][3], y[3], iL[3];
   double tr = 0.0;
 #pragma unroll
   for (int k = 0; k < DR; ++k)
@@ -236,6 +236,7 @@ __device__ __forceinline__ bool chol_solve(const double* A, const bool* act, con
       if (act[m]) s -= L[k][m] * L[k][m];
     if (!(s > thr)) return false;
     L[k][k] = sqrt(s);
+    iL[k] = 1.0 / L[k][k];
 #pragma unroll
     for (int i = k + 1; i < DR; ++i) {
       if (!act[i]) continue;
@@ -243,7 +244,7 @@ __device__ __forceinline__ bool chol_solve(const double* A, const bool* act, con
 #pragma unroll
       for (int m = 0; m < k; ++m)
         if (act[m]) t -= L[i][m] * L[k][m];
-      L[i][k] = t / L[k][k];
+      L[i][k] = t * iL[k];
     }
   }
 #pragma unroll
@@ -253,7 +254,7 @@ __device__ __forceinline__ bool chol_solve(const double* A, const bool* act, con
 #pragma unroll
     for (int m = 0; m < k; ++m)
       if (act[m]) t -= L[k][m] * y[m];
-    y[k] = t / L[k][k];
+    y[k] = t * iL[k];
   }
 #pragma unroll
   for (int k = DR - 1; k >= 0; --k) {
@@ -262,7 +263,7 @@ __device__ __forceinline__ bool chol_solve(const double* A, const bool* act, con
 #pragma unroll
     for (int m = k + 1; m < DR; ++m)
       if (act[m]) t -= L[m][k] * x[m];
-    x[k] = t / L[k][k];
+    x[k] = t * iL[k];
   }
   return true;
 }
@@ -372,74 +373,104 @@ __device__ __forceinline__ NewtonOut newton_warp(const double* __restrict__ sX,
                                                  const NewtonParams& P, double* sb) {
   using L = Lay<D, DR, N>;
   double* stash = sb + Scratch<DR, N>::STASH * FPX_WARP;
-  // seed: nearest GLL node, ties -> lowest lexicographic index (D7); exact.
+  // seed: nearest GLL node, ties -> lowest lexicographic index (D7); the
+  // distance is accumulated with fma exactly as the oracle does.
   double best = INFINITY;
   int bi = 0;
-  for (int q = 0; q < L::K; ++q) {
-    const int row = q / N, i = q - row * N;
-    double dd = 0.0;
+#pragma unroll 1
+  for (int row = 0; row < L::ROWS; ++row) {
 #pragma unroll
-    for (int c = 0; c < D; ++c) {
-      const double t = __dsub_rn(xs[c], sX[c * L::CS + row * L::NP + i]);
-      dd = __dadd_rn(dd, __dmul_rn(t, t));
-    }
-    if (dd < best) {
-      best = dd;
-      bi = q;
+    for (int i = 0; i < N; ++i) {
+      double dd = 0.0;
+#pragma unroll
+      for (int c = 0; c < D; ++c) {
+        const double t = __dsub_rn(xs[c], sX[c * L::CS + row * L::NP + i]);
+        dd = __fma_rn(t, t, dd);
+      }
+      if (dd < best) {
+        best = dd;
+        bi = row * N + i;
+      }
     }
   }
   double r[3] = {0.0, 0.0, 0.0};
   r[0] = z[bi % N];
   if (DR > 1) r[1] = z[(bi / N) % N];
   if (DR > 2) r[2] = z[bi / (N * N)];
+  // One evaluation site (the seed is evaluated as the first "trial") and one
+  // constrained_step site (the Hessian fallbacks loop over it) keep the
+  // kernel's code small: instruction fetch was the top stall when inlined.
   NState st;
-  if (__any_sync(FPX_FULL, active && on_boundary<DR>(r)))
-    eval_state<D, DR, N, true>(sX, z, scale, r, xs, st, sb);
-  else
-    eval_state<D, DR, N, false>(sX, z, scale, r, xs, st, sb);
-  double alpha = P.alpha0;
+  double rn[3] = {r[0], r[1], r[2]};
+  double alpha = P.alpha0, fcur = 0.0, pred = 0.0, smax = 0.0;
   int it = 0;
-  bool done = !active, conv = false;
-  while (__any_sync(FPX_FULL, !done)) {
-    double rn[3] = {r[0], r[1], r[2]};
-    double smax = 0.0, pred = 0.0;
-    const double fcur = st.f;
-    bool step = false;
+  bool done = !active, conv = false, first = true, step = active;
+  while (true) {
+    if (__any_sync(FPX_FULL, step && on_boundary<DR>(rn)))
+      eval_state<D, DR, N, true>(sX, z, scale, rn, xs, st, sb);
+    else
+      eval_state<D, DR, N, false>(sX, z, scale, rn, xs, st, sb);
+    // lanes not stepping evaluated at rn == r: their state is recomputed
+    // bit-identically (eval_state is a pure function of r)
+    if (first) {
+      first = false;
+    } else if (step) {
+      const double decr = fcur - st.f;
+      if (decr >= P.accept * pred) {
+        if (decr >= P.keep * pred) alpha *= P.grow;
+#pragma unroll
+        for (int a = 0; a < DR; ++a) r[a] = rn[a];
+      } else {
+        alpha *= P.shrink;
+        unstash_state(stash, st);
+        st.f = fcur;
+      }
+      if (smax < P.tol) {
+        conv = true;
+        done = true;
+      } else if (it >= P.max_iters) {
+        done = true;
+      }
+    }
+    step = false;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) rn[a] = r[a];
+    if (!__any_sync(FPX_FULL, !done)) break;
     if (!done) {
+      fcur = st.f;
       const bool beta = it > 0 && on_boundary<DR>(r);
       bool freem[3] = {true, true, true};
 #pragma unroll
       for (int a = 0; a < DR; ++a)
         if ((r[a] == 1.0 && st.J[a] < 0.0) || (r[a] == -1.0 && st.J[a] > 0.0)) freem[a] = false;
       double Hm[6], s[3] = {0.0, 0.0, 0.0};
-      bool fr[3] = {freem[0], freem[1], freem[2]};
       int hit = 0;
       bool ok = false;
-      if (beta) {
-#pragma unroll
-        for (int m = 0; m < 6; ++m) Hm[m] = st.H0[m] - st.Q[m];
-        ok = constrained_step<DR>(Hm, st.J, r, fr, alpha, s, hit);
-      }
-      if (!ok) {
-#pragma unroll
-        for (int m = 0; m < 6; ++m) Hm[m] = st.H0[m];
-        fr[0] = freem[0]; fr[1] = freem[1]; fr[2] = freem[2];
-        if (!constrained_step<DR>(Hm, st.J, r, fr, alpha, s, hit)) {
+      // model Hessians in order: beta=1 (faces), Gauss-Newton, regularised
+#pragma unroll 1
+      for (int att = beta ? 0 : 1; att < 3 && !ok; ++att) {
+        double lam = 0.0;
+        if (att == 2) {
           double tr = 0.0;
 #pragma unroll
           for (int a = 0; a < DR; ++a) tr += st.H0[a];
-          double lam = 1e-10 * tr / DR;
+          lam = 1e-10 * tr / DR;
           if (!(lam > 0.0)) lam = 1e-300;
-#pragma unroll
-          for (int a = 0; a < DR; ++a) Hm[a] = st.H0[a] + lam;
-          fr[0] = freem[0]; fr[1] = freem[1]; fr[2] = freem[2];
-          if (!constrained_step<DR>(Hm, st.J, r, fr, alpha, s, hit))
-#pragma unroll
-            for (int a = 0; a < DR; ++a) s[a] = 0.0;
         }
+#pragma unroll
+        for (int m = 0; m < 6; ++m)
+          Hm[m] = att == 0 ? st.H0[m] - st.Q[m] : st.H0[m] + (m < DR ? lam : 0.0);
+        bool fr[3] = {freem[0], freem[1], freem[2]};
+        ok = constrained_step<DR>(Hm, st.J, r, fr, alpha, s, hit);
+      }
+      if (!ok) {
+        hit = 0;
+#pragma unroll
+        for (int a = 0; a < DR; ++a) s[a] = 0.0;
       }
       ++it;
       double js = 0.0, shs = 0.0;
+      smax = 0.0;
 #pragma unroll
       for (int a = 0; a < DR; ++a) {
         js += st.J[a] * s[a];
@@ -466,30 +497,6 @@ __device__ __forceinline__ NewtonOut newton_warp(const double* __restrict__ sX,
       }
     }
     if (!__any_sync(FPX_FULL, step)) break;
-    if (__any_sync(FPX_FULL, step && on_boundary<DR>(rn)))
-      eval_state<D, DR, N, true>(sX, z, scale, rn, xs, st, sb);
-    else
-      eval_state<D, DR, N, false>(sX, z, scale, rn, xs, st, sb);
-    // lanes not stepping evaluated at rn == r: their state is recomputed
-    // bit-identically (eval_state is a pure function of r)
-    if (step) {
-      const double decr = fcur - st.f;
-      if (decr >= P.accept * pred) {
-        if (decr >= P.keep * pred) alpha *= P.grow;
-#pragma unroll
-        for (int a = 0; a < DR; ++a) r[a] = rn[a];
-      } else {
-        alpha *= P.shrink;
-        unstash_state(stash, st);
-        st.f = fcur;
-      }
-      if (smax < P.tol) {
-        conv = true;
-        done = true;
-      } else if (it >= P.max_iters) {
-        done = true;
-      }
-    }
   }
   NewtonOut o;
   o.r[0] = r[0];
@@ -755,9 +762,12 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
   }
 }
 
-// Round-2 merge per unresolved point (winner rule D6 over the round-1
-// candidate and its pairs: INTERIOR (lowest id) > min d* (ties lowest id))
-// and the field evaluation of the winner.
+// Merge of a round's pairs into the points' records (winner rule D6 over the
+// current record and the pairs: INTERIOR (lowest id) > min d* (ties lowest
+// id)).  pair_off == NULL: one pair per point at index u (next-best round).
+// Points still unresolved that have more than `min_pass` passing candidates
+// go to the next round when next_upts != NULL; all others are final and get
+// their field value.
 template <int D, int DR, int N>
 __global__ void k_round2_finalize(fpx_mesh_t m, const int64_t* __restrict__ nun_dev,
                                   const int32_t* __restrict__ upts,
@@ -768,6 +778,8 @@ __global__ void k_round2_finalize(fpx_mesh_t m, const int64_t* __restrict__ nun_
                                   const int32_t* __restrict__ piters, int32_t* code, int32_t* elem,
                                   double* r, double* dist, int32_t* iters,
                                   const double* __restrict__ field, int C, double* values,
+                                  const int32_t* __restrict__ npass, int min_pass,
+                                  int32_t* next_upts, int64_t* next_cnt, int64_t* nnext,
                                   int64_t* stats) {
   __shared__ double z[16], scale[16];
   if (threadIdx.x < N) {
@@ -785,9 +797,10 @@ __global__ void k_round2_finalize(fpx_mesh_t m, const int64_t* __restrict__ nun_
     double br[3] = {0, 0, 0};
     for (int a = 0; a < DR; ++a) br[a] = r[(int64_t)k * DR + a];
     int it = iters ? iters[k] : 0;
-    const int64_t p0 = pair_off[u], p1 = pair_off[u + 1];
+    const int64_t p0 = pair_off ? pair_off[u] : u, p1 = pair_off ? pair_off[u + 1] : u + 1;
     for (int64_t p = p0; p < p1 && p < pair_cap; ++p) {
       const int e = pair_elem[p];
+      if (e < 0) continue;
       const int c = pcode[p];
       const double dd = pdist[p];
       if (piters) it += piters[p];
@@ -806,6 +819,12 @@ __global__ void k_round2_finalize(fpx_mesh_t m, const int64_t* __restrict__ nun_
     dist[k] = bd;
     for (int a = 0; a < DR; ++a) r[(int64_t)k * DR + a] = br[a];
     if (iters) iters[k] = it;
+    if (next_upts && bc != kInterior && npass[k] > min_pass) {
+      const int slot = (int)atomicAdd((unsigned long long*)nnext, 1ull);
+      next_upts[slot] = k;
+      next_cnt[slot] = npass[k] - min_pass;
+      continue;
+    }
     if (field) {
       double v[DR][N];
       basis_values<DR, N>(z, scale, br, v);
@@ -969,13 +988,14 @@ struct Finalize {
                          const int32_t* pair_elem, const int32_t* pcode, const double* pr,
                          const double* pdist, const int32_t* piters, int32_t* code, int32_t* elem,
                          double* r, double* dist, int32_t* iters, const double* field, int C,
-                         double* values, int64_t* stats, cudaStream_t st) {
+                         double* values, const int32_t* npass, int min_pass, int32_t* next_upts,
+                         int64_t* next_cnt, int64_t* nnext, int64_t* stats, cudaStream_t st) {
     int64_t b = (nun_cap + 127) / 128;
     if (b > 148 * 16) b = 148 * 16;
     if (b < 1) b = 1;
     k_round2_finalize<D, DR, N><<<(unsigned)b, 128, 0, st>>>(
         m, nun_dev, upts, pair_off, pair_cap, pair_elem, pcode, pr, pdist, piters, code, elem, r,
-        dist, iters, field, C, values, stats);
+        dist, iters, field, C, values, npass, min_pass, next_upts, next_cnt, nnext, stats);
     return cudaGetLastError();
   }
 };

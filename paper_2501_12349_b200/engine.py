@@ -193,7 +193,7 @@ def setup(nodes, order: int | None = None, ref_dim: int | None = None, *,
 
 # ---------------------------------------------------------------- find
 def _workspace(S: EngineSetup, n: int, pair_cap: int) -> torch.Tensor:
-    need = _C.lib().fpx_find_workspace_bytes(S.E, n, pair_cap)
+    need = _C.lib().fpx_find_workspace_bytes(S.mesh_t, n, pair_cap)
     if S.workspace is None or S.workspace.numel() < need:
         S.workspace = torch.empty(need, dtype=torch.uint8, device=S.device)
     return S.workspace

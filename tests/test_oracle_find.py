@@ -201,3 +201,18 @@ def test_find_all_points_in_domain(n):
     assert np.all(rec["code"] != 2)
     assert np.mean(rec["code"] == 0) > 0.99
     assert np.all(rec["dist"][rec["code"] == 0] < 1e-10)
+
+
+def test_surface_classification_oracle():
+    """Acceptance 9: on-manifold points INTERIOR, points pushed
+    off the sphere along the normal BORDER under eps_d (cfg-4 style)."""
+    m = toolkit.sphere_mesh(4, 4)
+    S = O.OracleSetup(m.nodes, 3, 2, 4)
+    x, e, r, off = toolkit.surface_points(m, 2000, seed=4, offset_frac=0.3, max_offset=1e-5)
+    rec = S.find(x)
+    on = off == 0
+    assert np.mean(rec["code"][on] == 0) > 0.99
+    assert np.all(rec["code"][~on & (np.abs(off) > 1e-8)] == 1)
+    # off-surface points: d* = |offset| (closest point projection), r interior
+    sel = (~on) & (rec["code"] == 1)
+    np.testing.assert_allclose(rec["dist"][sel], np.abs(off[sel]), rtol=1e-3, atol=1e-9)
