@@ -451,10 +451,8 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
   FPX_CK(cudaMemsetAsync(w.g2.count, 0, sizeof(int32_t) * E, st));
   FPX_LAUNCH(fpx::launch_round_next_emit(M, n, w.nun, w.upts, x, w.best, w.tried2, w.pair_pt,
                                          w.pair_elem, w.g2.count, st));
-  g_launches += 3;
-  FPX_CK(w.g2.build(E, n, w.nun, w.pair_elem, nullptr, st));
-  FPX_LAUNCH(fpx::launch_newton_pairs(M, x, w.pair_pt, w.g2.sorted, w.g2.items, w.g2.nitems,
-                                      w.g2.items_cap, w.pcode, w.pr, w.pdist, w.piters, stats, st));
+  FPX_LAUNCH(fpx::launch_newton_sparse(M, x, w.pair_pt, w.pair_elem, w.nun, n, w.pcode, w.pr,
+                                       w.pdist, w.piters, stats, st));
   FPX_CK(cudaMemsetAsync(w.upair_cnt, 0, sizeof(int64_t) * (n + 1), st));
   FPX_CK(cudaMemsetAsync(w.nun3, 0, sizeof(int64_t), st));
   FPX_LAUNCH(fpx::launch_round2_finalize(M, n, w.nun, w.upts, nullptr, pair_cap, w.pair_elem,
@@ -470,10 +468,8 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
   g_launches += 1;
   k_pairs_total<<<1, 1, 0, st>>>(w.pair_off, w.nun, w.nun3, pair_cap, w.npairs, stats, n);
   FPX_CK(cudaGetLastError());
-  g_launches += 3;
-  FPX_CK(w.g2.build(E, pair_cap, w.npairs, w.pair_elem, nullptr, st));
-  FPX_LAUNCH(fpx::launch_newton_pairs(M, x, w.pair_pt, w.g2.sorted, w.g2.items, w.g2.nitems,
-                                      w.g2.items_cap, w.pcode, w.pr, w.pdist, w.piters, stats, st));
+  FPX_LAUNCH(fpx::launch_newton_sparse(M, x, w.pair_pt, w.pair_elem, w.npairs, pair_cap, w.pcode,
+                                       w.pr, w.pdist, w.piters, stats, st));
   FPX_LAUNCH(fpx::launch_round2_finalize(M, n, w.nun3, w.upts3, w.pair_off, pair_cap, w.pair_elem,
                                          w.pcode, w.pr, w.pdist, w.piters, code, elem, r, dist,
                                          iters, field, C, values, w.npass, 0, nullptr, nullptr,

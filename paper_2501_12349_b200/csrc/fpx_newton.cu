@@ -66,6 +66,14 @@ cudaError_t launch_newton_pairs(const fpx_mesh_t& m, const double* x, const int3
                          items_cap, pcode, pr, pdist, piters, (int32_t*)nullptr, stats, st);
 }
 
+cudaError_t launch_newton_sparse(const fpx_mesh_t& m, const double* x, const int32_t* pair_pt,
+                                 const int32_t* pair_elem, const int64_t* npairs_dev, int64_t cap,
+                                 int32_t* pcode, double* pr, double* pdist, int32_t* piters,
+                                 int64_t* stats, cudaStream_t st) {
+  return dispatch<Sparse>(m.d, m.dr, m.N, m, x, pair_pt, pair_elem, npairs_dev, cap, pcode, pr,
+                          pdist, piters, stats, st);
+}
+
 cudaError_t launch_round2_finalize(const fpx_mesh_t& m, int64_t nun_cap, const int64_t* nun_dev,
                                    const int32_t* upts, const int64_t* pair_off,
                                    int64_t pair_cap, const int32_t* pair_elem,

@@ -78,12 +78,16 @@ struct Scratch {
 
 // Sum-factorised forward map x(r), G (+ second derivatives when W2), reduced
 // on the fly into the Newton state (Eqs. 28-29).
-template <int D, int DR, int N, bool W2>
+template <int D, int DR, int N, bool W2, bool GEO = false>
 __device__ __forceinline__ void eval_state(const double* __restrict__ sX,
                                            const double* __restrict__ z,
                                            const double* __restrict__ scale, const double* r,
                                            const double* xs, NState& S, double* sb) {
-  using L = Lay<D, DR, N>;
+  // GEO = false: geometry staged in shared memory, rows padded to NP;
+  // GEO = true: geometry read in place from global memory ([d][N^dr]).
+  using Lp = Lay<D, DR, N>;
+  constexpr int GCS = GEO ? Lp::K : Lp::CS;
+  constexpr int GNP = GEO ? N : Lp::NP;
   double v0[N], g0[N], h0[N];
   lagrange<N, W2>(z, scale, r[0], v0, g0, h0);
 #pragma unroll
@@ -108,7 +112,7 @@ __device__ __forceinline__ void eval_state(const double* __restrict__ sX,
   }
 #pragma unroll 1
   for (int c = 0; c < D; ++c) {
-    const double* Xc = sX + c * L::CS;
+    const double* Xc = sX + c * GCS;
     double xv = 0.0, G[3] = {0.0, 0.0, 0.0}, H2[6] = {0, 0, 0, 0, 0, 0};
     if constexpr (DR == 3) {
 #pragma unroll 1
@@ -116,12 +120,13 @@ __device__ __forceinline__ void eval_state(const double* __restrict__ sX,
         double t00 = 0.0, t10 = 0.0, t01 = 0.0, t20 = 0.0, t11 = 0.0, t02 = 0.0;
 #pragma unroll
         for (int j = 0; j < N; ++j) {
-          const double* row = Xc + (j + N * k) * L::NP;
+          const double* row = Xc + (j + N * k) * GNP;
           double s0 = 0.0, s1 = 0.0, s2 = 0.0;
 #pragma unroll
           for (int i = 0; i < N; i += 2) {
             double2 p;
-            if (i + 1 < N) p = *reinterpret_cast<const double2*>(row + i);
+            if (GEO) p = make_double2(__ldg(row + i), i + 1 < N ? __ldg(row + i + 1) : 0.0);
+            else if (i + 1 < N) p = *reinterpret_cast<const double2*>(row + i);
             else p = make_double2(row[i], 0.0);
             s0 = fma(p.x, v0[i], s0);
             s1 = fma(p.x, g0[i], s1);
@@ -161,7 +166,7 @@ __device__ __forceinline__ void eval_state(const double* __restrict__ sX,
     } else if constexpr (DR == 2) {
 #pragma unroll
       for (int j = 0; j < N; ++j) {
-        const double* row = Xc + j * L::NP;
+        const double* row = Xc + j * GNP;
         double s0 = 0.0, s1 = 0.0, s2 = 0.0;
 #pragma unroll
         for (int i = 0; i < N; ++i) {
@@ -365,7 +370,7 @@ __device__ __forceinline__ void unstash_state(const double* sb, NState& S) {
 // predicted decrease is formed before the trial evaluation, the current
 // state is stashed in the lane's shared scratch and restored only when the
 // step is rejected.  sb: this lane's scratch (stride 32 doubles).
-template <int D, int DR, int N>
+template <int D, int DR, int N, bool GEO = false>
 __device__ __forceinline__ NewtonOut newton_warp(const double* __restrict__ sX,
                                                  const double* __restrict__ z,
                                                  const double* __restrict__ scale,
@@ -384,7 +389,8 @@ __device__ __forceinline__ NewtonOut newton_warp(const double* __restrict__ sX,
       double dd = 0.0;
 #pragma unroll
       for (int c = 0; c < D; ++c) {
-        const double t = __dsub_rn(xs[c], sX[c * L::CS + row * L::NP + i]);
+        const double xn = GEO ? __ldg(sX + c * L::K + row * N + i) : sX[c * L::CS + row * L::NP + i];
+        const double t = __dsub_rn(xs[c], xn);
         dd = __fma_rn(t, t, dd);
       }
       if (dd < best) {
@@ -407,9 +413,9 @@ __device__ __forceinline__ NewtonOut newton_warp(const double* __restrict__ sX,
   bool done = !active, conv = false, first = true, step = active;
   while (true) {
     if (__any_sync(FPX_FULL, step && on_boundary<DR>(rn)))
-      eval_state<D, DR, N, true>(sX, z, scale, rn, xs, st, sb);
+      eval_state<D, DR, N, true, GEO>(sX, z, scale, rn, xs, st, sb);
     else
-      eval_state<D, DR, N, false>(sX, z, scale, rn, xs, st, sb);
+      eval_state<D, DR, N, false, GEO>(sX, z, scale, rn, xs, st, sb);
     // lanes not stepping evaluated at rn == r: their state is recomputed
     // bit-identically (eval_state is a pure function of r)
     if (first) {
@@ -762,6 +768,64 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
   }
 }
 
+// Sparse rounds (2 and 3): one (point, element) pair per lane, geometry read
+// in place from global memory (L1/L2) -- no element grouping.  The rounds
+// carry ~1 pair per element, where the element-major mapping would leave a
+// warp with one active lane.
+template <int D, int DR, int N>
+__global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
+    k_newton_sparse(fpx_mesh_t m, const double* __restrict__ x,
+                    const int32_t* __restrict__ pair_pt, const int32_t* __restrict__ pair_elem,
+                    const int64_t* __restrict__ npairs_dev, int32_t* pcode, double* pr,
+                    double* pdist, int32_t* piters, int64_t* stats) {
+  using L = Lay<D, DR, N>;
+  extern __shared__ __align__(16) double smem[];
+  double* z = smem;
+  double* scale = smem + N;
+  const int warp = threadIdx.x / FPX_WARP, lane = threadIdx.x % FPX_WARP;
+  const int wpb = blockDim.x / FPX_WARP;
+  constexpr int SCR = Scratch<DR, N>::SLOTS * FPX_WARP;
+  double* sb = smem + 2 * ((N + 1) & ~1) + warp * SCR + lane;
+  if (threadIdx.x < N) {
+    z[threadIdx.x] = m.basis[FPX_BASIS_NODES(N, m.M) + threadIdx.x];
+    scale[threadIdx.x] = m.basis[FPX_BASIS_SCALE(N, m.M) + threadIdx.x];
+  }
+  __syncthreads();
+  const NewtonParams P = newton_of(m);
+  const int64_t npairs = *npairs_dev;
+  int64_t s_newton = 0, s_iters = 0;
+  // whole warps stride over the pairs so every lane reaches the shuffles
+  for (int64_t base = ((int64_t)blockIdx.x * wpb + warp) * FPX_WARP; base < npairs;
+       base += (int64_t)gridDim.x * wpb * FPX_WARP) {
+    const int64_t p = base + lane;
+    const int e = p < npairs ? pair_elem[p] : -1;
+    const bool active = e >= 0;
+    const int pt = active ? pair_pt[p] : 0;
+    double xs[3] = {0.0, 0.0, 0.0};
+    if (active)
+#pragma unroll
+      for (int c = 0; c < D; ++c) xs[c] = x[(int64_t)pt * D + c];
+    const double* X = m.nodes + (int64_t)(active ? e : 0) * D * L::K;
+    NewtonOut o = newton_warp<D, DR, N, true>(X, z, scale, xs, active, P, sb);
+    if (active) {
+      s_newton += 1;
+      s_iters += o.iters;
+      const double epsd = DR < D ? eps_d_of(m, e) : 0.0;
+      pcode[p] = classify<D, DR>(o.r, o.dist, epsd);
+#pragma unroll
+      for (int a = 0; a < DR; ++a) pr[p * DR + a] = o.r[a];
+      pdist[p] = o.dist;
+      if (piters) piters[p] = o.iters;
+    }
+  }
+  s_newton = warp_sum64(s_newton);
+  s_iters = warp_sum64(s_iters);
+  if (lane == 0) {
+    atomicAdd((unsigned long long*)&stats[FPX_STAT_NEWTON], (unsigned long long)s_newton);
+    atomicAdd((unsigned long long*)&stats[FPX_STAT_ITERS], (unsigned long long)s_iters);
+  }
+}
+
 // Merge of a round's pairs into the points' records (winner rule D6 over the
 // current record and the pairs: INTERIOR (lowest id) > min d* (ties lowest
 // id)).  pair_off == NULL: one pair per point at index u (next-best round).
@@ -977,6 +1041,25 @@ struct Pairs {
     unsigned blocks = persistent_blocks((const void*)fn, threads, smem, items_cap);
     fn<<<blocks, threads, smem, st>>>(m, x, pair_pt, sorted, items, nitems_dev, pcode, pr, pdist,
                                       piters, pconv, stats);
+    return cudaGetLastError();
+  }
+};
+
+template <int D, int DR, int N>
+struct Sparse {
+  static cudaError_t run(const fpx_mesh_t& m, const double* x, const int32_t* pair_pt,
+                         const int32_t* pair_elem, const int64_t* npairs_dev, int64_t cap,
+                         int32_t* pcode, double* pr, double* pdist, int32_t* piters,
+                         int64_t* stats, cudaStream_t st) {
+    const int threads = 128;
+    const size_t smem = newton_smem(Scratch<DR, N>::SLOTS * FPX_WARP, 0, N, threads / FPX_WARP);
+    auto fn = k_newton_sparse<D, DR, N>;
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    unsigned blocks = persistent_blocks((const void*)fn, threads, smem,
+                                        (cap + FPX_WARP - 1) / FPX_WARP);
+    fn<<<blocks, threads, smem, st>>>(m, x, pair_pt, pair_elem, npairs_dev, pcode, pr, pdist,
+                                      piters, stats);
     return cudaGetLastError();
   }
 };

@@ -1,0 +1,58 @@
+"""GPU: the multi-rank engine (real kernels per rank + Phase-B routing) on a
+block-partitioned Kershaw mesh gives the single-rank records (rank
+invariance) -- 2 ranks sharing cuda:0 over gloo."""
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+from paper_2501_12349_b200 import engine, toolkit
+
+pytestmark = pytest.mark.gpu
+WORKER = os.path.join(os.path.dirname(__file__), "mp", "engine_rank_worker.py")
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def test_two_rank_engine_matches_single_rank(tmp_path):
+    size, port = 2, _port()
+    procs, outs = [], []
+    for rk in range(size):
+        env = dict(os.environ, RANK=str(rk), WORLD_SIZE=str(size), MASTER_ADDR="127.0.0.1",
+                   MASTER_PORT=str(port))
+        outs.append(str(tmp_path / f"r{rk}.npz"))
+        procs.append(subprocess.Popen([sys.executable, WORKER, outs[-1]], env=env,
+                                      stdout=subprocess.PIPE, stderr=subprocess.STDOUT))
+    for p in procs:
+        o, _ = p.communicate(timeout=600)
+        assert p.returncode == 0, o.decode()[-3000:]
+    mesh = toolkit.kershaw_mesh(8, 4)
+    field = toolkit.analytic_field("smooth", mesh)
+    S = engine.setup(mesh)
+    blocks = toolkit.partition_blocks(mesh.num_elements, size)
+    for out in outs:
+        got = np.load(out)
+        vals, rec = engine.find_and_interpolate(S, field, got["x"])
+        code = rec.code.cpu().numpy()
+        assert np.array_equal(got["code"], code)
+        f = code != 2
+        for k, (a, b) in enumerate(blocks):
+            m = got["rank"] == k
+            assert np.all((got["elem"][m] >= a) & (got["elem"][m] < b))
+        dist = rec.dist.cpu().numpy()
+        np.testing.assert_allclose(got["dist"][f], dist[f], rtol=1e-9, atol=1e-12)
+        same = (got["elem"] == rec.elem.cpu().numpy()) & (code == 0)
+        v = vals.cpu().numpy()
+        np.testing.assert_allclose(got["values"][same], v[same], rtol=1e-10, atol=1e-12)
+        np.testing.assert_allclose(got["ivalues"][same], v[same], rtol=1e-10, atol=1e-12)
+        assert np.all(np.isnan(got["values"][~f]))
