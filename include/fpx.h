@@ -92,14 +92,14 @@ typedef struct fpx_mesh_t {
 #define FPX_STAT_BOXTESTS 1      /* candidate box tests (hash-list entries) */
 #define FPX_STAT_NEWTON 2        /* Newton-ed (point, element) candidates */
 #define FPX_STAT_ITERS 3         /* Newton iterations over all candidates */
-#define FPX_STAT_ROUND2_POINTS 4 /* points unresolved after round 1 (next-best round 2) */
-#define FPX_STAT_ROUND2_PAIRS 5  /* (point, element) pairs in rounds 2 and 3 */
-#define FPX_STAT_OVERFLOW 6      /* pairs dropped for lack of workspace (>0: rerun) */
+#define FPX_STAT_ROUND2_POINTS 4 /* points unresolved after round 1 (rest kernel) */
+#define FPX_STAT_R1_WARP_EVALS 5 /* round-1 map evaluations issued per warp (all lanes) */
+#define FPX_STAT_R1_W2_EVALS 6   /* ... of which with second derivatives */
 #define FPX_STAT_EVALS 7         /* fused field evaluations */
 #define FPX_STAT_NEWTON_R1 8     /* Newton solves in the round-1 (best-first) kernel */
 #define FPX_STAT_ITERS_R1 9      /* their iterations */
 #define FPX_STAT_EVALS_R1 10     /* field evaluations fused into the round-1 kernel */
-#define FPX_STAT_ROUND3_POINTS 11 /* points needing the exhaustive round 3 */
+#define FPX_STAT_R1_ITEMS 11     /* round-1 warp work items */
 #define FPX_STATS_LEN 12
 
 int fpx_abi_version(void);

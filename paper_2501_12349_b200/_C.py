@@ -17,8 +17,8 @@ LIB_PATH = os.environ.get("FPX_LIB") or os.path.join(HERE, "lib", "libfpx_sm100.
 ABI_VERSION = 1
 
 INTERIOR, BORDER, NOT_FOUND = 0, 1, 2
-STAT_NAMES = ["points", "box_tests", "newton", "iters", "round2_points", "round2_pairs",
-              "overflow", "evals", "newton_r1", "iters_r1", "evals_r1", "round3_points"]
+STAT_NAMES = ["points", "box_tests", "newton", "iters", "rest_points", "r1_warp_evals",
+              "r1_w2_evals", "evals", "newton_r1", "iters_r1", "evals_r1", "r1_items"]
 STATS_LEN = len(STAT_NAMES)
 
 P = C.c_void_p

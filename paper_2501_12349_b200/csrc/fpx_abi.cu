@@ -9,6 +9,7 @@
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -132,13 +133,9 @@ struct Group {
 };
 
 struct FindWs {
-  int32_t *best, *npass, *upts, *upts3, *tried2;
-  int64_t *upair_cnt, *pair_off, *nun, *nun3, *npairs;
-  int32_t *pair_pt, *pair_elem, *pcode, *piters;
-  double *pr, *pdist;
-  Group g1, g2;
-  void* scan2_temp;
-  size_t scan2_bytes;
+  int32_t *best, *npass, *upts, *clist, *cnum;
+  int64_t *nun, *counter;
+  Group g1;
   // point ordering by hash cell
   int32_t *cellid, *cell_count, *cell_off, *cell_cursor, *order;
   void* scan3_temp;
@@ -154,41 +151,23 @@ struct FindWs {
     scan3_bytes = scan_temp_i32(nc + 2);
     scan3_temp = c.take<char>(scan3_bytes);
   }
-  void carve(Carver& c, int64_t E, int64_t n, int64_t cap) {
+  void carve(Carver& c, int64_t E, int64_t n) {
     best = c.take<int32_t>(n);
     npass = c.take<int32_t>(n);
     upts = c.take<int32_t>(n);
-    upts3 = c.take<int32_t>(n);
-    tried2 = c.take<int32_t>(n);
-    upair_cnt = c.take<int64_t>(n + 1);
-    pair_off = c.take<int64_t>(n + 1);
+    clist = c.take<int32_t>(n * FPX_RK);
+    cnum = c.take<int32_t>(n);
     nun = c.take<int64_t>(1);
-    nun3 = c.take<int64_t>(1);
-    npairs = c.take<int64_t>(1);
-    if (cap < n) cap = n;   // the next-best round needs one pair per point
-    pair_pt = c.take<int32_t>(cap);
-    pair_elem = c.take<int32_t>(cap);
-    pcode = c.take<int32_t>(cap);
-    piters = c.take<int32_t>(cap);
-    pr = c.take<double>(3 * cap);
-    pdist = c.take<double>(cap);
+    counter = c.take<int64_t>(1);
     g1.carve(c, E, n);
-    g2.carve(c, E, cap);
-    scan2_bytes = scan_temp_i64(n + 1);
-    scan2_temp = c.take<char>(scan2_bytes);
   }
 };
 
-__global__ void k_pairs_total(const int64_t* __restrict__ pair_off, const int64_t* __restrict__ nun,
-                              const int64_t* __restrict__ nun3, int64_t cap, int64_t* npairs,
-                              int64_t* stats, int64_t n) {
-  const int64_t t = pair_off[*nun3];
-  *npairs = t < cap ? t : cap;
+__global__ void k_find_totals(const int64_t* __restrict__ nun, int64_t* stats, int64_t n) {
   stats[FPX_STAT_POINTS] = n;
-  stats[FPX_STAT_ROUND2_POINTS] = *nun;    // after round 1
-  stats[FPX_STAT_ROUND3_POINTS] = *nun3;   // after round 2
-  stats[FPX_STAT_ROUND2_PAIRS] = t + *nun; // next-best pairs + exhaustive pairs
+  stats[FPX_STAT_ROUND2_POINTS] = *nun;
 }
+
 
 __global__ void k_count_elems(int64_t n, const int32_t* __restrict__ elem, int32_t* count) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
@@ -393,31 +372,39 @@ static int64_t cells_of(const fpx_mesh_t* m) {
 }
 
 size_t fpx_find_workspace_bytes(const fpx_mesh_t* m, int64_t n, int64_t pair_cap) {
+  (void)pair_cap;  // ABI v1 argument; the rest kernel needs no pair buffers
   Carver c(nullptr, 0);
   FindWs w;
-  w.carve(c, m->E, n > 0 ? n : 1, pair_cap > 0 ? pair_cap : 1);
+  w.carve(c, m->E, n > 0 ? n : 1);
   w.carve_cells(c, n > 0 ? n : 1, cells_of(m));
   return c.off + 256;
 }
 
+// engine.find Phase A over n points:
+//   1. counting sort of the points by hash cell;
+//   2. prefilter: per cell, the hash list through the AABB/OBB filter, the
+//      best-first ranked candidates of each point (NOT_FOUND if none);
+//   3. round 1: element-major Newton on every point's best-first candidate
+//      (final if INTERIOR or the only candidate; fused field evaluation);
+//   4. rest: the remaining candidates of the unresolved points, best-first,
+//      stopping at the first INTERIOR, else the D6 winner (fused eval).
 int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int32_t* elem,
              double* r, double* dist, int32_t* iters, const double* field, int C,
              double* values, int64_t* stats, int64_t pair_cap, void* ws, size_t ws_bytes,
              void* stream) {
+  (void)pair_cap;
   int rc = check_mesh(m);
   if (rc) return rc;
   if (n < 0 || n > INT32_MAX) return fail(FPX_EINVAL, "bad point count %lld", (long long)n);
   if (!stats) return fail(FPX_EINVAL, "stats buffer required");
   if (field && (C < 1 || !values)) return fail(FPX_EINVAL, "field given without C/values");
-  if (pair_cap < n) pair_cap = n;   // matches FindWs::carve
-  if (pair_cap < 1) pair_cap = 1;
   cudaStream_t st = S(stream);
   FPX_CK(cudaMemsetAsync(stats, 0, sizeof(int64_t) * FPX_STATS_LEN, st));
   if (n == 0) return FPX_OK;
   const int64_t E = m->E;
   Carver cv(ws, ws_bytes);
   FindWs w;
-  w.carve(cv, E, n, pair_cap);
+  w.carve(cv, E, n);
   w.carve_cells(cv, n, cells_of(m));
   if (!cv.ok()) return fail(FPX_EINVAL, "find workspace too small (%zu < %zu)", ws_bytes, cv.off);
   const fpx_mesh_t& M = *m;
@@ -432,48 +419,32 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
   }
   FPX_CK(cudaMemsetAsync(w.cell_cursor, 0, sizeof(int32_t) * (nc + 2), st));
   FPX_LAUNCH(fpx::launch_point_scatter(n, w.cellid, w.cell_off, w.cell_cursor, w.order, st));
-  // --- prefilter: hash lookup + AABB/OBB filter + best-first candidate
+  // --- prefilter: hash list + AABB/OBB filter + best-first ranking
   FPX_CK(cudaMemsetAsync(w.g1.count, 0, sizeof(int32_t) * E, st));
-  FPX_LAUNCH(fpx::launch_find_prefilter(M, n, x, w.order, w.cellid, w.best, w.npass, code, elem,
-                                        r, dist, iters,
-                                    field ? values : nullptr, C, w.g1.count, stats, st));
+  static const int pf_mode = [] {
+    const char* v = getenv("FPX_PREFILTER");
+    return v && v[0] == '1' ? 1 : 0;
+  }();
+  FPX_LAUNCH(fpx::launch_prefilter(M, pf_mode, n, nc + 1, x, w.order, w.cellid, w.cell_off,
+                                   w.best, w.npass, code, elem, r, dist, iters,
+                                   field ? values : nullptr, C, w.g1.count, stats, st));
+  FPX_CK(cudaMemsetAsync(w.nun, 0, sizeof(int64_t), st));
+  FPX_CK(cudaMemsetAsync(w.counter, 0, sizeof(int64_t), st));
   // --- round 1: group by best-first element, Newton, fused eval
   g_launches += 3;
   FPX_CK(w.g1.build(E, n, nullptr, w.best, nullptr, st));
-  FPX_CK(cudaMemsetAsync(w.upair_cnt, 0, sizeof(int64_t) * (n + 1), st));
-  FPX_CK(cudaMemsetAsync(w.nun, 0, sizeof(int64_t), st));
   if (g_prof_start) FPX_CK(cudaEventRecord(g_prof_start, st));
-  FPX_LAUNCH(fpx::launch_newton_round1(M, n, x, w.g1.sorted, w.g1.items, w.g1.nitems, w.g1.items_cap,
-                                   w.npass, code, elem, r, dist, iters, field, C, values, w.upts,
-                                   w.upair_cnt, w.nun, stats, st));
+  FPX_LAUNCH(fpx::launch_newton_round1(M, n, x, w.g1.sorted, w.g1.items, w.g1.nitems,
+                                       w.g1.items_cap, w.npass, code, elem, r, dist, iters, field,
+                                       C, values, w.upts, nullptr, w.nun, stats, st));
   if (g_prof_stop) FPX_CK(cudaEventRecord(g_prof_stop, st));
-  // --- round 2: the next best-first candidate of every unresolved point
-  FPX_CK(cudaMemsetAsync(w.g2.count, 0, sizeof(int32_t) * E, st));
-  FPX_LAUNCH(fpx::launch_round_next_emit(M, n, w.nun, w.upts, x, w.best, w.tried2, w.pair_pt,
-                                         w.pair_elem, w.g2.count, st));
-  FPX_LAUNCH(fpx::launch_newton_sparse(M, x, w.pair_pt, w.pair_elem, w.nun, n, w.pcode, w.pr,
-                                       w.pdist, w.piters, stats, st));
-  FPX_CK(cudaMemsetAsync(w.upair_cnt, 0, sizeof(int64_t) * (n + 1), st));
-  FPX_CK(cudaMemsetAsync(w.nun3, 0, sizeof(int64_t), st));
-  FPX_LAUNCH(fpx::launch_round2_finalize(M, n, w.nun, w.upts, nullptr, pair_cap, w.pair_elem,
-                                         w.pcode, w.pr, w.pdist, w.piters, code, elem, r, dist,
-                                         iters, field, C, values, w.npass, 2, w.upts3,
-                                         w.upair_cnt, w.nun3, stats, st));
-  // --- round 3: every remaining passing candidate of the still unresolved
-  size_t tb = w.scan2_bytes;
-  FPX_CK(cub::DeviceScan::ExclusiveSum(w.scan2_temp, tb, w.upair_cnt, w.pair_off, (int)(n + 1), st));
-  FPX_CK(cudaMemsetAsync(w.g2.count, 0, sizeof(int32_t) * E, st));
-  FPX_LAUNCH(fpx::launch_round2_emit(M, n, w.nun3, w.upts3, x, w.best, w.tried2, w.pair_off,
-                                     pair_cap, w.pair_pt, w.pair_elem, w.g2.count, stats, st));
+  // --- rest: remaining candidates of the unresolved points
+  FPX_LAUNCH(fpx::launch_rest_lists(M, x, n, w.nun, w.upts, w.clist, w.cnum, st));
+  FPX_LAUNCH(fpx::launch_find_rest(M, x, n, w.nun, w.upts, w.clist, w.cnum, code, elem, r, dist,
+                                   iters, field, C, values, w.counter, stats, st));
   g_launches += 1;
-  k_pairs_total<<<1, 1, 0, st>>>(w.pair_off, w.nun, w.nun3, pair_cap, w.npairs, stats, n);
+  k_find_totals<<<1, 1, 0, st>>>(w.nun, stats, n);
   FPX_CK(cudaGetLastError());
-  FPX_LAUNCH(fpx::launch_newton_sparse(M, x, w.pair_pt, w.pair_elem, w.npairs, pair_cap, w.pcode,
-                                       w.pr, w.pdist, w.piters, stats, st));
-  FPX_LAUNCH(fpx::launch_round2_finalize(M, n, w.nun3, w.upts3, w.pair_off, pair_cap, w.pair_elem,
-                                         w.pcode, w.pr, w.pdist, w.piters, code, elem, r, dist,
-                                         iters, field, C, values, w.npass, 0, nullptr, nullptr,
-                                         nullptr, stats, st));
   return FPX_OK;
 }
 

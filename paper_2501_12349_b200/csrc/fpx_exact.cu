@@ -8,6 +8,7 @@
 
 #include "fpx_common.cuh"
 #include "fpx_kernels.cuh"
+#include "fpx_boxes.cuh"
 
 namespace fpx {
 
@@ -587,23 +588,6 @@ __global__ void k_hash_grid(int d, int64_t E, const double* __restrict__ box, in
   }
 }
 
-// cell_of; returns -1 outside, per-axis coords in ax.
-__device__ __forceinline__ int64_t cell_of(int d, const double* grid, int n, const double* x,
-                                           int* ax) {
-  int64_t idx = 0, mul = 1;
-  for (int c = 0; c < d; ++c) {
-    if (!(x[c] >= grid[c] && x[c] <= grid[3 + c])) return -1;
-    double t = (x[c] - grid[c]) / grid[6 + c];
-    int64_t q = (int64_t)floor(t);
-    q = q > n - 1 ? n - 1 : q;
-    q = q < 0 ? 0 : q;
-    ax[c] = (int)q;
-    idx += q * mul;
-    mul *= n;
-  }
-  return idx;
-}
-
 __device__ void box_cells(int d, const double* grid, int n, const double* b, int* a0, int* a1) {
   a0[0] = a0[1] = a0[2] = 0;
   a1[0] = a1[1] = a1[2] = 0;
@@ -708,38 +692,6 @@ __global__ void k_cell_of(int d, const double* __restrict__ grid, int n, int64_t
 }
 
 // ------------------------------------------------------------ find prefilter
-// aabb_contains / obb_contains (bounds.py:387-396) exactly as the oracle.
-__device__ __forceinline__ bool aabb_in(int d, const double* __restrict__ bx, const double* x) {
-  for (int c = 0; c < d; ++c)
-    if (!((x[c] - bx[c]) * (bx[d + c] - x[c]) >= 0.0)) return false;
-  return true;
-}
-__device__ __forceinline__ bool obb_in(int d, const double* __restrict__ cen,
-                                       const double* __restrict__ inv, const double* x) {
-  double dx[3];
-  for (int c = 0; c < d; ++c) dx[c] = x[c] - cen[c];
-  for (int c = 0; c < d; ++c) {
-    double y = 0.0;
-    for (int b = 0; b < d; ++b) y += inv[c * d + b] * dx[b];
-    if (!(fabs(y) <= 1.0)) return false;
-  }
-  return true;
-}
-
-// Best-first value of candidate e at x: |J_c^{-1}(x - x_c)|_inf.
-__device__ __forceinline__ double bestfirst_value(int d, const double* __restrict__ fr,
-                                                  const double* x) {
-  double dx[3];
-  for (int c = 0; c < d; ++c) dx[c] = x[c] - fr[c];
-  double v = 0.0;
-  for (int c = 0; c < d; ++c) {
-    double y = 0.0;
-    for (int b = 0; b < d; ++b) y += fr[d + c * d + b] * dx[b];
-    v = fabs(y) > v ? fabs(y) : v;
-  }
-  return v;
-}
-
 // Point ordering by hash cell (counting sort): adjacent lanes of the
 // prefilter then walk the same candidate lists and read the same element
 // records.  Points outside the grid go to the extra bucket `ncells`.
@@ -771,155 +723,174 @@ __global__ void k_point_scatter(int64_t n, const int32_t* __restrict__ cellid,
   }
 }
 
-// Candidate loop of engine.find Phase A up to the Newton solve: for each
-// point, the hash list (ascending ids), the AABB then OBB filter.  Emits the
-// best-first candidate (smallest |J_c^{-1}(x - x_c)|_inf, ties -> lower id)
-// and the number of candidates that passed.  Points with none are final
-// NOT_FOUND.
-__global__ void k_find_prefilter(fpx_mesh_t m, int64_t n, const double* __restrict__ x,
-                                 const int32_t* __restrict__ order,
-                                 const int32_t* __restrict__ cellid, int32_t* best,
-                                 int32_t* npass, int32_t* code, int32_t* elem, double* r,
-                                 double* dist, int32_t* iters, double* values, int C,
-                                 int32_t* elem_count, int64_t* stats) {
-  const int d = m.d, dr = m.dr;
+// Records of a point with no passing candidate: final NOT_FOUND (D10).
+__device__ __forceinline__ void write_not_found(int64_t k, int dr, int32_t* code, int32_t* elem,
+                                                double* r, double* dist, int32_t* iters,
+                                                double* values, int C) {
+  code[k] = kNotFound;
+  elem[k] = -1;
+  for (int a = 0; a < dr; ++a) r[k * dr + a] = NAN;
+  dist[k] = NAN;
+  if (iters) iters[k] = 0;
+  if (values)
+    for (int c = 0; c < C; ++c) values[k * C + c] = NAN;
+}
+
+// Candidate loop of engine.find Phase A up to the Newton solve (SPEC.md:
+// 404-413): the hash list of the point's cell through the AABB then OBB
+// filter.  Per point: npass (candidates that passed) and best, the
+// best-first candidate (smallest |J_c^{-1}(x - x_c)|_inf, ties -> lower id;
+// DESIGN.md §3 "Candidate order").  Points with none are final NOT_FOUND.
+// The rest kernel re-derives the further best-first candidates of the ~5%
+// of points round 1 leaves unresolved, so nothing else is stored.
+//
+// Thread per point, points in hash-cell order: the lanes of a warp share one
+// or two cells' lists, so the element records they read are the same
+// (broadcast) and the loop trip counts agree.
+template <int D>
+__global__ void __launch_bounds__(256)
+    k_prefilter_points(fpx_mesh_t m, int64_t n, const double* __restrict__ x,
+                       const int32_t* __restrict__ order, const int32_t* __restrict__ cellid,
+                       int32_t* best, int32_t* npass, int32_t* code, int32_t* elem, double* r,
+                       double* dist, int32_t* iters, double* values, int C, int32_t* elem_count,
+                       int64_t* stats) {
   int64_t nc = 1;
-  for (int c = 0; c < d; ++c) nc *= m.ncell;
+  for (int c = 0; c < D; ++c) nc *= m.ncell;
   int64_t boxtests = 0;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
        t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t k = order ? order[t] : t;
-    double xx[3] = {0, 0, 0};
-    for (int c = 0; c < d; ++c) xx[c] = x[k * d + c];
-    int ax[3];
-    int64_t cell;
-    if (cellid) {
-      cell = cellid[k];
-      if (cell == nc) cell = -1;
-    } else {
-      cell = cell_of(d, m.grid, m.ncell, xx, ax);
-    }
+    const int64_t k = order[t];
+    const int64_t cell = cellid[k];
+    double xx[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) xx[c] = x[k * D + c];
     int cnt = 0, bst = -1;
     double bval = INFINITY;
-    if (cell >= 0) {
-      const int s = m.offsets[cell], t = m.offsets[cell + 1];
-      boxtests += t - s;
-      for (int q = s; q < t; ++q) {
-        const int e = m.elems[q];
-        if (!aabb_in(d, m.aabb + (int64_t)e * 2 * d, xx)) continue;
-        if (m.obb_ok[e] && !obb_in(d, m.obb_c + (int64_t)e * d, m.obb_inv + (int64_t)e * d * d, xx))
-          continue;
+    if (cell < nc) {
+      const int s = m.offsets[cell], e1 = m.offsets[cell + 1];
+      boxtests += e1 - s;
+      for (int q = s; q < e1; ++q) {
+        const int64_t e = m.elems[q];
+        if (!aabb_in(D, m.aabb + e * 2 * D, xx)) continue;
+        if (m.obb_ok[e] && !obb_in(D, m.obb_c + e * D, m.obb_inv + e * D * D, xx)) continue;
         ++cnt;
-        const double v = bestfirst_value(d, m.frame + (int64_t)e * (d + d * d), xx);
+        const double v = bestfirst_value(D, m.frame + e * (D + D * D), xx);
         if (v < bval) {  // strict: ties keep the lower (earlier) id
           bval = v;
-          bst = e;
+          bst = (int)e;
         }
       }
     }
     best[k] = bst;
     npass[k] = cnt;
-    if (bst < 0) {
-      code[k] = kNotFound;
-      elem[k] = -1;
-      for (int a = 0; a < dr; ++a) r[k * dr + a] = NAN;
-      dist[k] = NAN;
-      if (iters) iters[k] = 0;
-      if (values)
-        for (int c = 0; c < C; ++c) values[k * C + c] = NAN;
-    } else {
-      atomicAdd(&elem_count[bst], 1);
-    }
+    if (bst < 0) write_not_found(k, m.dr, code, elem, r, dist, iters, values, C);
+    else atomicAdd(&elem_count[bst], 1);
   }
-  // warp-aggregated counter update
   for (int o = 16; o > 0; o >>= 1) boxtests += __shfl_xor_sync(FPX_FULL, boxtests, o);
-  if ((threadIdx.x & 31) == 0) atomicAdd((unsigned long long*)&stats[FPX_STAT_BOXTESTS],
-                                         (unsigned long long)boxtests);
+  if ((threadIdx.x & 31) == 0 && boxtests)
+    atomicAdd((unsigned long long*)&stats[FPX_STAT_BOXTESTS], (unsigned long long)boxtests);
 }
 
-// Round 2 emit: for every unresolved point, the passing candidates other
-// than its round-1 element, written contiguously at pair_off (point order),
-// and counted per element.
-// Round 2 emit: the next best-first candidate (smallest value, ties -> lower
-// id) of every unresolved point other than its round-1 element; one pair per
-// point at index u.
-__global__ void k_round_next_emit(fpx_mesh_t m, const int64_t* __restrict__ nun_dev,
-                                  const int32_t* __restrict__ upts, const double* __restrict__ x,
-                                  const int32_t* __restrict__ best, int32_t* tried2,
-                                  int32_t* pair_pt, int32_t* pair_elem, int32_t* elem_count) {
-  const int d = m.d;
-  const int64_t nun = *nun_dev;
-  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < nun;
-       u += (int64_t)gridDim.x * blockDim.x) {
-    const int k = upts[u];
-    double xx[3] = {0, 0, 0};
-    for (int c = 0; c < d; ++c) xx[c] = x[(int64_t)k * d + c];
-    int ax[3];
-    const int64_t cell = cell_of(d, m.grid, m.ncell, xx, ax);
-    const int skip = best[k];
-    int bst = -1;
-    double bval = INFINITY;
-    const int s = m.offsets[cell], t = m.offsets[cell + 1];
-    for (int q = s; q < t; ++q) {
-      const int e = m.elems[q];
-      if (e == skip) continue;
-      if (!aabb_in(d, m.aabb + (int64_t)e * 2 * d, xx)) continue;
-      if (m.obb_ok[e] && !obb_in(d, m.obb_c + (int64_t)e * d, m.obb_inv + (int64_t)e * d * d, xx))
-        continue;
-      const double v = bestfirst_value(d, m.frame + (int64_t)e * (d + d * d), xx);
-      if (v < bval) {
-        bval = v;
-        bst = e;
+// Warp per hash cell: lanes over the cell's list (records in registers when
+// it fits one warp), the warp walks the cell's points and reduces the
+// best-first candidate with shuffles.  Preferable when cells hold few points
+// and long lists (fine hash grids).
+template <int D>
+__global__ void __launch_bounds__(128)
+    k_prefilter_cells(fpx_mesh_t m, int64_t ncells_tot, const double* __restrict__ x,
+                      const int32_t* __restrict__ order, const int32_t* __restrict__ cell_off,
+                      int32_t* best, int32_t* npass, int32_t* code, int32_t* elem, double* r,
+                      double* dist, int32_t* iters, double* values, int C, int32_t* elem_count,
+                      int64_t* stats) {
+  const int warp = threadIdx.x / FPX_WARP, lane = threadIdx.x % FPX_WARP;
+  const int64_t nc = ncells_tot - 1;  // last bucket: points outside the grid
+  int64_t boxtests = 0;
+  for (int64_t c = (int64_t)blockIdx.x * (blockDim.x / FPX_WARP) + warp; c < ncells_tot;
+       c += (int64_t)gridDim.x * (blockDim.x / FPX_WARP)) {
+    const int p0 = cell_off[c], p1 = cell_off[c + 1];
+    if (p0 == p1) continue;
+    if (c == nc) {
+      for (int p = p0 + lane; p < p1; p += FPX_WARP) {
+        const int64_t k = order[p];
+        best[k] = -1;
+        npass[k] = 0;
+        write_not_found(k, m.dr, code, elem, r, dist, iters, values, C);
       }
+      continue;
     }
-    tried2[k] = bst;
-    pair_pt[u] = k;
-    pair_elem[u] = bst;
-    if (bst >= 0) atomicAdd(&elem_count[bst], 1);
-  }
-}
-
-// Round 3 emit: every remaining passing candidate (not the round-1 or
-// round-2 element) of the points still unresolved, written contiguously at
-// pair_off (point order) and counted per element.
-__global__ void k_round2_emit(fpx_mesh_t m, const int64_t* __restrict__ nun_dev,
-                              const int32_t* __restrict__ upts,
-                              const double* __restrict__ x, const int32_t* __restrict__ best,
-                              const int32_t* __restrict__ skip2,
-                              const int64_t* __restrict__ pair_off, int64_t pair_cap,
-                              int32_t* pair_pt, int32_t* pair_elem, int32_t* elem_count,
-                              int64_t* stats) {
-  const int d = m.d;
-  const int64_t nun = *nun_dev;
-  int64_t overflow = 0;
-  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < nun;
-       u += (int64_t)gridDim.x * blockDim.x) {
-    const int k = upts[u];
-    double xx[3] = {0, 0, 0};
-    for (int c = 0; c < d; ++c) xx[c] = x[(int64_t)k * d + c];
-    int ax[3];
-    int64_t cell = cell_of(d, m.grid, m.ncell, xx, ax);
-    int64_t o = pair_off[u];
-    const int skip = best[k];
-    const int skipb = skip2 ? skip2[k] : -1;
-    const int s = m.offsets[cell], t = m.offsets[cell + 1];
-    for (int q = s; q < t; ++q) {
-      const int e = m.elems[q];
-      if (e == skip || e == skipb) continue;
-      if (!aabb_in(d, m.aabb + (int64_t)e * 2 * d, xx)) continue;
-      if (m.obb_ok[e] && !obb_in(d, m.obb_c + (int64_t)e * d, m.obb_inv + (int64_t)e * d * d, xx))
-        continue;
-      if (o < pair_cap) {
-        pair_pt[o] = k;
-        pair_elem[o] = e;
-        atomicAdd(&elem_count[e], 1);
-      } else {
-        ++overflow;
+    const int s = m.offsets[c], L = m.offsets[c + 1] - s;
+    if (lane == 0) boxtests += (int64_t)L * (p1 - p0);
+    for (int q0 = 0; q0 < L || q0 == 0; q0 += FPX_WARP) {
+      // this chunk's records in registers (lane q holds entry q0 + q)
+      const bool have = q0 + lane < L;
+      const int e = have ? m.elems[s + q0 + lane] : 0;
+      const int64_t eo = have ? e : 0;
+      double bx[2 * D], cen[D], inv[D * D], fr[D + D * D];
+#pragma unroll
+      for (int t = 0; t < 2 * D; ++t) bx[t] = m.aabb[eo * 2 * D + t];
+#pragma unroll
+      for (int t = 0; t < D; ++t) cen[t] = m.obb_c[eo * D + t];
+#pragma unroll
+      for (int t = 0; t < D * D; ++t) inv[t] = m.obb_inv[eo * D * D + t];
+#pragma unroll
+      for (int t = 0; t < D + D * D; ++t) fr[t] = m.frame[eo * (D + D * D) + t];
+      const bool ok = m.obb_ok[eo] != 0;
+      const bool lastc = q0 + FPX_WARP >= L;
+      for (int pc = p0; pc < p1; pc += FPX_WARP) {
+        const int cnt = p1 - pc < FPX_WARP ? p1 - pc : FPX_WARP;
+        const int64_t kl = lane < cnt ? order[pc + lane] : 0;
+        double xl[D];
+#pragma unroll
+        for (int t = 0; t < D; ++t) xl[t] = lane < cnt ? x[kl * D + t] : 0.0;
+        // running (npass, best) of point pc + lane across chunks
+        int my_np = 0, my_b = -1;
+        double my_v = INFINITY;
+        if (q0 > 0 && lane < cnt) {
+          my_np = npass[kl];
+          my_b = best[kl];
+          my_v = my_b >= 0 ? bestfirst_value(D, m.frame + (int64_t)my_b * (D + D * D), xl)
+                           : INFINITY;
+        }
+        for (int pi = 0; pi < cnt; ++pi) {
+          double xx[D];
+#pragma unroll
+          for (int t = 0; t < D; ++t) xx[t] = __shfl_sync(FPX_FULL, xl[t], pi);
+          const bool pass = have && aabb_in(D, bx, xx) && (!ok || obb_in(D, cen, inv, xx));
+          double v = pass ? bestfirst_value(D, fr, xx) : INFINITY;
+          int be = pass ? e : 0x7fffffff;
+          const int np = __popc(__ballot_sync(FPX_FULL, pass));
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(FPX_FULL, v, o);
+            const int oe = __shfl_xor_sync(FPX_FULL, be, o);
+            if (ov < v || (ov == v && oe < be)) {
+              v = ov;
+              be = oe;
+            }
+          }
+          if (lane == pi) {
+            my_np += np;
+            if (np > 0 && (v < my_v || (v == my_v && be < my_b) || my_b < 0)) {
+              my_v = v;
+              my_b = be;
+            }
+          }
+        }
+        if (lane < cnt) {
+          npass[kl] = my_np;
+          best[kl] = my_b;
+          if (lastc) {
+            if (my_b < 0) write_not_found(kl, m.dr, code, elem, r, dist, iters, values, C);
+            else atomicAdd(&elem_count[my_b], 1);
+          }
+        }
       }
-      ++o;
+      if (L == 0) break;
     }
   }
-  if (overflow) atomicAdd((unsigned long long*)&stats[FPX_STAT_OVERFLOW], (unsigned long long)overflow);
+  for (int o = 16; o > 0; o >>= 1) boxtests += __shfl_xor_sync(FPX_FULL, boxtests, o);
+  if (lane == 0 && boxtests)
+    atomicAdd((unsigned long long*)&stats[FPX_STAT_BOXTESTS], (unsigned long long)boxtests);
 }
 
 // ------------------------------------------------------------ host launchers
@@ -1003,14 +974,24 @@ cudaError_t launch_cell_of(int d, const double* grid, int n, int64_t npts, const
   k_cell_of<<<grid_for(npts, 256), 256, 0, st>>>(d, grid, n, npts, x, cell);
   return cudaGetLastError();
 }
-cudaError_t launch_find_prefilter(const fpx_mesh_t& m, int64_t n, const double* x,
-                                  const int32_t* order, const int32_t* cellid, int32_t* best,
-                                  int32_t* npass, int32_t* code, int32_t* elem, double* r,
-                                  double* dist, int32_t* iters, double* values, int C,
-                                  int32_t* elem_count, int64_t* stats, cudaStream_t st) {
-  k_find_prefilter<<<grid_for(n, 256), 256, 0, st>>>(m, n, x, order, cellid, best, npass, code,
-                                                     elem, r, dist, iters, values, C, elem_count,
-                                                     stats);
+cudaError_t launch_prefilter(const fpx_mesh_t& m, int mode, int64_t n, int64_t ncells_tot,
+                             const double* x, const int32_t* order, const int32_t* cellid,
+                             const int32_t* cell_off, int32_t* best, int32_t* npass,
+                             int32_t* code, int32_t* elem, double* r, double* dist,
+                             int32_t* iters, double* values, int C, int32_t* elem_count,
+                             int64_t* stats, cudaStream_t st) {
+  if (mode == 1) {
+    int64_t b = (ncells_tot + 3) / 4;
+    if (b > 148 * 64) b = 148 * 64;
+    if (b < 1) b = 1;
+    auto fn = m.d == 3 ? k_prefilter_cells<3> : k_prefilter_cells<2>;
+    fn<<<(unsigned)b, 128, 0, st>>>(m, ncells_tot, x, order, cell_off, best, npass, code, elem, r,
+                                    dist, iters, values, C, elem_count, stats);
+  } else {
+    auto fn = m.d == 3 ? k_prefilter_points<3> : k_prefilter_points<2>;
+    fn<<<grid_for(n, 256), 256, 0, st>>>(m, n, x, order, cellid, best, npass, code, elem, r, dist,
+                                         iters, values, C, elem_count, stats);
+  }
   return cudaGetLastError();
 }
 cudaError_t launch_point_cells(const fpx_mesh_t& m, int64_t n, const double* x, int32_t* cellid,
@@ -1023,24 +1004,4 @@ cudaError_t launch_point_scatter(int64_t n, const int32_t* cellid, const int32_t
   k_point_scatter<<<grid_for(n, 256), 256, 0, st>>>(n, cellid, cell_off, cursor, order);
   return cudaGetLastError();
 }
-cudaError_t launch_round2_emit(const fpx_mesh_t& m, int64_t nun_cap, const int64_t* nun_dev,
-                               const int32_t* upts, const double* x, const int32_t* best,
-                               const int32_t* skip2, const int64_t* pair_off, int64_t pair_cap,
-                               int32_t* pair_pt, int32_t* pair_elem, int32_t* elem_count,
-                               int64_t* stats, cudaStream_t st) {
-  k_round2_emit<<<grid_for(nun_cap, 128), 128, 0, st>>>(m, nun_dev, upts, x, best, skip2,
-                                                        pair_off, pair_cap, pair_pt, pair_elem,
-                                                        elem_count, stats);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_round_next_emit(const fpx_mesh_t& m, int64_t nun_cap, const int64_t* nun_dev,
-                                   const int32_t* upts, const double* x, const int32_t* best,
-                                   int32_t* tried2, int32_t* pair_pt, int32_t* pair_elem,
-                                   int32_t* elem_count, cudaStream_t st) {
-  k_round_next_emit<<<grid_for(nun_cap, 128), 128, 0, st>>>(m, nun_dev, upts, x, best, tried2,
-                                                            pair_pt, pair_elem, elem_count);
-  return cudaGetLastError();
-}
-
 }  // namespace fpx

@@ -7,6 +7,7 @@
 
 #define FPX_SETUP_MAXN 16  // setup kernels: nodes per axis <= 16 (p <= 15)
 #define FPX_ITEM 32        // (point|pair) slots per warp work item
+#define FPX_RK 16          // best-first ranked candidates listed per rest point
 
 namespace fpx {
 
@@ -37,25 +38,17 @@ cudaError_t launch_hash_sort(int64_t ncells, const int32_t* offsets, int32_t* el
                              int32_t* max_list, cudaStream_t st);
 cudaError_t launch_cell_of(int d, const double* grid, int n, int64_t npts, const double* x,
                            int64_t* cell, cudaStream_t st);
-cudaError_t launch_find_prefilter(const fpx_mesh_t& m, int64_t n, const double* x,
-                                  const int32_t* order, const int32_t* cellid, int32_t* best,
-                                  int32_t* npass, int32_t* code, int32_t* elem, double* r,
-                                  double* dist, int32_t* iters, double* values, int C,
-                                  int32_t* elem_count, int64_t* stats, cudaStream_t st);
+// mode 0: thread per point (k_prefilter_points); 1: warp per cell.
+cudaError_t launch_prefilter(const fpx_mesh_t& m, int mode, int64_t n, int64_t ncells_tot,
+                             const double* x, const int32_t* order, const int32_t* cellid,
+                             const int32_t* cell_off, int32_t* best, int32_t* npass,
+                             int32_t* code, int32_t* elem, double* r, double* dist,
+                             int32_t* iters, double* values, int C, int32_t* elem_count,
+                             int64_t* stats, cudaStream_t st);
 cudaError_t launch_point_cells(const fpx_mesh_t& m, int64_t n, const double* x, int32_t* cellid,
                                int32_t* cell_count, cudaStream_t st);
 cudaError_t launch_point_scatter(int64_t n, const int32_t* cellid, const int32_t* cell_off,
                                  int32_t* cursor, int32_t* order, cudaStream_t st);
-cudaError_t launch_round2_emit(const fpx_mesh_t& m, int64_t nun_cap, const int64_t* nun_dev,
-                               const int32_t* upts, const double* x, const int32_t* best,
-                               const int32_t* skip2, const int64_t* pair_off, int64_t pair_cap,
-                               int32_t* pair_pt, int32_t* pair_elem, int32_t* elem_count,
-                               int64_t* stats, cudaStream_t st);
-cudaError_t launch_round_next_emit(const fpx_mesh_t& m, int64_t nun_cap, const int64_t* nun_dev,
-                                   const int32_t* upts, const double* x, const int32_t* best,
-                                   int32_t* tried2, int32_t* pair_pt, int32_t* pair_elem,
-                                   int32_t* elem_count, cudaStream_t st);
-
 // Element grouping (fpx_group.cu): count -> packed scan -> items + scatter.
 cudaError_t launch_make_items(int64_t E, const int32_t* count, const uint64_t* packed_off,
                               Item* items, int64_t* nitems_dev, cudaStream_t st);
@@ -80,23 +73,17 @@ cudaError_t launch_newton_pairs(const fpx_mesh_t& m, const double* x, const int3
                                 const int64_t* nitems_dev, int64_t items_cap, int32_t* pcode,
                                 double* pr, double* pdist, int32_t* piters, int64_t* stats,
                                 cudaStream_t st);
-// Merge pairs into records (D6).  pair_off == NULL: one pair per point at
-// index u.  next_upts != NULL: points still unresolved with more than
-// `min_pass` passing candidates are appended to (next_upts, next_cnt, nnext)
-// instead of being evaluated.
-cudaError_t launch_newton_sparse(const fpx_mesh_t& m, const double* x, const int32_t* pair_pt,
-                                 const int32_t* pair_elem, const int64_t* npairs_dev, int64_t cap,
-                                 int32_t* pcode, double* pr, double* pdist, int32_t* piters,
-                                 int64_t* stats, cudaStream_t st);
-cudaError_t launch_round2_finalize(const fpx_mesh_t& m, int64_t nun_cap, const int64_t* nun_dev,
-                                   const int32_t* upts, const int64_t* pair_off,
-                                   int64_t pair_cap, const int32_t* pair_elem,
-                                   const int32_t* pcode, const double* pr, const double* pdist,
-                                   const int32_t* piters, int32_t* code, int32_t* elem, double* r,
-                                   double* dist, int32_t* iters, const double* field, int C,
-                                   double* values, const int32_t* npass, int min_pass,
-                                   int32_t* next_upts, int64_t* next_cnt, int64_t* nnext,
-                                   int64_t* stats, cudaStream_t st);
+// Remaining candidates of the points round 1 left unresolved: their
+// best-first candidate lists (k_rest_lists), then the lane-per-point Newton
+// (k_rest_lanes).
+cudaError_t launch_rest_lists(const fpx_mesh_t& m, const double* x, int64_t nun_cap,
+                              const int64_t* nun_dev, const int32_t* upts, int32_t* clist,
+                              int32_t* cnum, cudaStream_t st);
+cudaError_t launch_find_rest(const fpx_mesh_t& m, const double* x, int64_t nun_cap,
+                             const int64_t* nun_dev, const int32_t* upts, const int32_t* clist,
+                             const int32_t* cnum, int32_t* code, int32_t* elem, double* r,
+                             double* dist, int32_t* iters, const double* field, int C,
+                             double* values, int64_t* counter, int64_t* stats, cudaStream_t st);
 cudaError_t launch_eval_items(int dr, int Nf, const double* fbasis, int C, const double* field,
                               const double* r, const int32_t* sorted_pts, const Item* items,
                               const int64_t* nitems_dev, int64_t items_cap, double* values,

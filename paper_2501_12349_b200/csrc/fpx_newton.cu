@@ -66,27 +66,25 @@ cudaError_t launch_newton_pairs(const fpx_mesh_t& m, const double* x, const int3
                          items_cap, pcode, pr, pdist, piters, (int32_t*)nullptr, stats, st);
 }
 
-cudaError_t launch_newton_sparse(const fpx_mesh_t& m, const double* x, const int32_t* pair_pt,
-                                 const int32_t* pair_elem, const int64_t* npairs_dev, int64_t cap,
-                                 int32_t* pcode, double* pr, double* pdist, int32_t* piters,
-                                 int64_t* stats, cudaStream_t st) {
-  return dispatch<Sparse>(m.d, m.dr, m.N, m, x, pair_pt, pair_elem, npairs_dev, cap, pcode, pr,
-                          pdist, piters, stats, st);
+template <int D, int DR, int N>
+struct RestLists {
+  template <typename... A>
+  static cudaError_t run(A... a) { return Rest<D, DR, N>::lists(a...); }
+};
+
+cudaError_t launch_rest_lists(const fpx_mesh_t& m, const double* x, int64_t nun_cap,
+                              const int64_t* nun_dev, const int32_t* upts, int32_t* clist,
+                              int32_t* cnum, cudaStream_t st) {
+  return dispatch<RestLists>(m.d, m.dr, m.N, m, x, nun_cap, nun_dev, upts, clist, cnum, st);
 }
 
-cudaError_t launch_round2_finalize(const fpx_mesh_t& m, int64_t nun_cap, const int64_t* nun_dev,
-                                   const int32_t* upts, const int64_t* pair_off,
-                                   int64_t pair_cap, const int32_t* pair_elem,
-                                   const int32_t* pcode, const double* pr, const double* pdist,
-                                   const int32_t* piters, int32_t* code, int32_t* elem, double* r,
-                                   double* dist, int32_t* iters, const double* field, int C,
-                                   double* values, const int32_t* npass, int min_pass,
-                                   int32_t* next_upts, int64_t* next_cnt, int64_t* nnext,
-                                   int64_t* stats, cudaStream_t st) {
-  return dispatch<Finalize>(m.d, m.dr, m.N, m, nun_cap, nun_dev, upts, pair_off, pair_cap,
-                            pair_elem, pcode, pr, pdist, piters, code, elem, r, dist, iters,
-                            field, C, values, npass, min_pass, next_upts, next_cnt, nnext, stats,
-                            st);
+cudaError_t launch_find_rest(const fpx_mesh_t& m, const double* x, int64_t nun_cap,
+                             const int64_t* nun_dev, const int32_t* upts, const int32_t* clist,
+                             const int32_t* cnum, int32_t* code, int32_t* elem, double* r,
+                             double* dist, int32_t* iters, const double* field, int C,
+                             double* values, int64_t* counter, int64_t* stats, cudaStream_t st) {
+  return dispatch<Rest>(m.d, m.dr, m.N, m, x, nun_cap, nun_dev, upts, clist, cnum, code, elem, r,
+                        dist, iters, field, C, values, counter, stats, st);
 }
 
 cudaError_t launch_forward_map(const fpx_mesh_t& m, int64_t n, const int32_t* elem,

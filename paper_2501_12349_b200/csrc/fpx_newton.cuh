@@ -17,6 +17,7 @@
 
 #include "fpx_common.cuh"
 #include "fpx_kernels.cuh"
+#include "fpx_boxes.cuh"
 
 #ifndef FPX_NEWTON_MINB
 #define FPX_NEWTON_MINB 2  // CTAs of 128 threads per SM the Newton kernels are built for
@@ -78,16 +79,18 @@ struct Scratch {
 
 // Sum-factorised forward map x(r), G (+ second derivatives when W2), reduced
 // on the fly into the Newton state (Eqs. 28-29).
-template <int D, int DR, int N, bool W2, bool GEO = false>
+template <int D, int DR, int N, bool W2, int LAY = 0>
 __device__ __forceinline__ void eval_state(const double* __restrict__ sX,
                                            const double* __restrict__ z,
                                            const double* __restrict__ scale, const double* r,
                                            const double* xs, NState& S, double* sb) {
-  // GEO = false: geometry staged in shared memory, rows padded to NP;
-  // GEO = true: geometry read in place from global memory ([d][N^dr]).
+  // LAY 0: geometry staged in shared memory, rows padded to NP;
+  // LAY 1: read in place from global memory ([d][N^dr]);
+  // LAY 2: a per-lane shared slot holding [d][N^dr] unpadded.
   using Lp = Lay<D, DR, N>;
-  constexpr int GCS = GEO ? Lp::K : Lp::CS;
-  constexpr int GNP = GEO ? N : Lp::NP;
+  constexpr bool GEO = LAY == 1;
+  constexpr int GCS = LAY != 0 ? Lp::K : Lp::CS;
+  constexpr int GNP = LAY != 0 ? N : Lp::NP;
   double v0[N], g0[N], h0[N];
   lagrange<N, W2>(z, scale, r[0], v0, g0, h0);
 #pragma unroll
@@ -126,6 +129,7 @@ __device__ __forceinline__ void eval_state(const double* __restrict__ sX,
           for (int i = 0; i < N; i += 2) {
             double2 p;
             if (GEO) p = make_double2(__ldg(row + i), i + 1 < N ? __ldg(row + i + 1) : 0.0);
+            else if (LAY == 2) p = make_double2(row[i], i + 1 < N ? row[i + 1] : 0.0);
             else if (i + 1 < N) p = *reinterpret_cast<const double2*>(row + i);
             else p = make_double2(row[i], 0.0);
             s0 = fma(p.x, v0[i], s0);
@@ -370,12 +374,13 @@ __device__ __forceinline__ void unstash_state(const double* sb, NState& S) {
 // predicted decrease is formed before the trial evaluation, the current
 // state is stashed in the lane's shared scratch and restored only when the
 // step is rejected.  sb: this lane's scratch (stride 32 doubles).
-template <int D, int DR, int N, bool GEO = false>
+template <int D, int DR, int N, int LAY = 0>
 __device__ __forceinline__ NewtonOut newton_warp(const double* __restrict__ sX,
                                                  const double* __restrict__ z,
                                                  const double* __restrict__ scale,
                                                  const double* xs, bool active,
-                                                 const NewtonParams& P, double* sb) {
+                                                 const NewtonParams& P, double* sb,
+                                                 int64_t* nev = nullptr) {
   using L = Lay<D, DR, N>;
   double* stash = sb + Scratch<DR, N>::STASH * FPX_WARP;
   // seed: nearest GLL node, ties -> lowest lexicographic index (D7); the
@@ -389,7 +394,9 @@ __device__ __forceinline__ NewtonOut newton_warp(const double* __restrict__ sX,
       double dd = 0.0;
 #pragma unroll
       for (int c = 0; c < D; ++c) {
-        const double xn = GEO ? __ldg(sX + c * L::K + row * N + i) : sX[c * L::CS + row * L::NP + i];
+        const double xn = LAY == 1   ? __ldg(sX + c * L::K + row * N + i)
+                          : LAY == 2 ? sX[c * L::K + row * N + i]
+                                     : sX[c * L::CS + row * L::NP + i];
         const double t = __dsub_rn(xs[c], xn);
         dd = __fma_rn(t, t, dd);
       }
@@ -412,10 +419,15 @@ __device__ __forceinline__ NewtonOut newton_warp(const double* __restrict__ sX,
   int it = 0;
   bool done = !active, conv = false, first = true, step = active;
   while (true) {
-    if (__any_sync(FPX_FULL, step && on_boundary<DR>(rn)))
-      eval_state<D, DR, N, true, GEO>(sX, z, scale, rn, xs, st, sb);
+    const bool w2 = __any_sync(FPX_FULL, step && on_boundary<DR>(rn));
+    if (nev) {
+      nev[0] += 1;
+      nev[1] += w2 ? 1 : 0;
+    }
+    if (w2)
+      eval_state<D, DR, N, true, LAY>(sX, z, scale, rn, xs, st, sb);
     else
-      eval_state<D, DR, N, false, GEO>(sX, z, scale, rn, xs, st, sb);
+      eval_state<D, DR, N, false, LAY>(sX, z, scale, rn, xs, st, sb);
     // lanes not stepping evaluated at rn == r: their state is recomputed
     // bit-identically (eval_state is a pure function of r)
     if (first) {
@@ -652,10 +664,11 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
   __syncthreads();
   const NewtonParams P = newton_of(m);
   const int64_t nitems = *nitems_dev;
-  int64_t s_newton = 0, s_iters = 0, s_evals = 0;
+  int64_t s_newton = 0, s_iters = 0, s_evals = 0, nev[2] = {0, 0}, s_items = 0;
   for (int64_t w = (int64_t)blockIdx.x * wpb + warp; w < nitems; w += (int64_t)gridDim.x * wpb) {
     const Item itm = items[w];
     const int e = itm.elem;
+    ++s_items;
     stage_block<DR, N>(sX, m.nodes + (int64_t)e * D * L::K, D, lane);
     if (field) stage_block<DR, N>(sU, field + (int64_t)e * C * L::K, C, lane);
     cp_async_wait_all();
@@ -666,7 +679,7 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
     if (active)
 #pragma unroll
       for (int c = 0; c < D; ++c) xs[c] = x[(int64_t)pt * D + c];
-    NewtonOut o = newton_warp<D, DR, N>(sX, z, scale, xs, active, P, sb);
+    NewtonOut o = newton_warp<D, DR, N>(sX, z, scale, xs, active, P, sb, nev);
     if (active) {
       s_newton += 1;
       s_iters += o.iters;
@@ -689,7 +702,7 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
       } else {
         const int slot = (int)atomicAdd((unsigned long long*)nun_dev, 1ull);
         upts[slot] = pt;
-        upair_cnt[slot] = npass[pt] - 1;
+        if (upair_cnt) upair_cnt[slot] = npass[pt] - 1;
       }
     }
     __syncwarp();
@@ -704,6 +717,9 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
     atomicAdd((unsigned long long*)&stats[FPX_STAT_NEWTON_R1], (unsigned long long)s_newton);
     atomicAdd((unsigned long long*)&stats[FPX_STAT_ITERS_R1], (unsigned long long)s_iters);
     atomicAdd((unsigned long long*)&stats[FPX_STAT_EVALS_R1], (unsigned long long)s_evals);
+    atomicAdd((unsigned long long*)&stats[FPX_STAT_R1_WARP_EVALS], (unsigned long long)nev[0]);
+    atomicAdd((unsigned long long*)&stats[FPX_STAT_R1_W2_EVALS], (unsigned long long)nev[1]);
+    atomicAdd((unsigned long long*)&stats[FPX_STAT_R1_ITEMS], (unsigned long long)s_items);
   }
 }
 
@@ -768,138 +784,415 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
   }
 }
 
-// Sparse rounds (2 and 3): one (point, element) pair per lane, geometry read
-// in place from global memory (L1/L2) -- no element grouping.  The rounds
-// carry ~1 pair per element, where the element-major mapping would leave a
-// warp with one active lane.
+// The projected trust-region step from state st at r (D8; the same
+// arithmetic as newton_warp).  Returns false when the predicted decrease is
+// below what |dx|^2 resolves (converged); else the trial point rn.
+template <int DR>
+__device__ __forceinline__ bool propose_step(const NState& st, const double* r, int it,
+                                             double alpha, double* rn, double& pred,
+                                             double& smax) {
+  const double fcur = st.f;
+  const bool beta = it > 0 && on_boundary<DR>(r);
+  bool freem[3] = {true, true, true};
+#pragma unroll
+  for (int a = 0; a < DR; ++a)
+    if ((r[a] == 1.0 && st.J[a] < 0.0) || (r[a] == -1.0 && st.J[a] > 0.0)) freem[a] = false;
+  double Hm[6], s[3] = {0.0, 0.0, 0.0};
+  int hit = 0;
+  bool ok = false;
+#pragma unroll 1
+  for (int att = beta ? 0 : 1; att < 3 && !ok; ++att) {
+    double lam = 0.0;
+    if (att == 2) {
+      double tr = 0.0;
+#pragma unroll
+      for (int a = 0; a < DR; ++a) tr += st.H0[a];
+      lam = 1e-10 * tr / DR;
+      if (!(lam > 0.0)) lam = 1e-300;
+    }
+#pragma unroll
+    for (int m = 0; m < 6; ++m)
+      Hm[m] = att == 0 ? st.H0[m] - st.Q[m] : st.H0[m] + (m < DR ? lam : 0.0);
+    bool fr[3] = {freem[0], freem[1], freem[2]};
+    ok = constrained_step<DR>(Hm, st.J, r, fr, alpha, s, hit);
+  }
+  if (!ok) {
+    hit = 0;
+#pragma unroll
+    for (int a = 0; a < DR; ++a) s[a] = 0.0;
+  }
+  double js = 0.0, shs = 0.0;
+  smax = 0.0;
+#pragma unroll
+  for (int a = 0; a < DR; ++a) {
+    js += st.J[a] * s[a];
+    double t = 0.0;
+#pragma unroll
+    for (int b = 0; b < DR; ++b) t += Hm[symi(a, b)] * s[b];
+    shs += s[a] * t;
+    smax = fabs(s[a]) > smax ? fabs(s[a]) : smax;
+  }
+  pred = -(2.0 * js + shs);
+  if (!(pred > 1e-15 * fcur)) return false;
+#pragma unroll
+  for (int a = 0; a < DR; ++a) {
+    double v = r[a] + s[a];
+    if (hit & (1 << a)) v = s[a] > 0.0 ? 1.0 : -1.0;  // lands on the face
+    v = v < -1.0 ? -1.0 : (v > 1.0 ? 1.0 : v);
+    rn[a] = v;
+  }
+  return true;
+}
+
+// ---------------------------------------------------------------- rest kernel
+// Points left unresolved by round 1 (a BORDER record with more than one
+// passing candidate, ~5% of the points) visit their remaining candidates in
+// best-first order, stop at the first INTERIOR and otherwise keep the D6
+// winner.  These (point, candidate) pairs hit ~1 pair per element, so the
+// element-major mapping of round 1 would run warps with one live lane.
+// Instead every lane owns one point and a private shared-memory slot for
+// its current candidate's geometry: the lanes run their own Newton solves in
+// lockstep (one warp-uniform map evaluation per pass, as in round 1), and a
+// lane whose candidate finished picks its next candidate (or point) at once,
+// so no lane waits for the slowest one.  The warp cooperates on the
+// irregular parts: the geometry copies (cp.async, completion on the owning
+// lane's mbarrier, polled without blocking) and the nearest-node seeds.
+// Slot stride is odd in doubles, so the 32 lanes' 8-byte loads at equal
+// offsets fall into distinct bank pairs.
+
 template <int D, int DR, int N>
-__global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
-    k_newton_sparse(fpx_mesh_t m, const double* __restrict__ x,
-                    const int32_t* __restrict__ pair_pt, const int32_t* __restrict__ pair_elem,
-                    const int64_t* __restrict__ npairs_dev, int32_t* pcode, double* pr,
-                    double* pdist, int32_t* piters, int64_t* stats) {
-  using L = Lay<D, DR, N>;
+struct RestLay {
+  static constexpr int K = Pow<DR, N>::K;
+  static constexpr int SS = (D * K) | 1;                 // slot stride (doubles)
+  static constexpr int SCR = Scratch<DR, N>::SLOTS;      // per-lane scratch slots
+  static constexpr size_t lane_bytes() { return (size_t)(SS + SCR) * 8 + 8; }
+};
+
+__device__ __forceinline__ void mbar_init(uint64_t* mb, unsigned count) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(mb);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* mb) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(mb);
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* mb, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(mb);
+  unsigned ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      " selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(a), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+
+// Best-first ranked candidate lists of the rest points: the passing
+// entries of the hash list sorted by (v, e), FPX_RK per point
+// kept; beyond that the rest kernel scans the list itself.
+template <int D>
+__global__ void __launch_bounds__(128)
+    k_rest_lists(fpx_mesh_t m, const double* __restrict__ x, const int64_t* __restrict__ nun_dev,
+                 const int32_t* __restrict__ upts, int32_t* clist, int32_t* cnum) {
+  // warp per rest point: lanes over hash-list chunks, rank of each passing
+  // entry = number of passing entries before it in (v, e) order
+  __shared__ double s_v[4][FPX_WARP];
+  __shared__ int s_e[4][FPX_WARP];
+  const int warp = threadIdx.x / FPX_WARP, lane = threadIdx.x % FPX_WARP;
+  const int64_t nun = *nun_dev;
+  for (int64_t u = (int64_t)blockIdx.x * 4 + warp; u < nun; u += (int64_t)gridDim.x * 4) {
+    const int64_t k = upts[u];
+    double xs[D];
+#pragma unroll
+    for (int c = 0; c < D; ++c) xs[c] = x[k * D + c];
+    int ax[3];
+    const int64_t cell = cell_of(D, m.grid, m.ncell, xs, ax);
+    const int qs = cell >= 0 ? m.offsets[cell] : 0, qe = cell >= 0 ? m.offsets[cell + 1] : 0;
+    int np = 0;
+    for (int q0 = qs; q0 < qe; q0 += FPX_WARP) {
+      const int q = q0 + lane;
+      const int e = q < qe ? m.elems[q] : -1;
+      const bool pass = e >= 0 && candidate_passes_t<D>(m, e, xs);
+      const double v = pass ? bestfirst_value(D, m.frame + (int64_t)e * (D + D * D), xs) : 0.0;
+      np += __popc(__ballot_sync(FPX_FULL, pass));
+    }
+    // ranks: every passing entry against every passing entry (chunks)
+    for (int q0 = qs; q0 < qe; q0 += FPX_WARP) {
+      const int q = q0 + lane;
+      const int e = q < qe ? m.elems[q] : -1;
+      const bool pass = e >= 0 && candidate_passes_t<D>(m, e, xs);
+      const double v = pass ? bestfirst_value(D, m.frame + (int64_t)e * (D + D * D), xs) : 0.0;
+      int rank = 0;
+      for (int p0 = qs; p0 < qe; p0 += FPX_WARP) {
+        const int pq = p0 + lane;
+        const int pe = pq < qe ? m.elems[pq] : -1;
+        const bool pp = pe >= 0 && candidate_passes_t<D>(m, pe, xs);
+        __syncwarp();
+        s_v[warp][lane] = pp ? bestfirst_value(D, m.frame + (int64_t)pe * (D + D * D), xs) : 0.0;
+        s_e[warp][lane] = pe;
+        __syncwarp();
+        const unsigned pm = __ballot_sync(FPX_FULL, pp);
+        if (pass)
+          for (unsigned mm = pm; mm; mm &= mm - 1) {
+            const int j = __ffs(mm) - 1;
+            rank += bf_less(s_v[warp][j], s_e[warp][j], v, e) ? 1 : 0;
+          }
+      }
+      if (pass && rank < FPX_RK) clist[u * FPX_RK + rank] = e;
+    }
+    if (lane == 0) cnum[u] = np > FPX_RK ? -FPX_RK : np;  // negative: more beyond the list
+  }
+}
+
+template <int D, int DR, int N, int LANES>
+__global__ void __launch_bounds__(64, 1)
+    k_rest_lanes(fpx_mesh_t m, const double* __restrict__ x, const int64_t* __restrict__ nun_dev,
+                 const int32_t* __restrict__ upts, const int32_t* __restrict__ clist,
+                 const int32_t* __restrict__ cnum, int32_t* code, int32_t* elem, double* r,
+                 double* dist, int32_t* iters, const double* __restrict__ field, int C,
+                 double* values, int64_t* counter, int64_t* stats) {
+  using RL = RestLay<D, DR, N>;
+  constexpr int K = RL::K;
   extern __shared__ __align__(16) double smem[];
   double* z = smem;
   double* scale = smem + N;
   const int warp = threadIdx.x / FPX_WARP, lane = threadIdx.x % FPX_WARP;
-  const int wpb = blockDim.x / FPX_WARP;
-  constexpr int SCR = Scratch<DR, N>::SLOTS * FPX_WARP;
-  double* sb = smem + 2 * ((N + 1) & ~1) + warp * SCR + lane;
+  double* slots = smem + 2 * ((N + 1) & ~1) + (size_t)warp * (LANES * RL::SS + RL::SCR * FPX_WARP);
+  const bool live = lane < LANES;
+  double* mine = slots + (live ? lane : 0) * RL::SS;
+  double* sb = slots + LANES * RL::SS + lane;  // per-lane scratch, stride 32
+  double* stash = sb + Scratch<DR, N>::STASH * FPX_WARP;
+  uint64_t* mbars = reinterpret_cast<uint64_t*>(smem + 2 * ((N + 1) & ~1) +
+                                                (size_t)(blockDim.x / FPX_WARP) *
+                                                    (LANES * RL::SS + RL::SCR * FPX_WARP)) +
+                    warp * FPX_WARP;
   if (threadIdx.x < N) {
     z[threadIdx.x] = m.basis[FPX_BASIS_NODES(N, m.M) + threadIdx.x];
     scale[threadIdx.x] = m.basis[FPX_BASIS_SCALE(N, m.M) + threadIdx.x];
   }
+  if (live) {
+    for (int t = 0; t < RL::SS; ++t) mine[t] = 0.0;  // idle lanes evaluate finite data
+    mbar_init(&mbars[lane], FPX_WARP);
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   __syncthreads();
   const NewtonParams P = newton_of(m);
-  const int64_t npairs = *npairs_dev;
-  int64_t s_newton = 0, s_iters = 0;
-  // whole warps stride over the pairs so every lane reaches the shuffles
-  for (int64_t base = ((int64_t)blockIdx.x * wpb + warp) * FPX_WARP; base < npairs;
-       base += (int64_t)gridDim.x * wpb * FPX_WARP) {
-    const int64_t p = base + lane;
-    const int e = p < npairs ? pair_elem[p] : -1;
-    const bool active = e >= 0;
-    const int pt = active ? pair_pt[p] : 0;
-    double xs[3] = {0.0, 0.0, 0.0};
-    if (active)
+  const int64_t nun = *nun_dev;
+  int64_t s_newton = 0, s_iters = 0, s_evals = 0;
+  // point state
+  bool have_point = false, point_done = false;
+  int64_t u = 0, k = 0;
+  double xs[3] = {0.0, 0.0, 0.0};
+  int bc = -1, be = -1, it_tot = 0, rank = 0, nlist = 0, te = -1, qs = 0, qe = 0;
+  bool over = false;
+  double bd = INFINITY, br[3] = {0.0, 0.0, 0.0}, tv = -INFINITY;
+  // candidate state: 0 needs a candidate, 1 copy requested, 2 copy in flight,
+  // 3 iterating, 4 no work left
+  int phase = live ? 0 : 4;
+  unsigned parity = 0;
+  int e = -1, it = 0;
+  bool first = true;
+  double rc[3] = {0.0, 0.0, 0.0}, rn[3] = {0.0, 0.0, 0.0};
+  double alpha = 1.0, fcur = 0.0, pred = 0.0, smax = 0.0;
+  NState st;
+  while (true) {
+    // (a) lanes without a candidate pick the next one (or finish the point)
+    if (phase == 0) {
+      while (true) {
+        if (!have_point) {
+          u = (int64_t)atomicAdd((unsigned long long*)counter, 1ull);
+          if (u >= nun) {
+            phase = 4;
+            break;
+          }
+          k = upts[u];
 #pragma unroll
-      for (int c = 0; c < D; ++c) xs[c] = x[(int64_t)pt * D + c];
-    const double* X = m.nodes + (int64_t)(active ? e : 0) * D * L::K;
-    NewtonOut o = newton_warp<D, DR, N, true>(X, z, scale, xs, active, P, sb);
-    if (active) {
+          for (int c = 0; c < D; ++c) xs[c] = x[k * D + c];
+          bc = code[k];
+          be = elem[k];
+          bd = dist[k];
+#pragma unroll
+          for (int a = 0; a < DR; ++a) br[a] = r[k * DR + a];
+          it_tot = iters ? iters[k] : 0;
+          const int cn = cnum[u];
+          nlist = cn < 0 ? -cn : cn;
+          over = cn < 0;
+          rank = 1;  // rank 0 is round 1's candidate
+          have_point = true;
+          point_done = false;
+        }
+        e = -1;
+        if (!point_done) {
+          if (rank < nlist) {
+            e = clist[u * FPX_RK + rank++];
+            if (rank == nlist && over) {  // continue after the last listed one
+              tv = bestfirst_value(D, m.frame + (int64_t)e * (D + D * D), xs);
+              te = e;
+              int ax[3];
+              const int64_t cell = cell_of(D, m.grid, m.ncell, xs, ax);
+              qs = m.offsets[cell];
+              qe = m.offsets[cell + 1];
+            }
+          } else if (over) {
+            double bv = INFINITY;
+            int bb = 0x7fffffff;
+            for (int q = qs; q < qe; ++q) {
+              const int ee = m.elems[q];
+              if (!candidate_passes_t<D>(m, ee, xs)) continue;
+              const double v = bestfirst_value(D, m.frame + (int64_t)ee * (D + D * D), xs);
+              if (bf_less(tv, te, v, ee) && bf_less(v, ee, bv, bb)) {
+                bv = v;
+                bb = ee;
+              }
+            }
+            if (bb != 0x7fffffff) {
+              e = bb;
+              tv = bv;
+              te = bb;
+            }
+          }
+        }
+        if (e >= 0) {
+          phase = 1;
+          break;
+        }
+        // the point is complete: record (+ field value)
+        code[k] = bc;
+        elem[k] = be;
+        dist[k] = bd;
+        if (iters) iters[k] = it_tot;
+#pragma unroll
+        for (int a = 0; a < DR; ++a) r[k * DR + a] = br[a];
+        if (field) {
+          double v[DR][N];
+          basis_values<DR, N>(z, scale, br, v);
+          for (int c = 0; c < C; ++c)
+            values[k * C + c] = contract_gmem<DR, N>(field + ((int64_t)be * C + c) * K, v);
+          ++s_evals;
+        }
+        have_point = false;
+      }
+    }
+    // (b) the warp copies the requested candidates' geometry into their
+    // owners' slots; every lane arrives on the owner's mbarrier
+    for (unsigned req = __ballot_sync(FPX_FULL, phase == 1); req; req &= req - 1) {
+      const int j = __ffs(req) - 1;
+      const int ej = __shfl_sync(FPX_FULL, e, j);
+      const double* src = m.nodes + (int64_t)ej * D * K;
+      double* dst = slots + j * RL::SS;
+      for (int t = lane; t < D * K; t += FPX_WARP) cp_async8(dst + t, src + t);
+      cp_async_arrive_noinc(&mbars[j]);
+    }
+    if (phase == 1) phase = 2;
+    // (c) lanes whose copy landed get their seed (warp-cooperative, D7)
+    const bool landed = phase == 2 && mbar_test(&mbars[lane], parity);
+    if (landed) parity ^= 1u;
+    for (unsigned rdy = __ballot_sync(FPX_FULL, landed); rdy; rdy &= rdy - 1) {
+      const int j = __ffs(rdy) - 1;
+      double xj[3];
+#pragma unroll
+      for (int c = 0; c < D; ++c) xj[c] = __shfl_sync(FPX_FULL, xs[c], j);
+      const double* sj = slots + j * RL::SS;
+      double best = INFINITY;
+      int bi = 0x7fffffff;
+      for (int t = lane; t < K; t += FPX_WARP) {
+        double dd = 0.0;
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          const double tt = __dsub_rn(xj[c], sj[c * K + t]);
+          dd = __fma_rn(tt, tt, dd);
+        }
+        if (dd < best) {
+          best = dd;
+          bi = t;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(FPX_FULL, best, o);
+        const int oi = __shfl_xor_sync(FPX_FULL, bi, o);
+        if (ob < best || (ob == best && oi < bi)) {
+          best = ob;
+          bi = oi;
+        }
+      }
+      if (lane == j) {
+        rc[0] = z[bi % N];
+        rc[1] = DR > 1 ? z[(bi / N) % N] : 0.0;
+        rc[2] = DR > 2 ? z[bi / (N * N)] : 0.0;
+      }
+    }
+    if (landed) {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) rn[a] = rc[a];
+      first = true;
+      it = 0;
+      alpha = P.alpha0;
+      phase = 3;
+    }
+    if (!__any_sync(FPX_FULL, phase != 4)) break;
+    if (!__any_sync(FPX_FULL, phase == 3)) continue;  // copies in flight
+    // (d) one map evaluation for every lane of the warp
+    if (__any_sync(FPX_FULL, phase == 3 && on_boundary<DR>(rn)))
+      eval_state<D, DR, N, true, 2>(mine, z, scale, rn, xs, st, sb);
+    else
+      eval_state<D, DR, N, false, 2>(mine, z, scale, rn, xs, st, sb);
+    if (phase != 3) continue;
+    // (e) this lane's trust-region Newton update (as newton_warp, D8)
+    bool done = false;
+    if (first) {
+      first = false;
+    } else {
+      const double decr = fcur - st.f;
+      if (decr >= P.accept * pred) {
+        if (decr >= P.keep * pred) alpha *= P.grow;
+#pragma unroll
+        for (int a = 0; a < DR; ++a) rc[a] = rn[a];
+      } else {
+        alpha *= P.shrink;
+        unstash_state(stash, st);
+        st.f = fcur;
+      }
+      if (smax < P.tol) done = true;
+      else if (it >= P.max_iters) done = true;
+    }
+    if (!done) {
+      fcur = st.f;
+      const bool go = propose_step<DR>(st, rc, it, alpha, rn, pred, smax);
+      ++it;
+      if (!go) done = true;
+      else stash_state(stash, st);
+    }
+    if (done) {
+      const double dd = sqrt(st.f);
       s_newton += 1;
-      s_iters += o.iters;
+      s_iters += it;
+      it_tot += it;
       const double epsd = DR < D ? eps_d_of(m, e) : 0.0;
-      pcode[p] = classify<D, DR>(o.r, o.dist, epsd);
+      const int cd = classify<D, DR>(rc, dd, epsd);
+      bool take;
+      if (cd == kInterior) take = bc != kInterior || e < be;
+      else take = bc != kInterior && (dd < bd || (dd == bd && e < be));
+      if (take) {
+        bc = cd;
+        be = e;
+        bd = dd;
 #pragma unroll
-      for (int a = 0; a < DR; ++a) pr[p * DR + a] = o.r[a];
-      pdist[p] = o.dist;
-      if (piters) piters[p] = o.iters;
+        for (int a = 0; a < DR; ++a) br[a] = rc[a];
+      }
+      if (bc == kInterior) point_done = true;
+      phase = 0;
     }
   }
   s_newton = warp_sum64(s_newton);
   s_iters = warp_sum64(s_iters);
+  s_evals = warp_sum64(s_evals);
   if (lane == 0) {
     atomicAdd((unsigned long long*)&stats[FPX_STAT_NEWTON], (unsigned long long)s_newton);
     atomicAdd((unsigned long long*)&stats[FPX_STAT_ITERS], (unsigned long long)s_iters);
+    if (s_evals) atomicAdd((unsigned long long*)&stats[FPX_STAT_EVALS], (unsigned long long)s_evals);
   }
-}
-
-// Merge of a round's pairs into the points' records (winner rule D6 over the
-// current record and the pairs: INTERIOR (lowest id) > min d* (ties lowest
-// id)).  pair_off == NULL: one pair per point at index u (next-best round).
-// Points still unresolved that have more than `min_pass` passing candidates
-// go to the next round when next_upts != NULL; all others are final and get
-// their field value.
-template <int D, int DR, int N>
-__global__ void k_round2_finalize(fpx_mesh_t m, const int64_t* __restrict__ nun_dev,
-                                  const int32_t* __restrict__ upts,
-                                  const int64_t* __restrict__ pair_off, int64_t pair_cap,
-                                  const int32_t* __restrict__ pair_elem,
-                                  const int32_t* __restrict__ pcode, const double* __restrict__ pr,
-                                  const double* __restrict__ pdist,
-                                  const int32_t* __restrict__ piters, int32_t* code, int32_t* elem,
-                                  double* r, double* dist, int32_t* iters,
-                                  const double* __restrict__ field, int C, double* values,
-                                  const int32_t* __restrict__ npass, int min_pass,
-                                  int32_t* next_upts, int64_t* next_cnt, int64_t* nnext,
-                                  int64_t* stats) {
-  __shared__ double z[16], scale[16];
-  if (threadIdx.x < N) {
-    z[threadIdx.x] = m.basis[FPX_BASIS_NODES(N, m.M) + threadIdx.x];
-    scale[threadIdx.x] = m.basis[FPX_BASIS_SCALE(N, m.M) + threadIdx.x];
-  }
-  __syncthreads();
-  const int64_t nun = *nun_dev;
-  int64_t s_evals = 0;
-  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < nun;
-       u += (int64_t)gridDim.x * blockDim.x) {
-    const int k = upts[u];
-    int bc = code[k], be = elem[k];
-    double bd = dist[k];
-    double br[3] = {0, 0, 0};
-    for (int a = 0; a < DR; ++a) br[a] = r[(int64_t)k * DR + a];
-    int it = iters ? iters[k] : 0;
-    const int64_t p0 = pair_off ? pair_off[u] : u, p1 = pair_off ? pair_off[u + 1] : u + 1;
-    for (int64_t p = p0; p < p1 && p < pair_cap; ++p) {
-      const int e = pair_elem[p];
-      if (e < 0) continue;
-      const int c = pcode[p];
-      const double dd = pdist[p];
-      if (piters) it += piters[p];
-      bool take;
-      if (c == kInterior) take = bc != kInterior || e < be;
-      else take = bc != kInterior && (dd < bd || (dd == bd && e < be));
-      if (take) {
-        bc = c;
-        be = e;
-        bd = dd;
-        for (int a = 0; a < DR; ++a) br[a] = pr[p * DR + a];
-      }
-    }
-    code[k] = bc;
-    elem[k] = be;
-    dist[k] = bd;
-    for (int a = 0; a < DR; ++a) r[(int64_t)k * DR + a] = br[a];
-    if (iters) iters[k] = it;
-    if (next_upts && bc != kInterior && npass[k] > min_pass) {
-      const int slot = (int)atomicAdd((unsigned long long*)nnext, 1ull);
-      next_upts[slot] = k;
-      next_cnt[slot] = npass[k] - min_pass;
-      continue;
-    }
-    if (field) {
-      double v[DR][N];
-      basis_values<DR, N>(z, scale, br, v);
-      for (int c = 0; c < C; ++c)
-        values[(int64_t)k * C + c] =
-            contract_gmem<DR, N>(field + ((int64_t)be * C + c) * Pow<DR, N>::K, v);
-      ++s_evals;
-    }
-  }
-  if (field && s_evals)
-    atomicAdd((unsigned long long*)&stats[FPX_STAT_EVALS], (unsigned long long)s_evals);
 }
 
 // findpts_eval over element-grouped records: warp per item, field block in
@@ -1046,39 +1339,40 @@ struct Pairs {
 };
 
 template <int D, int DR, int N>
-struct Sparse {
-  static cudaError_t run(const fpx_mesh_t& m, const double* x, const int32_t* pair_pt,
-                         const int32_t* pair_elem, const int64_t* npairs_dev, int64_t cap,
-                         int32_t* pcode, double* pr, double* pdist, int32_t* piters,
-                         int64_t* stats, cudaStream_t st) {
-    const int threads = 128;
-    const size_t smem = newton_smem(Scratch<DR, N>::SLOTS * FPX_WARP, 0, N, threads / FPX_WARP);
-    auto fn = k_newton_sparse<D, DR, N>;
+struct Rest {
+  using RL = RestLay<D, DR, N>;
+  // lanes per warp whose slots fit two warps (or one) in ~220 KB of smem
+  static constexpr size_t BUDGET = 220 * 1024;
+  static constexpr int L2W = (int)((BUDGET / 2) / RL::lane_bytes());
+  static constexpr int L1W = (int)(BUDGET / RL::lane_bytes());
+  static constexpr int WARPS = L2W >= 16 ? 2 : 1;
+  static constexpr int LANES0 = WARPS == 2 ? L2W : L1W;
+  static constexpr int LANES = LANES0 > 32 ? 32 : (LANES0 < 1 ? 1 : LANES0);
+  static cudaError_t run(const fpx_mesh_t& m, const double* x, int64_t nun_cap,
+                         const int64_t* nun_dev, const int32_t* upts, const int32_t* clist,
+                         const int32_t* cnum, int32_t* code, int32_t* elem, double* r,
+                         double* dist, int32_t* iters, const double* field, int C,
+                         double* values, int64_t* counter, int64_t* stats, cudaStream_t st) {
+    const int threads = WARPS * FPX_WARP;
+    const size_t smem = (size_t)(2 * ((N + 1) & ~1)) * 8 +
+                        (size_t)WARPS * (LANES * RL::SS + RL::SCR * FPX_WARP) * 8 +
+                        (size_t)WARPS * FPX_WARP * 8;
+    auto fn = k_rest_lanes<D, DR, N, LANES>;
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     unsigned blocks = persistent_blocks((const void*)fn, threads, smem,
-                                        (cap + FPX_WARP - 1) / FPX_WARP);
-    fn<<<blocks, threads, smem, st>>>(m, x, pair_pt, pair_elem, npairs_dev, pcode, pr, pdist,
-                                      piters, stats);
+                                        (nun_cap + LANES - 1) / LANES);
+    fn<<<blocks, threads, smem, st>>>(m, x, nun_dev, upts, clist, cnum, code, elem, r, dist, iters,
+                                      field, C, values, counter, stats);
     return cudaGetLastError();
   }
-};
-
-template <int D, int DR, int N>
-struct Finalize {
-  static cudaError_t run(const fpx_mesh_t& m, int64_t nun_cap, const int64_t* nun_dev,
-                         const int32_t* upts, const int64_t* pair_off, int64_t pair_cap,
-                         const int32_t* pair_elem, const int32_t* pcode, const double* pr,
-                         const double* pdist, const int32_t* piters, int32_t* code, int32_t* elem,
-                         double* r, double* dist, int32_t* iters, const double* field, int C,
-                         double* values, const int32_t* npass, int min_pass, int32_t* next_upts,
-                         int64_t* next_cnt, int64_t* nnext, int64_t* stats, cudaStream_t st) {
-    int64_t b = (nun_cap + 127) / 128;
+  static cudaError_t lists(const fpx_mesh_t& m, const double* x, int64_t nun_cap,
+                           const int64_t* nun_dev, const int32_t* upts, int32_t* clist,
+                           int32_t* cnum, cudaStream_t st) {
+    int64_t b = (nun_cap + 3) / 4;
     if (b > 148 * 16) b = 148 * 16;
     if (b < 1) b = 1;
-    k_round2_finalize<D, DR, N><<<(unsigned)b, 128, 0, st>>>(
-        m, nun_dev, upts, pair_off, pair_cap, pair_elem, pcode, pr, pdist, piters, code, elem, r,
-        dist, iters, field, C, values, npass, min_pass, next_upts, next_cnt, nnext, stats);
+    k_rest_lists<D><<<(unsigned)b, 128, 0, st>>>(m, x, nun_dev, upts, clist, cnum);
     return cudaGetLastError();
   }
 };

@@ -17,6 +17,9 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field as dfield
 
+from collections.abc import Mapping
+import os
+
 import numpy as np
 import torch
 
@@ -41,8 +44,8 @@ class EngineOptions:
     newton: NewtonSettings = dfield(default_factory=NewtonSettings)
     eps_d: float | None = None        # absolute surface threshold; None -> relative
     eps_d_rel: float = 1e-10
-    pair_capacity: float = 2.0        # round-2 pair workspace, x n (grows on demand)
-    hash_refine: int = 2              # local cells per axis = hash_refine * SPEC rule (perf only)
+    # local cells per axis = hash_refine * SPEC rule (perf only; FPX_HASH_REFINE overrides)
+    hash_refine: int = dfield(default_factory=lambda: int(os.environ.get("FPX_HASH_REFINE", "2")))
 
 
 @dataclass
@@ -203,6 +206,31 @@ def _stats_dict(st: np.ndarray) -> dict:
     return {k: int(v) for k, v in zip(_C.STAT_NAMES, st)}
 
 
+class DeviceStats(Mapping):
+    """The kernel counters of one find (int64[FPX_STATS_LEN] on the device),
+    read back on first access so a find does not synchronise the stream."""
+
+    def __init__(self, t: torch.Tensor):
+        self._t, self._d = t, None
+
+    def _load(self) -> dict:
+        if self._d is None:
+            self._d = _stats_dict(self._t.cpu().numpy())
+        return self._d
+
+    def __getitem__(self, k):
+        return self._load()[k]
+
+    def __iter__(self):
+        return iter(self._load())
+
+    def __len__(self) -> int:
+        return _C.STATS_LEN
+
+    def __repr__(self) -> str:
+        return repr(self._load())
+
+
 def _find_local(S: EngineSetup, x: torch.Tensor, field: Field | None = None,
                 want_iters: bool = False):
     """Phase A on this rank: the fpx_find kernel pipeline.  Returns a dict of
@@ -224,18 +252,13 @@ def _find_local(S: EngineSetup, x: torch.Tensor, field: Field | None = None,
     stats = torch.zeros(_C.STATS_LEN, dtype=torch.int64, device=dev)
     if n == 0:
         return out, _stats_dict(np.zeros(_C.STATS_LEN, np.int64))
-    cap = max(1024, int(S.options.pair_capacity * n))
-    while True:
-        ws = _workspace(S, n, cap)
-        _C.check(_C.lib().fpx_find(
-            S.mesh_t, n, _C.ptr(x), _C.ptr(out["code"]), _C.ptr(out["elem"]), _C.ptr(out["r"]),
-            _C.ptr(out["dist"]), _C.ptr(out["iters"]), _C.ptr(blocks), C,
-            _C.ptr(out.get("values")), _C.ptr(stats), cap, _C.ptr(ws), ws.numel(),
-            _C.stream_handle()), "fpx_find")
-        st = stats.cpu().numpy()   # synchronises: records are complete here
-        if st[_C.STAT_NAMES.index("overflow")] == 0:
-            return out, _stats_dict(st)
-        cap = int(st[_C.STAT_NAMES.index("round2_pairs")]) + 1024   # rerun, exact size
+    ws = _workspace(S, n, n)
+    _C.check(_C.lib().fpx_find(
+        S.mesh_t, n, _C.ptr(x), _C.ptr(out["code"]), _C.ptr(out["elem"]), _C.ptr(out["r"]),
+        _C.ptr(out["dist"]), _C.ptr(out["iters"]), _C.ptr(blocks), C,
+        _C.ptr(out.get("values")), _C.ptr(stats), n, _C.ptr(ws), ws.numel(),
+        _C.stream_handle()), "fpx_find")
+    return out, DeviceStats(stats)
 
 
 def _prep_points(S: EngineSetup, x) -> torch.Tensor:
