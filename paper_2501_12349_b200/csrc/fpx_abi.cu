@@ -134,7 +134,7 @@ struct Group {
 
 struct FindWs {
   int32_t *best, *npass, *upts, *clist, *cnum;
-  int64_t *nun, *counter;
+  int64_t *nun, *counter, *chunk_ctr;
   Group g1;
   // point ordering by hash cell
   int32_t *cellid, *cell_count, *cell_off, *cell_cursor, *order;
@@ -159,6 +159,7 @@ struct FindWs {
     cnum = c.take<int32_t>(n);
     nun = c.take<int64_t>(1);
     counter = c.take<int64_t>(1);
+    chunk_ctr = c.take<int64_t>(1);
     g1.carve(c, E, n);
   }
 };
@@ -434,9 +435,20 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
   g_launches += 3;
   FPX_CK(w.g1.build(E, n, nullptr, w.best, nullptr, st));
   if (g_prof_start) FPX_CK(cudaEventRecord(g_prof_start, st));
-  FPX_LAUNCH(fpx::launch_newton_round1(M, n, x, w.g1.sorted, w.g1.items, w.g1.nitems,
-                                       w.g1.items_cap, w.npass, code, elem, r, dist, iters, field,
-                                       C, values, w.upts, nullptr, w.nun, stats, st));
+  static const bool r1_items = [] {
+    const char* v = getenv("FPX_R1");
+    return v && v[0] == 'i';
+  }();
+  if (r1_items) {
+    FPX_LAUNCH(fpx::launch_newton_round1(M, n, x, w.g1.sorted, w.g1.items, w.g1.nitems,
+                                         w.g1.items_cap, w.npass, code, elem, r, dist, iters,
+                                         field, C, values, w.upts, nullptr, w.nun, stats, st));
+  } else {
+    FPX_CK(cudaMemsetAsync(w.chunk_ctr, 0, sizeof(int64_t), st));
+    FPX_LAUNCH(fpx::launch_newton_stream(M, n, x, w.g1.sorted, w.g1.packed_off, w.g1.count,
+                                         w.best, w.npass, code, elem, r, dist, iters, field, C,
+                                         values, w.upts, w.nun, w.chunk_ctr, stats, st));
+  }
   if (g_prof_stop) FPX_CK(cudaEventRecord(g_prof_stop, st));
   // --- rest: remaining candidates of the unresolved points
   FPX_LAUNCH(fpx::launch_rest_lists(M, x, n, w.nun, w.upts, w.clist, w.cnum, st));

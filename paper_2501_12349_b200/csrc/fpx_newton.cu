@@ -57,6 +57,18 @@ cudaError_t launch_newton_round1(const fpx_mesh_t& m, int64_t n, const double* x
                           stats, st);
 }
 
+cudaError_t launch_newton_stream(const fpx_mesh_t& m, int64_t n, const double* x,
+                                 const int32_t* sorted, const uint64_t* packed_off,
+                                 const int32_t* ecount, const int32_t* best, const int32_t* npass,
+                                 int32_t* code, int32_t* elem, double* r, double* dist,
+                                 int32_t* iters, const double* field, int C, double* values,
+                                 int32_t* upts, int64_t* nun_dev, int64_t* chunk_ctr,
+                                 int64_t* stats, cudaStream_t st) {
+  return dispatch<Stream>(m.d, m.dr, m.N, m, x, sorted, packed_off, ecount, best, npass, code,
+                          elem, r, dist, iters, field, C, values, upts, nun_dev, chunk_ctr, n,
+                          stats, st);
+}
+
 cudaError_t launch_newton_pairs(const fpx_mesh_t& m, const double* x, const int32_t* pair_pt,
                                 const int32_t* sorted_pairs, const Item* items,
                                 const int64_t* nitems_dev, int64_t items_cap, int32_t* pcode,

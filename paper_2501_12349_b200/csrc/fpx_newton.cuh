@@ -1195,6 +1195,319 @@ __global__ void __launch_bounds__(64, 1)
   }
 }
 
+// ---------------------------------------------------------------- round 1, streamed
+// Element-major round 1 without fixed work items.  The points are sorted by
+// their best-first element; a warp consumes chunks of that stream through a
+// ring of S shared-memory element slots (geometry + field block, loaded
+// asynchronously ahead of use, completion on a per-slot mbarrier).  A lane
+// takes the next point as soon as its own solve finishes, so a warp never
+// waits for its slowest lane and never runs with lanes left empty by a
+// small element; the lanes of one warp read at most S distinct slots per
+// load, whose bank offsets differ (slot stride = 16 mod 128 bytes), so the
+// loads stay single-wavefront broadcasts.  Seeds are warp-cooperative.
+#define FPX_CHUNK 256
+
+template <int S>
+struct StreamMeta {
+  uint64_t mbar[S];
+  int elem[S], start[S], end[S];
+  unsigned parity[S];
+};
+
+template <int D, int DR, int N, int S>
+__global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
+    k_newton_stream(fpx_mesh_t m, const double* __restrict__ x, const int32_t* __restrict__ sorted,
+                    const uint64_t* __restrict__ packed_off, const int32_t* __restrict__ ecount,
+                    const int32_t* __restrict__ best, const int32_t* __restrict__ npass,
+                    int32_t* code, int32_t* elem, double* r, double* dist, int32_t* iters,
+                    const double* __restrict__ field, int C, double* values, int32_t* upts,
+                    int64_t* nun_dev, int64_t* chunk_ctr, int slot_stride, int64_t* stats) {
+  using L = Lay<D, DR, N>;
+  constexpr int K = L::K;
+  constexpr int SCR = Scratch<DR, N>::SLOTS;
+  extern __shared__ __align__(16) double smem[];
+  double* z = smem;
+  double* scale = smem + N;
+  const int warp = threadIdx.x / FPX_WARP, lane = threadIdx.x % FPX_WARP;
+  const int wpb = blockDim.x / FPX_WARP;
+  double* slots = smem + 2 * ((N + 1) & ~1) + (size_t)warp * (S * slot_stride + SCR * FPX_WARP);
+  double* sb = slots + S * slot_stride + lane;
+  double* stash = sb + Scratch<DR, N>::STASH * FPX_WARP;
+  StreamMeta<S>* meta =
+      reinterpret_cast<StreamMeta<S>*>(smem + 2 * ((N + 1) & ~1) +
+                                       (size_t)wpb * (S * slot_stride + SCR * FPX_WARP)) +
+      warp;
+  if (threadIdx.x < N) {
+    z[threadIdx.x] = m.basis[FPX_BASIS_NODES(N, m.M) + threadIdx.x];
+    scale[threadIdx.x] = m.basis[FPX_BASIS_SCALE(N, m.M) + threadIdx.x];
+  }
+  for (int t = lane; t < S * slot_stride; t += FPX_WARP) slots[t] = 0.0;
+  if (lane < S) {
+    mbar_init(&meta->mbar[lane], FPX_WARP);
+    meta->parity[lane] = 0;
+    meta->start[lane] = meta->end[lane] = 0;
+    meta->elem[lane] = -1;
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncthreads();
+  const NewtonParams P = newton_of(m);
+  const int64_t nu = (int64_t)(packed_off[m.E] & 0xffffffffull);
+  // warp-local unit sequence = claimed chunk A then chunk B
+  int64_t a0 = 0, b0 = 0;
+  int alen = 0, blen = 0;
+  bool exhausted = false, bclaimed = false;
+  int q = 0, ld = 0, nord = 0;
+  unsigned ready = 0;  // slots whose current load has landed
+  // lane state: 0 idle, 1 needs seed, 2 iterating
+  int phase = 0, myslot = 0, pt = 0, it = 0;
+  bool first = true;
+  double xs[3] = {0.0, 0.0, 0.0}, rc[3] = {0.0, 0.0, 0.0}, rn[3] = {0.0, 0.0, 0.0};
+  double alpha = 1.0, fcur = 0.0, pred = 0.0, smax = 0.0;
+  NState st;
+  int64_t s_newton = 0, s_iters = 0, s_evals = 0, nev = 0, nev2 = 0, s_chunks = 0;
+  // first chunk
+  {
+    int64_t c = 0;
+    if (lane == 0) c = (int64_t)atomicAdd((unsigned long long*)chunk_ctr, (unsigned long long)FPX_CHUNK);
+    c = __shfl_sync(FPX_FULL, c, 0);
+    if (c >= nu) exhausted = true;
+    else {
+      a0 = c;
+      alen = (int)(nu - c < FPX_CHUNK ? nu - c : FPX_CHUNK);
+      ++s_chunks;
+    }
+  }
+  while (true) {
+    // ---- loader: schedule the next element of the stream into the ring
+    while (!exhausted || ld < alen + blen) {
+      if (ld >= alen + blen) {  // need chunk B
+        if (bclaimed) break;
+        int64_t c = 0;
+        if (lane == 0)
+          c = (int64_t)atomicAdd((unsigned long long*)chunk_ctr, (unsigned long long)FPX_CHUNK);
+        c = __shfl_sync(FPX_FULL, c, 0);
+        if (c >= nu) {
+          exhausted = true;
+          break;
+        }
+        b0 = c;
+        blen = (int)(nu - c < FPX_CHUNK ? nu - c : FPX_CHUNK);
+        bclaimed = true;
+        ++s_chunks;
+      }
+      const int s = nord % S;
+      const bool busy = __any_sync(FPX_FULL, phase != 0 && myslot == s);
+      if (busy || meta->end[s] > q) break;  // slot still has lanes or unassigned units
+      const int64_t g = ld < alen ? a0 + ld : b0 + (ld - alen);
+      const int e = best[sorted[g]];
+      const int64_t gend = (int64_t)(packed_off[e] & 0xffffffffull) + ecount[e];
+      const int64_t cend = ld < alen ? a0 + alen : b0 + blen;
+      const int lend = ld + (int)((gend < cend ? gend : cend) - g);
+      __syncwarp();
+      double* sl = slots + s * slot_stride;
+      const double* gx = m.nodes + (int64_t)e * D * K;
+      for (int t = lane; t < D * K; t += FPX_WARP) {
+        const int c = t / K, qq = t - c * K;
+        const int row = qq / N, i = qq - row * N;
+        cp_async8(sl + c * L::CS + row * L::NP + i, gx + t);
+      }
+      if (field) {
+        const double* gu = field + (int64_t)e * C * K;
+        for (int t = lane; t < C * K; t += FPX_WARP) {
+          const int c = t / K, qq = t - c * K;
+          const int row = qq / N, i = qq - row * N;
+          cp_async8(sl + L::GEO + c * L::CS + row * L::NP + i, gu + t);
+        }
+      }
+      cp_async_arrive_noinc(&meta->mbar[s]);
+      __syncwarp();
+      if (lane == 0) {
+        meta->elem[s] = e;
+        meta->start[s] = ld;
+        meta->end[s] = lend;
+      }
+      __syncwarp();
+      ready &= ~(1u << s);
+      ++nord;
+      ld = lend;
+    }
+    // ---- which pending slot loads have landed
+    {
+      bool ok = false;
+      if (lane < S && !(ready & (1u << lane)) && meta->end[lane] > meta->start[lane])
+        ok = mbar_test(&meta->mbar[lane], meta->parity[lane]);
+      const unsigned landed = __ballot_sync(FPX_FULL, ok);
+      if (ok) meta->parity[lane] ^= 1u;
+      ready |= landed;
+      __syncwarp();
+    }
+    // ---- refill idle lanes with the next units whose slot is ready
+    {
+      const unsigned idle = __ballot_sync(FPX_FULL, phase == 0);
+      int avail = 0;
+      for (int o = 0; o < S && idle; ++o) {  // slots in stream order from q
+        int sq = -1;
+#pragma unroll
+        for (int s2 = 0; s2 < S; ++s2)
+          if (meta->start[s2] <= q + avail && q + avail < meta->end[s2]) sq = s2;
+        if (sq < 0 || !(ready & (1u << sq))) break;
+        avail = meta->end[sq] - q;
+      }
+      const int take = avail < __popc(idle) ? avail : __popc(idle);
+      const int rk = __popc(idle & ((1u << lane) - 1u));
+      if (phase == 0 && rk < take) {
+        const int p = q + rk;
+        const int64_t g = p < alen ? a0 + p : b0 + (p - alen);
+        pt = sorted[g];
+#pragma unroll
+        for (int s2 = 0; s2 < S; ++s2)
+          if (meta->start[s2] <= p && p < meta->end[s2]) myslot = s2;
+#pragma unroll
+        for (int c = 0; c < D; ++c) xs[c] = x[(int64_t)pt * D + c];
+        phase = 1;
+      }
+      q += take;
+      if (q >= alen && bclaimed) {  // chunk A consumed: B becomes A
+        const int sh = alen;
+        a0 = b0;
+        alen = blen;
+        blen = 0;
+        bclaimed = false;
+        q -= sh;
+        ld -= sh;
+        if (lane < S) {
+          meta->start[lane] -= sh;
+          meta->end[lane] -= sh;
+        }
+        __syncwarp();
+      }
+    }
+    // ---- cooperative seeds (D7) of the lanes that just got a point
+    for (unsigned sd = __ballot_sync(FPX_FULL, phase == 1); sd; sd &= sd - 1) {
+      const int j = __ffs(sd) - 1;
+      double xj[3];
+#pragma unroll
+      for (int c = 0; c < D; ++c) xj[c] = __shfl_sync(FPX_FULL, xs[c], j);
+      const double* sj = slots + __shfl_sync(FPX_FULL, myslot, j) * slot_stride;
+      double bestd = INFINITY;
+      int bi = 0x7fffffff;
+      for (int t = lane; t < K; t += FPX_WARP) {
+        const int row = t / N, i = t - row * N;
+        double dd = 0.0;
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          const double tt = __dsub_rn(xj[c], sj[c * L::CS + row * L::NP + i]);
+          dd = __fma_rn(tt, tt, dd);
+        }
+        if (dd < bestd) {
+          bestd = dd;
+          bi = t;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(FPX_FULL, bestd, o);
+        const int oi = __shfl_xor_sync(FPX_FULL, bi, o);
+        if (ob < bestd || (ob == bestd && oi < bi)) {
+          bestd = ob;
+          bi = oi;
+        }
+      }
+      if (lane == j) {
+        rc[0] = z[bi % N];
+        rc[1] = DR > 1 ? z[(bi / N) % N] : 0.0;
+        rc[2] = DR > 2 ? z[bi / (N * N)] : 0.0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) rn[a] = rc[a];
+        first = true;
+        it = 0;
+        alpha = P.alpha0;
+        phase = 2;
+      }
+    }
+    const bool any_iter = __any_sync(FPX_FULL, phase == 2);
+    if (!any_iter) {
+      if (exhausted && q >= alen + blen) break;  // stream done, all lanes idle
+      continue;                                   // waiting for a slot load
+    }
+    // ---- one map evaluation for every lane of the warp
+    double* sX = slots + myslot * slot_stride;
+    const bool w2 = __any_sync(FPX_FULL, phase == 2 && on_boundary<DR>(rn));
+    ++nev;
+    nev2 += w2 ? 1 : 0;
+    if (w2) eval_state<D, DR, N, true, 0>(sX, z, scale, rn, xs, st, sb);
+    else eval_state<D, DR, N, false, 0>(sX, z, scale, rn, xs, st, sb);
+    if (phase != 2) continue;
+    // ---- this lane's trust-region Newton update (newton_warp, D8)
+    bool done = false;
+    if (first) {
+      first = false;
+    } else {
+      const double decr = fcur - st.f;
+      if (decr >= P.accept * pred) {
+        if (decr >= P.keep * pred) alpha *= P.grow;
+#pragma unroll
+        for (int a = 0; a < DR; ++a) rc[a] = rn[a];
+      } else {
+        alpha *= P.shrink;
+        unstash_state(stash, st);
+        st.f = fcur;
+      }
+      if (smax < P.tol) done = true;
+      else if (it >= P.max_iters) done = true;
+    }
+    if (!done) {
+      fcur = st.f;
+      const bool go = propose_step<DR>(st, rc, it, alpha, rn, pred, smax);
+      ++it;
+      if (!go) done = true;
+      else stash_state(stash, st);
+    }
+    if (done) {
+      const double dd = sqrt(st.f);
+      const int e = meta->elem[myslot];
+      s_newton += 1;
+      s_iters += it;
+      const double epsd = DR < D ? eps_d_of(m, e) : 0.0;
+      const int cd = classify<D, DR>(rc, dd, epsd);
+      const bool final = cd == kInterior || npass[pt] <= 1;
+      code[pt] = cd;
+      elem[pt] = e;
+#pragma unroll
+      for (int a = 0; a < DR; ++a) r[(int64_t)pt * DR + a] = rc[a];
+      dist[pt] = dd;
+      if (iters) iters[pt] = it;
+      if (final) {
+        if (field) {
+          double v[DR][N];
+          basis_values<DR, N>(z, scale, rc, v);
+          for (int c = 0; c < C; ++c)
+            values[(int64_t)pt * C + c] = contract_smem<DR, N>(sX + L::GEO + c * L::CS, v);
+          ++s_evals;
+        }
+      } else {
+        const int slot = (int)atomicAdd((unsigned long long*)nun_dev, 1ull);
+        upts[slot] = pt;
+      }
+      phase = 0;
+    }
+  }
+  s_newton = warp_sum64(s_newton);
+  s_iters = warp_sum64(s_iters);
+  s_evals = warp_sum64(s_evals);
+  if (lane == 0) {
+    atomicAdd((unsigned long long*)&stats[FPX_STAT_NEWTON], (unsigned long long)s_newton);
+    atomicAdd((unsigned long long*)&stats[FPX_STAT_ITERS], (unsigned long long)s_iters);
+    atomicAdd((unsigned long long*)&stats[FPX_STAT_EVALS], (unsigned long long)s_evals);
+    atomicAdd((unsigned long long*)&stats[FPX_STAT_NEWTON_R1], (unsigned long long)s_newton);
+    atomicAdd((unsigned long long*)&stats[FPX_STAT_ITERS_R1], (unsigned long long)s_iters);
+    atomicAdd((unsigned long long*)&stats[FPX_STAT_EVALS_R1], (unsigned long long)s_evals);
+    atomicAdd((unsigned long long*)&stats[FPX_STAT_R1_WARP_EVALS], (unsigned long long)nev);
+    atomicAdd((unsigned long long*)&stats[FPX_STAT_R1_W2_EVALS], (unsigned long long)nev2);
+    atomicAdd((unsigned long long*)&stats[FPX_STAT_R1_ITEMS], (unsigned long long)s_chunks);
+  }
+}
+
 // findpts_eval over element-grouped records: warp per item, field block in
 // shared memory, one point per lane.
 template <int DR, int N>
@@ -1314,6 +1627,37 @@ struct Round1 {
     unsigned blocks = persistent_blocks((const void*)fn, threads, smem, items_cap);
     fn<<<blocks, threads, smem, st>>>(m, x, sorted, items, nitems_dev, npass, code, elem, r, dist,
                                       iters, field, C, values, upts, upair_cnt, nun_dev, stats);
+    return cudaGetLastError();
+  }
+};
+
+template <int D, int DR, int N>
+struct Stream {
+  static constexpr int S = 3;
+  static cudaError_t run(const fpx_mesh_t& m, const double* x, const int32_t* sorted,
+                         const uint64_t* packed_off, const int32_t* ecount, const int32_t* best,
+                         const int32_t* npass, int32_t* code, int32_t* elem, double* r,
+                         double* dist, int32_t* iters, const double* field, int C, double* values,
+                         int32_t* upts, int64_t* nun_dev, int64_t* chunk_ctr, int64_t n_cap,
+                         int64_t* stats, cudaStream_t st) {
+    using L = Lay<D, DR, N>;
+    int ss = L::GEO + (field ? C * L::CS : 0);
+    ss = (ss + 13) / 16 * 16 + 2;  // slot stride = 16 bytes mod 128: distinct bank groups
+    const size_t per_warp =
+        (size_t)(S * ss + Scratch<DR, N>::SLOTS * FPX_WARP) * 8 + sizeof(StreamMeta<S>);
+    int wpb = 4;
+    while (wpb > 1 && (size_t)wpb * per_warp + 256 > 220 * 1024) --wpb;
+    if ((size_t)wpb * per_warp + 256 > 227 * 1024) return cudaErrorInvalidValue;
+    const int threads = wpb * FPX_WARP;
+    const size_t smem = (size_t)(2 * ((N + 1) & ~1)) * 8 + (size_t)wpb * per_warp;
+    auto fn = k_newton_stream<D, DR, N, S>;
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    unsigned blocks = persistent_blocks((const void*)fn, threads, smem,
+                                        (n_cap + FPX_CHUNK - 1) / FPX_CHUNK);
+    fn<<<blocks, threads, smem, st>>>(m, x, sorted, packed_off, ecount, best, npass, code, elem, r,
+                                      dist, iters, field, C, values, upts, nun_dev, chunk_ctr, ss,
+                                      stats);
     return cudaGetLastError();
   }
 };
