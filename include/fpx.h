@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define FPX_ABI_VERSION 1
+#define FPX_ABI_VERSION 2
 
 /* error codes */
 #define FPX_OK 0
@@ -85,7 +85,13 @@ typedef struct fpx_mesh_t {
   double tol, grow, keep, accept, shrink, alpha0;
   /* surface classification eps_d: abs >= 0 wins, else rel*diag */
   double eps_d_abs, eps_d_rel;
+  /* (ABI 2) per-element candidate filter record, FPX_FREC doubles each:
+   * aabb lo,hi [2d] | obb_c [d] | obb_inv [d*d] | frame x_c,J_c^-1 [d+d*d] |
+   * ... | obb_ok as 0.0/1.0 at index FPX_FREC-1 (fpx_filter_records). */
+  const double* frec;
 } fpx_mesh_t;
+
+#define FPX_FREC 32
 
 /* Diagnostic counters written by fpx_find (device int64[FPX_STATS_LEN]). */
 #define FPX_STAT_POINTS 0        /* points processed */
@@ -100,7 +106,10 @@ typedef struct fpx_mesh_t {
 #define FPX_STAT_ITERS_R1 9      /* their iterations */
 #define FPX_STAT_EVALS_R1 10     /* field evaluations fused into the round-1 kernel */
 #define FPX_STAT_R1_ITEMS 11     /* round-1 warp work items */
-#define FPX_STATS_LEN 12
+#define FPX_STAT_REST_WARP_EVALS 12 /* rest kernel: map evaluations issued per warp */
+#define FPX_STAT_REST_W2_EVALS 13   /* ... of which with second derivatives */
+#define FPX_STAT_REST_LANE_EVALS 14 /* ... summed over the lanes that were iterating */
+#define FPX_STATS_LEN 16
 
 int fpx_abi_version(void);
 const char* fpx_last_error(void);
@@ -132,6 +141,12 @@ int fpx_setup_bounds(int d, int dr, int N, int M, int64_t E, const double* basis
 /* bound_function_1d (dr=1, values [nf][N] -> lower/upper [nf][M]) and
  * bound_function_2d (dr=2, values [nf][N*N] with i fastest -> [nf][M][M]),
  * replacing bounds.py:155-171 and bounds.py:174-201. */
+/* Packs aabb/obb/frame/obb_ok into the per-element filter records (mesh.frec,
+ * [E][FPX_FREC] doubles, 256-byte aligned rows) read by the find prefilter. */
+int fpx_filter_records(int d, int64_t E, const double* aabb, const double* obb_c,
+                       const double* obb_inv, const uint8_t* obb_ok, const double* frame,
+                       double* frec, void* stream);
+
 int fpx_bound_function(int dr, int N, int M, int64_t nf, const double* basis,
                        const double* values, double* lower, double* upper, void* stream);
 

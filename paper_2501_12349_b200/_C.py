@@ -14,12 +14,14 @@ import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FPX_LIB") or os.path.join(HERE, "lib", "libfpx_sm100.so")
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 INTERIOR, BORDER, NOT_FOUND = 0, 1, 2
 STAT_NAMES = ["points", "box_tests", "newton", "iters", "rest_points", "r1_warp_evals",
-              "r1_w2_evals", "evals", "newton_r1", "iters_r1", "evals_r1", "r1_items"]
+              "r1_w2_evals", "evals", "newton_r1", "iters_r1", "evals_r1", "r1_items",
+              "rest_warp_evals", "rest_w2_evals", "rest_lane_evals", "spare"]
 STATS_LEN = len(STAT_NAMES)
+FREC = 32            # FPX_FREC: doubles per element filter record
 
 P = C.c_void_p
 
@@ -42,6 +44,7 @@ class MeshT(C.Structure):
         ("tol", C.c_double), ("grow", C.c_double), ("keep", C.c_double),
         ("accept", C.c_double), ("shrink", C.c_double), ("alpha0", C.c_double),
         ("eps_d_abs", C.c_double), ("eps_d_rel", C.c_double),
+        ("frec", P),
     ]
 
 
@@ -67,6 +70,7 @@ def lib():
         "fpx_profile_round1": ([P, P], i32),
         "fpx_probe_fp64": ([P, P], i32),
         "fpx_setup_bounds": ([i32, i32, i32, i32, i64, P, P, f64, P, P, P, P, P, P, P, P], i32),
+        "fpx_filter_records": ([i32, i64, P, P, P, P, P, P, P], i32),
         "fpx_bound_function": ([i32, i32, i32, i64, P, P, P, P, P], i32),
         "fpx_hash_workspace_bytes": ([i32, i64, i32], sz),
         "fpx_hash_build": ([i32, i64, P, P, P, P, i32, P, P, P, i64, P, P, P, sz, P], i32),
@@ -93,7 +97,7 @@ def lib():
 def exported_symbols():
     """Names declared in include/fpx.h (checked by the CPU test suite)."""
     return ["fpx_abi_version", "fpx_last_error", "fpx_launch_count", "fpx_profile_round1",
-            "fpx_probe_fp64", "fpx_supported", "fpx_setup_bounds",
+            "fpx_probe_fp64", "fpx_supported", "fpx_setup_bounds", "fpx_filter_records",
             "fpx_bound_function", "fpx_hash_workspace_bytes", "fpx_hash_build", "fpx_cell_of",
             "fpx_find_workspace_bytes", "fpx_find", "fpx_eval_workspace_bytes",
             "fpx_findpts_eval", "fpx_invert_pairs", "fpx_forward_map", "fpx_route_count",

@@ -297,6 +297,17 @@ int fpx_setup_bounds(int d, int dr, int N, int M, int64_t E, const double* basis
   return FPX_OK;
 }
 
+int fpx_filter_records(int d, int64_t E, const double* aabb, const double* obb_c,
+                       const double* obb_inv, const uint8_t* obb_ok, const double* frame,
+                       double* frec, void* stream) {
+  if (!(d == 2 || d == 3)) return fail(FPX_EINVAL, "filter records: bad d=%d", d);
+  if (4 * d + 2 * d * d + 1 > FPX_FREC) return fail(FPX_EINVAL, "filter record too small");
+  if (E <= 0) return FPX_OK;
+  FPX_LAUNCH(fpx::launch_filter_records(d, E, aabb, obb_c, obb_inv, obb_ok, frame, frec,
+                                        S(stream)));
+  return FPX_OK;
+}
+
 int fpx_bound_function(int dr, int N, int M, int64_t nf, const double* basis,
                        const double* values, double* lower, double* upper, void* stream) {
   if (dr != 1 && dr != 2) return fail(FPX_EINVAL, "bound_function: dr must be 1 or 2");
@@ -408,6 +419,7 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
   w.carve(cv, E, n);
   w.carve_cells(cv, n, cells_of(m));
   if (!cv.ok()) return fail(FPX_EINVAL, "find workspace too small (%zu < %zu)", ws_bytes, cv.off);
+  if (!m->frec) return fail(FPX_EINVAL, "mesh has no filter records (fpx_filter_records)");
   const fpx_mesh_t& M = *m;
   // --- order the points by hash cell (counting sort)
   const int64_t nc = w.ncells;

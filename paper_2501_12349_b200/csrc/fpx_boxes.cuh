@@ -79,6 +79,31 @@ __device__ __forceinline__ bool candidate_passes_t(const fpx_mesh_t& m, int e, c
   return true;
 }
 
+// Packed filter record of element e (mesh.frec, FPX_FREC doubles, 16-byte
+// vector loads: one round trip for the whole record).
+struct FRec {
+  double v[FPX_FREC];
+};
+__device__ __forceinline__ void load_frec(const double* __restrict__ frec, int64_t e, FRec& R) {
+  const double2* p = reinterpret_cast<const double2*>(frec + e * FPX_FREC);
+#pragma unroll
+  for (int i = 0; i < FPX_FREC / 2; ++i) {
+    const double2 t = __ldg(p + i);
+    R.v[2 * i] = t.x;
+    R.v[2 * i + 1] = t.y;
+  }
+}
+// aabb_in, then obb_in unless the OBB frame is singular (decision D4).
+template <int D>
+__device__ __forceinline__ bool frec_passes(const FRec& R, const double* x) {
+  if (!aabb_in(D, R.v, x)) return false;
+  return R.v[FPX_FREC - 1] == 0.0 || obb_in(D, R.v + 2 * D, R.v + 3 * D, x);
+}
+template <int D>
+__device__ __forceinline__ double frec_bestfirst(const FRec& R, const double* x) {
+  return bestfirst_value(D, R.v + 3 * D + D * D, x);
+}
+
 // (v, e) lexicographic order of the best-first ranking (ties -> lower id).
 __device__ __forceinline__ bool bf_less(double v1, int e1, double v2, int e2) {
   return v1 < v2 || (v1 == v2 && e1 < e2);

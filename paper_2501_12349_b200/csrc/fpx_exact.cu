@@ -769,15 +769,18 @@ __global__ void __launch_bounds__(256)
     if (cell < nc) {
       const int s = m.offsets[cell], e1 = m.offsets[cell + 1];
       boxtests += e1 - s;
+      int en = s < e1 ? m.elems[s] : 0;  // list entry prefetched one ahead
       for (int q = s; q < e1; ++q) {
-        const int64_t e = m.elems[q];
-        if (!aabb_in(D, m.aabb + e * 2 * D, xx)) continue;
-        if (m.obb_ok[e] && !obb_in(D, m.obb_c + e * D, m.obb_inv + e * D * D, xx)) continue;
+        const int e = en;
+        if (q + 1 < e1) en = m.elems[q + 1];
+        FRec R;
+        load_frec(m.frec, e, R);
+        if (!frec_passes<D>(R, xx)) continue;
         ++cnt;
-        const double v = bestfirst_value(D, m.frame + e * (D + D * D), xx);
+        const double v = frec_bestfirst<D>(R, xx);
         if (v < bval) {  // strict: ties keep the lower (earlier) id
           bval = v;
-          bst = (int)e;
+          bst = e;
         }
       }
     }
@@ -893,6 +896,26 @@ __global__ void __launch_bounds__(128)
     atomicAdd((unsigned long long*)&stats[FPX_STAT_BOXTESTS], (unsigned long long)boxtests);
 }
 
+// Packed candidate-filter records (include/fpx.h, FPX_FREC): one 256-byte
+// row per element so the prefilter fetches a candidate in one round trip.
+__global__ void k_filter_records(int d, int64_t E, const double* __restrict__ aabb,
+                                 const double* __restrict__ obb_c,
+                                 const double* __restrict__ obb_inv,
+                                 const uint8_t* __restrict__ obb_ok,
+                                 const double* __restrict__ frame, double* frec) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    double* R = frec + e * FPX_FREC;
+    int o = 0;
+    for (int t = 0; t < 2 * d; ++t) R[o++] = aabb[e * 2 * d + t];
+    for (int t = 0; t < d; ++t) R[o++] = obb_c[e * d + t];
+    for (int t = 0; t < d * d; ++t) R[o++] = obb_inv[e * d * d + t];
+    for (int t = 0; t < d + d * d; ++t) R[o++] = frame[e * (d + d * d) + t];
+    while (o < FPX_FREC - 1) R[o++] = 0.0;
+    R[FPX_FREC - 1] = obb_ok[e] ? 1.0 : 0.0;
+  }
+}
+
 // ------------------------------------------------------------ host launchers
 static int setup_warps(size_t per_warp_bytes, size_t base_bytes) {
   int w = 4;
@@ -945,6 +968,13 @@ static unsigned grid_for(int64_t n, int threads) {
   return (unsigned)b;
 }
 
+cudaError_t launch_filter_records(int d, int64_t E, const double* aabb, const double* obb_c,
+                                  const double* obb_inv, const uint8_t* obb_ok,
+                                  const double* frame, double* frec, cudaStream_t st) {
+  k_filter_records<<<grid_for(E, 256), 256, 0, st>>>(d, E, aabb, obb_c, obb_inv, obb_ok, frame,
+                                                     frec);
+  return cudaGetLastError();
+}
 cudaError_t launch_hash_grid(int d, int64_t E, const double* box, int ncell, double* grid,
                              cudaStream_t st) {
   k_hash_grid<<<1, 1024, 0, st>>>(d, E, box, ncell, grid);

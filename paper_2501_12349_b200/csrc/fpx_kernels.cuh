@@ -25,6 +25,9 @@ cudaError_t launch_setup_bounds(int d, int dr, int N, int M, int64_t E, const do
 cudaError_t launch_bound_function(int dr, int N, int M, int64_t nf, const double* basis,
                                   const double* values, double* lower, double* upper,
                                   cudaStream_t st);
+cudaError_t launch_filter_records(int d, int64_t E, const double* aabb, const double* obb_c,
+                                  const double* obb_inv, const uint8_t* obb_ok,
+                                  const double* frame, double* frec, cudaStream_t st);
 cudaError_t launch_hash_grid(int d, int64_t E, const double* box, int ncell, double* grid,
                              cudaStream_t st);
 cudaError_t launch_hash_count(int d, int64_t E, const double* box, const double* obb_c,

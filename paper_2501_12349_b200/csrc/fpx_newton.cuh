@@ -860,14 +860,6 @@ __device__ __forceinline__ bool propose_step(const NState& st, const double* r, 
 // Slot stride is odd in doubles, so the 32 lanes' 8-byte loads at equal
 // offsets fall into distinct bank pairs.
 
-template <int D, int DR, int N>
-struct RestLay {
-  static constexpr int K = Pow<DR, N>::K;
-  static constexpr int SS = (D * K) | 1;                 // slot stride (doubles)
-  static constexpr int SCR = Scratch<DR, N>::SLOTS;      // per-lane scratch slots
-  static constexpr size_t lane_bytes() { return (size_t)(SS + SCR) * 8 + 8; }
-};
-
 __device__ __forceinline__ void mbar_init(uint64_t* mb, unsigned count) {
   const unsigned a = (unsigned)__cvta_generic_to_shared(mb);
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count) : "memory");
@@ -891,14 +883,16 @@ __device__ __forceinline__ bool mbar_test(uint64_t* mb, unsigned parity) {
 // Best-first ranked candidate lists of the rest points: the passing
 // entries of the hash list sorted by (v, e), FPX_RK per point
 // kept; beyond that the rest kernel scans the list itself.
+#define FPX_LISTMAX 256
 template <int D>
 __global__ void __launch_bounds__(128)
     k_rest_lists(fpx_mesh_t m, const double* __restrict__ x, const int64_t* __restrict__ nun_dev,
                  const int32_t* __restrict__ upts, int32_t* clist, int32_t* cnum) {
-  // warp per rest point: lanes over hash-list chunks, rank of each passing
-  // entry = number of passing entries before it in (v, e) order
-  __shared__ double s_v[4][FPX_WARP];
-  __shared__ int s_e[4][FPX_WARP];
+  // warp per rest point: lanes test the hash-list entries (one filter record
+  // each), (v, e) of the passing ones go to shared memory, and the rank of
+  // each is the number of passing entries before it in (v, e) order
+  __shared__ double s_v[4][FPX_LISTMAX];
+  __shared__ int s_e[4][FPX_LISTMAX];
   const int warp = threadIdx.x / FPX_WARP, lane = threadIdx.x % FPX_WARP;
   const int64_t nun = *nun_dev;
   for (int64_t u = (int64_t)blockIdx.x * 4 + warp; u < nun; u += (int64_t)gridDim.x * 4) {
@@ -909,87 +903,227 @@ __global__ void __launch_bounds__(128)
     int ax[3];
     const int64_t cell = cell_of(D, m.grid, m.ncell, xs, ax);
     const int qs = cell >= 0 ? m.offsets[cell] : 0, qe = cell >= 0 ? m.offsets[cell + 1] : 0;
+    const int L = qe - qs < FPX_LISTMAX ? qe - qs : FPX_LISTMAX;
+    for (int q = lane; q < L; q += FPX_WARP) {
+      const int e = m.elems[qs + q];
+      FRec R;
+      load_frec(m.frec, e, R);
+      const bool pass = frec_passes<D>(R, xs);
+      s_v[warp][q] = pass ? frec_bestfirst<D>(R, xs) : INFINITY;
+      s_e[warp][q] = pass ? e : -1;
+    }
+    __syncwarp();
     int np = 0;
-    for (int q0 = qs; q0 < qe; q0 += FPX_WARP) {
-      const int q = q0 + lane;
-      const int e = q < qe ? m.elems[q] : -1;
-      const bool pass = e >= 0 && candidate_passes_t<D>(m, e, xs);
-      const double v = pass ? bestfirst_value(D, m.frame + (int64_t)e * (D + D * D), xs) : 0.0;
-      np += __popc(__ballot_sync(FPX_FULL, pass));
-    }
-    // ranks: every passing entry against every passing entry (chunks)
-    for (int q0 = qs; q0 < qe; q0 += FPX_WARP) {
-      const int q = q0 + lane;
-      const int e = q < qe ? m.elems[q] : -1;
-      const bool pass = e >= 0 && candidate_passes_t<D>(m, e, xs);
-      const double v = pass ? bestfirst_value(D, m.frame + (int64_t)e * (D + D * D), xs) : 0.0;
+    for (int q = lane; q < L; q += FPX_WARP) {
+      const int e = s_e[warp][q];
+      if (e < 0) continue;
+      ++np;
+      const double v = s_v[warp][q];
       int rank = 0;
-      for (int p0 = qs; p0 < qe; p0 += FPX_WARP) {
-        const int pq = p0 + lane;
-        const int pe = pq < qe ? m.elems[pq] : -1;
-        const bool pp = pe >= 0 && candidate_passes_t<D>(m, pe, xs);
-        __syncwarp();
-        s_v[warp][lane] = pp ? bestfirst_value(D, m.frame + (int64_t)pe * (D + D * D), xs) : 0.0;
-        s_e[warp][lane] = pe;
-        __syncwarp();
-        const unsigned pm = __ballot_sync(FPX_FULL, pp);
-        if (pass)
-          for (unsigned mm = pm; mm; mm &= mm - 1) {
-            const int j = __ffs(mm) - 1;
-            rank += bf_less(s_v[warp][j], s_e[warp][j], v, e) ? 1 : 0;
-          }
+      for (int j = 0; j < L; ++j) {
+        const int ej = s_e[warp][j];
+        rank += (ej >= 0 && bf_less(s_v[warp][j], ej, v, e)) ? 1 : 0;
       }
-      if (pass && rank < FPX_RK) clist[u * FPX_RK + rank] = e;
+      if (rank < FPX_RK) clist[u * FPX_RK + rank] = e;
     }
-    if (lane == 0) cnum[u] = np > FPX_RK ? -FPX_RK : np;  // negative: more beyond the list
+    for (int o = 16; o > 0; o >>= 1) np += __shfl_xor_sync(FPX_FULL, np, o);
+    // more than FPX_RK passing: the rest kernel scans after the last listed
+    // one; lists longer than FPX_LISTMAX: it scans everything after rank 0
+    if (lane == 0)
+      cnum[u] = qe - qs > L ? -1 : (np > FPX_RK ? -FPX_RK : np);
+    __syncwarp();
   }
 }
 
-template <int D, int DR, int N, int LANES>
-__global__ void __launch_bounds__(64, 1)
-    k_rest_lanes(fpx_mesh_t m, const double* __restrict__ x, const int64_t* __restrict__ nun_dev,
+// Per-point slot: geometry [D][N^DR] | axis-1.. basis values | Newton stash,
+// odd stride in doubles (the 16 points of a warp hit distinct bank pairs).
+template <int D, int DR, int N>
+struct PairLay {
+  static constexpr int K = Pow<DR, N>::K;
+  static constexpr int BAS = (DR - 1) * 3 * N;   // v, d1, d2 of axes 1..DR-1
+  static constexpr int STASH = D * K + BAS;      // 16 doubles
+  static constexpr int SS = (D * K + BAS + 16) | 1;
+};
+
+// Forward map + Newton state at r for one point evaluated by a lane pair:
+// lane `part` takes the rows q = part, part + 2, ... of every coordinate,
+// the per-coordinate partial sums are added across the pair (xor 1, the same
+// order on both lanes, so both hold bitwise identical states).  sp: the
+// point's slot; its basis block is written by lane 0 of the pair.
+template <int D, int DR, int N, bool W2>
+__device__ __forceinline__ void eval_state_pair(const double* __restrict__ sp,
+                                                const double* __restrict__ z,
+                                                const double* __restrict__ scale, const double* r,
+                                                const double* xs, NState& S, int part) {
+  using PL = PairLay<D, DR, N>;
+  constexpr int K = PL::K, R = K / N;
+  double* sbas = const_cast<double*>(sp) + D * K;
+  double v0[N], g0[N], h0[N];
+  lagrange<N, W2>(z, scale, r[0], v0, g0, h0);
+  __syncwarp();
+#pragma unroll
+  for (int a = 1; a < DR; ++a) {
+    if (part == 0) {
+      double v[N], g[N], h[N];
+      lagrange<N, W2>(z, scale, r[a], v, g, h);
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        sbas[((a - 1) * 3 + 0) * N + j] = v[j];
+        sbas[((a - 1) * 3 + 1) * N + j] = g[j];
+        if (W2) sbas[((a - 1) * 3 + 2) * N + j] = h[j];
+      }
+    }
+  }
+  __syncwarp();
+#define PSB(a, kind, j) sbas[(((a)-1) * 3 + (kind)) * N + (j)]
+  double X[D], GG[D][3], HH[D][6];
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    const double* Xc = sp + c * K;
+    double xv = 0.0, g_0 = 0.0, g_1 = 0.0, g_2 = 0.0;
+    double h00 = 0.0, h11 = 0.0, h22 = 0.0, h01 = 0.0, h02 = 0.0, h12 = 0.0;
+#pragma unroll 3
+    for (int q = part; q < R; q += 2) {
+      const double* row = Xc + q * N;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const double p = row[i];
+        s0 = fma(p, v0[i], s0);
+        s1 = fma(p, g0[i], s1);
+        if (W2) s2 = fma(p, h0[i], s2);
+      }
+      if constexpr (DR == 3) {
+        const int j = q % N, k = q / N;
+        const double vj = PSB(1, 0, j), gj = PSB(1, 1, j), vk = PSB(2, 0, k), gk = PSB(2, 1, k);
+        const double wvv = vj * vk, wgv = gj * vk, wvg = vj * gk;
+        xv = fma(s0, wvv, xv);
+        g_0 = fma(s1, wvv, g_0);
+        g_1 = fma(s0, wgv, g_1);
+        g_2 = fma(s0, wvg, g_2);
+        if (W2) {
+          h00 = fma(s2, wvv, h00);
+          h11 = fma(s0, PSB(1, 2, j) * vk, h11);
+          h22 = fma(s0, vj * PSB(2, 2, k), h22);
+          h01 = fma(s1, wgv, h01);
+          h02 = fma(s1, wvg, h02);
+          h12 = fma(s0, gj * gk, h12);
+        }
+      } else if constexpr (DR == 2) {
+        const double vj = PSB(1, 0, q), gj = PSB(1, 1, q);
+        xv = fma(s0, vj, xv);
+        g_0 = fma(s1, vj, g_0);
+        g_1 = fma(s0, gj, g_1);
+        if (W2) {
+          h00 = fma(s2, vj, h00);
+          h11 = fma(s0, PSB(1, 2, q), h11);
+          h01 = fma(s1, gj, h01);
+        }
+      } else {
+        xv = s0;
+        g_0 = s1;
+        if (W2) h00 = s2;
+      }
+    }
+    X[c] = xv;
+    GG[c][0] = g_0;
+    GG[c][1] = g_1;
+    GG[c][2] = g_2;
+    HH[c][0] = h00;
+    HH[c][1] = h11;
+    HH[c][2] = h22;
+    HH[c][3] = h01;
+    HH[c][4] = h02;
+    HH[c][5] = h12;
+  }
+#undef PSB
+  // pair sums (both lanes add the same two numbers)
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    X[c] += __shfl_xor_sync(FPX_FULL, X[c], 1);
+#pragma unroll
+    for (int a = 0; a < DR; ++a) GG[c][a] += __shfl_xor_sync(FPX_FULL, GG[c][a], 1);
+    if (W2) {
+#pragma unroll
+      for (int t = 0; t < 6; ++t) {
+        if (DR < 3 && (t == 2 || t >= 4)) continue;
+        if (DR < 2 && t != 0) continue;
+        HH[c][t] += __shfl_xor_sync(FPX_FULL, HH[c][t], 1);
+      }
+    }
+  }
+  S.f = 0.0;
+#pragma unroll
+  for (int t = 0; t < 3; ++t) S.J[t] = 0.0;
+#pragma unroll
+  for (int t = 0; t < 6; ++t) {
+    S.H0[t] = 0.0;
+    S.Q[t] = 0.0;
+  }
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    const double dx = xs[c] - X[c];
+    S.f = fma(dx, dx, S.f);
+#pragma unroll
+    for (int a = 0; a < DR; ++a) S.J[a] = fma(-GG[c][a], dx, S.J[a]);
+    S.H0[0] = fma(GG[c][0], GG[c][0], S.H0[0]);
+    if (DR > 1) {
+      S.H0[1] = fma(GG[c][1], GG[c][1], S.H0[1]);
+      S.H0[3] = fma(GG[c][0], GG[c][1], S.H0[3]);
+    }
+    if (DR > 2) {
+      S.H0[2] = fma(GG[c][2], GG[c][2], S.H0[2]);
+      S.H0[4] = fma(GG[c][0], GG[c][2], S.H0[4]);
+      S.H0[5] = fma(GG[c][1], GG[c][2], S.H0[5]);
+    }
+    if (W2) {
+#pragma unroll
+      for (int t = 0; t < 6; ++t) S.Q[t] = fma(dx, HH[c][t], S.Q[t]);
+    }
+  }
+}
+
+template <int D, int DR, int N, int WPB>
+__global__ void __launch_bounds__(WPB * 32, 1)
+    k_rest_pairs(fpx_mesh_t m, const double* __restrict__ x, const int64_t* __restrict__ nun_dev,
                  const int32_t* __restrict__ upts, const int32_t* __restrict__ clist,
                  const int32_t* __restrict__ cnum, int32_t* code, int32_t* elem, double* r,
-                 double* dist, int32_t* iters, const double* __restrict__ field, int C,
-                 double* values, int64_t* counter, int64_t* stats) {
-  using RL = RestLay<D, DR, N>;
-  constexpr int K = RL::K;
+                 double* dist, int32_t* iters, int64_t* counter, int64_t* stats) {
+  using PL = PairLay<D, DR, N>;
+  constexpr int K = PL::K;
+  constexpr int PPW = FPX_WARP / 2;  // points per warp
   extern __shared__ __align__(16) double smem[];
   double* z = smem;
   double* scale = smem + N;
   const int warp = threadIdx.x / FPX_WARP, lane = threadIdx.x % FPX_WARP;
-  double* slots = smem + 2 * ((N + 1) & ~1) + (size_t)warp * (LANES * RL::SS + RL::SCR * FPX_WARP);
-  const bool live = lane < LANES;
-  double* mine = slots + (live ? lane : 0) * RL::SS;
-  double* sb = slots + LANES * RL::SS + lane;  // per-lane scratch, stride 32
-  double* stash = sb + Scratch<DR, N>::STASH * FPX_WARP;
-  uint64_t* mbars = reinterpret_cast<uint64_t*>(smem + 2 * ((N + 1) & ~1) +
-                                                (size_t)(blockDim.x / FPX_WARP) *
-                                                    (LANES * RL::SS + RL::SCR * FPX_WARP)) +
-                    warp * FPX_WARP;
+  const int pslot = lane >> 1, part = lane & 1;
+  double* slots = smem + 2 * ((N + 1) & ~1) + (size_t)warp * PPW * PL::SS;
+  double* mine = slots + pslot * PL::SS;
+  double* stash = mine + PL::STASH;
+  uint64_t* mbars =
+      reinterpret_cast<uint64_t*>(smem + 2 * ((N + 1) & ~1) + (size_t)WPB * PPW * PL::SS) +
+      warp * PPW;
   if (threadIdx.x < N) {
     z[threadIdx.x] = m.basis[FPX_BASIS_NODES(N, m.M) + threadIdx.x];
     scale[threadIdx.x] = m.basis[FPX_BASIS_SCALE(N, m.M) + threadIdx.x];
   }
-  if (live) {
-    for (int t = 0; t < RL::SS; ++t) mine[t] = 0.0;  // idle lanes evaluate finite data
-    mbar_init(&mbars[lane], FPX_WARP);
-  }
+  for (int t = lane; t < PPW * PL::SS; t += FPX_WARP) slots[t] = 0.0;
+  if (lane < PPW) mbar_init(&mbars[lane], FPX_WARP);
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   __syncthreads();
   const NewtonParams P = newton_of(m);
   const int64_t nun = *nun_dev;
-  int64_t s_newton = 0, s_iters = 0, s_evals = 0;
-  // point state
+  int64_t s_newton = 0, s_iters = 0, nev = 0, nev2 = 0, nlev = 0;
+  // point state (identical on both lanes of the pair)
   bool have_point = false, point_done = false;
   int64_t u = 0, k = 0;
   double xs[3] = {0.0, 0.0, 0.0};
   int bc = -1, be = -1, it_tot = 0, rank = 0, nlist = 0, te = -1, qs = 0, qe = 0;
   bool over = false;
   double bd = INFINITY, br[3] = {0.0, 0.0, 0.0}, tv = -INFINITY;
-  // candidate state: 0 needs a candidate, 1 copy requested, 2 copy in flight,
-  // 3 iterating, 4 no work left
-  int phase = live ? 0 : 4;
+  // 0 needs a candidate, 1 copy requested, 2 copy in flight, 3 iterating,
+  // 4 no work left
+  int phase = 0;
   unsigned parity = 0;
   int e = -1, it = 0;
   bool first = true;
@@ -997,11 +1131,13 @@ __global__ void __launch_bounds__(64, 1)
   double alpha = 1.0, fcur = 0.0, pred = 0.0, smax = 0.0;
   NState st;
   while (true) {
-    // (a) lanes without a candidate pick the next one (or finish the point)
+    // (a) points without a candidate pick the next one (or finish)
     if (phase == 0) {
       while (true) {
         if (!have_point) {
-          u = (int64_t)atomicAdd((unsigned long long*)counter, 1ull);
+          int64_t uu = 0;
+          if (part == 0) uu = (int64_t)atomicAdd((unsigned long long*)counter, 1ull);
+          u = __shfl_sync(__activemask(), uu, lane & ~1);
           if (u >= nun) {
             phase = 4;
             break;
@@ -1019,6 +1155,16 @@ __global__ void __launch_bounds__(64, 1)
           nlist = cn < 0 ? -cn : cn;
           over = cn < 0;
           rank = 1;  // rank 0 is round 1's candidate
+          if (over) {
+            FRec R;
+            load_frec(m.frec, be, R);
+            tv = frec_bestfirst<D>(R, xs);
+            te = be;
+            int ax[3];
+            const int64_t cell = cell_of(D, m.grid, m.ncell, xs, ax);
+            qs = m.offsets[cell];
+            qe = m.offsets[cell + 1];
+          }
           have_point = true;
           point_done = false;
         }
@@ -1026,21 +1172,21 @@ __global__ void __launch_bounds__(64, 1)
         if (!point_done) {
           if (rank < nlist) {
             e = clist[u * FPX_RK + rank++];
-            if (rank == nlist && over) {  // continue after the last listed one
-              tv = bestfirst_value(D, m.frame + (int64_t)e * (D + D * D), xs);
+            if (over) {
+              FRec R;
+              load_frec(m.frec, e, R);
+              tv = frec_bestfirst<D>(R, xs);
               te = e;
-              int ax[3];
-              const int64_t cell = cell_of(D, m.grid, m.ncell, xs, ax);
-              qs = m.offsets[cell];
-              qe = m.offsets[cell + 1];
             }
           } else if (over) {
             double bv = INFINITY;
             int bb = 0x7fffffff;
             for (int q = qs; q < qe; ++q) {
               const int ee = m.elems[q];
-              if (!candidate_passes_t<D>(m, ee, xs)) continue;
-              const double v = bestfirst_value(D, m.frame + (int64_t)ee * (D + D * D), xs);
+              FRec R;
+              load_frec(m.frec, ee, R);
+              if (!frec_passes<D>(R, xs)) continue;
+              const double v = frec_bestfirst<D>(R, xs);
               if (bf_less(tv, te, v, ee) && bf_less(v, ee, bv, bb)) {
                 bv = v;
                 bb = ee;
@@ -1057,44 +1203,38 @@ __global__ void __launch_bounds__(64, 1)
           phase = 1;
           break;
         }
-        // the point is complete: record (+ field value)
-        code[k] = bc;
-        elem[k] = be;
-        dist[k] = bd;
-        if (iters) iters[k] = it_tot;
+        // the point is complete (its field value is evaluated afterwards)
+        if (part == 0) {
+          code[k] = bc;
+          elem[k] = be;
+          dist[k] = bd;
+          if (iters) iters[k] = it_tot;
 #pragma unroll
-        for (int a = 0; a < DR; ++a) r[k * DR + a] = br[a];
-        if (field) {
-          double v[DR][N];
-          basis_values<DR, N>(z, scale, br, v);
-          for (int c = 0; c < C; ++c)
-            values[k * C + c] = contract_gmem<DR, N>(field + ((int64_t)be * C + c) * K, v);
-          ++s_evals;
+          for (int a = 0; a < DR; ++a) r[k * DR + a] = br[a];
         }
         have_point = false;
       }
     }
-    // (b) the warp copies the requested candidates' geometry into their
-    // owners' slots; every lane arrives on the owner's mbarrier
-    for (unsigned req = __ballot_sync(FPX_FULL, phase == 1); req; req &= req - 1) {
+    // (b) the warp copies the requested candidates into their slots
+    for (unsigned req = __ballot_sync(FPX_FULL, phase == 1 && part == 0); req; req &= req - 1) {
       const int j = __ffs(req) - 1;
       const int ej = __shfl_sync(FPX_FULL, e, j);
       const double* src = m.nodes + (int64_t)ej * D * K;
-      double* dst = slots + j * RL::SS;
+      double* dst = slots + (j >> 1) * PL::SS;
       for (int t = lane; t < D * K; t += FPX_WARP) cp_async8(dst + t, src + t);
-      cp_async_arrive_noinc(&mbars[j]);
+      cp_async_arrive_noinc(&mbars[j >> 1]);
     }
     if (phase == 1) phase = 2;
-    // (c) lanes whose copy landed get their seed (warp-cooperative, D7)
-    const bool landed = phase == 2 && mbar_test(&mbars[lane], parity);
+    // (c) points whose copy landed get their seed (warp-cooperative, D7)
+    const bool landed = phase == 2 && mbar_test(&mbars[pslot], parity);
     if (landed) parity ^= 1u;
-    for (unsigned rdy = __ballot_sync(FPX_FULL, landed); rdy; rdy &= rdy - 1) {
+    for (unsigned rdy = __ballot_sync(FPX_FULL, landed && part == 0); rdy; rdy &= rdy - 1) {
       const int j = __ffs(rdy) - 1;
       double xj[3];
 #pragma unroll
       for (int c = 0; c < D; ++c) xj[c] = __shfl_sync(FPX_FULL, xs[c], j);
-      const double* sj = slots + j * RL::SS;
-      double best = INFINITY;
+      const double* sj = slots + (j >> 1) * PL::SS;
+      double bestd = INFINITY;
       int bi = 0x7fffffff;
       for (int t = lane; t < K; t += FPX_WARP) {
         double dd = 0.0;
@@ -1103,21 +1243,21 @@ __global__ void __launch_bounds__(64, 1)
           const double tt = __dsub_rn(xj[c], sj[c * K + t]);
           dd = __fma_rn(tt, tt, dd);
         }
-        if (dd < best) {
-          best = dd;
+        if (dd < bestd) {
+          bestd = dd;
           bi = t;
         }
       }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(FPX_FULL, best, o);
+        const double ob = __shfl_xor_sync(FPX_FULL, bestd, o);
         const int oi = __shfl_xor_sync(FPX_FULL, bi, o);
-        if (ob < best || (ob == best && oi < bi)) {
-          best = ob;
+        if (ob < bestd || (ob == bestd && oi < bi)) {
+          bestd = ob;
           bi = oi;
         }
       }
-      if (lane == j) {
+      if ((lane >> 1) == (j >> 1)) {
         rc[0] = z[bi % N];
         rc[1] = DR > 1 ? z[(bi / N) % N] : 0.0;
         rc[2] = DR > 2 ? z[bi / (N * N)] : 0.0;
@@ -1133,13 +1273,15 @@ __global__ void __launch_bounds__(64, 1)
     }
     if (!__any_sync(FPX_FULL, phase != 4)) break;
     if (!__any_sync(FPX_FULL, phase == 3)) continue;  // copies in flight
-    // (d) one map evaluation for every lane of the warp
-    if (__any_sync(FPX_FULL, phase == 3 && on_boundary<DR>(rn)))
-      eval_state<D, DR, N, true, 2>(mine, z, scale, rn, xs, st, sb);
-    else
-      eval_state<D, DR, N, false, 2>(mine, z, scale, rn, xs, st, sb);
+    // (d) one map evaluation for every point of the warp
+    const bool w2 = __any_sync(FPX_FULL, phase == 3 && on_boundary<DR>(rn));
+    ++nev;
+    nev2 += w2 ? 1 : 0;
+    nlev += (phase == 3 && part == 0) ? 1 : 0;
+    if (w2) eval_state_pair<D, DR, N, true>(mine, z, scale, rn, xs, st, part);
+    else eval_state_pair<D, DR, N, false>(mine, z, scale, rn, xs, st, part);
     if (phase != 3) continue;
-    // (e) this lane's trust-region Newton update (as newton_warp, D8)
+    // (e) the point's trust-region Newton update (newton_warp, D8)
     bool done = false;
     if (first) {
       first = false;
@@ -1151,7 +1293,13 @@ __global__ void __launch_bounds__(64, 1)
         for (int a = 0; a < DR; ++a) rc[a] = rn[a];
       } else {
         alpha *= P.shrink;
-        unstash_state(stash, st);
+#pragma unroll
+        for (int t = 0; t < 3; ++t) st.J[t] = stash[t];
+#pragma unroll
+        for (int t = 0; t < 6; ++t) {
+          st.H0[t] = stash[3 + t];
+          st.Q[t] = stash[9 + t];
+        }
         st.f = fcur;
       }
       if (smax < P.tol) done = true;
@@ -1161,13 +1309,24 @@ __global__ void __launch_bounds__(64, 1)
       fcur = st.f;
       const bool go = propose_step<DR>(st, rc, it, alpha, rn, pred, smax);
       ++it;
-      if (!go) done = true;
-      else stash_state(stash, st);
+      if (!go) {
+        done = true;
+      } else if (part == 0) {
+#pragma unroll
+        for (int t = 0; t < 3; ++t) stash[t] = st.J[t];
+#pragma unroll
+        for (int t = 0; t < 6; ++t) {
+          stash[3 + t] = st.H0[t];
+          stash[9 + t] = st.Q[t];
+        }
+      }
     }
     if (done) {
       const double dd = sqrt(st.f);
-      s_newton += 1;
-      s_iters += it;
+      if (part == 0) {
+        s_newton += 1;
+        s_iters += it;
+      }
       it_tot += it;
       const double epsd = DR < D ? eps_d_of(m, e) : 0.0;
       const int cd = classify<D, DR>(rc, dd, epsd);
@@ -1187,12 +1346,53 @@ __global__ void __launch_bounds__(64, 1)
   }
   s_newton = warp_sum64(s_newton);
   s_iters = warp_sum64(s_iters);
-  s_evals = warp_sum64(s_evals);
+  nlev = warp_sum64(nlev);
   if (lane == 0) {
     atomicAdd((unsigned long long*)&stats[FPX_STAT_NEWTON], (unsigned long long)s_newton);
     atomicAdd((unsigned long long*)&stats[FPX_STAT_ITERS], (unsigned long long)s_iters);
-    if (s_evals) atomicAdd((unsigned long long*)&stats[FPX_STAT_EVALS], (unsigned long long)s_evals);
+    atomicAdd((unsigned long long*)&stats[FPX_STAT_REST_WARP_EVALS], (unsigned long long)nev);
+    atomicAdd((unsigned long long*)&stats[FPX_STAT_REST_W2_EVALS], (unsigned long long)nev2);
+    atomicAdd((unsigned long long*)&stats[FPX_STAT_REST_LANE_EVALS], (unsigned long long)nlev);
   }
+}
+
+// Field values of the rest points (after k_rest_pairs settled their
+// records): thread per point, NaN for NOT_FOUND (D12).
+template <int DR, int N>
+__global__ void k_rest_values(const double* __restrict__ fbasis, int M,
+                              const int64_t* __restrict__ nun_dev,
+                              const int32_t* __restrict__ upts, const int32_t* __restrict__ code,
+                              const int32_t* __restrict__ elem, const double* __restrict__ r,
+                              const double* __restrict__ field, int C, double* values,
+                              int64_t* stats) {
+  __shared__ double z[16], scale[16];
+  if (threadIdx.x < N) {
+    z[threadIdx.x] = fbasis[FPX_BASIS_NODES(N, M) + threadIdx.x];
+    scale[threadIdx.x] = fbasis[FPX_BASIS_SCALE(N, M) + threadIdx.x];
+  }
+  __syncthreads();
+  const int64_t nun = *nun_dev;
+  int64_t s_evals = 0;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < nun;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = upts[u];
+    if (code[k] == kNotFound) {
+      for (int c = 0; c < C; ++c) values[k * C + c] = NAN;
+      continue;
+    }
+    double rr[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int a = 0; a < DR; ++a) rr[a] = r[k * DR + a];
+    double v[DR][N];
+    basis_values<DR, N>(z, scale, rr, v);
+    const int64_t e = elem[k];
+    for (int c = 0; c < C; ++c)
+      values[k * C + c] = contract_gmem<DR, N>(field + (e * C + c) * Pow<DR, N>::K, v);
+    ++s_evals;
+  }
+  for (int o = 16; o > 0; o >>= 1) s_evals += __shfl_xor_sync(FPX_FULL, s_evals, o);
+  if ((threadIdx.x & 31) == 0 && s_evals)
+    atomicAdd((unsigned long long*)&stats[FPX_STAT_EVALS], (unsigned long long)s_evals);
 }
 
 // ---------------------------------------------------------------- round 1, streamed
@@ -1684,30 +1884,33 @@ struct Pairs {
 
 template <int D, int DR, int N>
 struct Rest {
-  using RL = RestLay<D, DR, N>;
-  // lanes per warp whose slots fit two warps (or one) in ~220 KB of smem
-  static constexpr size_t BUDGET = 220 * 1024;
-  static constexpr int L2W = (int)((BUDGET / 2) / RL::lane_bytes());
-  static constexpr int L1W = (int)(BUDGET / RL::lane_bytes());
-  static constexpr int WARPS = L2W >= 16 ? 2 : 1;
-  static constexpr int LANES0 = WARPS == 2 ? L2W : L1W;
-  static constexpr int LANES = LANES0 > 32 ? 32 : (LANES0 < 1 ? 1 : LANES0);
+  using PL = PairLay<D, DR, N>;
+  // warps per block (16 points each) whose slots fit ~220 KB
+  static constexpr size_t WARP_BYTES = (size_t)16 * PL::SS * 8 + 16 * 8;
+  static constexpr int WPB0 = (int)((220 * 1024 - 256) / WARP_BYTES);
+  static constexpr int WPB = WPB0 > 4 ? 4 : (WPB0 < 1 ? 1 : WPB0);
   static cudaError_t run(const fpx_mesh_t& m, const double* x, int64_t nun_cap,
                          const int64_t* nun_dev, const int32_t* upts, const int32_t* clist,
                          const int32_t* cnum, int32_t* code, int32_t* elem, double* r,
                          double* dist, int32_t* iters, const double* field, int C,
                          double* values, int64_t* counter, int64_t* stats, cudaStream_t st) {
-    const int threads = WARPS * FPX_WARP;
-    const size_t smem = (size_t)(2 * ((N + 1) & ~1)) * 8 +
-                        (size_t)WARPS * (LANES * RL::SS + RL::SCR * FPX_WARP) * 8 +
-                        (size_t)WARPS * FPX_WARP * 8;
-    auto fn = k_rest_lanes<D, DR, N, LANES>;
+    const int threads = WPB * FPX_WARP;
+    const size_t smem = (size_t)(2 * ((N + 1) & ~1)) * 8 + (size_t)WPB * WARP_BYTES;
+    if (smem > 227 * 1024) return cudaErrorInvalidValue;
+    auto fn = k_rest_pairs<D, DR, N, WPB>;
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     unsigned blocks = persistent_blocks((const void*)fn, threads, smem,
-                                        (nun_cap + LANES - 1) / LANES);
+                                        (nun_cap * 2 + FPX_WARP - 1) / FPX_WARP);
     fn<<<blocks, threads, smem, st>>>(m, x, nun_dev, upts, clist, cnum, code, elem, r, dist, iters,
-                                      field, C, values, counter, stats);
+                                      counter, stats);
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess || !field) return err;
+    int64_t b = (nun_cap + 127) / 128;
+    if (b > 148 * 8) b = 148 * 8;
+    if (b < 1) b = 1;
+    k_rest_values<DR, N><<<(unsigned)b, 128, 0, st>>>(m.basis, m.M, nun_dev, upts, code, elem, r,
+                                                      field, C, values, stats);
     return cudaGetLastError();
   }
   static cudaError_t lists(const fpx_mesh_t& m, const double* x, int64_t nun_cap,

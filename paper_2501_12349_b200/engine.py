@@ -179,6 +179,12 @@ def setup(nodes, order: int | None = None, ref_dim: int | None = None, *,
     opt.newton.apply(m)
     m.eps_d_abs = -1.0 if opt.eps_d is None else float(opt.eps_d)
     m.eps_d_rel = float(opt.eps_d_rel)
+    # packed candidate-filter records (one 256-byte row per element)
+    S.frec = torch.empty((E, _C.FREC), dtype=torch.float64, device=dev)
+    _C.check(_C.lib().fpx_filter_records(
+        d, E, _C.ptr(S.aabb), _C.ptr(S.obb_c), _C.ptr(S.obb_inv), _C.ptr(S.obb_ok),
+        _C.ptr(S.frame), _C.ptr(S.frec), _C.stream_handle()), "fpx_filter_records")
+    m.frec = S.frec.data_ptr()
     S.mesh_t = m
     # multi-rank: global map Psi_G over the union of all ranks' boxes
     S.group = group or transport.RankGroup()
