@@ -89,6 +89,9 @@ typedef struct fpx_mesh_t {
    * aabb lo,hi [2d] | obb_c [d] | obb_inv [d*d] | frame x_c,J_c^-1 [d+d*d] |
    * ... | obb_ok as 0.0/1.0 at index FPX_FREC-1 (fpx_filter_records). */
   const double* frec;
+  /* (ABI 2) nodes with rows padded to an even length NP (N rounded up):
+   * [E][d][N^(dr-1)][NP], 16-byte aligned rows (fpx_pad_nodes). */
+  const double* nodes_pad;
 } fpx_mesh_t;
 
 #define FPX_FREC 32
@@ -146,6 +149,10 @@ int fpx_setup_bounds(int d, int dr, int N, int M, int64_t E, const double* basis
 int fpx_filter_records(int d, int64_t E, const double* aabb, const double* obb_c,
                        const double* obb_inv, const uint8_t* obb_ok, const double* frame,
                        double* frec, void* stream);
+
+/* Copies nodes [E][d][N^dr] into the row-padded layout of mesh.nodes_pad. */
+int fpx_pad_nodes(int d, int dr, int N, int64_t E, const double* nodes, double* nodes_pad,
+                  void* stream);
 
 int fpx_bound_function(int dr, int N, int M, int64_t nf, const double* basis,
                        const double* values, double* lower, double* upper, void* stream);

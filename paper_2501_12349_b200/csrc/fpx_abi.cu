@@ -133,7 +133,10 @@ struct Group {
 };
 
 struct FindWs {
-  int32_t *best, *npass, *upts, *clist, *cnum;
+  int32_t *best, *npass, *upts, *clist, *cnum, *found, *lock, *nps, *perm, *hist, *bstart, *bcur,
+      *maxnp;
+  int64_t* cum;
+  int4* pairs;
   int64_t *nun, *counter, *chunk_ctr;
   Group g1;
   // point ordering by hash cell
@@ -157,6 +160,16 @@ struct FindWs {
     upts = c.take<int32_t>(n);
     clist = c.take<int32_t>(n * FPX_RK);
     cnum = c.take<int32_t>(n);
+    found = c.take<int32_t>(n);
+    lock = c.take<int32_t>(n);
+    nps = c.take<int32_t>(n);
+    perm = c.take<int32_t>(n);
+    hist = c.take<int32_t>(3 * FPX_HMAX);  // hist | bcur | bstart (one memset)
+    bcur = hist + FPX_HMAX;
+    bstart = hist + 2 * FPX_HMAX;
+    maxnp = c.take<int32_t>(1);
+    cum = c.take<int64_t>(FPX_HMAX + 1);
+    pairs = c.take<int4>(2 * n + 1024);  // pair list (beyond: rebuilt by the kernel)
     nun = c.take<int64_t>(1);
     counter = c.take<int64_t>(1);
     chunk_ctr = c.take<int64_t>(1);
@@ -308,6 +321,15 @@ int fpx_filter_records(int d, int64_t E, const double* aabb, const double* obb_c
   return FPX_OK;
 }
 
+int fpx_pad_nodes(int d, int dr, int N, int64_t E, const double* nodes, double* nodes_pad,
+                  void* stream) {
+  if (!(d == 2 || d == 3) || dr < 1 || dr > d) return fail(FPX_EINVAL, "pad: bad d/dr %d/%d", d, dr);
+  if (N < 2) return fail(FPX_EINVAL, "pad: bad N=%d", N);
+  if (E <= 0) return FPX_OK;
+  FPX_LAUNCH(fpx::launch_pad_nodes(d, dr, N, E, nodes, nodes_pad, S(stream)));
+  return FPX_OK;
+}
+
 int fpx_bound_function(int dr, int N, int M, int64_t nf, const double* basis,
                        const double* values, double* lower, double* upper, void* stream) {
   if (dr != 1 && dr != 2) return fail(FPX_EINVAL, "bound_function: dr must be 1 or 2");
@@ -420,6 +442,7 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
   w.carve_cells(cv, n, cells_of(m));
   if (!cv.ok()) return fail(FPX_EINVAL, "find workspace too small (%zu < %zu)", ws_bytes, cv.off);
   if (!m->frec) return fail(FPX_EINVAL, "mesh has no filter records (fpx_filter_records)");
+  if (!m->nodes_pad) return fail(FPX_EINVAL, "mesh has no padded nodes (fpx_pad_nodes)");
   const fpx_mesh_t& M = *m;
   // --- order the points by hash cell (counting sort)
   const int64_t nc = w.ncells;
@@ -463,9 +486,17 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
   }
   if (g_prof_stop) FPX_CK(cudaEventRecord(g_prof_stop, st));
   // --- rest: remaining candidates of the unresolved points
-  FPX_LAUNCH(fpx::launch_rest_lists(M, x, n, w.nun, w.upts, w.clist, w.cnum, st));
-  FPX_LAUNCH(fpx::launch_find_rest(M, x, n, w.nun, w.upts, w.clist, w.cnum, code, elem, r, dist,
-                                   iters, field, C, values, w.counter, stats, st));
+  FPX_CK(cudaMemsetAsync(w.hist, 0, sizeof(int32_t) * 2 * FPX_HMAX, st));
+  g_launches += 2;
+  FPX_LAUNCH(fpx::launch_rest_lists(M, x, n, w.nun, w.upts, w.clist, w.cnum, w.nps, w.hist,
+                                    w.bstart, w.bcur, w.perm, w.cum, w.maxnp, w.pairs, st));
+  FPX_CK(cudaMemsetAsync(w.found, 0, sizeof(int32_t) * n, st));
+  FPX_CK(cudaMemsetAsync(w.lock, 0, sizeof(int32_t) * n, st));
+  FPX_LAUNCH(fpx::launch_find_rest(M, x, n, w.nun, w.upts, w.clist, w.cnum, w.nps, w.perm,
+                                   w.cum, w.maxnp, w.best, w.pairs, w.found, w.lock, code, elem,
+                                   r, dist,
+                                   iters,
+                                   field, C, values, w.counter, stats, st));
   g_launches += 1;
   k_find_totals<<<1, 1, 0, st>>>(w.nun, stats, n);
   FPX_CK(cudaGetLastError());

@@ -968,6 +968,25 @@ static unsigned grid_for(int64_t n, int threads) {
   return (unsigned)b;
 }
 
+// nodes [E][d][K] -> [E][d][K/N][NP] (NP = N rounded up to even; pad = 0).
+__global__ void k_pad_nodes(int d, int N, int K, int64_t E, const double* __restrict__ nodes,
+                            double* pad) {
+  const int NP = N + (N & 1), R = K / N;
+  const int64_t tot = E * d * R * NP;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < tot;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(t % NP);
+    const int64_t rowg = t / NP;  // (e, c, row)
+    pad[t] = i < N ? nodes[rowg * N + i] : 0.0;
+  }
+}
+cudaError_t launch_pad_nodes(int d, int dr, int N, int64_t E, const double* nodes, double* pad,
+                             cudaStream_t st) {
+  const int K = dr == 1 ? N : (dr == 2 ? N * N : N * N * N);
+  const int64_t tot = E * d * (K / N) * (N + (N & 1));
+  k_pad_nodes<<<grid_for(tot, 256), 256, 0, st>>>(d, N, K, E, nodes, pad);
+  return cudaGetLastError();
+}
 cudaError_t launch_filter_records(int d, int64_t E, const double* aabb, const double* obb_c,
                                   const double* obb_inv, const uint8_t* obb_ok,
                                   const double* frame, double* frec, cudaStream_t st) {

@@ -8,6 +8,7 @@
 #define FPX_SETUP_MAXN 16  // setup kernels: nodes per axis <= 16 (p <= 15)
 #define FPX_ITEM 32        // (point|pair) slots per warp work item
 #define FPX_RK 16          // best-first ranked candidates listed per rest point
+#define FPX_HMAX 1024      // rest kernel: candidate-count histogram bins
 
 namespace fpx {
 
@@ -25,6 +26,8 @@ cudaError_t launch_setup_bounds(int d, int dr, int N, int M, int64_t E, const do
 cudaError_t launch_bound_function(int dr, int N, int M, int64_t nf, const double* basis,
                                   const double* values, double* lower, double* upper,
                                   cudaStream_t st);
+cudaError_t launch_pad_nodes(int d, int dr, int N, int64_t E, const double* nodes, double* pad,
+                             cudaStream_t st);
 cudaError_t launch_filter_records(int d, int64_t E, const double* aabb, const double* obb_c,
                                   const double* obb_inv, const uint8_t* obb_ok,
                                   const double* frame, double* frec, cudaStream_t st);
@@ -90,12 +93,17 @@ cudaError_t launch_newton_pairs(const fpx_mesh_t& m, const double* x, const int3
 // (k_rest_lanes).
 cudaError_t launch_rest_lists(const fpx_mesh_t& m, const double* x, int64_t nun_cap,
                               const int64_t* nun_dev, const int32_t* upts, int32_t* clist,
-                              int32_t* cnum, cudaStream_t st);
+                              int32_t* cnum, int32_t* nps, int32_t* hist, int32_t* bstart,
+                              int32_t* bcur, int32_t* perm, int64_t* cum, int32_t* maxnp,
+                              int4* pairs, cudaStream_t st);
 cudaError_t launch_find_rest(const fpx_mesh_t& m, const double* x, int64_t nun_cap,
                              const int64_t* nun_dev, const int32_t* upts, const int32_t* clist,
-                             const int32_t* cnum, int32_t* code, int32_t* elem, double* r,
-                             double* dist, int32_t* iters, const double* field, int C,
-                             double* values, int64_t* counter, int64_t* stats, cudaStream_t st);
+                             const int32_t* cnum, const int32_t* nps, const int32_t* perm,
+                             const int64_t* cum, const int32_t* maxnp, const int32_t* best,
+                             const int4* pairs, int32_t* found,
+                             int32_t* lock, int32_t* code, int32_t* elem, double* r, double* dist,
+                             int32_t* iters, const double* field, int C, double* values,
+                             int64_t* counter, int64_t* stats, cudaStream_t st);
 cudaError_t launch_eval_items(int dr, int Nf, const double* fbasis, int C, const double* field,
                               const double* r, const int32_t* sorted_pts, const Item* items,
                               const int64_t* nitems_dev, int64_t items_cap, double* values,

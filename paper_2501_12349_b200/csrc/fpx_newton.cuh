@@ -14,6 +14,7 @@
 // distance uses explicit non-FMA intrinsics so the seed node is bit-identical.
 #pragma once
 #include <math.h>
+#include <stdlib.h>
 
 #include "fpx_common.cuh"
 #include "fpx_kernels.cuh"
@@ -88,9 +89,10 @@ __device__ __forceinline__ void eval_state(const double* __restrict__ sX,
   // LAY 1: read in place from global memory ([d][N^dr]);
   // LAY 2: a per-lane shared slot holding [d][N^dr] unpadded.
   using Lp = Lay<D, DR, N>;
+  // LAY 3: global memory, rows padded to NP (mesh.nodes_pad)
   constexpr bool GEO = LAY == 1;
-  constexpr int GCS = LAY != 0 ? Lp::K : Lp::CS;
-  constexpr int GNP = LAY != 0 ? N : Lp::NP;
+  constexpr int GCS = (LAY == 1 || LAY == 2) ? Lp::K : Lp::CS;
+  constexpr int GNP = (LAY == 1 || LAY == 2) ? N : Lp::NP;
   double v0[N], g0[N], h0[N];
   lagrange<N, W2>(z, scale, r[0], v0, g0, h0);
 #pragma unroll
@@ -130,6 +132,7 @@ __device__ __forceinline__ void eval_state(const double* __restrict__ sX,
             double2 p;
             if (GEO) p = make_double2(__ldg(row + i), i + 1 < N ? __ldg(row + i + 1) : 0.0);
             else if (LAY == 2) p = make_double2(row[i], i + 1 < N ? row[i + 1] : 0.0);
+            else if (LAY == 3) p = __ldg(reinterpret_cast<const double2*>(row + i));
             else if (i + 1 < N) p = *reinterpret_cast<const double2*>(row + i);
             else p = make_double2(row[i], 0.0);
             s0 = fma(p.x, v0[i], s0);
@@ -887,7 +890,8 @@ __device__ __forceinline__ bool mbar_test(uint64_t* mb, unsigned parity) {
 template <int D>
 __global__ void __launch_bounds__(128)
     k_rest_lists(fpx_mesh_t m, const double* __restrict__ x, const int64_t* __restrict__ nun_dev,
-                 const int32_t* __restrict__ upts, int32_t* clist, int32_t* cnum) {
+                 const int32_t* __restrict__ upts, int32_t* clist, int32_t* cnum, int32_t* nps,
+                 int32_t* hist) {
   // warp per rest point: lanes test the hash-list entries (one filter record
   // each), (v, e) of the passing ones go to shared memory, and the rank of
   // each is the number of passing entries before it in (v, e) order
@@ -929,10 +933,78 @@ __global__ void __launch_bounds__(128)
     for (int o = 16; o > 0; o >>= 1) np += __shfl_xor_sync(FPX_FULL, np, o);
     // more than FPX_RK passing: the rest kernel scans after the last listed
     // one; lists longer than FPX_LISTMAX: it scans everything after rank 0
-    if (lane == 0)
+    if (qe - qs > L) {  // list longer than the buffer: count the rest
+      for (int q = qs + L + lane; q < qe; q += FPX_WARP) {
+        FRec R;
+        load_frec(m.frec, m.elems[q], R);
+        np += __popc(__ballot_sync(__activemask(), frec_passes<D>(R, xs)));
+      }
+      np = __shfl_sync(FPX_FULL, np, 0);
+    }
+    if (lane == 0) {
       cnum[u] = qe - qs > L ? -1 : (np > FPX_RK ? -FPX_RK : np);
+      nps[u] = np;
+      atomicAdd(&hist[np < FPX_HMAX - 1 ? np : FPX_HMAX - 1], 1);
+    }
     __syncwarp();
   }
+}
+
+// Nearest-node seeds (D7: smallest physical distance, ties -> lowest
+// lexicographic index; the distance accumulates exactly as in newton_warp)
+// for up to 4 lanes of the warp at once: every lane scans K/32 nodes of each
+// of the seeded points' slots and the four argmin reductions run
+// interleaved.  PAD: slot rows padded to Lay::NP (round-1 ring slots).
+// Returns the seeded node index to lane js[s] (and -1 to the others).
+template <int D, int DR, int N, bool PAD>
+__device__ __forceinline__ int seed_batch(const unsigned* js, int cnt, const double* const* sj,
+                                          const double (*xj)[3], int lane) {
+  using L = Lay<D, DR, N>;
+  constexpr int K = L::K;
+  constexpr int CS = PAD ? L::CS : K;
+  double best[4];
+  int bi[4];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) {
+    best[s] = INFINITY;
+    bi[s] = 0x7fffffff;
+  }
+  for (int t = lane; t < K; t += FPX_WARP) {
+    const int row = t / N, i = t - row * N;
+    const int off = PAD ? row * L::NP + i : t;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      if (s < cnt) {
+        double dd = 0.0;
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+          const double tt = __dsub_rn(xj[s][c], sj[s][c * CS + off]);
+          dd = __fma_rn(tt, tt, dd);
+        }
+        if (dd < best[s]) {
+          best[s] = dd;
+          bi[s] = t;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const double ob = __shfl_xor_sync(FPX_FULL, best[s], o);
+      const int oi = __shfl_xor_sync(FPX_FULL, bi[s], o);
+      if (ob < best[s] || (ob == best[s] && oi < bi[s])) {
+        best[s] = ob;
+        bi[s] = oi;
+      }
+    }
+  }
+  int mine = -1;
+#pragma unroll
+  for (int s = 0; s < 4; ++s)
+    if (s < cnt && (unsigned)lane == js[s]) mine = bi[s];
+  return mine;
 }
 
 // Per-point slot: geometry [D][N^DR] | axis-1.. basis values | Newton stash,
@@ -950,7 +1022,7 @@ struct PairLay {
 // the per-coordinate partial sums are added across the pair (xor 1, the same
 // order on both lanes, so both hold bitwise identical states).  sp: the
 // point's slot; its basis block is written by lane 0 of the pair.
-template <int D, int DR, int N, bool W2>
+template <int D, int DR, int N, int G, bool W2>
 __device__ __forceinline__ void eval_state_pair(const double* __restrict__ sp,
                                                 const double* __restrict__ z,
                                                 const double* __restrict__ scale, const double* r,
@@ -983,7 +1055,7 @@ __device__ __forceinline__ void eval_state_pair(const double* __restrict__ sp,
     double xv = 0.0, g_0 = 0.0, g_1 = 0.0, g_2 = 0.0;
     double h00 = 0.0, h11 = 0.0, h22 = 0.0, h01 = 0.0, h02 = 0.0, h12 = 0.0;
 #pragma unroll 3
-    for (int q = part; q < R; q += 2) {
+    for (int q = part; q < R; q += G) {
       const double* row = Xc + q * N;
       double s0 = 0.0, s1 = 0.0, s2 = 0.0;
 #pragma unroll
@@ -1037,18 +1109,22 @@ __device__ __forceinline__ void eval_state_pair(const double* __restrict__ sp,
     HH[c][5] = h12;
   }
 #undef PSB
-  // pair sums (both lanes add the same two numbers)
+  // group sums (xor butterfly: every lane adds the same numbers in the same
+  // order, so the group holds bitwise identical states)
 #pragma unroll
-  for (int c = 0; c < D; ++c) {
-    X[c] += __shfl_xor_sync(FPX_FULL, X[c], 1);
+  for (int o = 1; o < G; o <<= 1) {
 #pragma unroll
-    for (int a = 0; a < DR; ++a) GG[c][a] += __shfl_xor_sync(FPX_FULL, GG[c][a], 1);
-    if (W2) {
+    for (int c = 0; c < D; ++c) {
+      X[c] += __shfl_xor_sync(FPX_FULL, X[c], o);
 #pragma unroll
-      for (int t = 0; t < 6; ++t) {
-        if (DR < 3 && (t == 2 || t >= 4)) continue;
-        if (DR < 2 && t != 0) continue;
-        HH[c][t] += __shfl_xor_sync(FPX_FULL, HH[c][t], 1);
+      for (int a = 0; a < DR; ++a) GG[c][a] += __shfl_xor_sync(FPX_FULL, GG[c][a], o);
+      if (W2) {
+#pragma unroll
+        for (int t = 0; t < 6; ++t) {
+          if (DR < 3 && (t == 2 || t >= 4)) continue;
+          if (DR < 2 && t != 0) continue;
+          HH[c][t] += __shfl_xor_sync(FPX_FULL, HH[c][t], o);
+        }
       }
     }
   }
@@ -1083,7 +1159,7 @@ __device__ __forceinline__ void eval_state_pair(const double* __restrict__ sp,
   }
 }
 
-template <int D, int DR, int N, int WPB>
+template <int D, int DR, int N, int G, int WPB>
 __global__ void __launch_bounds__(WPB * 32, 1)
     k_rest_pairs(fpx_mesh_t m, const double* __restrict__ x, const int64_t* __restrict__ nun_dev,
                  const int32_t* __restrict__ upts, const int32_t* __restrict__ clist,
@@ -1091,12 +1167,12 @@ __global__ void __launch_bounds__(WPB * 32, 1)
                  double* dist, int32_t* iters, int64_t* counter, int64_t* stats) {
   using PL = PairLay<D, DR, N>;
   constexpr int K = PL::K;
-  constexpr int PPW = FPX_WARP / 2;  // points per warp
+  constexpr int PPW = FPX_WARP / G;  // points per warp
   extern __shared__ __align__(16) double smem[];
   double* z = smem;
   double* scale = smem + N;
   const int warp = threadIdx.x / FPX_WARP, lane = threadIdx.x % FPX_WARP;
-  const int pslot = lane >> 1, part = lane & 1;
+  const int pslot = lane / G, part = lane % G, glead = lane & ~(G - 1);
   double* slots = smem + 2 * ((N + 1) & ~1) + (size_t)warp * PPW * PL::SS;
   double* mine = slots + pslot * PL::SS;
   double* stash = mine + PL::STASH;
@@ -1137,7 +1213,7 @@ __global__ void __launch_bounds__(WPB * 32, 1)
         if (!have_point) {
           int64_t uu = 0;
           if (part == 0) uu = (int64_t)atomicAdd((unsigned long long*)counter, 1ull);
-          u = __shfl_sync(__activemask(), uu, lane & ~1);
+          u = __shfl_sync(__activemask(), uu, glead);
           if (u >= nun) {
             phase = 4;
             break;
@@ -1220,44 +1296,33 @@ __global__ void __launch_bounds__(WPB * 32, 1)
       const int j = __ffs(req) - 1;
       const int ej = __shfl_sync(FPX_FULL, e, j);
       const double* src = m.nodes + (int64_t)ej * D * K;
-      double* dst = slots + (j >> 1) * PL::SS;
+      double* dst = slots + (j / G) * PL::SS;
       for (int t = lane; t < D * K; t += FPX_WARP) cp_async8(dst + t, src + t);
-      cp_async_arrive_noinc(&mbars[j >> 1]);
+      cp_async_arrive_noinc(&mbars[j / G]);
     }
     if (phase == 1) phase = 2;
     // (c) points whose copy landed get their seed (warp-cooperative, D7)
     const bool landed = phase == 2 && mbar_test(&mbars[pslot], parity);
     if (landed) parity ^= 1u;
-    for (unsigned rdy = __ballot_sync(FPX_FULL, landed && part == 0); rdy; rdy &= rdy - 1) {
-      const int j = __ffs(rdy) - 1;
-      double xj[3];
+    for (unsigned rdy = __ballot_sync(FPX_FULL, landed && part == 0); rdy;) {
+      unsigned js[4];
+      const double* sj[4];
+      double xj[4][3];
+      int cnt = 0;
 #pragma unroll
-      for (int c = 0; c < D; ++c) xj[c] = __shfl_sync(FPX_FULL, xs[c], j);
-      const double* sj = slots + (j >> 1) * PL::SS;
-      double bestd = INFINITY;
-      int bi = 0x7fffffff;
-      for (int t = lane; t < K; t += FPX_WARP) {
-        double dd = 0.0;
+      for (int s2 = 0; s2 < 4; ++s2) {
+        js[s2] = rdy ? (unsigned)(__ffs(rdy) - 1) : 0u;
+        if (rdy) {
+          rdy &= rdy - 1;
+          cnt = s2 + 1;
+        }
+        sj[s2] = slots + (js[s2] / G) * PL::SS;
 #pragma unroll
-        for (int c = 0; c < D; ++c) {
-          const double tt = __dsub_rn(xj[c], sj[c * K + t]);
-          dd = __fma_rn(tt, tt, dd);
-        }
-        if (dd < bestd) {
-          bestd = dd;
-          bi = t;
-        }
+        for (int c = 0; c < D; ++c) xj[s2][c] = __shfl_sync(FPX_FULL, xs[c], js[s2]);
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(FPX_FULL, bestd, o);
-        const int oi = __shfl_xor_sync(FPX_FULL, bi, o);
-        if (ob < bestd || (ob == bestd && oi < bi)) {
-          bestd = ob;
-          bi = oi;
-        }
-      }
-      if ((lane >> 1) == (j >> 1)) {
+      int bi = seed_batch<D, DR, N, false>(js, cnt, sj, xj, lane);
+      bi = __shfl_sync(FPX_FULL, bi, glead);  // the group leader holds the seed
+      if (bi >= 0 && landed) {
         rc[0] = z[bi % N];
         rc[1] = DR > 1 ? z[(bi / N) % N] : 0.0;
         rc[2] = DR > 2 ? z[bi / (N * N)] : 0.0;
@@ -1278,8 +1343,8 @@ __global__ void __launch_bounds__(WPB * 32, 1)
     ++nev;
     nev2 += w2 ? 1 : 0;
     nlev += (phase == 3 && part == 0) ? 1 : 0;
-    if (w2) eval_state_pair<D, DR, N, true>(mine, z, scale, rn, xs, st, part);
-    else eval_state_pair<D, DR, N, false>(mine, z, scale, rn, xs, st, part);
+    if (w2) eval_state_pair<D, DR, N, G, true>(mine, z, scale, rn, xs, st, part);
+    else eval_state_pair<D, DR, N, G, false>(mine, z, scale, rn, xs, st, part);
     if (phase != 3) continue;
     // (e) the point's trust-region Newton update (newton_warp, D8)
     bool done = false;
@@ -1341,6 +1406,334 @@ __global__ void __launch_bounds__(WPB * 32, 1)
         for (int a = 0; a < DR; ++a) br[a] = rc[a];
       }
       if (bc == kInterior) point_done = true;
+      phase = 0;
+    }
+  }
+  s_newton = warp_sum64(s_newton);
+  s_iters = warp_sum64(s_iters);
+  nlev = warp_sum64(nlev);
+  if (lane == 0) {
+    atomicAdd((unsigned long long*)&stats[FPX_STAT_NEWTON], (unsigned long long)s_newton);
+    atomicAdd((unsigned long long*)&stats[FPX_STAT_ITERS], (unsigned long long)s_iters);
+    atomicAdd((unsigned long long*)&stats[FPX_STAT_REST_WARP_EVALS], (unsigned long long)nev);
+    atomicAdd((unsigned long long*)&stats[FPX_STAT_REST_W2_EVALS], (unsigned long long)nev2);
+    atomicAdd((unsigned long long*)&stats[FPX_STAT_REST_LANE_EVALS], (unsigned long long)nlev);
+  }
+}
+
+
+// Pair enumeration of the rest kernel: rest points sorted by candidate count
+// (descending) so that the points with a rank-r candidate are a prefix;
+// cum[r] = number of pairs of rank < r (r >= 1).  One block.
+static __global__ void k_rest_order(const int32_t* __restrict__ hist, int32_t* bstart, int64_t* cum,
+                             int32_t* maxnp) {
+  if (threadIdx.x != 0) return;
+  int pos = 0, mx = 0;
+  for (int v = FPX_HMAX - 1; v >= 0; --v) {  // descending buckets
+    bstart[v] = pos;
+    pos += hist[v];
+    if (hist[v] && v > mx) mx = v;
+  }
+  // points with npass > r: suffix sums
+  int64_t c = 0, above = 0;
+  for (int v = FPX_HMAX - 1; v > 0; --v) above += hist[v];  // npass >= 1
+  // above = #points with npass > 0; iterate r = 1.. with cnt_r = #(npass > r)
+  int64_t gt = above - hist[1 < FPX_HMAX ? 1 : 0];          // npass > 1
+  cum[0] = 0;
+  cum[1] = 0;
+  for (int rr = 1; rr < FPX_HMAX - 1; ++rr) {
+    c += gt;  // pairs of rank rr
+    cum[rr + 1] = c;
+    gt -= hist[rr + 1];
+  }
+  *maxnp = mx;
+}
+
+static __global__ void k_rest_scatter(const int64_t* __restrict__ nun_dev, const int32_t* __restrict__ nps,
+                               const int32_t* __restrict__ bstart, int32_t* bcur, int32_t* perm) {
+  const int64_t nun = *nun_dev;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < nun;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const int v = nps[u] < FPX_HMAX - 1 ? nps[u] : FPX_HMAX - 1;
+    perm[bstart[v] + atomicAdd(&bcur[v], 1)] = (int32_t)u;
+  }
+}
+
+// Rank-major pair list: pair g = cum[r] + (position of u in perm) for every
+// rest point u and rank 1 <= r < npass(u): {point k, element (or -1 when
+// beyond the ranked list), u, r}.
+static __global__ void k_rest_pairlist(const int64_t* __restrict__ nun_dev,
+                                       const int32_t* __restrict__ upts,
+                                       const int32_t* __restrict__ perm,
+                                       const int32_t* __restrict__ nps,
+                                       const int32_t* __restrict__ clist,
+                                       const int32_t* __restrict__ cnum,
+                                       const int64_t* __restrict__ cum, int4* pairs,
+                                       int64_t pair_cap) {
+  const int64_t nun = *nun_dev;
+  for (int64_t pp = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; pp < nun;
+       pp += (int64_t)gridDim.x * blockDim.x) {
+    const int u = perm[pp];
+    const int np = nps[u] < FPX_HMAX - 1 ? nps[u] : FPX_HMAX - 1;
+    const int cn = cnum[u];
+    const int nl = cn < 0 ? -cn : cn;
+    const int k = upts[u];
+    for (int rr = 1; rr < np; ++rr) {
+      const int64_t g = cum[rr] + pp;
+      if (g >= pair_cap) break;  // the rest kernel rebuilds these itself
+      pairs[g] = make_int4(k, rr < nl ? clist[(int64_t)u * FPX_RK + rr] : -1, u, rr);
+    }
+  }
+}
+
+// Rest kernel, L1 variant: the unit of work is one (point, candidate rank)
+// pair, so a point with many candidates spreads over many lanes instead of
+// serialising on one.  Pairs are enumerated rank-major (all rank-1 pairs,
+// then all rank-2, ...); a pair whose point already has an INTERIOR result
+// is skipped, which keeps the work close to the sequential early-exit order
+// (SPEC.md:407).  Results are merged into the point's record under a
+// per-point lock with the D6 rule.  The candidate's geometry is read in
+// place (mesh.nodes_pad, 16-byte loads through L1/L2), so the number of
+// pairs in flight is bounded by registers, not shared memory.
+template <int D, int DR, int N>
+__global__ void __launch_bounds__(128, 2)
+    k_rest_l1(fpx_mesh_t m, const double* __restrict__ x, const int64_t* __restrict__ nun_dev,
+              const int32_t* __restrict__ upts, const int32_t* __restrict__ clist,
+              const int32_t* __restrict__ cnum, const int32_t* __restrict__ nps,
+              const int32_t* __restrict__ perm, const int64_t* __restrict__ cum,
+              const int32_t* __restrict__ maxnp_dev, const int32_t* __restrict__ best,
+              const int4* __restrict__ pairs, int64_t pair_cap, int32_t* found, int32_t* lock,
+              int32_t* code,
+              int32_t* elem, double* r, double* dist, int32_t* iters, int64_t* counter,
+              int64_t* stats) {
+  using L = Lay<D, DR, N>;
+  constexpr int ES = L::GEO;  // doubles per element in nodes_pad
+  extern __shared__ __align__(16) double smem[];
+  double* z = smem;
+  double* scale = smem + N;
+  const int warp = threadIdx.x / FPX_WARP, lane = threadIdx.x % FPX_WARP;
+  double* sb = smem + 2 * ((N + 1) & ~1) + warp * Scratch<DR, N>::SLOTS * FPX_WARP + lane;
+  double* stash = sb + Scratch<DR, N>::STASH * FPX_WARP;
+  if (threadIdx.x < N) {
+    z[threadIdx.x] = m.basis[FPX_BASIS_NODES(N, m.M) + threadIdx.x];
+    scale[threadIdx.x] = m.basis[FPX_BASIS_SCALE(N, m.M) + threadIdx.x];
+  }
+  __syncthreads();
+  const NewtonParams P = newton_of(m);
+  (void)nun_dev;
+  const int maxnp = *maxnp_dev;
+  const int64_t gmax = cum[maxnp];  // all pairs of ranks 1 .. maxnp-1
+  int64_t s_newton = 0, s_iters = 0, nev = 0, nev2 = 0, nlev = 0;
+  int64_t u = 0, k = 0;
+  double xs[3] = {0.0, 0.0, 0.0};
+  int phase = 0;  // 0 needs a pair, 3 iterating, 4 done
+  int e = 0, it = 0;
+  bool first = true;
+  double rc[3] = {0.0, 0.0, 0.0}, rn[3] = {0.0, 0.0, 0.0};
+  double alpha = 1.0, fcur = 0.0, pred = 0.0, smax = 0.0;
+  NState st;
+  while (true) {
+    // (a) lanes without a pair claim the next ones (warp-aggregated) until
+    // they find one still to do
+    while (true) {
+      const unsigned need = __ballot_sync(FPX_FULL, phase == 0);
+      if (!need) break;
+      int64_t base = 0;
+      if (lane == __ffs(need) - 1)
+        base = (int64_t)atomicAdd((unsigned long long*)counter, (unsigned long long)__popc(need));
+      base = __shfl_sync(FPX_FULL, base, __ffs(need) - 1);
+      if (phase != 0) continue;
+      const int64_t g = base + __popc(need & ((1u << lane) - 1u));
+      if (g >= gmax) {
+        phase = 4;
+        continue;
+      }
+      int4 pr;
+      if (g < pair_cap) {
+        pr = pairs[g];
+      } else {  // beyond the pair-list capacity: locate (rank, point) directly
+        int lo = 1, hi = maxnp;  // cum[lo] <= g < cum[hi]
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (cum[mid] <= g) lo = mid;
+          else hi = mid;
+        }
+        const int uu = perm[g - cum[lo]];
+        const int cn = cnum[uu];
+        const int nl = cn < 0 ? -cn : cn;
+        pr = make_int4(upts[uu], lo < nl ? clist[(int64_t)uu * FPX_RK + lo] : -1, uu, lo);
+      }
+      u = pr.z;
+      if (*(volatile int32_t*)&found[u]) continue;  // an INTERIOR was found already
+      k = pr.x;
+      const int rank = pr.w;
+#pragma unroll
+      for (int c = 0; c < D; ++c) xs[c] = x[k * D + c];
+      int en = pr.y;
+      if (en < 0) {
+        // beyond the ranked list: the (rank - nlist)-th passing candidate
+        // ranked after the last listed one, in hash-list order (lists longer
+        // than the ranking buffer, cn == -1: every passing candidate but the
+        // round-1 one)
+        const int cn = cnum[u];
+        const int nlist = cn < 0 ? -cn : cn;
+        const bool all = cn == -1;
+        const int te = all ? best[k] : clist[u * FPX_RK + nlist - 1];
+        FRec R;
+        load_frec(m.frec, te, R);
+        const double tv = frec_bestfirst<D>(R, xs);
+        int ax[3];
+        const int64_t cell = cell_of(D, m.grid, m.ncell, xs, ax);
+        int want = rank - nlist;
+        for (int q = m.offsets[cell]; q < m.offsets[cell + 1]; ++q) {
+          const int ee = m.elems[q];
+          if (all && ee == te) continue;
+          load_frec(m.frec, ee, R);
+          if (!frec_passes<D>(R, xs)) continue;
+          if (!all && !bf_less(tv, te, frec_bestfirst<D>(R, xs), ee)) continue;
+          if (want-- == 0) {
+            en = ee;
+            break;
+          }
+        }
+      }
+      if (en < 0) continue;
+      e = en;
+      phase = 1;  // needs its seed
+    }
+    // seeds (D7) of the lanes that just got a pair, 4 at a time: the warp
+    // reads each candidate's nodes with coalesced loads
+    for (unsigned sd = __ballot_sync(FPX_FULL, phase == 1); sd;) {
+      int js[4], ej[4];
+      double xj[4][3];
+      int cnt = 0;
+#pragma unroll
+      for (int s2 = 0; s2 < 4; ++s2) {
+        js[s2] = sd ? __ffs(sd) - 1 : 0;
+        if (sd) {
+          sd &= sd - 1;
+          cnt = s2 + 1;
+        }
+        ej[s2] = __shfl_sync(FPX_FULL, e, js[s2]);
+#pragma unroll
+        for (int c = 0; c < D; ++c) xj[s2][c] = __shfl_sync(FPX_FULL, xs[c], js[s2]);
+      }
+      double bst[4];
+      int bi[4];
+#pragma unroll
+      for (int s2 = 0; s2 < 4; ++s2) {
+        bst[s2] = INFINITY;
+        bi[s2] = 0x7fffffff;
+      }
+      for (int t = lane; t < L::K; t += FPX_WARP) {
+        const int row = t / N, i = t - row * N;
+        const int off = row * L::NP + i;
+#pragma unroll
+        for (int s2 = 0; s2 < 4; ++s2) {
+          if (s2 < cnt) {
+            const double* X = m.nodes_pad + (int64_t)ej[s2] * ES;
+            double dd = 0.0;
+#pragma unroll
+            for (int c = 0; c < D; ++c) {
+              const double tt = __dsub_rn(xj[s2][c], __ldg(X + c * L::CS + off));
+              dd = __fma_rn(tt, tt, dd);
+            }
+            if (dd < bst[s2]) {
+              bst[s2] = dd;
+              bi[s2] = t;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int s2 = 0; s2 < 4; ++s2) {
+          const double ob = __shfl_xor_sync(FPX_FULL, bst[s2], o);
+          const int oi = __shfl_xor_sync(FPX_FULL, bi[s2], o);
+          if (ob < bst[s2] || (ob == bst[s2] && oi < bi[s2])) {
+            bst[s2] = ob;
+            bi[s2] = oi;
+          }
+        }
+      }
+#pragma unroll
+      for (int s2 = 0; s2 < 4; ++s2) {
+        if (s2 < cnt && lane == js[s2]) {
+          const int b = bi[s2];
+          rc[0] = z[b % N];
+          rc[1] = DR > 1 ? z[(b / N) % N] : 0.0;
+          rc[2] = DR > 2 ? z[b / (N * N)] : 0.0;
+#pragma unroll
+          for (int a = 0; a < 3; ++a) rn[a] = rc[a];
+          first = true;
+          it = 0;
+          alpha = P.alpha0;
+          phase = 3;
+        }
+      }
+    }
+    if (!__any_sync(FPX_FULL, phase != 4)) break;
+    // (b) one map evaluation for every lane of the warp
+    const bool w2 = __any_sync(FPX_FULL, phase == 3 && on_boundary<DR>(rn));
+    ++nev;
+    nev2 += w2 ? 1 : 0;
+    nlev += phase == 3 ? 1 : 0;
+    const double* X = m.nodes_pad + (int64_t)(phase == 3 ? e : 0) * ES;
+    if (w2) eval_state<D, DR, N, true, 3>(X, z, scale, rn, xs, st, sb);
+    else eval_state<D, DR, N, false, 3>(X, z, scale, rn, xs, st, sb);
+    if (phase != 3) continue;
+    // (c) trust-region Newton update (newton_warp, D8)
+    bool done = false;
+    if (first) {
+      first = false;
+    } else {
+      const double decr = fcur - st.f;
+      if (decr >= P.accept * pred) {
+        if (decr >= P.keep * pred) alpha *= P.grow;
+#pragma unroll
+        for (int a = 0; a < DR; ++a) rc[a] = rn[a];
+      } else {
+        alpha *= P.shrink;
+        unstash_state(stash, st);
+        st.f = fcur;
+      }
+      if (smax < P.tol) done = true;
+      else if (it >= P.max_iters) done = true;
+    }
+    if (!done) {
+      fcur = st.f;
+      const bool go = propose_step<DR>(st, rc, it, alpha, rn, pred, smax);
+      ++it;
+      if (!go) done = true;
+      else stash_state(stash, st);
+    }
+    if (done) {
+      const double dd = sqrt(st.f);
+      s_newton += 1;
+      s_iters += it;
+      const double epsd = DR < D ? eps_d_of(m, e) : 0.0;
+      const int cd = classify<D, DR>(rc, dd, epsd);
+      // D6 merge into the point's record under its lock
+      while (atomicCAS(&lock[u], 0, 1) != 0) {
+      }
+      __threadfence();
+      const int bc = *(volatile int32_t*)&code[k], be = *(volatile int32_t*)&elem[k];
+      const double bd = *(volatile double*)&dist[k];
+      bool take;
+      if (cd == kInterior) take = bc != kInterior || e < be;
+      else take = bc != kInterior && (dd < bd || (dd == bd && e < be));
+      if (take) {
+        code[k] = cd;
+        elem[k] = e;
+        dist[k] = dd;
+#pragma unroll
+        for (int a = 0; a < DR; ++a) r[k * DR + a] = rc[a];
+      }
+      if (iters) iters[k] += it;
+      if (cd == kInterior) found[u] = 1;
+      __threadfence();
+      atomicExch(&lock[u], 0);
       phase = 0;
     }
   }
@@ -1583,37 +1976,24 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
       }
     }
     // ---- cooperative seeds (D7) of the lanes that just got a point
-    for (unsigned sd = __ballot_sync(FPX_FULL, phase == 1); sd; sd &= sd - 1) {
-      const int j = __ffs(sd) - 1;
-      double xj[3];
+    for (unsigned sd = __ballot_sync(FPX_FULL, phase == 1); sd;) {
+      unsigned js[4];
+      const double* sj[4];
+      double xj[4][3];
+      int cnt = 0;
 #pragma unroll
-      for (int c = 0; c < D; ++c) xj[c] = __shfl_sync(FPX_FULL, xs[c], j);
-      const double* sj = slots + __shfl_sync(FPX_FULL, myslot, j) * slot_stride;
-      double bestd = INFINITY;
-      int bi = 0x7fffffff;
-      for (int t = lane; t < K; t += FPX_WARP) {
-        const int row = t / N, i = t - row * N;
-        double dd = 0.0;
+      for (int s2 = 0; s2 < 4; ++s2) {
+        js[s2] = sd ? (unsigned)(__ffs(sd) - 1) : 0u;
+        if (sd) {
+          sd &= sd - 1;
+          cnt = s2 + 1;
+        }
+        sj[s2] = slots + __shfl_sync(FPX_FULL, myslot, js[s2]) * slot_stride;
 #pragma unroll
-        for (int c = 0; c < D; ++c) {
-          const double tt = __dsub_rn(xj[c], sj[c * L::CS + row * L::NP + i]);
-          dd = __fma_rn(tt, tt, dd);
-        }
-        if (dd < bestd) {
-          bestd = dd;
-          bi = t;
-        }
+        for (int c = 0; c < D; ++c) xj[s2][c] = __shfl_sync(FPX_FULL, xs[c], js[s2]);
       }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const double ob = __shfl_xor_sync(FPX_FULL, bestd, o);
-        const int oi = __shfl_xor_sync(FPX_FULL, bi, o);
-        if (ob < bestd || (ob == bestd && oi < bi)) {
-          bestd = ob;
-          bi = oi;
-        }
-      }
-      if (lane == j) {
+      const int bi = seed_batch<D, DR, N, true>(js, cnt, sj, xj, lane);
+      if (bi >= 0) {
         rc[0] = z[bi % N];
         rc[1] = DR > 1 ? z[(bi / N) % N] : 0.0;
         rc[2] = DR > 2 ? z[bi / (N * N)] : 0.0;
@@ -1882,29 +2262,55 @@ struct Pairs {
   }
 };
 
+#ifndef FPX_REST_G
+#define FPX_REST_G 4
+#endif
 template <int D, int DR, int N>
 struct Rest {
   using PL = PairLay<D, DR, N>;
-  // warps per block (16 points each) whose slots fit ~220 KB
-  static constexpr size_t WARP_BYTES = (size_t)16 * PL::SS * 8 + 16 * 8;
+  static constexpr int G = FPX_REST_G;  // lanes per point
+  // warps per block (32/G points each) whose slots fit ~220 KB
+  static constexpr size_t WARP_BYTES = (size_t)(FPX_WARP / G) * (PL::SS * 8 + 8);
   static constexpr int WPB0 = (int)((220 * 1024 - 256) / WARP_BYTES);
-  static constexpr int WPB = WPB0 > 4 ? 4 : (WPB0 < 1 ? 1 : WPB0);
+  static constexpr int WPB = WPB0 > 16 ? 16 : (WPB0 < 1 ? 1 : WPB0);
   static cudaError_t run(const fpx_mesh_t& m, const double* x, int64_t nun_cap,
                          const int64_t* nun_dev, const int32_t* upts, const int32_t* clist,
-                         const int32_t* cnum, int32_t* code, int32_t* elem, double* r,
+                         const int32_t* cnum, const int32_t* nps, const int32_t* perm,
+                         const int64_t* cum, const int32_t* maxnp, const int32_t* best,
+                         const int4* pairs, int32_t* found, int32_t* lock, int32_t* code,
+                         int32_t* elem, double* r,
                          double* dist, int32_t* iters, const double* field, int C,
                          double* values, int64_t* counter, int64_t* stats, cudaStream_t st) {
-    const int threads = WPB * FPX_WARP;
-    const size_t smem = (size_t)(2 * ((N + 1) & ~1)) * 8 + (size_t)WPB * WARP_BYTES;
-    if (smem > 227 * 1024) return cudaErrorInvalidValue;
-    auto fn = k_rest_pairs<D, DR, N, WPB>;
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    unsigned blocks = persistent_blocks((const void*)fn, threads, smem,
-                                        (nun_cap * 2 + FPX_WARP - 1) / FPX_WARP);
-    fn<<<blocks, threads, smem, st>>>(m, x, nun_dev, upts, clist, cnum, code, elem, r, dist, iters,
-                                      counter, stats);
-    cudaError_t err = cudaGetLastError();
+    static const bool l1 = [] {
+      const char* v = getenv("FPX_REST");
+      return !(v && v[0] == 's');
+    }();
+    cudaError_t err;
+    if (l1) {
+      const int threads = 128;
+      const size_t smem = (size_t)(2 * ((N + 1) & ~1) + 4 * Scratch<DR, N>::SLOTS * FPX_WARP) * 8;
+      auto fn = k_rest_l1<D, DR, N>;
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      unsigned blocks = persistent_blocks((const void*)fn, threads, smem,
+                                          (nun_cap + FPX_WARP - 1) / FPX_WARP);
+      fn<<<blocks, threads, smem, st>>>(m, x, nun_dev, upts, clist, cnum, nps, perm, cum, maxnp,
+                                        best, pairs, 2 * nun_cap + 1024, found, lock, code, elem,
+                                        r, dist, iters, counter, stats);
+      err = cudaGetLastError();
+    } else {
+      const int threads = WPB * FPX_WARP;
+      const size_t smem = (size_t)(2 * ((N + 1) & ~1)) * 8 + (size_t)WPB * WARP_BYTES;
+      if (smem > 227 * 1024) return cudaErrorInvalidValue;
+      auto fn = k_rest_pairs<D, DR, N, G, WPB>;
+      if (smem > 48 * 1024)
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      unsigned blocks = persistent_blocks((const void*)fn, threads, smem,
+                                          (nun_cap * G + FPX_WARP - 1) / FPX_WARP);
+      fn<<<blocks, threads, smem, st>>>(m, x, nun_dev, upts, clist, cnum, code, elem, r, dist,
+                                        iters, counter, stats);
+      err = cudaGetLastError();
+    }
     if (err != cudaSuccess || !field) return err;
     int64_t b = (nun_cap + 127) / 128;
     if (b > 148 * 8) b = 148 * 8;
@@ -1915,11 +2321,20 @@ struct Rest {
   }
   static cudaError_t lists(const fpx_mesh_t& m, const double* x, int64_t nun_cap,
                            const int64_t* nun_dev, const int32_t* upts, int32_t* clist,
-                           int32_t* cnum, cudaStream_t st) {
+                           int32_t* cnum, int32_t* nps, int32_t* hist, int32_t* bstart,
+                           int32_t* bcur, int32_t* perm, int64_t* cum, int32_t* maxnp,
+                           int4* pairs, cudaStream_t st) {
     int64_t b = (nun_cap + 3) / 4;
     if (b > 148 * 16) b = 148 * 16;
     if (b < 1) b = 1;
-    k_rest_lists<D><<<(unsigned)b, 128, 0, st>>>(m, x, nun_dev, upts, clist, cnum);
+    k_rest_lists<D><<<(unsigned)b, 128, 0, st>>>(m, x, nun_dev, upts, clist, cnum, nps, hist);
+    k_rest_order<<<1, 32, 0, st>>>(hist, bstart, cum, maxnp);
+    int64_t b2 = (nun_cap + 255) / 256;
+    if (b2 > 148 * 8) b2 = 148 * 8;
+    if (b2 < 1) b2 = 1;
+    k_rest_scatter<<<(unsigned)b2, 256, 0, st>>>(nun_dev, nps, bstart, bcur, perm);
+    k_rest_pairlist<<<(unsigned)b2, 256, 0, st>>>(nun_dev, upts, perm, nps, clist, cnum, cum, pairs,
+                                                  2 * nun_cap + 1024);
     return cudaGetLastError();
   }
 };

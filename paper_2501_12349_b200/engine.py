@@ -185,6 +185,12 @@ def setup(nodes, order: int | None = None, ref_dim: int | None = None, *,
         d, E, _C.ptr(S.aabb), _C.ptr(S.obb_c), _C.ptr(S.obb_inv), _C.ptr(S.obb_ok),
         _C.ptr(S.frame), _C.ptr(S.frec), _C.stream_handle()), "fpx_filter_records")
     m.frec = S.frec.data_ptr()
+    # rows padded to even length: 16-byte vector loads of the geometry
+    NP = N + (N % 2)
+    S.nodes_pad = torch.empty((E, d, (N ** ref_dim) // N, NP), dtype=torch.float64, device=dev)
+    _C.check(_C.lib().fpx_pad_nodes(d, ref_dim, N, E, _C.ptr(X), _C.ptr(S.nodes_pad),
+                                    _C.stream_handle()), "fpx_pad_nodes")
+    m.nodes_pad = S.nodes_pad.data_ptr()
     S.mesh_t = m
     # multi-rank: global map Psi_G over the union of all ranks' boxes
     S.group = group or transport.RankGroup()
