@@ -14,7 +14,7 @@ JSON line (rank 0): value = total points / max-over-ranks device step time
 (inputs resident in HBM; L2 flushed between timed steps); e2e = the same
 through the public API with host points copied in and values + records
 copied out inside the timed region; roofline of the dominant kernel
-(k_newton_round1, FP64-bound); cpu_baseline = the oracle port on the host
+(k_newton_stream, FP64-bound); cpu_baseline = the oracle port on the host
 cores over a bounded sample.
 --impl reference: the reference's CPU path (the C oracle port; the reference
 package itself has no find/eval code) on all host cores.
@@ -257,7 +257,7 @@ def run_ours(args):
     _C.check(L.fpx_probe_fp64(tf.ctypes.data, _C.stream_handle()), "fpx_probe_fp64")
     achieved = flops_r1 / (kern_ms * 1e-3) / 1e12
     traffic = None
-    tpath = os.path.join(ROOT, "profiles", "newton_round1_dram.json")
+    tpath = os.path.join(ROOT, "profiles", "newton_stream_dram.json")
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get("bytes_per_launch")
     flops_all = (st["newton"] * (f_seed(N) + f_iter(N)) + st["iters"] * f_iter(N)
@@ -276,7 +276,7 @@ def run_ours(args):
             "e2e": {"value": n * world / (e2e_max * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_max},
-            "roofline": {"bound": "fp64", "kernel": "k_newton_round1<3,3,5>",
+            "roofline": {"bound": "fp64", "kernel": "k_newton_stream<3,3,5,3> (round 1)",
                          "achieved": achieved, "peak": float(tf[0]), "unit": "TFLOP/s",
                          "frac": achieved / float(tf[0]), "traffic": traffic,
                          "peak_source": "fpx_probe_fp64 DFMA chains, measured in this run "

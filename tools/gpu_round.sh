@@ -12,7 +12,7 @@ for w in $WHAT; do
     ncu)
       timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
         --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 3 --cpu-sample 2000 > /dev/null 2>&1; echo "ncu-list rc=$?"
-      timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_newton_round1 -s 3 -c 1 \
-        -o gpurun_out/newton_$TAG -f python bench.py --steps 1 --warmup 3 --cpu-sample 2000 > gpurun_out/ncu_full_$TAG.log 2>&1; echo "ncu-full rc=$?" ;;
+      python tools/launches.py gpurun_out/launches_$TAG.csv > gpurun_out/launches_$TAG.txt
+      bash tools/ncu_kernels.sh $TAG k_newton_stream k_rest_l1 k_prefilter_points ;;
   esac
 done
