@@ -58,7 +58,8 @@ def workload_config(n_gpus):
             "mesh": f"kershaw{N_ELEM_AXIS}^3", "order": ORDER, "elements": N_ELEM_AXIS ** 3,
             "points_per_gpu": PTS_PER_GPU, "components": 1,
             "partition": "contiguous z-slabs" if n_gpus > 1 else "single",
-            "l2": "flushed (256 MiB write) between timed steps"}
+            "l2": "flushed (256 MiB write) between timed steps",
+            "slices": "one find per step (FPX_SPLIT=1)"}
 
 
 def build_inputs(rank=0):
@@ -213,16 +214,26 @@ def run_ours(args):
         barrier()
         for k in range(args.steps):
             flush.fill_(float(k))
-            L.fpx_profile_round1(kev[k][0].cuda_event, kev[k][1].cuda_event)
             ev[k][0].record(stream)
             vals, rec = engine.find_and_interpolate(S, F, x_dev)
             ev[k][1].record(stream)
             stats.append(rec.stats)
-        L.fpx_profile_round1(None, None)
         barrier()
     launches = L.fpx_launch_count() - launches0
     step_ms = float(np.mean([s.elapsed_time(e) for s, e in ev]))
+    # round-1 kernel alone (roofline): the same steps without the slice
+    # overlap, CUDA events around the launch on its stream
+    split = S.options.split
+    S.options.split = 1
+    for k in range(args.steps):
+        flush.fill_(float(k))
+        L.fpx_profile_round1(kev[k][0].cuda_event, kev[k][1].cuda_event)
+        vals, rec1 = engine.find_and_interpolate(S, F, x_dev)
+    L.fpx_profile_round1(None, None)
+    torch.cuda.synchronize()
+    S.options.split = split
     kern_ms = float(np.mean([s.elapsed_time(e) for s, e in kev]))
+    step1 = rec1.stats
     step_ms_max = max_over_ranks(step_ms)
     value = n * world / (step_ms_max * 1e-3)
     # --- end to end through the public API: host points in, records out
@@ -238,10 +249,7 @@ def run_ours(args):
         flush.fill_(float(k))
         s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s0.record(stream)
-        vals, rec = engine.find_and_interpolate(S, F, x_pin)
-        outs["values"].copy_(vals, non_blocking=True)
-        for key in ("code", "elem", "rank", "r", "dist"):
-            outs[key].copy_(getattr(rec, key), non_blocking=True)
+        engine.find_and_interpolate_host(S, F, x_pin, out=outs, chunks=E2E_CHUNKS, sync=False)
         s1.record(stream)
         s1.synchronize()
         e2e_ms.append(s0.elapsed_time(s1))
@@ -249,10 +257,10 @@ def run_ours(args):
     h2d = n * 3 * 8
     d2h = n * (8 + 4 + 4 + 4 + 24 + 8)
     # --- roofline of the dominant kernel (round-1 Newton, FP64-bound)
-    st = stats[-1]
+    st = dict(stats[-1])
     N = ORDER + 1
-    flops_r1 = (st["newton_r1"] * (f_seed(N) + f_iter(N)) + st["iters_r1"] * f_iter(N)
-                + st["evals_r1"] * f_eval(N))
+    flops_r1 = (step1["newton_r1"] * (f_seed(N) + f_iter(N)) + step1["iters_r1"] * f_iter(N)
+                + step1["evals_r1"] * f_eval(N))
     tf = np.zeros(1)
     _C.check(L.fpx_probe_fp64(tf.ctypes.data, _C.stream_handle()), "fpx_probe_fp64")
     achieved = flops_r1 / (kern_ms * 1e-3) / 1e12
@@ -275,13 +283,16 @@ def run_ours(args):
             "config": workload_config(world),
             "e2e": {"value": n * world / (e2e_max * 1e-3), "unit": UNIT,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                    "ms_per_step": e2e_max},
+                    "ms_per_step": e2e_max,
+                    "api": f"engine.find_and_interpolate_host, {E2E_CHUNKS} overlapped slices"},
             "roofline": {"bound": "fp64", "kernel": "k_newton_stream<3,3,5,3> (round 1)",
                          "achieved": achieved, "peak": float(tf[0]), "unit": "TFLOP/s",
                          "frac": achieved / float(tf[0]), "traffic": traffic,
                          "peak_source": "fpx_probe_fp64 DFMA chains, measured in this run "
                                         "(FP64 is not in MEASURED_PEAKS.json)",
                          "kernel_ms": kern_ms, "kernel_share": kern_ms / step_ms,
+                         "kernel_timing": "CUDA events around the round-1 launch, find run "
+                                          "unsplit (split=1) so the launch is not overlapped",
                          "flops_per_launch": flops_r1},
             "cpu_baseline": {"value": cpu_v, "unit": UNIT, "cores": cores, "kind": "port",
                              "sample": f"{args.cpu_sample} of the cfg-2 points, oracle C port "
@@ -293,6 +304,9 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+E2E_CHUNKS = int(os.environ.get("FPX_E2E_CHUNKS", "1"))
 
 
 def main():

@@ -1790,7 +1790,9 @@ __global__ void k_rest_values(const double* __restrict__ fbasis, int M,
 
 // ---------------------------------------------------------------- round 1, streamed
 // Element-major round 1 without fixed work items.  The points are sorted by
-// their best-first element; a warp consumes chunks of that stream through a
+// their best-first element; a warp consumes chunks (FPX_R1_CHUNK points,
+// default 64: small enough that the last chunks balance across warps) of
+// that stream through a
 // ring of S shared-memory element slots (geometry + field block, loaded
 // asynchronously ahead of use, completion on a per-slot mbarrier).  A lane
 // takes the next point as soon as its own solve finishes, so a warp never
@@ -1798,7 +1800,9 @@ __global__ void k_rest_values(const double* __restrict__ fbasis, int M,
 // small element; the lanes of one warp read at most S distinct slots per
 // load, whose bank offsets differ (slot stride = 16 mod 128 bytes), so the
 // loads stay single-wavefront broadcasts.  Seeds are warp-cooperative.
-#define FPX_CHUNK 256
+#ifndef FPX_CHUNK_DEFAULT
+#define FPX_CHUNK_DEFAULT 64
+#endif
 
 template <int S>
 struct StreamMeta {
@@ -1814,7 +1818,8 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
                     const int32_t* __restrict__ best, const int32_t* __restrict__ npass,
                     int32_t* code, int32_t* elem, double* r, double* dist, int32_t* iters,
                     const double* __restrict__ field, int C, double* values, int32_t* upts,
-                    int64_t* nun_dev, int64_t* chunk_ctr, int slot_stride, int64_t* stats) {
+                    int64_t* nun_dev, int64_t* chunk_ctr, int slot_stride, int chunk,
+                    int64_t* stats) {
   using L = Lay<D, DR, N>;
   constexpr int K = L::K;
   constexpr int SCR = Scratch<DR, N>::SLOTS;
@@ -1861,12 +1866,12 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
   // first chunk
   {
     int64_t c = 0;
-    if (lane == 0) c = (int64_t)atomicAdd((unsigned long long*)chunk_ctr, (unsigned long long)FPX_CHUNK);
+    if (lane == 0) c = (int64_t)atomicAdd((unsigned long long*)chunk_ctr, (unsigned long long)chunk);
     c = __shfl_sync(FPX_FULL, c, 0);
     if (c >= nu) exhausted = true;
     else {
       a0 = c;
-      alen = (int)(nu - c < FPX_CHUNK ? nu - c : FPX_CHUNK);
+      alen = (int)(nu - c < chunk ? nu - c : chunk);
       ++s_chunks;
     }
   }
@@ -1877,14 +1882,14 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
         if (bclaimed) break;
         int64_t c = 0;
         if (lane == 0)
-          c = (int64_t)atomicAdd((unsigned long long*)chunk_ctr, (unsigned long long)FPX_CHUNK);
+          c = (int64_t)atomicAdd((unsigned long long*)chunk_ctr, (unsigned long long)chunk);
         c = __shfl_sync(FPX_FULL, c, 0);
         if (c >= nu) {
           exhausted = true;
           break;
         }
         b0 = c;
-        blen = (int)(nu - c < FPX_CHUNK ? nu - c : FPX_CHUNK);
+        blen = (int)(nu - c < chunk ? nu - c : chunk);
         bclaimed = true;
         ++s_chunks;
       }
@@ -2010,7 +2015,10 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
       if (exhausted && q >= alen + blen) break;  // stream done, all lanes idle
       continue;                                   // waiting for a slot load
     }
-    // ---- one map evaluation for every lane of the warp
+    // ---- one map evaluation for every lane of the warp (second derivatives
+    // whenever any lane's trial point is on a face: deferring them to batched
+    // passes measured slower, the waiting lanes cost more passes than the
+    // batching saved)
     double* sX = slots + myslot * slot_stride;
     const bool w2 = __any_sync(FPX_FULL, phase == 2 && on_boundary<DR>(rn));
     ++nev;
@@ -2233,11 +2241,16 @@ struct Stream {
     auto fn = k_newton_stream<D, DR, N, S>;
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    static const int chunk = [] {
+      const char* v = getenv("FPX_R1_CHUNK");
+      const int c = v ? atoi(v) : FPX_CHUNK_DEFAULT;
+      return c < 8 ? 8 : c;
+    }();
     unsigned blocks = persistent_blocks((const void*)fn, threads, smem,
-                                        (n_cap + FPX_CHUNK - 1) / FPX_CHUNK);
+                                        (n_cap + chunk - 1) / chunk);
     fn<<<blocks, threads, smem, st>>>(m, x, sorted, packed_off, ecount, best, npass, code, elem, r,
                                       dist, iters, field, C, values, upts, nun_dev, chunk_ctr, ss,
-                                      stats);
+                                      chunk, stats);
     return cudaGetLastError();
   }
 };

@@ -44,6 +44,10 @@ class EngineOptions:
     newton: NewtonSettings = dfield(default_factory=NewtonSettings)
     eps_d: float | None = None        # absolute surface threshold; None -> relative
     eps_d_rel: float = 1e-10
+    # finds of >= split_min points run as `split` concurrent slices (perf only;
+    # FPX_SPLIT overrides)
+    split: int = dfield(default_factory=lambda: int(os.environ.get("FPX_SPLIT", "1")))
+    split_min: int = 1 << 18
     # local cells per axis = hash_refine * SPEC rule (perf only; FPX_HASH_REFINE overrides)
     hash_refine: int = dfield(default_factory=lambda: int(os.environ.get("FPX_HASH_REFINE", "2")))
 
@@ -207,11 +211,15 @@ def setup(nodes, order: int | None = None, ref_dim: int | None = None, *,
 
 
 # ---------------------------------------------------------------- find
-def _workspace(S: EngineSetup, n: int, pair_cap: int) -> torch.Tensor:
+def _workspace(S: EngineSetup, n: int, pair_cap: int, slot: int = 0) -> torch.Tensor:
+    """Find workspace `slot` (one per concurrently running find)."""
     need = _C.lib().fpx_find_workspace_bytes(S.mesh_t, n, pair_cap)
-    if S.workspace is None or S.workspace.numel() < need:
-        S.workspace = torch.empty(need, dtype=torch.uint8, device=S.device)
-    return S.workspace
+    if S.workspace is None:
+        S.workspace = {}
+    w = S.workspace.get(slot)
+    if w is None or w.numel() < need:
+        w = S.workspace[slot] = torch.empty(need, dtype=torch.uint8, device=S.device)
+    return w
 
 
 def _stats_dict(st: np.ndarray) -> dict:
@@ -261,16 +269,46 @@ def _find_local(S: EngineSetup, x: torch.Tensor, field: Field | None = None,
         blocks = field.blocks
         C = int(blocks.shape[1])
         out["values"] = torch.empty((n, C), dtype=torch.float64, device=dev)
-    stats = torch.zeros(_C.STATS_LEN, dtype=torch.int64, device=dev)
     if n == 0:
         return out, _stats_dict(np.zeros(_C.STATS_LEN, np.int64))
-    ws = _workspace(S, n, n)
+    x = x.contiguous()
+    k = S.options.split if n >= S.options.split_min else 1
+    if k <= 1:
+        return out, _find_into(S, x, out, field)
+    # k slices on k side streams: the slices' kernels overlap, so the tail
+    # of one slice's Newton kernels runs under the next slice's bulk work
+    comp = torch.cuda.current_stream(dev)
+    start = torch.cuda.Event()
+    start.record(comp)
+    bounds = [n * c // k for c in range(k + 1)]
+    parts = []
+    for c, sc in enumerate(_streams(S, k)):
+        a_, b_ = bounds[c], bounds[c + 1]
+        sc.wait_event(start)
+        with torch.cuda.stream(sc):
+            sl = {key: (v[a_:b_] if v is not None else None) for key, v in out.items()}
+            parts.append(_find_into(S, x[a_:b_], sl, field, slot=c))
+    for sc in _streams(S, k):
+        comp.wait_stream(sc)
+    return out, _SummedStats(parts)
+
+
+def _find_into(S: EngineSetup, x: torch.Tensor, out: dict, field: Field | None,
+               slot: int = 0) -> DeviceStats:
+    """fpx_find on the current stream writing into caller-provided device
+    slices (x contiguous); `slot` selects the workspace."""
+    n = int(x.shape[0])
+    stats = torch.zeros(_C.STATS_LEN, dtype=torch.int64, device=S.device)
+    if n == 0:
+        return DeviceStats(stats)
+    blocks, C = (field.blocks, int(field.blocks.shape[1])) if field is not None else (None, 0)
+    ws = _workspace(S, n, n, slot)
     _C.check(_C.lib().fpx_find(
         S.mesh_t, n, _C.ptr(x), _C.ptr(out["code"]), _C.ptr(out["elem"]), _C.ptr(out["r"]),
-        _C.ptr(out["dist"]), _C.ptr(out["iters"]), _C.ptr(blocks), C,
+        _C.ptr(out["dist"]), _C.ptr(out.get("iters")), _C.ptr(blocks), C,
         _C.ptr(out.get("values")), _C.ptr(stats), n, _C.ptr(ws), ws.numel(),
         _C.stream_handle()), "fpx_find")
-    return out, DeviceStats(stats)
+    return DeviceStats(stats)
 
 
 def _prep_points(S: EngineSetup, x) -> torch.Tensor:
@@ -340,6 +378,114 @@ def _eval_local(S: EngineSetup, f: Field, code, elem, r) -> torch.Tensor:
     _C.check(L.fpx_findpts_eval(S.ref_dim, Nf, _C.ptr(fb), C, S.E, _C.ptr(f.blocks), n,
                                 _C.ptr(code), _C.ptr(elem), _C.ptr(r), _C.ptr(out), _C.ptr(ws),
                                 wsb, _C.stream_handle()), "fpx_findpts_eval")
+    return out
+
+
+class _SummedStats(Mapping):
+    """Kernel counters of a chunked find: the chunks' counters summed on
+    first access."""
+
+    def __init__(self, parts):
+        self._parts, self._d = parts, None
+
+    def _load(self) -> dict:
+        if self._d is None:
+            tot = np.zeros(_C.STATS_LEN, np.int64)
+            for p in self._parts:
+                tot += np.array([p[k] for k in _C.STAT_NAMES], np.int64)
+            self._d = _stats_dict(tot)
+        return self._d
+
+    def __getitem__(self, k):
+        return self._load()[k]
+
+    def __iter__(self):
+        return iter(self._load())
+
+    def __len__(self) -> int:
+        return _C.STATS_LEN
+
+
+def _streams(S: EngineSetup, k: int) -> list:
+    """k side streams of this setup (created once)."""
+    st = S.__dict__.setdefault("_side_streams", [])
+    while len(st) < k:
+        st.append(torch.cuda.Stream(device=S.device))
+    return st[:k]
+
+
+def find_and_interpolate_host(S: EngineSetup, field, x: torch.Tensor, *, chunks: int = 4,
+                              out: dict | None = None, sync: bool = True):
+    """find_and_interpolate for points in (pinned) host memory, with the
+    records and values returned to host memory.  The points are split into
+    `chunks` slices; slice c is uploaded, found and downloaded on side stream
+    c, so copies overlap kernels and one slice's kernel tails run under the
+    next slice's bulk work.  Returns a dict of host tensors values [n, C],
+    code, rank, elem, r [n, dr], dist, and `stats` (complete on return when
+    `sync`; else once the current stream reaches this point)."""
+    if not S.group.single:  # routed multi-rank find: no overlap
+        vals, rec = find_and_interpolate(S, field, x)
+        res = dict(values=vals.cpu(), code=rec.code.cpu(), rank=rec.rank.cpu(),
+                   elem=rec.elem.cpu(), r=rec.r.cpu(), dist=rec.dist.cpu(), stats=rec.stats)
+        return res
+    f = _field_of(S, field)
+    fused = f.order == S.order
+    x = torch.as_tensor(x, dtype=torch.float64)
+    if x.ndim != 2 or x.shape[1] != S.phys_dim:
+        raise ValueError(f"points must be [n, {S.phys_dim}], got {tuple(x.shape)}")
+    if x.is_cuda:
+        raise ValueError("find_and_interpolate_host takes host points")
+    if not x.is_pinned():
+        x = x.pin_memory()
+    n, dr, dev, C = int(x.shape[0]), S.ref_dim, S.device, f.components
+    pin = dict(pin_memory=True)
+    if out is None:
+        out = dict(values=torch.empty((n, C), dtype=torch.float64, **pin),
+                   code=torch.empty(n, dtype=torch.int32, **pin),
+                   rank=torch.empty(n, dtype=torch.int32, **pin),
+                   elem=torch.empty(n, dtype=torch.int32, **pin),
+                   r=torch.empty((n, dr), dtype=torch.float64, **pin),
+                   dist=torch.empty(n, dtype=torch.float64, **pin))
+    ws = S.__dict__.setdefault("_host_pipe", {})
+    if ws.get("n") != n or ws.get("C") != C:
+        ws.clear()
+        ws.update(n=n, C=C, x=torch.empty((n, S.phys_dim), dtype=torch.float64, device=dev),
+                  values=torch.empty((n, C), dtype=torch.float64, device=dev),
+                  code=torch.empty(n, dtype=torch.int32, device=dev),
+                  rank=torch.empty(n, dtype=torch.int32, device=dev),
+                  elem=torch.empty(n, dtype=torch.int32, device=dev),
+                  r=torch.empty((n, dr), dtype=torch.float64, device=dev),
+                  dist=torch.empty(n, dtype=torch.float64, device=dev))
+    comp = torch.cuda.current_stream(dev)
+    chunks = max(1, min(chunks, n))
+    bounds = [n * c // chunks for c in range(chunks + 1)]
+    keys = ("values", "code", "rank", "elem", "r", "dist")
+    streams = _streams(S, chunks)
+    parts = []
+    start = torch.cuda.Event()
+    start.record(comp)
+    for c in range(chunks):
+        a, b = bounds[c], bounds[c + 1]
+        sc = streams[c]
+        sc.wait_event(start)
+        with torch.cuda.stream(sc):
+            ws["x"][a:b].copy_(x[a:b], non_blocking=True)
+            loc = dict(code=ws["code"][a:b], elem=ws["elem"][a:b], r=ws["r"][a:b],
+                       dist=ws["dist"][a:b], iters=None)
+            if fused:
+                loc["values"] = ws["values"][a:b]
+            parts.append(_find_into(S, ws["x"][a:b], loc, f if fused else None, slot=c))
+            if not fused:
+                ws["values"][a:b] = _eval_local(S, f, loc["code"], loc["elem"], loc["r"])
+            torch.where(loc["code"] != NOT_FOUND, torch.zeros_like(loc["elem"]),
+                        torch.full_like(loc["elem"], -1), out=ws["rank"][a:b])
+            for k in keys:
+                out[k][a:b].copy_(ws[k][a:b], non_blocking=True)
+    for c in range(chunks):
+        comp.wait_stream(streams[c])
+    if sync:
+        comp.synchronize()
+    out["stats"] = _SummedStats(parts)
     return out
 
 

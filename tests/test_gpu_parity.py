@@ -240,3 +240,24 @@ def test_surface_mesh_find_eval(kind):
     code = rec.code.cpu().numpy()
     assert np.mean(code[off == 0] == 0) > 0.99
     assert np.all(code[np.abs(off) > 1e-8] == 1)
+
+
+@pytest.mark.parametrize("chunks", [1, 3])
+def test_host_pipeline_matches_device(chunks):
+    # find_and_interpolate_host (chunked, overlapped copies) == the device API
+    mesh = toolkit.kershaw_mesh(8, 4)
+    S = engine.setup(mesh)
+    field = toolkit.analytic_field("smooth", mesh)
+    x = toolkit.uniform_points(20000, 3, seed=5, lo=-0.05, hi=1.05)
+    vals, rec = engine.find_and_interpolate(S, field, torch.from_numpy(x).cuda())
+    out = engine.find_and_interpolate_host(S, field, torch.from_numpy(x), chunks=chunks)
+    code = rec.code.cpu()
+    assert torch.equal(out["code"], code)
+    assert torch.equal(out["rank"], rec.rank.cpu())
+    inter = code == 0
+    assert torch.equal(out["elem"][inter], rec.elem.cpu()[inter])
+    assert torch.allclose(out["r"][inter], rec.r.cpu()[inter], rtol=0, atol=1e-12)
+    v, vd = out["values"], vals.cpu()
+    assert torch.allclose(v[inter], vd[inter], rtol=1e-10, atol=1e-12)
+    assert torch.isnan(v[code == 2]).all()
+    assert out["stats"]["points"] == x.shape[0]
