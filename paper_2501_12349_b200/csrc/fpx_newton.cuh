@@ -20,11 +20,17 @@
 #include "fpx_kernels.cuh"
 #include "fpx_boxes.cuh"
 
+#ifndef FPX_KUNROLL
+#define FPX_KUNROLL 1  // k-planes of the contraction per loop trip (ILP vs registers)
+#endif
+
 #ifndef FPX_NEWTON_MINB
 #define FPX_NEWTON_MINB 2  // CTAs of 128 threads per SM the Newton kernels are built for
 #endif
 
 namespace fpx {
+
+constexpr int kUnrollK = FPX_KUNROLL;
 
 template <int D, int DR, int N>
 struct Lay {
@@ -120,7 +126,7 @@ __device__ __forceinline__ void eval_state(const double* __restrict__ sX,
     const double* Xc = sX + c * GCS;
     double xv = 0.0, G[3] = {0.0, 0.0, 0.0}, H2[6] = {0, 0, 0, 0, 0, 0};
     if constexpr (DR == 3) {
-#pragma unroll 1
+#pragma unroll kUnrollK
       for (int k = 0; k < N; ++k) {
         double t00 = 0.0, t10 = 0.0, t01 = 0.0, t20 = 0.0, t11 = 0.0, t02 = 0.0;
 #pragma unroll

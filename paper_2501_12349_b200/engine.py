@@ -460,6 +460,22 @@ def find_and_interpolate_host(S: EngineSetup, field, x: torch.Tensor, *, chunks:
     chunks = max(1, min(chunks, n))
     bounds = [n * c // chunks for c in range(chunks + 1)]
     keys = ("values", "code", "rank", "elem", "r", "dist")
+    if chunks == 1:  # upload, find, download in order on the caller's stream
+        ws["x"].copy_(x, non_blocking=True)
+        loc = dict(code=ws["code"], elem=ws["elem"], r=ws["r"], dist=ws["dist"], iters=None)
+        if fused:
+            loc["values"] = ws["values"]
+        st = _find_into(S, ws["x"], loc, f if fused else None)
+        if not fused:
+            ws["values"].copy_(_eval_local(S, f, loc["code"], loc["elem"], loc["r"]))
+        torch.where(loc["code"] != NOT_FOUND, torch.zeros_like(loc["elem"]),
+                    torch.full_like(loc["elem"], -1), out=ws["rank"])
+        for k in keys:
+            out[k].copy_(ws[k], non_blocking=True)
+        if sync:
+            comp.synchronize()
+        out["stats"] = st
+        return out
     streams = _streams(S, chunks)
     parts = []
     start = torch.cuda.Event()
