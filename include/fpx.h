@@ -210,6 +210,15 @@ int fpx_forward_map(const fpx_mesh_t* m, int64_t n, const int32_t* elem, const d
 /* Multi-rank routing helpers (engine Phase B):
  * global-grid cell owner of each point and the destination counts for an
  * all-to-allv: dest[n] in [-1, nranks), counts [nranks] (device int64). */
+/* Lagrangian particle step (Algorithm 1, ParticleRHS + Integrate +
+ * ParticleBC): a = (u - v)/tau, AB2 update of x and v (forward Euler when
+ * `first`), periodic wrap of axis c of the box (lo[d], hi[d] in host memory)
+ * when bit c of `periodic` is set.  x, v, u, v_prev, a_prev: device [n][d];
+ * v_prev / a_prev receive this step's v and a for the next AB2 step. */
+int fpx_particles_advance(int d, int64_t n, double* x, double* v, const double* u,
+                          double* v_prev, double* a_prev, double tau, double dt, int first,
+                          const double* box, int periodic, void* stream);
+
 int fpx_route_count(int64_t n, const int32_t* dest, int nranks, int64_t* counts, void* stream);
 /* Stable pack by destination: perm[n] = position of point i in the send buffer
  * (-1 for dest < 0); offsets [nranks] = exclusive scan of counts. */

@@ -72,6 +72,7 @@ def lib():
         "fpx_setup_bounds": ([i32, i32, i32, i32, i64, P, P, f64, P, P, P, P, P, P, P, P], i32),
         "fpx_filter_records": ([i32, i64, P, P, P, P, P, P, P], i32),
         "fpx_pad_nodes": ([i32, i32, i32, i64, P, P, P], i32),
+        "fpx_particles_advance": ([i32, i64, P, P, P, P, P, f64, f64, i32, P, i32, P], i32),
         "fpx_bound_function": ([i32, i32, i32, i64, P, P, P, P, P], i32),
         "fpx_hash_workspace_bytes": ([i32, i64, i32], sz),
         "fpx_hash_build": ([i32, i64, P, P, P, P, i32, P, P, P, i64, P, P, P, sz, P], i32),
@@ -99,6 +100,7 @@ def exported_symbols():
     """Names declared in include/fpx.h (checked by the CPU test suite)."""
     return ["fpx_abi_version", "fpx_last_error", "fpx_launch_count", "fpx_profile_round1",
             "fpx_probe_fp64", "fpx_supported", "fpx_setup_bounds", "fpx_filter_records", "fpx_pad_nodes",
+            "fpx_particles_advance",
             "fpx_bound_function", "fpx_hash_workspace_bytes", "fpx_hash_build", "fpx_cell_of",
             "fpx_find_workspace_bytes", "fpx_find", "fpx_eval_workspace_bytes",
             "fpx_findpts_eval", "fpx_invert_pairs", "fpx_forward_map", "fpx_route_count",

@@ -569,6 +569,19 @@ int fpx_forward_map(const fpx_mesh_t* m, int64_t n, const int32_t* elem, const d
   return FPX_OK;
 }
 
+int fpx_particles_advance(int d, int64_t n, double* x, double* v, const double* u,
+                          double* v_prev, double* a_prev, double tau, double dt, int first,
+                          const double* box, int periodic, void* stream) {
+  if (d < 1 || d > 3) return fail(FPX_EINVAL, "particles: bad d=%d", d);
+  if (!(tau > 0.0) || !(dt > 0.0)) return fail(FPX_EINVAL, "particles: need tau > 0, dt > 0");
+  if (periodic && !box) return fail(FPX_EINVAL, "particles: periodic axes need a box");
+  if (n <= 0) return FPX_OK;
+  const double unit[6] = {0, 0, 0, 1, 1, 1};
+  FPX_LAUNCH(fpx::launch_particles_advance(d, n, x, v, u, v_prev, a_prev, tau, dt, first,
+                                           box ? box : unit, periodic, S(stream)));
+  return FPX_OK;
+}
+
 int fpx_route_count(int64_t n, const int32_t* dest, int nranks, int64_t* counts, void* stream) {
   if (nranks < 1) return fail(FPX_EINVAL, "route: nranks < 1");
   cudaStream_t st = S(stream);

@@ -118,4 +118,10 @@ cudaError_t launch_forward_map(const fpx_mesh_t& m, int64_t n, const int32_t* el
                                const double* r, double* x, double* G, double* H2,
                                cudaStream_t st);
 
+// Particle update (fpx_particles.cu): Stokes RHS + AB2 + periodic wrap.
+cudaError_t launch_particles_advance(int d, int64_t n, double* x, double* v, const double* u,
+                                     double* v_prev, double* a_prev, double tau, double dt,
+                                     int first, const double* box, int periodic,
+                                     cudaStream_t st);
+
 }  // namespace fpx

@@ -208,6 +208,15 @@ def analytic_field(name: str, mesh: MeshData, order: int | None = None, **kw) ->
         xc, yc, r = kw.get("xc", -0.05), kw.get("yc", -0.05), kw.get("r", 0.7)
         rr = np.sqrt((X[:, 0] - xc) ** 2 + (X[:, 1] - yc) ** 2)
         return np.arctan(a * (rr - r))[:, None, :]
+    if name == "uniform_velocity":  # constant vector field (particle demo)
+        val = np.asarray(kw.get("value", (1.0,) + (0.0,) * (d - 1)), dtype=float)
+        return np.broadcast_to(val[None, :, None], (X.shape[0], d, X.shape[2])).copy()
+    if name == "taylor_green":  # periodic, divergence-free in the x-y plane
+        x, y = 2 * np.pi * X[:, 0], 2 * np.pi * X[:, 1]
+        u = np.zeros((X.shape[0], d, X.shape[2]))
+        u[:, 0] = np.sin(x) * np.cos(y)
+        u[:, 1] = -np.cos(x) * np.sin(y)
+        return u
     raise ValueError(f"unknown field {name!r}")
 
 

@@ -56,3 +56,27 @@ def test_two_rank_engine_matches_single_rank(tmp_path):
         np.testing.assert_allclose(got["values"][same], v[same], rtol=1e-10, atol=1e-12)
         np.testing.assert_allclose(got["ivalues"][same], v[same], rtol=1e-10, atol=1e-12)
         assert np.all(np.isnan(got["values"][~f]))
+
+
+def test_two_rank_particle_migration():
+    # Algorithm 1: all particles start on rank 0 of a 2-slab partition; half
+    # are owned by rank 1 (non-local fraction 0.5 > 0.1) and migrate; the
+    # total is conserved and nothing is non-local afterwards
+    import json
+    worker = os.path.join(os.path.dirname(__file__), "mp", "particles_rank_worker.py")
+    size, port = 2, _port()
+    procs = []
+    for rk in range(size):
+        env = dict(os.environ, RANK=str(rk), WORLD_SIZE=str(size), MASTER_ADDR="127.0.0.1",
+                   MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, worker], env=env,
+                                      stdout=subprocess.PIPE, stderr=subprocess.STDOUT))
+    res = []
+    for p in procs:
+        o, _ = p.communicate(timeout=600)
+        assert p.returncode == 0, o.decode()[-3000:]
+        res.append(json.loads(o.decode().strip().splitlines()[-1]))
+    for r in res:
+        assert r["total"] == 400
+        assert r["frac0"] > 0.1 and r["frac1"] == 0.0 and r["migrations"] == 1
+    assert all(r["n"] > 0 for r in res)
