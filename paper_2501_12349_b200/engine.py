@@ -124,6 +124,94 @@ def _as_device_nodes(nodes, dev) -> torch.Tensor:
     return t.to(dev).contiguous()
 
 
+def _assemble(S: EngineSetup) -> None:
+    """The device mesh struct and its derived arrays (filter records, padded
+    nodes) from the setup arrays (shared by setup and load_setup)."""
+    opt, d, dr, N, E, dev = S.options, S.phys_dim, S.ref_dim, S.order + 1, S.E, S.device
+    m = _C.MeshT()
+    m.d, m.dr, m.N, m.M, m.E = d, dr, N, S.envelope.interval_points.size, E
+    m.basis, m.nodes = S.basis_dev.data_ptr(), S.nodes.data_ptr()
+    m.aabb, m.obb_c, m.obb_inv = S.aabb.data_ptr(), S.obb_c.data_ptr(), S.obb_inv.data_ptr()
+    m.obb_ok, m.frame, m.grid = S.obb_ok.data_ptr(), S.frame.data_ptr(), S.grid_dev.data_ptr()
+    m.ncell, m.max_list = S.ncell, S.max_list
+    m.offsets, m.elems = S.offsets.data_ptr(), S.elems.data_ptr()
+    opt.newton.apply(m)
+    m.eps_d_abs = -1.0 if opt.eps_d is None else float(opt.eps_d)
+    m.eps_d_rel = float(opt.eps_d_rel)
+    # packed candidate-filter records (one 256-byte row per element)
+    S.frec = torch.empty((E, _C.FREC), dtype=torch.float64, device=dev)
+    _C.check(_C.lib().fpx_filter_records(
+        d, E, _C.ptr(S.aabb), _C.ptr(S.obb_c), _C.ptr(S.obb_inv), _C.ptr(S.obb_ok),
+        _C.ptr(S.frame), _C.ptr(S.frec), _C.stream_handle()), "fpx_filter_records")
+    m.frec = S.frec.data_ptr()
+    # rows padded to even length: 16-byte vector loads of the geometry
+    NP = N + (N % 2)
+    S.nodes_pad = torch.empty((E, d, (N ** dr) // N, NP), dtype=torch.float64, device=dev)
+    _C.check(_C.lib().fpx_pad_nodes(d, dr, N, E, _C.ptr(S.nodes), _C.ptr(S.nodes_pad),
+                                    _C.stream_handle()), "fpx_pad_nodes")
+    m.nodes_pad = S.nodes_pad.data_ptr()
+    S.mesh_t = m
+
+
+SETUP_CACHE_VERSION = 1
+_CACHE_ARRAYS = ("nodes", "aabb", "obb_c", "obb_inv", "obb_ok", "frame", "hbox", "grid_dev",
+                 "offsets", "elems")
+
+
+def save_setup(S: EngineSetup, path: str) -> None:
+    """Serialised setup: a versioned header and the
+    device arrays of this rank's setup, little-endian, in one .npz file.
+    The global map of a multi-rank setup is rebuilt on load (collective)."""
+    opt = S.options
+    hdr = dict(version=SETUP_CACHE_VERSION, d=S.phys_dim, dr=S.ref_dim, order=S.order, E=S.E,
+               ncell=S.ncell, max_list=S.max_list, elem_offset=S.elem_offset,
+               expansion=opt.expansion, interval_count=opt.interval_count,
+               cells_global=opt.cells_global, hash_refine=opt.hash_refine,
+               eps_d=opt.eps_d, eps_d_rel=opt.eps_d_rel, newton=vars(opt.newton))
+    import json
+    arrs = {k: getattr(S, k).cpu().numpy() for k in _CACHE_ARRAYS}
+    np.savez(path, header=np.frombuffer(json.dumps(hdr).encode(), dtype=np.uint8), **arrs)
+
+
+def load_setup(path: str, *, group: transport.RankGroup | None = None) -> EngineSetup:
+    """Inverse of save_setup: uploads the arrays and reassembles the device
+    mesh without recomputing bounds or the local map."""
+    import json
+    from .invmap import NewtonSettings
+    from .spatial_hash import CartesianGrid, LocalMap
+    z = np.load(path if path.endswith(".npz") else path + ".npz")
+    hdr = json.loads(bytes(z["header"]).decode())
+    if hdr.get("version") != SETUP_CACHE_VERSION:
+        raise ValueError(f"setup cache version {hdr.get('version')} != {SETUP_CACHE_VERSION}")
+    dev = _C.require_cuda()
+    opt = EngineOptions(expansion=hdr["expansion"], interval_count=hdr["interval_count"],
+                        cells_global=hdr["cells_global"], hash_refine=hdr["hash_refine"],
+                        eps_d=hdr["eps_d"], eps_d_rel=hdr["eps_d_rel"],
+                        newton=NewtonSettings(**hdr["newton"]))
+    S = EngineSetup()
+    S.device, S.phys_dim, S.ref_dim, S.order, S.E = dev, hdr["d"], hdr["dr"], hdr["order"], hdr["E"]
+    S.basis = ReferenceBasis(S.order, opt.interval_count)
+    S.envelope = build_basis_envelope(S.basis)
+    S.basis_dev, S.options = device_basis(S.envelope, dev), opt
+    for k in _CACHE_ARRAYS:
+        setattr(S, k, torch.from_numpy(z[k]).to(dev).contiguous())
+    S.ncell, S.max_list = hdr["ncell"], hdr["max_list"]
+    g = CartesianGrid.from_packed(z["grid_dev"], S.phys_dim, S.ncell)
+    S.local_map = LocalMap(g, S.offsets, S.elems, S.max_list, S.grid_dev)
+    _assemble(S)
+    S.group = group or transport.RankGroup()
+    S.elem_offset = hdr["elem_offset"]
+    S.global_map = None
+    if not S.group.single:
+        lo = S.hbox[:, 0].amin(0).cpu()
+        hi = S.hbox[:, 1].amax(0).cpu()
+        glo, ghi = transport.reduce_domain_bbox(S.group, lo, hi)
+        etot = sum(transport.allgather_counts(S.group, S.E))
+        ng = opt.cells_global or n_cells(etot, S.phys_dim)
+        S.global_map = build_global_map(S.group, S.hbox, glo.numpy(), ghi.numpy(), ng)
+    return S
+
+
 def setup(nodes, order: int | None = None, ref_dim: int | None = None, *,
           options: EngineOptions | None = None, group: transport.RankGroup | None = None,
           elem_offset: int = 0) -> EngineSetup:
@@ -173,29 +261,7 @@ def setup(nodes, order: int | None = None, ref_dim: int | None = None, *,
     S.grid_dev, S.offsets, S.elems, S.ncell, S.max_list = \
         lmap.grid_dev, lmap.offsets, lmap.elems if lmap.entries else \
         torch.zeros(1, dtype=torch.int32, device=dev), lmap.grid.cells, lmap.max_list
-    m = _C.MeshT()
-    m.d, m.dr, m.N, m.M, m.E = d, ref_dim, N, env.interval_points.size, E
-    m.basis, m.nodes = bdev.data_ptr(), X.data_ptr()
-    m.aabb, m.obb_c, m.obb_inv = S.aabb.data_ptr(), S.obb_c.data_ptr(), S.obb_inv.data_ptr()
-    m.obb_ok, m.frame, m.grid = S.obb_ok.data_ptr(), S.frame.data_ptr(), S.grid_dev.data_ptr()
-    m.ncell, m.max_list = S.ncell, S.max_list
-    m.offsets, m.elems = S.offsets.data_ptr(), S.elems.data_ptr()
-    opt.newton.apply(m)
-    m.eps_d_abs = -1.0 if opt.eps_d is None else float(opt.eps_d)
-    m.eps_d_rel = float(opt.eps_d_rel)
-    # packed candidate-filter records (one 256-byte row per element)
-    S.frec = torch.empty((E, _C.FREC), dtype=torch.float64, device=dev)
-    _C.check(_C.lib().fpx_filter_records(
-        d, E, _C.ptr(S.aabb), _C.ptr(S.obb_c), _C.ptr(S.obb_inv), _C.ptr(S.obb_ok),
-        _C.ptr(S.frame), _C.ptr(S.frec), _C.stream_handle()), "fpx_filter_records")
-    m.frec = S.frec.data_ptr()
-    # rows padded to even length: 16-byte vector loads of the geometry
-    NP = N + (N % 2)
-    S.nodes_pad = torch.empty((E, d, (N ** ref_dim) // N, NP), dtype=torch.float64, device=dev)
-    _C.check(_C.lib().fpx_pad_nodes(d, ref_dim, N, E, _C.ptr(X), _C.ptr(S.nodes_pad),
-                                    _C.stream_handle()), "fpx_pad_nodes")
-    m.nodes_pad = S.nodes_pad.data_ptr()
-    S.mesh_t = m
+    _assemble(S)
     # multi-rank: global map Psi_G over the union of all ranks' boxes
     S.group = group or transport.RankGroup()
     S.elem_offset = elem_offset

@@ -260,3 +260,86 @@ def partition_blocks(E: int, nranks: int) -> list[tuple[int, int]]:
         out.append((start, start + cnt))
         start += cnt
     return out
+
+
+# ---------------------------------------------------------------- file formats
+# SPEC.md "DESIGN DECISIONS": mesh text / binary files, points and records CSV.
+MESH_MAGIC = b"FPXMESH1"
+
+
+def write_mesh(path: str, mesh: MeshData, binary: bool = False) -> None:
+    """Text: header `fpx-mesh v1; d; d_r; p; N_E`, then per element N^dr
+    lines of d floats (repr precision), lexicographic node order.  Binary:
+    magic, int32 d, d_r, p, int64 N_E, then the nodes as little-endian f64
+    [E][N^dr][d]."""
+    X = np.ascontiguousarray(mesh.nodes)            # [E, d, K]
+    E, d, K = X.shape
+    rows = np.transpose(X, (0, 2, 1))               # [E, K, d]
+    if binary:
+        with open(path, "wb") as f:
+            f.write(MESH_MAGIC)
+            f.write(np.array([d, mesh.ref_dim, mesh.order], "<i4").tobytes())
+            f.write(np.array([E], "<i8").tobytes())
+            f.write(np.ascontiguousarray(rows, dtype="<f8").tobytes())
+        return
+    with open(path, "w") as f:
+        f.write(f"fpx-mesh v1; {d}; {mesh.ref_dim}; {mesh.order}; {E}\n")
+        for e in range(E):
+            for k in range(K):
+                f.write(" ".join(repr(float(v)) for v in rows[e, k]) + "\n")
+
+
+def read_mesh(path: str) -> MeshData:
+    with open(path, "rb") as f:
+        head = f.read(len(MESH_MAGIC))
+        if head == MESH_MAGIC:
+            d, dr, p = (int(v) for v in np.frombuffer(f.read(12), "<i4"))
+            E = int(np.frombuffer(f.read(8), "<i8")[0])
+            K = (p + 1) ** dr
+            rows = np.frombuffer(f.read(E * K * d * 8), "<f8").reshape(E, K, d)
+            return MeshData(np.ascontiguousarray(np.transpose(rows, (0, 2, 1))), d, dr, p)
+    with open(path) as f:
+        hdr = [t.strip() for t in f.readline().split(";")]
+        if hdr[0] != "fpx-mesh v1" or len(hdr) != 5:
+            raise ValueError(f"{path}: not an fpx-mesh v1 file")
+        d, dr, p, E = (int(t) for t in hdr[1:])
+        K = (p + 1) ** dr
+        rows = np.loadtxt(f, dtype=float, ndmin=2)
+    if rows.shape != (E * K, d):
+        raise ValueError(f"{path}: expected {E * K} rows of {d} values, got {rows.shape}")
+    X = np.transpose(rows.reshape(E, K, d), (0, 2, 1))
+    return MeshData(np.ascontiguousarray(X), d, dr, p)
+
+
+def write_points(path: str, x) -> None:
+    """Points CSV: one point per line, d columns."""
+    np.savetxt(path, np.asarray(x, dtype=float), delimiter=",", fmt="%.17g")
+
+
+def read_points(path: str) -> np.ndarray:
+    return np.loadtxt(path, delimiter=",", dtype=float, ndmin=2)
+
+
+def write_records(path: str, records) -> None:
+    """Records CSV: `idx, code, rank, elem, r0..r{dr-1}, dist`."""
+    code = np.asarray(records.code.cpu() if hasattr(records.code, "cpu") else records.code)
+    rank = np.asarray(records.rank.cpu() if hasattr(records.rank, "cpu") else records.rank)
+    elem = np.asarray(records.elem.cpu() if hasattr(records.elem, "cpu") else records.elem)
+    r = np.asarray(records.r.cpu() if hasattr(records.r, "cpu") else records.r)
+    dist = np.asarray(records.dist.cpu() if hasattr(records.dist, "cpu") else records.dist)
+    dr = r.shape[1]
+    with open(path, "w") as f:
+        f.write("idx,code,rank,elem," + ",".join(f"r{a}" for a in range(dr)) + ",dist\n")
+        for i in range(code.shape[0]):
+            f.write(f"{i},{int(code[i])},{int(rank[i])},{int(elem[i])},"
+                    + ",".join(repr(float(v)) for v in r[i]) + f",{float(dist[i])!r}\n")
+
+
+def read_records(path: str) -> dict:
+    """Inverse of write_records: dict of numpy arrays code, rank, elem, r, dist."""
+    with open(path) as f:
+        cols = f.readline().strip().split(",")
+    a = np.loadtxt(path, delimiter=",", skiprows=1, ndmin=2)
+    dr = sum(1 for c in cols if c.startswith("r") and c[1:].isdigit())
+    return {"code": a[:, 1].astype(np.int32), "rank": a[:, 2].astype(np.int32),
+            "elem": a[:, 3].astype(np.int32), "r": a[:, 4:4 + dr], "dist": a[:, 4 + dr]}
