@@ -955,8 +955,17 @@ static int on_boundary(int dr, const double* r) {
 
 /* invert_point with the frozen
  * mechanics of decision D8. */
+/* Diagnostic (tests only): the first iteration at which the current iterate
+ * was on a face with the descent direction leaving through it (-1: never). */
+int fpxo_diag_abort_it = -1;
+int fpxo_diag_abort_it2 = -1;   /* first iteration held for the 2nd consecutive time */
+double fpxo_diag_abort_f = 0.0;  /* |dx|^2 when the rule first fired */
+
 void fpxo_invert(const fpxo_basis* B, int d, int dr, const double* X, const double* xs,
                  const fpxo_newton* S, double* r_out, double* dist, int* iters, int* conv) {
+  fpxo_diag_abort_it = -1;
+  fpxo_diag_abort_it2 = -1;
+  int held_prev = 0;
   int N = B->N;
   int K = dr == 1 ? N : (dr == 2 ? N * N : N * N * N);
   /* seed: nearest GLL node, ties -> lowest lexicographic index (D7) */
@@ -995,6 +1004,12 @@ void fpxo_invert(const fpxo_basis* B, int d, int dr, const double* X, const doub
     int freem[3] = {1, 1, 1};
     for (int a = 0; a < dr; ++a)
       if ((r[a] == 1.0 && J[a] < 0.0) || (r[a] == -1.0 && J[a] > 0.0)) freem[a] = 0;
+    {
+      const int held = it >= 1 && !(freem[0] && freem[1] && freem[2]);
+      if (fpxo_diag_abort_it < 0 && held) { fpxo_diag_abort_it = it; fpxo_diag_abort_f = f; }
+      if (fpxo_diag_abort_it2 < 0 && held && held_prev) fpxo_diag_abort_it2 = it;
+      held_prev = held;
+    }
     double s[3] = {0, 0, 0};
     const double(*Hm)[3] = H0;
     double Hr[3][3];

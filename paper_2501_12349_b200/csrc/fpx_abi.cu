@@ -135,8 +135,8 @@ struct Group {
 struct FindWs {
   int32_t *best, *npass, *upts, *clist, *cnum, *found, *lock, *nps, *perm, *hist, *bstart, *bcur,
       *maxnp;
-  int64_t* cum;
-  int4* pairs;
+  int64_t *cum, *npairs, *nredo;
+  int4 *pairs, *redo;
   int64_t *nun, *counter, *chunk_ctr;
   Group g1;
   // point ordering by hash cell
@@ -170,8 +170,11 @@ struct FindWs {
     maxnp = c.take<int32_t>(1);
     cum = c.take<int64_t>(FPX_HMAX + 1);
     pairs = c.take<int4>(2 * n + 1024);  // pair list (beyond: rebuilt by the kernel)
+    redo = c.take<int4>(2 * n + 1024);   // pairs stopped on a face (second pass)
+    npairs = c.take<int64_t>(1);
+    nredo = c.take<int64_t>(1);
     nun = c.take<int64_t>(1);
-    counter = c.take<int64_t>(1);
+    counter = c.take<int64_t>(2);
     chunk_ctr = c.take<int64_t>(1);
     g1.carve(c, E, n);
   }
@@ -465,7 +468,8 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
                                    w.best, w.npass, code, elem, r, dist, iters,
                                    field ? values : nullptr, C, w.g1.count, stats, st));
   FPX_CK(cudaMemsetAsync(w.nun, 0, sizeof(int64_t), st));
-  FPX_CK(cudaMemsetAsync(w.counter, 0, sizeof(int64_t), st));
+  FPX_CK(cudaMemsetAsync(w.counter, 0, 2 * sizeof(int64_t), st));
+  FPX_CK(cudaMemsetAsync(w.nredo, 0, sizeof(int64_t), st));
   // --- round 1: group by best-first element, Newton, fused eval
   g_launches += 3;
   FPX_CK(w.g1.build(E, n, nullptr, w.best, nullptr, st));
@@ -489,11 +493,13 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
   FPX_CK(cudaMemsetAsync(w.hist, 0, sizeof(int32_t) * 2 * FPX_HMAX, st));
   g_launches += 2;
   FPX_LAUNCH(fpx::launch_rest_lists(M, x, n, w.nun, w.upts, w.clist, w.cnum, w.nps, w.hist,
-                                    w.bstart, w.bcur, w.perm, w.cum, w.maxnp, w.pairs, st));
+                                    w.bstart, w.bcur, w.perm, w.cum, w.maxnp, w.pairs, w.npairs,
+                                    st));
   FPX_CK(cudaMemsetAsync(w.found, 0, sizeof(int32_t) * n, st));
   FPX_CK(cudaMemsetAsync(w.lock, 0, sizeof(int32_t) * n, st));
   FPX_LAUNCH(fpx::launch_find_rest(M, x, n, w.nun, w.upts, w.clist, w.cnum, w.nps, w.perm,
-                                   w.cum, w.maxnp, w.best, w.pairs, w.found, w.lock, code, elem,
+                                   w.cum, w.maxnp, w.best, w.pairs, w.npairs, w.redo, w.nredo,
+                                   w.found, w.lock, code, elem,
                                    r, dist,
                                    iters,
                                    field, C, values, w.counter, stats, st));

@@ -95,12 +95,13 @@ cudaError_t launch_rest_lists(const fpx_mesh_t& m, const double* x, int64_t nun_
                               const int64_t* nun_dev, const int32_t* upts, int32_t* clist,
                               int32_t* cnum, int32_t* nps, int32_t* hist, int32_t* bstart,
                               int32_t* bcur, int32_t* perm, int64_t* cum, int32_t* maxnp,
-                              int4* pairs, cudaStream_t st);
+                              int4* pairs, int64_t* npairs, cudaStream_t st);
 cudaError_t launch_find_rest(const fpx_mesh_t& m, const double* x, int64_t nun_cap,
                              const int64_t* nun_dev, const int32_t* upts, const int32_t* clist,
                              const int32_t* cnum, const int32_t* nps, const int32_t* perm,
                              const int64_t* cum, const int32_t* maxnp, const int32_t* best,
-                             const int4* pairs, int32_t* found,
+                             const int4* pairs, const int64_t* npairs, int4* redo,
+                             int64_t* nredo, int32_t* found,
                              int32_t* lock, int32_t* code, int32_t* elem, double* r, double* dist,
                              int32_t* iters, const double* field, int C, double* values,
                              int64_t* counter, int64_t* stats, cudaStream_t st);

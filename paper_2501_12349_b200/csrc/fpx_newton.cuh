@@ -1432,27 +1432,29 @@ __global__ void __launch_bounds__(WPB * 32, 1)
 // (descending) so that the points with a rank-r candidate are a prefix;
 // cum[r] = number of pairs of rank < r (r >= 1).  One block.
 static __global__ void k_rest_order(const int32_t* __restrict__ hist, int32_t* bstart, int64_t* cum,
-                             int32_t* maxnp) {
+                                    int32_t* maxnp, int64_t* npairs) {
+  __shared__ int32_t h[FPX_HMAX];
+  for (int v = threadIdx.x; v < FPX_HMAX; v += blockDim.x) h[v] = hist[v];
+  __syncthreads();
   if (threadIdx.x != 0) return;
   int pos = 0, mx = 0;
   for (int v = FPX_HMAX - 1; v >= 0; --v) {  // descending buckets
     bstart[v] = pos;
-    pos += hist[v];
-    if (hist[v] && v > mx) mx = v;
+    pos += h[v];
+    if (h[v] && v > mx) mx = v;
   }
-  // points with npass > r: suffix sums
-  int64_t c = 0, above = 0;
-  for (int v = FPX_HMAX - 1; v > 0; --v) above += hist[v];  // npass >= 1
-  // above = #points with npass > 0; iterate r = 1.. with cnt_r = #(npass > r)
-  int64_t gt = above - hist[1 < FPX_HMAX ? 1 : 0];          // npass > 1
+  // cnt_r = #(points with npass > r); cum[r] = pairs of rank < r (r >= 1)
+  int64_t c = 0, gt = 0;
+  for (int v = FPX_HMAX - 1; v > 1; --v) gt += h[v];  // npass > 1
   cum[0] = 0;
   cum[1] = 0;
   for (int rr = 1; rr < FPX_HMAX - 1; ++rr) {
     c += gt;  // pairs of rank rr
     cum[rr + 1] = c;
-    gt -= hist[rr + 1];
+    gt -= h[rr + 1];
   }
   *maxnp = mx;
+  *npairs = cum[mx];
 }
 
 static __global__ void k_rest_scatter(const int64_t* __restrict__ nun_dev, const int32_t* __restrict__ nps,
@@ -1508,10 +1510,10 @@ __global__ void __launch_bounds__(128, 2)
               const int32_t* __restrict__ cnum, const int32_t* __restrict__ nps,
               const int32_t* __restrict__ perm, const int64_t* __restrict__ cum,
               const int32_t* __restrict__ maxnp_dev, const int32_t* __restrict__ best,
-              const int4* __restrict__ pairs, int64_t pair_cap, int32_t* found, int32_t* lock,
-              int32_t* code,
-              int32_t* elem, double* r, double* dist, int32_t* iters, int64_t* counter,
-              int64_t* stats) {
+              const int4* __restrict__ pairs, int64_t pair_cap, const int64_t* __restrict__ npairs,
+              int abortable, int4* redo, int64_t* nredo, int32_t* found, int32_t* lock,
+              int32_t* code, int32_t* elem, double* r, double* dist, int32_t* iters,
+              int64_t* counter, int64_t* stats) {
   using L = Lay<D, DR, N>;
   constexpr int ES = L::GEO;  // doubles per element in nodes_pad
   extern __shared__ __align__(16) double smem[];
@@ -1527,13 +1529,16 @@ __global__ void __launch_bounds__(128, 2)
   __syncthreads();
   const NewtonParams P = newton_of(m);
   (void)nun_dev;
-  const int maxnp = *maxnp_dev;
-  const int64_t gmax = cum[maxnp];  // all pairs of ranks 1 .. maxnp-1
+  const int maxnp = maxnp_dev ? *maxnp_dev : 0;
+  // all pairs of ranks 1 .. maxnp-1, or the redo list (clamped: its slots
+  // beyond the capacity were never used, those pairs ran in full)
+  const int64_t gmax = abortable || !(*npairs > pair_cap) ? *npairs : pair_cap;
   int64_t s_newton = 0, s_iters = 0, nev = 0, nev2 = 0, nlev = 0;
   int64_t u = 0, k = 0;
   double xs[3] = {0.0, 0.0, 0.0};
   int phase = 0;  // 0 needs a pair, 3 iterating, 4 done
   int e = 0, it = 0;
+  int4 cur = make_int4(0, 0, 0, 0);  // the pair being solved
   bool first = true;
   double rc[3] = {0.0, 0.0, 0.0}, rn[3] = {0.0, 0.0, 0.0};
   double alpha = 1.0, fcur = 0.0, pred = 0.0, smax = 0.0;
@@ -1572,6 +1577,7 @@ __global__ void __launch_bounds__(128, 2)
       u = pr.z;
       if (*(volatile int32_t*)&found[u]) continue;  // an INTERIOR was found already
       k = pr.x;
+      cur = pr;
       const int rank = pr.w;
 #pragma unroll
       for (int c = 0; c < D; ++c) xs[c] = x[k * D + c];
@@ -1605,6 +1611,7 @@ __global__ void __launch_bounds__(128, 2)
       }
       if (en < 0) continue;
       e = en;
+      cur.y = en;
       phase = 1;  // needs its seed
     }
     // seeds (D7) of the lanes that just got a pair, 4 at a time: the warp
@@ -1707,6 +1714,23 @@ __global__ void __launch_bounds__(128, 2)
       if (smax < P.tol) done = true;
       else if (it >= P.max_iters) done = true;
     }
+    bool aborted = false;
+    if (!done && abortable && it >= 1) {
+      // on a face with the descent direction leaving through it: this
+      // candidate is most likely not the owner.  Stop; the pair is redone in
+      // full (second pass) only if its point ends without an INTERIOR.
+      bool held = false;
+#pragma unroll
+      for (int a = 0; a < DR; ++a)
+        held |= (rc[a] == 1.0 && st.J[a] < 0.0) || (rc[a] == -1.0 && st.J[a] > 0.0);
+      if (held) {
+        const int64_t slot = (int64_t)atomicAdd((unsigned long long*)nredo, 1ull);
+        if (slot < pair_cap) {
+          redo[slot] = cur;
+          aborted = done = true;
+        }
+      }
+    }
     if (!done) {
       fcur = st.f;
       const bool go = propose_step<DR>(st, rc, it, alpha, rn, pred, smax);
@@ -1714,7 +1738,11 @@ __global__ void __launch_bounds__(128, 2)
       if (!go) done = true;
       else stash_state(stash, st);
     }
-    if (done) {
+    if (done && aborted) {
+      s_newton += 1;
+      s_iters += it;
+      phase = 0;
+    } else if (done) {
       const double dd = sqrt(st.f);
       s_newton += 1;
       s_iters += it;
@@ -2296,8 +2324,8 @@ struct Rest {
                          const int64_t* nun_dev, const int32_t* upts, const int32_t* clist,
                          const int32_t* cnum, const int32_t* nps, const int32_t* perm,
                          const int64_t* cum, const int32_t* maxnp, const int32_t* best,
-                         const int4* pairs, int32_t* found, int32_t* lock, int32_t* code,
-                         int32_t* elem, double* r,
+                         const int4* pairs, const int64_t* npairs, int4* redo, int64_t* nredo,
+                         int32_t* found, int32_t* lock, int32_t* code, int32_t* elem, double* r,
                          double* dist, int32_t* iters, const double* field, int C,
                          double* values, int64_t* counter, int64_t* stats, cudaStream_t st) {
     static const bool l1 = [] {
@@ -2313,9 +2341,24 @@ struct Rest {
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       unsigned blocks = persistent_blocks((const void*)fn, threads, smem,
                                           (nun_cap + FPX_WARP - 1) / FPX_WARP);
+      const int64_t cap = 2 * nun_cap + 1024;
+      // FPX_REST_ABORT=1: pass 1 stops candidates whose iterate sits on a
+      // face with the descent direction leaving it, pass 2 redoes them in
+      // full for points still without an INTERIOR (exact either way).
+      // Measured: pass 1 -22%, but pass 2's own latency tail makes the sum
+      // slower on cfg-2, so it is off by default.
+      static const bool abort_pass = [] {
+        const char* v = getenv("FPX_REST_ABORT");
+        return v && v[0] == '1';
+      }();
       fn<<<blocks, threads, smem, st>>>(m, x, nun_dev, upts, clist, cnum, nps, perm, cum, maxnp,
-                                        best, pairs, 2 * nun_cap + 1024, found, lock, code, elem,
-                                        r, dist, iters, counter, stats);
+                                        best, pairs, cap, npairs, abort_pass ? 1 : 0, redo, nredo,
+                                        found, lock, code, elem, r, dist, iters, counter, stats);
+      if (abort_pass)
+        fn<<<blocks, threads, smem, st>>>(m, x, nun_dev, upts, clist, cnum, nps, perm, cum,
+                                          nullptr, best, redo, cap, nredo, 0, nullptr, nullptr,
+                                          found, lock, code, elem, r, dist, iters, counter + 1,
+                                          stats);
       err = cudaGetLastError();
     } else {
       const int threads = WPB * FPX_WARP;
@@ -2342,12 +2385,12 @@ struct Rest {
                            const int64_t* nun_dev, const int32_t* upts, int32_t* clist,
                            int32_t* cnum, int32_t* nps, int32_t* hist, int32_t* bstart,
                            int32_t* bcur, int32_t* perm, int64_t* cum, int32_t* maxnp,
-                           int4* pairs, cudaStream_t st) {
+                           int4* pairs, int64_t* npairs, cudaStream_t st) {
     int64_t b = (nun_cap + 3) / 4;
     if (b > 148 * 16) b = 148 * 16;
     if (b < 1) b = 1;
     k_rest_lists<D><<<(unsigned)b, 128, 0, st>>>(m, x, nun_dev, upts, clist, cnum, nps, hist);
-    k_rest_order<<<1, 32, 0, st>>>(hist, bstart, cum, maxnp);
+    k_rest_order<<<1, 256, 0, st>>>(hist, bstart, cum, maxnp, npairs);
     int64_t b2 = (nun_cap + 255) / 256;
     if (b2 > 148 * 8) b2 = 148 * 8;
     if (b2 < 1) b2 = 1;
