@@ -32,6 +32,7 @@ namespace {
 thread_local std::string g_err;
 std::atomic<int64_t> g_launches{0};
 cudaEvent_t g_prof_start = nullptr, g_prof_stop = nullptr;
+thread_local cudaEvent_t g_round1_done = nullptr;
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -271,6 +272,44 @@ int fpx_profile_round1(void* ev_start, void* ev_stop) {
   return FPX_OK;
 }
 
+int fpx_set_round1_event(void* ev) {
+  g_round1_done = reinterpret_cast<cudaEvent_t>(ev);
+  return FPX_OK;
+}
+
+int fpx_rest_gather(int dr, int C, int64_t n, const void* ws, size_t ws_bytes,
+                    const fpx_mesh_t* m, const int32_t* code, const int32_t* elem,
+                    const double* r, const double* dist, const double* values, int64_t cap,
+                    double* packed, void* stream) {
+  int rc = check_mesh(m);
+  if (rc) return rc;
+  Carver cv(const_cast<void*>(ws), ws_bytes);
+  FindWs w;
+  w.carve(cv, m->E, n);
+  if (!cv.ok()) return fail(FPX_EINVAL, "rest gather: workspace too small");
+  FPX_LAUNCH(fpx::launch_rest_gather(dr, C, w.nun, w.upts, code, elem, r, dist, values, cap,
+                                     packed, S(stream)));
+  return FPX_OK;
+}
+
+int fpx_scatter_packed_host(int dr, int C, const double* packed, int64_t cap, int32_t* code,
+                            int32_t* elem, double* r, double* dist, double* values) {
+  const int64_t cnt = (int64_t)packed[0];
+  if (cnt > cap) return fail(FPX_EINVAL, "packed rest records: %lld > capacity %lld",
+                             (long long)cnt, (long long)cap);
+  const int W = 4 + dr + C;
+  for (int64_t u = 0; u < cnt; ++u) {
+    const double* row = packed + (u + 1) * W;
+    const int64_t k = (int64_t)row[0];
+    code[k] = (int32_t)row[1];
+    elem[k] = (int32_t)row[2];
+    for (int a = 0; a < dr; ++a) r[k * dr + a] = row[3 + a];
+    dist[k] = row[3 + dr];
+    for (int c = 0; c < C; ++c) values[k * C + c] = row[4 + dr + c];
+  }
+  return FPX_OK;
+}
+
 int fpx_probe_fp64(double* tflops_host, void* stream) {
   cudaStream_t st = S(stream);
   int dev = 0, sms = 148;
@@ -489,6 +528,7 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
                                          values, w.upts, w.nun, w.chunk_ctr, stats, st));
   }
   if (g_prof_stop) FPX_CK(cudaEventRecord(g_prof_stop, st));
+  if (g_round1_done) FPX_CK(cudaEventRecord(g_round1_done, st));
   // --- rest: remaining candidates of the unresolved points
   FPX_CK(cudaMemsetAsync(w.hist, 0, sizeof(int32_t) * 2 * FPX_HMAX, st));
   g_launches += 2;

@@ -1530,9 +1530,12 @@ __global__ void __launch_bounds__(128, 2)
   const NewtonParams P = newton_of(m);
   (void)nun_dev;
   const int maxnp = maxnp_dev ? *maxnp_dev : 0;
-  // all pairs of ranks 1 .. maxnp-1, or the redo list (clamped: its slots
-  // beyond the capacity were never used, those pairs ran in full)
-  const int64_t gmax = abortable || !(*npairs > pair_cap) ? *npairs : pair_cap;
+  // all pairs of ranks 1 .. maxnp-1 (those beyond the list capacity are
+  // rebuilt below from cum/perm), or the redo list (maxnp_dev == NULL;
+  // clamped: its slots beyond the capacity were never used, those pairs ran
+  // in full)
+  const bool redo_pass = maxnp_dev == nullptr;
+  const int64_t gmax = redo_pass && *npairs > pair_cap ? pair_cap : *npairs;
   int64_t s_newton = 0, s_iters = 0, nev = 0, nev2 = 0, nlev = 0;
   int64_t u = 0, k = 0;
   double xs[3] = {0.0, 0.0, 0.0};

@@ -49,7 +49,7 @@ class EngineOptions:
     split: int = dfield(default_factory=lambda: int(os.environ.get("FPX_SPLIT", "1")))
     split_min: int = 1 << 18
     # local cells per axis = hash_refine * SPEC rule (perf only; FPX_HASH_REFINE overrides)
-    hash_refine: int = dfield(default_factory=lambda: int(os.environ.get("FPX_HASH_REFINE", "2")))
+    hash_refine: int = dfield(default_factory=lambda: int(os.environ.get("FPX_HASH_REFINE", "3")))
 
 
 @dataclass
@@ -472,6 +472,63 @@ class _SummedStats(Mapping):
         return _C.STATS_LEN
 
 
+def _host_overlapped(S: EngineSetup, f: Field, x: torch.Tensor, out: dict, ws: dict,
+                     sync: bool) -> dict:
+    """One find with its download split in two: after round 1 every record
+    except the ~5% the rest phase revisits is final, so the full download runs
+    on a side stream under the rest kernels; the revisited records follow as
+    one small packed gather (fpx_rest_gather) scattered on the host."""
+    L = _C.lib()
+    comp = torch.cuda.current_stream(S.device)
+    side = _streams(S, 1)[0]
+    n, dr, C = int(x.shape[0]), S.ref_dim, f.components
+    W = 4 + dr + C
+    cap = max(4096, n // 16)
+    if ws.get("packed") is None or ws["packed"].shape[0] < cap + 1 or ws["packed"].shape[1] != W:
+        ws["packed"] = torch.empty((cap + 1, W), dtype=torch.float64, device=S.device)
+        ws["packed_host"] = torch.empty((cap + 1, W), dtype=torch.float64, pin_memory=True)
+        ws["r1_event"] = torch.cuda.Event()
+    ev = ws["r1_event"]
+    ws["x"].copy_(x, non_blocking=True)
+    loc = dict(code=ws["code"], elem=ws["elem"], r=ws["r"], dist=ws["dist"], iters=None,
+               values=ws["values"])
+    L.fpx_set_round1_event(ev.cuda_event)
+    try:
+        st = _find_into(S, ws["x"], loc, f)
+    finally:
+        L.fpx_set_round1_event(None)
+    side.wait_event(ev)
+    # copies only on the side stream: a kernel there would wait for an SM
+    # behind the persistent rest kernels
+    with torch.cuda.stream(side):  # final for all but the rest points
+        for k in ("values", "code", "elem", "r", "dist"):
+            out[k].copy_(ws[k], non_blocking=True)
+    torch.where(loc["code"] != NOT_FOUND, torch.zeros_like(loc["elem"]),
+                torch.full_like(loc["elem"], -1), out=ws["rank"])
+    out["rank"].copy_(ws["rank"], non_blocking=True)
+    wsf = _workspace(S, n, n)
+    _C.check(L.fpx_rest_gather(dr, C, n, _C.ptr(wsf), wsf.numel(), S.mesh_t, _C.ptr(ws["code"]),
+                               _C.ptr(ws["elem"]), _C.ptr(ws["r"]), _C.ptr(ws["dist"]),
+                               _C.ptr(ws["values"]), cap, _C.ptr(ws["packed"]),
+                               _C.stream_handle()), "fpx_rest_gather")
+    ph = ws["packed_host"]
+    ph.copy_(ws["packed"], non_blocking=True)
+    comp.wait_stream(side)
+    if not sync:
+        raise ValueError("the overlapped host path completes on the host (sync=True)")
+    comp.synchronize()  # the host scatter below needs both downloads
+    if int(ph[0, 0]) > cap:  # more revisited points than the gather holds
+        for k in ("values", "code", "elem", "r", "dist"):
+            out[k].copy_(ws[k])
+    else:
+        _C.check(L.fpx_scatter_packed_host(dr, C, ph.data_ptr(), cap, out["code"].data_ptr(),
+                                           out["elem"].data_ptr(), out["r"].data_ptr(),
+                                           out["dist"].data_ptr(), out["values"].data_ptr()),
+                 "fpx_scatter_packed_host")
+    out["stats"] = st
+    return out
+
+
 def _streams(S: EngineSetup, k: int) -> list:
     """k side streams of this setup (created once)."""
     st = S.__dict__.setdefault("_side_streams", [])
@@ -480,7 +537,7 @@ def _streams(S: EngineSetup, k: int) -> list:
     return st[:k]
 
 
-def find_and_interpolate_host(S: EngineSetup, field, x: torch.Tensor, *, chunks: int = 4,
+def find_and_interpolate_host(S: EngineSetup, field, x: torch.Tensor, *, chunks: int = 1,
                               out: dict | None = None, sync: bool = True):
     """find_and_interpolate for points in (pinned) host memory, with the
     records and values returned to host memory.  The points are split into
@@ -526,14 +583,13 @@ def find_and_interpolate_host(S: EngineSetup, field, x: torch.Tensor, *, chunks:
     chunks = max(1, min(chunks, n))
     bounds = [n * c // chunks for c in range(chunks + 1)]
     keys = ("values", "code", "rank", "elem", "r", "dist")
+    if chunks == 1 and fused:
+        return _host_overlapped(S, f, x, out, ws, sync)
     if chunks == 1:  # upload, find, download in order on the caller's stream
         ws["x"].copy_(x, non_blocking=True)
         loc = dict(code=ws["code"], elem=ws["elem"], r=ws["r"], dist=ws["dist"], iters=None)
-        if fused:
-            loc["values"] = ws["values"]
-        st = _find_into(S, ws["x"], loc, f if fused else None)
-        if not fused:
-            ws["values"].copy_(_eval_local(S, f, loc["code"], loc["elem"], loc["r"]))
+        st = _find_into(S, ws["x"], loc, None)
+        ws["values"].copy_(_eval_local(S, f, loc["code"], loc["elem"], loc["r"]))
         torch.where(loc["code"] != NOT_FOUND, torch.zeros_like(loc["elem"]),
                     torch.full_like(loc["elem"], -1), out=ws["rank"])
         for k in keys:
