@@ -528,7 +528,8 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
                                          values, w.upts, w.nun, w.chunk_ctr, stats, st));
   }
   if (g_prof_stop) FPX_CK(cudaEventRecord(g_prof_stop, st));
-  if (g_round1_done) FPX_CK(cudaEventRecord(g_round1_done, st));
+  // external record: also a real event node when captured into a CUDA graph
+  if (g_round1_done) FPX_CK(cudaEventRecordWithFlags(g_round1_done, st, cudaEventRecordExternal));
   // --- rest: remaining candidates of the unresolved points
   FPX_CK(cudaMemsetAsync(w.hist, 0, sizeof(int32_t) * 2 * FPX_HMAX, st));
   g_launches += 2;

@@ -48,6 +48,8 @@ class EngineOptions:
     # FPX_SPLIT overrides)
     split: int = dfield(default_factory=lambda: int(os.environ.get("FPX_SPLIT", "1")))
     split_min: int = 1 << 18
+    # host-buffer API: replay its device part as a CUDA graph (FPX_GRAPHS=0: off)
+    graphs: bool = dfield(default_factory=lambda: os.environ.get("FPX_GRAPHS", "1") != "0")
     # local cells per axis = hash_refine * SPEC rule (perf only; FPX_HASH_REFINE overrides)
     hash_refine: int = dfield(default_factory=lambda: int(os.environ.get("FPX_HASH_REFINE", "3")))
 
@@ -490,33 +492,34 @@ def _host_overlapped(S: EngineSetup, f: Field, x: torch.Tensor, out: dict, ws: d
         ws["r1_event"] = torch.cuda.Event()
     ev = ws["r1_event"]
     ws["x"].copy_(x, non_blocking=True)
-    loc = dict(code=ws["code"], elem=ws["elem"], r=ws["r"], dist=ws["dist"], iters=None,
-               values=ws["values"])
-    L.fpx_set_round1_event(ev.cuda_event)
-    try:
-        st = _find_into(S, ws["x"], loc, f)
-    finally:
-        L.fpx_set_round1_event(None)
+    gkey = (n, f.blocks.data_ptr(), C, out["code"].data_ptr(), out["values"].data_ptr())
+    if S.options.graphs and ws.get("graph_key") != gkey:
+        # capture the single-stream device part once per buffers; a replay
+        # costs one launch instead of ~60 (the round-1 event is an external
+        # event node, so the side stream below can wait on it)
+        _host_device_part(S, f, out, ws, ev, cap)  # warm-up outside capture
+        comp.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            st = _host_device_part(S, f, out, ws, ev, cap)
+        ws.update(graph=g, graph_key=gkey, graph_stats=st)
+    if S.options.graphs:
+        ws["graph"].replay()
+        st = ws["graph_stats"]
+    else:
+        st = _host_device_part(S, f, out, ws, ev, cap)
+    # after round 1 every record but the rest points' is final: download them
+    # on the side stream (copies only: a kernel there would wait for an SM
+    # behind the persistent rest kernels) while the rest kernels run
     side.wait_event(ev)
-    # copies only on the side stream: a kernel there would wait for an SM
-    # behind the persistent rest kernels
-    with torch.cuda.stream(side):  # final for all but the rest points
+    with torch.cuda.stream(side):
         for k in ("values", "code", "elem", "r", "dist"):
             out[k].copy_(ws[k], non_blocking=True)
-    torch.where(loc["code"] != NOT_FOUND, torch.zeros_like(loc["elem"]),
-                torch.full_like(loc["elem"], -1), out=ws["rank"])
-    out["rank"].copy_(ws["rank"], non_blocking=True)
-    wsf = _workspace(S, n, n)
-    _C.check(L.fpx_rest_gather(dr, C, n, _C.ptr(wsf), wsf.numel(), S.mesh_t, _C.ptr(ws["code"]),
-                               _C.ptr(ws["elem"]), _C.ptr(ws["r"]), _C.ptr(ws["dist"]),
-                               _C.ptr(ws["values"]), cap, _C.ptr(ws["packed"]),
-                               _C.stream_handle()), "fpx_rest_gather")
-    ph = ws["packed_host"]
-    ph.copy_(ws["packed"], non_blocking=True)
     comp.wait_stream(side)
     if not sync:
         raise ValueError("the overlapped host path completes on the host (sync=True)")
     comp.synchronize()  # the host scatter below needs both downloads
+    ph = ws["packed_host"]
     if int(ph[0, 0]) > cap:  # more revisited points than the gather holds
         for k in ("values", "code", "elem", "r", "dist"):
             out[k].copy_(ws[k])
@@ -527,6 +530,31 @@ def _host_overlapped(S: EngineSetup, f: Field, x: torch.Tensor, out: dict, ws: d
                  "fpx_scatter_packed_host")
     out["stats"] = st
     return out
+
+
+def _host_device_part(S: EngineSetup, f: Field, out: dict, ws: dict, ev, cap: int):
+    """Single-stream device work of _host_overlapped (capturable): the find
+    (recording `ev` after round 1), the rank fill and rank download, the rest
+    gather and its download."""
+    L = _C.lib()
+    n, dr, C = int(ws["x"].shape[0]), S.ref_dim, f.components
+    loc = dict(code=ws["code"], elem=ws["elem"], r=ws["r"], dist=ws["dist"], iters=None,
+               values=ws["values"])
+    L.fpx_set_round1_event(ev.cuda_event)
+    try:
+        st = _find_into(S, ws["x"], loc, f)
+    finally:
+        L.fpx_set_round1_event(None)
+    torch.where(loc["code"] != NOT_FOUND, torch.zeros_like(loc["elem"]),
+                torch.full_like(loc["elem"], -1), out=ws["rank"])
+    out["rank"].copy_(ws["rank"], non_blocking=True)
+    wsf = _workspace(S, n, n)
+    _C.check(L.fpx_rest_gather(dr, C, n, _C.ptr(wsf), wsf.numel(), S.mesh_t, _C.ptr(ws["code"]),
+                               _C.ptr(ws["elem"]), _C.ptr(ws["r"]), _C.ptr(ws["dist"]),
+                               _C.ptr(ws["values"]), cap, _C.ptr(ws["packed"]),
+                               _C.stream_handle()), "fpx_rest_gather")
+    ws["packed_host"].copy_(ws["packed"], non_blocking=True)
+    return st
 
 
 def _streams(S: EngineSetup, k: int) -> list:
