@@ -523,9 +523,18 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
                                          field, C, values, w.upts, nullptr, w.nun, stats, st));
   } else {
     FPX_CK(cudaMemsetAsync(w.chunk_ctr, 0, sizeof(int64_t), st));
+    // candidates held on a face twice in a row stop early (redo pass; see
+    // k_rest_l1).  FPX_ABORT=0, or the shared-slot rest variant, disable it.
+    static const bool abort_r1 = [] {
+      const char* v = getenv("FPX_ABORT");
+      const char* rv = getenv("FPX_REST");
+      return !(v && v[0] == '0') && !(rv && rv[0] == 's');
+    }();
     FPX_LAUNCH(fpx::launch_newton_stream(M, n, x, w.g1.sorted, w.g1.packed_off, w.g1.count,
                                          w.best, w.npass, code, elem, r, dist, iters, field, C,
-                                         values, w.upts, w.nun, w.chunk_ctr, stats, st));
+                                         values, w.upts, w.nun, w.chunk_ctr,
+                                         abort_r1 ? w.redo : nullptr, w.nredo, 2 * n + 1024,
+                                         stats, st));
   }
   if (g_prof_stop) FPX_CK(cudaEventRecord(g_prof_stop, st));
   // external record: also a real event node when captured into a CUDA graph

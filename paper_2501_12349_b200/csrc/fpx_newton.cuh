@@ -1013,6 +1013,16 @@ __device__ __forceinline__ int seed_batch(const unsigned* js, int cnt, const dou
   return mine;
 }
 
+// The abort rule (round 1 and rest pass 1): some axis of r is on a face and
+// the descent direction -J leaves the element through it.
+template <int DR>
+__device__ __forceinline__ bool held_on_face(const double* r, const double* J) {
+  bool held = false;
+#pragma unroll
+  for (int a = 0; a < DR; ++a) held |= (r[a] == 1.0 && J[a] < 0.0) || (r[a] == -1.0 && J[a] > 0.0);
+  return held;
+}
+
 // Per-point slot: geometry [D][N^DR] | axis-1.. basis values | Newton stash,
 // odd stride in doubles (the 16 points of a warp hit distinct bank pairs).
 template <int D, int DR, int N>
@@ -1541,6 +1551,7 @@ __global__ void __launch_bounds__(128, 2)
   double xs[3] = {0.0, 0.0, 0.0};
   int phase = 0;  // 0 needs a pair, 3 iterating, 4 done
   int e = 0, it = 0;
+  bool held_prev = false;
   int4 cur = make_int4(0, 0, 0, 0);  // the pair being solved
   bool first = true;
   double rc[3] = {0.0, 0.0, 0.0}, rn[3] = {0.0, 0.0, 0.0};
@@ -1683,6 +1694,7 @@ __global__ void __launch_bounds__(128, 2)
 #pragma unroll
           for (int a = 0; a < 3; ++a) rn[a] = rc[a];
           first = true;
+          held_prev = false;
           it = 0;
           alpha = P.alpha0;
           phase = 3;
@@ -1719,20 +1731,19 @@ __global__ void __launch_bounds__(128, 2)
     }
     bool aborted = false;
     if (!done && abortable && it >= 1) {
-      // on a face with the descent direction leaving through it: this
-      // candidate is most likely not the owner.  Stop; the pair is redone in
-      // full (second pass) only if its point ends without an INTERIOR.
-      bool held = false;
-#pragma unroll
-      for (int a = 0; a < DR; ++a)
-        held |= (rc[a] == 1.0 && st.J[a] < 0.0) || (rc[a] == -1.0 && st.J[a] > 0.0);
-      if (held) {
+      // held on a face (descent direction leaving it) for two consecutive
+      // iterations: this candidate is most likely not the owner.  Stop; the
+      // pair is redone in full (second pass) only if its point ends without
+      // an INTERIOR.
+      const bool held = held_on_face<DR>(rc, st.J);
+      if (held && held_prev) {
         const int64_t slot = (int64_t)atomicAdd((unsigned long long*)nredo, 1ull);
         if (slot < pair_cap) {
           redo[slot] = cur;
           aborted = done = true;
         }
       }
+      held_prev = held;
     }
     if (!done) {
       fcur = st.f;
@@ -1856,7 +1867,7 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
                     int32_t* code, int32_t* elem, double* r, double* dist, int32_t* iters,
                     const double* __restrict__ field, int C, double* values, int32_t* upts,
                     int64_t* nun_dev, int64_t* chunk_ctr, int slot_stride, int chunk,
-                    int64_t* stats) {
+                    int4* redo, int64_t* nredo, int64_t redo_cap, int64_t* stats) {
   using L = Lay<D, DR, N>;
   constexpr int K = L::K;
   constexpr int SCR = Scratch<DR, N>::SLOTS;
@@ -1895,7 +1906,7 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
   unsigned ready = 0;  // slots whose current load has landed
   // lane state: 0 idle, 1 needs seed, 2 iterating
   int phase = 0, myslot = 0, pt = 0, it = 0;
-  bool first = true;
+  bool first = true, held_prev = false;
   double xs[3] = {0.0, 0.0, 0.0}, rc[3] = {0.0, 0.0, 0.0}, rn[3] = {0.0, 0.0, 0.0};
   double alpha = 1.0, fcur = 0.0, pred = 0.0, smax = 0.0;
   NState st;
@@ -2042,6 +2053,7 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
 #pragma unroll
         for (int a = 0; a < 3; ++a) rn[a] = rc[a];
         first = true;
+        held_prev = false;
         it = 0;
         alpha = P.alpha0;
         phase = 2;
@@ -2080,6 +2092,33 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
       }
       if (smax < P.tol) done = true;
       else if (it >= P.max_iters) done = true;
+    }
+    if (!done && redo && it >= 1) {
+      // the abort rule of the rest kernel: held on a face for two
+      // consecutive iterations -> stop, hand the point to the rest phase
+      // (its other candidates) and this candidate to the redo pass, which
+      // runs it in full only if no candidate turns out INTERIOR
+      const bool held = held_on_face<DR>(rc, st.J);
+      if (held && held_prev) {
+        const int64_t rs = (int64_t)atomicAdd((unsigned long long*)nredo, 1ull);
+        if (rs < redo_cap) {
+          const int e = meta->elem[myslot];
+          const int slot = (int)atomicAdd((unsigned long long*)nun_dev, 1ull);
+          upts[slot] = pt;
+          redo[rs] = make_int4(pt, e, slot, 0);
+          code[pt] = kBorder;  // placeholder: any computed record replaces it
+          elem[pt] = e;
+          dist[pt] = INFINITY;
+#pragma unroll
+          for (int a = 0; a < DR; ++a) r[(int64_t)pt * DR + a] = rc[a];
+          if (iters) iters[pt] = it;
+          s_newton += 1;
+          s_iters += it;
+          phase = 0;
+          continue;
+        }
+      }
+      held_prev = held;
     }
     if (!done) {
       fcur = st.f;
@@ -2264,7 +2303,8 @@ struct Stream {
                          const int32_t* npass, int32_t* code, int32_t* elem, double* r,
                          double* dist, int32_t* iters, const double* field, int C, double* values,
                          int32_t* upts, int64_t* nun_dev, int64_t* chunk_ctr, int64_t n_cap,
-                         int64_t* stats, cudaStream_t st) {
+                         int4* redo, int64_t* nredo, int64_t redo_cap, int64_t* stats,
+                         cudaStream_t st) {
     using L = Lay<D, DR, N>;
     int ss = L::GEO + (field ? C * L::CS : 0);
     ss = (ss + 13) / 16 * 16 + 2;  // slot stride = 16 bytes mod 128: distinct bank groups
@@ -2287,7 +2327,7 @@ struct Stream {
                                         (n_cap + chunk - 1) / chunk);
     fn<<<blocks, threads, smem, st>>>(m, x, sorted, packed_off, ecount, best, npass, code, elem, r,
                                       dist, iters, field, C, values, upts, nun_dev, chunk_ctr, ss,
-                                      chunk, stats);
+                                      chunk, redo, nredo, redo_cap, stats);
     return cudaGetLastError();
   }
 };
@@ -2345,20 +2385,18 @@ struct Rest {
       unsigned blocks = persistent_blocks((const void*)fn, threads, smem,
                                           (nun_cap + FPX_WARP - 1) / FPX_WARP);
       const int64_t cap = 2 * nun_cap + 1024;
-      // FPX_REST_ABORT=1: pass 1 stops candidates whose iterate sits on a
-      // face with the descent direction leaving it, pass 2 redoes them in
-      // full for points still without an INTERIOR (exact either way).
-      // Measured: pass 1 -22%, but pass 2's own latency tail makes the sum
-      // slower on cfg-2, so it is off by default.
+      // Pass 1 stops candidates held on a face (descent direction leaving
+      // it) for two consecutive iterations; pass 2 redoes every stopped
+      // candidate (of round 1 and of pass 1) in full for points still without
+      // an INTERIOR.  Exact either way; FPX_ABORT=0 disables both.
       static const bool abort_pass = [] {
-        const char* v = getenv("FPX_REST_ABORT");
-        return v && v[0] == '1';
+        const char* v = getenv("FPX_ABORT");
+        return !(v && v[0] == '0');
       }();
       fn<<<blocks, threads, smem, st>>>(m, x, nun_dev, upts, clist, cnum, nps, perm, cum, maxnp,
                                         best, pairs, cap, npairs, abort_pass ? 1 : 0, redo, nredo,
                                         found, lock, code, elem, r, dist, iters, counter, stats);
-      if (abort_pass)
-        fn<<<blocks, threads, smem, st>>>(m, x, nun_dev, upts, clist, cnum, nps, perm, cum,
+      fn<<<blocks, threads, smem, st>>>(m, x, nun_dev, upts, clist, cnum, nps, perm, cum,
                                           nullptr, best, redo, cap, nredo, 0, nullptr, nullptr,
                                           found, lock, code, elem, r, dist, iters, counter + 1,
                                           stats);

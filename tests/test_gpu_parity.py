@@ -261,3 +261,23 @@ def test_host_pipeline_matches_device(chunks):
     assert torch.allclose(v[inter], vd[inter], rtol=1e-10, atol=1e-12)
     assert torch.isnan(v[code == 2]).all()
     assert out["stats"]["points"] == x.shape[0]
+
+
+def test_spiral_newton_efficiency_gpu():
+    # acceptance 6 on the device: the p=9 spiral element,
+    # 10^4 interior points: every solve converges within 50 iterations, mean
+    # <= 15, r* recovered to 1e-9; and the same iteration counts as the oracle
+    m = toolkit.spiral_mesh(9)
+    S = engine.setup(m)
+    rng = np.random.default_rng(6)
+    rh = rng.uniform(-0.98, 0.98, (10000, 2))
+    bc = BasisConstants.of(S.basis, S.envelope)
+    B = O.basis_from_arrays(bc.nodes, bc.scale, bc.proj0, bc.proj1, bc.eta, bc.lo, bc.hi)
+    xs = np.stack([O.forward_map(B, 2, 2, m.nodes[0], q)[0] for q in rh])
+    r, dist, it, cv = invmap.invert_points(S, torch.from_numpy(xs), torch.zeros(10000, dtype=torch.int32))
+    it = it.cpu().numpy()
+    assert bool(cv.all()) and it.max() <= 50
+    assert it.mean() <= 15
+    assert np.max(np.abs(r.cpu().numpy() - rh)) < 1e-9
+    rec = engine.find(S, xs)
+    assert (rec.code.cpu().numpy() == 0).all()
