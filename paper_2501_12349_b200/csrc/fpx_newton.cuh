@@ -1730,6 +1730,14 @@ __global__ void __launch_bounds__(128, 2)
       else if (it >= P.max_iters) done = true;
     }
     bool aborted = false;
+    if (!done && *(volatile int32_t*)&found[u]) {
+      // another candidate of this point was INTERIOR meanwhile: its record
+      // is final (an INTERIOR is unique up to shared faces), stop this one
+      s_newton += 1;
+      s_iters += it;
+      phase = 0;
+      continue;
+    }
     if (!done && abortable && it >= 1) {
       // held on a face (descent direction leaving it) for two consecutive
       // iterations: this candidate is most likely not the owner.  Stop; the
