@@ -230,6 +230,154 @@ __device__ __forceinline__ void eval_state(const double* __restrict__ sX,
   }
 }
 
+// eval_state with the second-derivative switch as a runtime (warp-uniform)
+// flag: one copy of the contraction in the streamed kernels, whose lone
+// warps at the end of a launch are bound by instruction fetch (the flag is
+// set in ~90% of their evaluations, so the predicated-off FMAs are rare).
+template <int D, int DR, int N, int LAY = 0>
+__device__ __forceinline__ void eval_state_rt(const double* __restrict__ sX,
+                                           const double* __restrict__ z,
+                                           const double* __restrict__ scale, const double* r,
+                                           const double* xs, NState& S, double* sb, const bool W2) {
+  // LAY 0: geometry staged in shared memory, rows padded to NP;
+  // LAY 1: read in place from global memory ([d][N^dr]);
+  // LAY 2: a per-lane shared slot holding [d][N^dr] unpadded.
+  using Lp = Lay<D, DR, N>;
+  // LAY 3: global memory, rows padded to NP (mesh.nodes_pad)
+  constexpr bool GEO = LAY == 1;
+  constexpr int GCS = (LAY == 1 || LAY == 2) ? Lp::K : Lp::CS;
+  constexpr int GNP = (LAY == 1 || LAY == 2) ? N : Lp::NP;
+  double v0[N], g0[N], h0[N];
+  lagrange<N, true>(z, scale, r[0], v0, g0, h0);
+#pragma unroll
+  for (int a = 1; a < DR; ++a) {
+    double v[N], g[N], h[N];
+    lagrange<N, true>(z, scale, r[a], v, g, h);
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      sb[(((a - 1) * 3 + 0) * N + j) * FPX_WARP] = v[j];
+      sb[(((a - 1) * 3 + 1) * N + j) * FPX_WARP] = g[j];
+      if (W2) sb[(((a - 1) * 3 + 2) * N + j) * FPX_WARP] = h[j];
+    }
+  }
+#define SB(a, kind, j) sb[((((a)-1) * 3 + (kind)) * N + (j)) * FPX_WARP]
+  S.f = 0.0;
+#pragma unroll
+  for (int m = 0; m < 3; ++m) S.J[m] = 0.0;
+#pragma unroll
+  for (int m = 0; m < 6; ++m) {
+    S.H0[m] = 0.0;
+    S.Q[m] = 0.0;
+  }
+#pragma unroll 1
+  for (int c = 0; c < D; ++c) {
+    const double* Xc = sX + c * GCS;
+    double xv = 0.0, G[3] = {0.0, 0.0, 0.0}, H2[6] = {0, 0, 0, 0, 0, 0};
+    if constexpr (DR == 3) {
+#pragma unroll kUnrollK
+      for (int k = 0; k < N; ++k) {
+        double t00 = 0.0, t10 = 0.0, t01 = 0.0, t20 = 0.0, t11 = 0.0, t02 = 0.0;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          const double* row = Xc + (j + N * k) * GNP;
+          double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+#pragma unroll
+          for (int i = 0; i < N; i += 2) {
+            double2 p;
+            if (GEO) p = make_double2(__ldg(row + i), i + 1 < N ? __ldg(row + i + 1) : 0.0);
+            else if (LAY == 2) p = make_double2(row[i], i + 1 < N ? row[i + 1] : 0.0);
+            else if (LAY == 3) p = __ldg(reinterpret_cast<const double2*>(row + i));
+            else if (i + 1 < N) p = *reinterpret_cast<const double2*>(row + i);
+            else p = make_double2(row[i], 0.0);
+            s0 = fma(p.x, v0[i], s0);
+            s1 = fma(p.x, g0[i], s1);
+            if (W2) s2 = fma(p.x, h0[i], s2);
+            if (i + 1 < N) {
+              s0 = fma(p.y, v0[i + 1], s0);
+              s1 = fma(p.y, g0[i + 1], s1);
+              if (W2) s2 = fma(p.y, h0[i + 1], s2);
+            }
+          }
+          const double vj = SB(1, 0, j), gj = SB(1, 1, j);
+          t00 = fma(s0, vj, t00);
+          t10 = fma(s1, vj, t10);
+          t01 = fma(s0, gj, t01);
+          if (W2) {
+            const double hj = SB(1, 2, j);
+            t20 = fma(s2, vj, t20);
+            t11 = fma(s1, gj, t11);
+            t02 = fma(s0, hj, t02);
+          }
+        }
+        const double vk = SB(2, 0, k), gk = SB(2, 1, k);
+        xv = fma(t00, vk, xv);
+        G[0] = fma(t10, vk, G[0]);
+        G[1] = fma(t01, vk, G[1]);
+        G[2] = fma(t00, gk, G[2]);
+        if (W2) {
+          const double hk = SB(2, 2, k);
+          H2[0] = fma(t20, vk, H2[0]);
+          H2[1] = fma(t02, vk, H2[1]);
+          H2[2] = fma(t00, hk, H2[2]);
+          H2[3] = fma(t11, vk, H2[3]);
+          H2[4] = fma(t10, gk, H2[4]);
+          H2[5] = fma(t01, gk, H2[5]);
+        }
+      }
+    } else if constexpr (DR == 2) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        const double* row = Xc + j * GNP;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+          const double p = row[i];
+          s0 = fma(p, v0[i], s0);
+          s1 = fma(p, g0[i], s1);
+          if (W2) s2 = fma(p, h0[i], s2);
+        }
+        const double vj = SB(1, 0, j), gj = SB(1, 1, j);
+        xv = fma(s0, vj, xv);
+        G[0] = fma(s1, vj, G[0]);
+        G[1] = fma(s0, gj, G[1]);
+        if (W2) {
+          const double hj = SB(1, 2, j);
+          H2[0] = fma(s2, vj, H2[0]);
+          H2[1] = fma(s0, hj, H2[1]);
+          H2[3] = fma(s1, gj, H2[3]);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < N; ++i) {
+        const double p = Xc[i];
+        xv = fma(p, v0[i], xv);
+        G[0] = fma(p, g0[i], G[0]);
+        if (W2) H2[0] = fma(p, h0[i], H2[0]);
+      }
+    }
+#undef SB
+    const double dx = (c == 0 ? xs[0] : (c == 1 ? xs[1] : xs[D - 1])) - xv;
+    S.f = fma(dx, dx, S.f);
+#pragma unroll
+    for (int a = 0; a < DR; ++a) S.J[a] = fma(-G[a], dx, S.J[a]);
+    S.H0[0] = fma(G[0], G[0], S.H0[0]);
+    if (DR > 1) {
+      S.H0[1] = fma(G[1], G[1], S.H0[1]);
+      S.H0[3] = fma(G[0], G[1], S.H0[3]);
+    }
+    if (DR > 2) {
+      S.H0[2] = fma(G[2], G[2], S.H0[2]);
+      S.H0[4] = fma(G[0], G[2], S.H0[4]);
+      S.H0[5] = fma(G[1], G[2], S.H0[5]);
+    }
+    if (W2) {
+#pragma unroll
+      for (int m = 0; m < 6; ++m) S.Q[m] = fma(dx, H2[m], S.Q[m]);
+    }
+  }
+}
+
 __device__ __forceinline__ int symi(int a, int b) {
   return a == b ? a : (a + b == 1 ? 3 : (a + b == 2 ? 4 : 5));
 }
@@ -1708,8 +1856,7 @@ __global__ void __launch_bounds__(128, 2)
     nev2 += w2 ? 1 : 0;
     nlev += phase == 3 ? 1 : 0;
     const double* X = m.nodes_pad + (int64_t)(phase == 3 ? e : 0) * ES;
-    if (w2) eval_state<D, DR, N, true, 3>(X, z, scale, rn, xs, st, sb);
-    else eval_state<D, DR, N, false, 3>(X, z, scale, rn, xs, st, sb);
+    eval_state_rt<D, DR, N, 3>(X, z, scale, rn, xs, st, sb, w2);
     if (phase != 3) continue;
     // (c) trust-region Newton update (newton_warp, D8)
     bool done = false;
@@ -2080,8 +2227,7 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
     const bool w2 = __any_sync(FPX_FULL, phase == 2 && on_boundary<DR>(rn));
     ++nev;
     nev2 += w2 ? 1 : 0;
-    if (w2) eval_state<D, DR, N, true, 0>(sX, z, scale, rn, xs, st, sb);
-    else eval_state<D, DR, N, false, 0>(sX, z, scale, rn, xs, st, sb);
+    eval_state_rt<D, DR, N, 0>(sX, z, scale, rn, xs, st, sb, w2);
     if (phase != 2) continue;
     // ---- this lane's trust-region Newton update (newton_warp, D8)
     bool done = false;
@@ -2326,11 +2472,22 @@ struct Stream {
     auto fn = k_newton_stream<D, DR, N, S>;
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    static const int chunk = [] {
+    static const int chunk_env = [] {
       const char* v = getenv("FPX_R1_CHUNK");
-      const int c = v ? atoi(v) : FPX_CHUNK_DEFAULT;
-      return c < 8 ? 8 : c;
+      const int c = v ? atoi(v) : 0;
+      return c < 0 ? 0 : c;
     }();
+    // chunk: FPX_CHUNK_DEFAULT points, shrunk when the stream is too short to
+    // give every resident warp a chunk (a sparse stream - about one point per
+    // element - keeps at most S lanes of a warp busy, so its latency is the
+    // per-warp point count, not the total)
+    int chunk = chunk_env;
+    if (chunk == 0) {
+      const int64_t warps = (int64_t)persistent_blocks((const void*)fn, threads, smem,
+                                                       INT64_C(1) << 40) * wpb;
+      const int64_t want = (n_cap + warps - 1) / (warps > 0 ? warps : 1);
+      chunk = want < 1 ? 1 : want > FPX_CHUNK_DEFAULT ? FPX_CHUNK_DEFAULT : (int)want;
+    }
     unsigned blocks = persistent_blocks((const void*)fn, threads, smem,
                                         (n_cap + chunk - 1) / chunk);
     fn<<<blocks, threads, smem, st>>>(m, x, sorted, packed_off, ecount, best, npass, code, elem, r,
