@@ -1586,33 +1586,62 @@ __global__ void __launch_bounds__(WPB * 32, 1)
 }
 
 
+// Block-wide inclusive sum over FPX_HMAX threads (one value per thread).
+__device__ __forceinline__ int64_t block_incl_sum(int64_t v, int64_t* ws) {
+  const int lane = threadIdx.x % FPX_WARP, warp = threadIdx.x / FPX_WARP;
+#pragma unroll
+  for (int o = 1; o < FPX_WARP; o <<= 1) {
+    const int64_t y = __shfl_up_sync(FPX_FULL, v, o);
+    if (lane >= o) v += y;
+  }
+  if (lane == FPX_WARP - 1) ws[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    int64_t w = lane < (int)(blockDim.x / FPX_WARP) ? ws[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < FPX_WARP; o <<= 1) {
+      const int64_t y = __shfl_up_sync(FPX_FULL, w, o);
+      if (lane >= o) w += y;
+    }
+    ws[lane] = w;
+  }
+  __syncthreads();
+  if (warp > 0) v += ws[warp - 1];
+  __syncthreads();
+  return v;
+}
+
 // Pair enumeration of the rest kernel: rest points sorted by candidate count
 // (descending) so that the points with a rank-r candidate are a prefix;
 // cum[r] = number of pairs of rank < r (r >= 1).  One block.
-static __global__ void k_rest_order(const int32_t* __restrict__ hist, int32_t* bstart, int64_t* cum,
-                                    int32_t* maxnp, int64_t* npairs) {
-  __shared__ int32_t h[FPX_HMAX];
-  for (int v = threadIdx.x; v < FPX_HMAX; v += blockDim.x) h[v] = hist[v];
+static __global__ void __launch_bounds__(FPX_HMAX)
+    k_rest_order(const int32_t* __restrict__ hist, int32_t* bstart, int64_t* cum,
+                 int32_t* maxnp, int64_t* npairs) {
+  // one thread per bucket, two block scans:
+  //   bstart[v] = #(points with npass > v)          (descending bucket order)
+  //   cum[r+1]  = sum_{1<=r'<=r} #(npass > r')       (pairs of rank <= r)
+  __shared__ int64_t ws[FPX_WARP];
+  __shared__ int64_t gt[FPX_HMAX];
+  __shared__ int smx;
+  const int t = threadIdx.x;
+  if (t == 0) smx = 0;
+  const int v = FPX_HMAX - 1 - t;
+  const int hv = hist[v];
   __syncthreads();
-  if (threadIdx.x != 0) return;
-  int pos = 0, mx = 0;
-  for (int v = FPX_HMAX - 1; v >= 0; --v) {  // descending buckets
-    bstart[v] = pos;
-    pos += h[v];
-    if (h[v] && v > mx) mx = v;
+  if (hv) atomicMax(&smx, v);
+  const int64_t suf = block_incl_sum(hv, ws) - hv;  // sum over buckets > v
+  bstart[v] = (int32_t)suf;
+  gt[v] = suf;
+  __syncthreads();
+  const int mx = smx;
+  const int64_t c = block_incl_sum(t >= 1 && t < FPX_HMAX - 1 ? gt[t] : 0, ws);
+  if (t < 2) cum[t] = 0;
+  if (t >= 1 && t < FPX_HMAX - 1) cum[t + 1] = c;
+  if (t == 0) {
+    *maxnp = mx;
+    if (mx <= 1) *npairs = 0;
   }
-  // cnt_r = #(points with npass > r); cum[r] = pairs of rank < r (r >= 1)
-  int64_t c = 0, gt = 0;
-  for (int v = FPX_HMAX - 1; v > 1; --v) gt += h[v];  // npass > 1
-  cum[0] = 0;
-  cum[1] = 0;
-  for (int rr = 1; rr < FPX_HMAX - 1; ++rr) {
-    c += gt;  // pairs of rank rr
-    cum[rr + 1] = c;
-    gt -= h[rr + 1];
-  }
-  *maxnp = mx;
-  *npairs = cum[mx];
+  if (mx >= 2 && t + 1 == mx) *npairs = c;
 }
 
 static __global__ void k_rest_scatter(const int64_t* __restrict__ nun_dev, const int32_t* __restrict__ nps,
@@ -2596,7 +2625,7 @@ struct Rest {
     if (b > 148 * 16) b = 148 * 16;
     if (b < 1) b = 1;
     k_rest_lists<D><<<(unsigned)b, 128, 0, st>>>(m, x, nun_dev, upts, clist, cnum, nps, hist);
-    k_rest_order<<<1, 256, 0, st>>>(hist, bstart, cum, maxnp, npairs);
+    k_rest_order<<<1, FPX_HMAX, 0, st>>>(hist, bstart, cum, maxnp, npairs);
     int64_t b2 = (nun_cap + 255) / 256;
     if (b2 > 148 * 8) b2 = 148 * 8;
     if (b2 < 1) b2 = 1;
