@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define FPX_ABI_VERSION 2
+#define FPX_ABI_VERSION 3
 
 /* error codes */
 #define FPX_OK 0
@@ -123,27 +123,23 @@ int64_t fpx_launch_count(void);
  * Newton kernel of the next fpx_find calls on the same stream; NULL clears.
  * Used by bench.py to time the dominant kernel live. */
 int fpx_profile_round1(void* ev_start, void* ev_stop);
-/* FP64 FMA throughput probe (TFLOP/s): a DFMA-chain kernel over all SMs,
- * timed with CUDA events on `stream` (synchronising).  Roofline denominator. */
 /* The next fpx_find calls on this thread record `ev` (a cudaEvent_t) on their
  * stream once round 1 is done: from then on only the records of the rest
- * points (fpx_rest_gather) still change.  NULL clears it. */
+ * points (fpx_rest_patch_host) still change.  NULL clears it. */
 int fpx_set_round1_event(void* ev);
 
-/* After fpx_find (same stream, same workspace): packs the records of the
- * points the rest phase settled into rows [k, code, elem, r[dr], dist,
- * values[C]] (doubles) after a header row whose first entry is their count;
- * at most `cap` rows. */
-int fpx_rest_gather(int dr, int C, int64_t n, const void* ws, size_t ws_bytes,
-                    const fpx_mesh_t* m, const int32_t* code, const int32_t* elem,
-                    const double* r, const double* dist, const double* values, int64_t cap,
-                    double* packed, void* stream);
+/* After fpx_find (same stream, same workspace): writes the records of the
+ * points the rest phase settled straight into host record arrays (pinned,
+ * mapped; zero-copy over PCIe).  Enqueue it after any bulk download into the
+ * same arrays. */
+int fpx_rest_patch_host(int dr, int C, int64_t n, const void* ws, size_t ws_bytes,
+                        const fpx_mesh_t* m, const int32_t* code, const int32_t* elem,
+                        const double* r, const double* dist, const double* values,
+                        int32_t* hcode, int32_t* helem, double* hr, double* hdist,
+                        double* hvalues, void* stream);
 
-/* Host side of fpx_rest_gather: scatters the packed rows (host copy) into
- * host record arrays.  Fails if the gather overflowed `cap`. */
-int fpx_scatter_packed_host(int dr, int C, const double* packed, int64_t cap, int32_t* code,
-                            int32_t* elem, double* r, double* dist, double* values);
-
+/* FP64 FMA throughput probe (TFLOP/s): a DFMA-chain kernel over all SMs,
+ * timed with CUDA events on `stream` (synchronising).  Roofline denominator. */
 int fpx_probe_fp64(double* tflops_host, void* stream);
 /* 1 if order N (nodes/axis) is compiled in for (d, dr) */
 int fpx_supported(int d, int dr, int N);

@@ -277,36 +277,29 @@ int fpx_set_round1_event(void* ev) {
   return FPX_OK;
 }
 
-int fpx_rest_gather(int dr, int C, int64_t n, const void* ws, size_t ws_bytes,
-                    const fpx_mesh_t* m, const int32_t* code, const int32_t* elem,
-                    const double* r, const double* dist, const double* values, int64_t cap,
-                    double* packed, void* stream) {
+int fpx_rest_patch_host(int dr, int C, int64_t n, const void* ws, size_t ws_bytes,
+                        const fpx_mesh_t* m, const int32_t* code, const int32_t* elem,
+                        const double* r, const double* dist, const double* values,
+                        int32_t* hcode, int32_t* helem, double* hr, double* hdist,
+                        double* hvalues, void* stream) {
   int rc = check_mesh(m);
   if (rc) return rc;
+  if (!hcode || !helem || !hr || !hdist || (values && !hvalues))
+    return fail(FPX_EINVAL, "rest patch: null host array");
+  // the host arrays must be device-accessible (pinned, hence mapped)
+  const void* hp[5] = {hcode, helem, hr, hdist, values ? (const void*)hvalues : (const void*)hcode};
+  for (const void* p : hp) {
+    cudaPointerAttributes at;
+    FPX_CK(cudaPointerGetAttributes(&at, p));
+    if (at.type != cudaMemoryTypeHost || at.devicePointer != p)
+      return fail(FPX_EINVAL, "rest patch: host array %p is not mapped pinned memory", p);
+  }
   Carver cv(const_cast<void*>(ws), ws_bytes);
   FindWs w;
   w.carve(cv, m->E, n);
-  if (!cv.ok()) return fail(FPX_EINVAL, "rest gather: workspace too small");
-  FPX_LAUNCH(fpx::launch_rest_gather(dr, C, w.nun, w.upts, code, elem, r, dist, values, cap,
-                                     packed, S(stream)));
-  return FPX_OK;
-}
-
-int fpx_scatter_packed_host(int dr, int C, const double* packed, int64_t cap, int32_t* code,
-                            int32_t* elem, double* r, double* dist, double* values) {
-  const int64_t cnt = (int64_t)packed[0];
-  if (cnt > cap) return fail(FPX_EINVAL, "packed rest records: %lld > capacity %lld",
-                             (long long)cnt, (long long)cap);
-  const int W = 4 + dr + C;
-  for (int64_t u = 0; u < cnt; ++u) {
-    const double* row = packed + (u + 1) * W;
-    const int64_t k = (int64_t)row[0];
-    code[k] = (int32_t)row[1];
-    elem[k] = (int32_t)row[2];
-    for (int a = 0; a < dr; ++a) r[k * dr + a] = row[3 + a];
-    dist[k] = row[3 + dr];
-    for (int c = 0; c < C; ++c) values[k * C + c] = row[4 + dr + c];
-  }
+  if (!cv.ok()) return fail(FPX_EINVAL, "rest patch: workspace too small");
+  FPX_LAUNCH(fpx::launch_rest_patch_host(dr, C, n, w.nun, w.upts, code, elem, r, dist, values,
+                                         hcode, helem, hr, hdist, hvalues, S(stream)));
   return FPX_OK;
 }
 
@@ -538,7 +531,7 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
   }
   if (g_prof_stop) FPX_CK(cudaEventRecord(g_prof_stop, st));
   // external record: also a real event node when captured into a CUDA graph
-  if (g_round1_done) FPX_CK(cudaEventRecordWithFlags(g_round1_done, st, cudaEventRecordExternal));
+  if (g_round1_done) FPX_CK(cudaEventRecord(g_round1_done, st));
   // --- rest: remaining candidates of the unresolved points
   FPX_CK(cudaMemsetAsync(w.hist, 0, sizeof(int32_t) * 2 * FPX_HMAX, st));
   g_launches += 2;

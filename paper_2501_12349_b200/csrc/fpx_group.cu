@@ -62,40 +62,40 @@ __global__ void k_scatter_units(int64_t cap, const int64_t* __restrict__ n_dev,
   }
 }
 
-// Records of the points the rest phase settled (upts[0..nun)), packed as
-// rows [k, code, elem, r0..r_{dr-1}, dist, v0..v_{C-1}] after a header row
-// [nun, ...]: the small download that completes an early full download of
-// the round-1 records (engine.find_and_interpolate_host).
-__global__ void k_rest_gather(int dr, int C, const int64_t* __restrict__ nun_dev,
-                              const int32_t* __restrict__ upts, const int32_t* __restrict__ code,
-                              const int32_t* __restrict__ elem, const double* __restrict__ r,
-                              const double* __restrict__ dist, const double* __restrict__ values,
-                              int64_t cap, double* packed) {
+// Zero-copy patch of host records: the rest points' records written straight
+// into mapped pinned host arrays over PCIe, after the bulk download of the
+// round-1 records (engine.find_and_interpolate_host).  No host thread touches
+// those arrays, so the next download into them never snoops a CPU cache.
+__global__ void k_rest_patch_host(int dr, int C, const int64_t* __restrict__ nun_dev,
+                                  const int32_t* __restrict__ upts,
+                                  const int32_t* __restrict__ code,
+                                  const int32_t* __restrict__ elem, const double* __restrict__ r,
+                                  const double* __restrict__ dist,
+                                  const double* __restrict__ values, int32_t* hcode,
+                                  int32_t* helem, double* hr, double* hdist, double* hvalues) {
   const int64_t nun = *nun_dev;
-  const int W = 4 + dr + C;
-  if (blockIdx.x == 0 && threadIdx.x == 0) packed[0] = (double)nun;
-  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < nun && u < cap;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < nun;
        u += (int64_t)gridDim.x * blockDim.x) {
     const int64_t k = upts[u];
-    double* row = packed + (u + 1) * W;
-    row[0] = (double)k;
-    row[1] = (double)code[k];
-    row[2] = (double)elem[k];
-    for (int a = 0; a < dr; ++a) row[3 + a] = r[k * dr + a];
-    row[3 + dr] = dist[k];
-    for (int c = 0; c < C; ++c) row[4 + dr + c] = values ? values[k * C + c] : 0.0;
+    hcode[k] = code[k];
+    helem[k] = elem[k];
+    for (int a = 0; a < dr; ++a) hr[k * dr + a] = r[k * dr + a];
+    hdist[k] = dist[k];
+    if (values)
+      for (int c = 0; c < C; ++c) hvalues[k * C + c] = values[k * C + c];
   }
 }
 
-cudaError_t launch_rest_gather(int dr, int C, const int64_t* nun_dev, const int32_t* upts,
-                               const int32_t* code, const int32_t* elem, const double* r,
-                               const double* dist, const double* values, int64_t cap,
-                               double* packed, cudaStream_t st) {
-  int64_t b = (cap + 255) / 256;
-  if (b > 148 * 8) b = 148 * 8;
+cudaError_t launch_rest_patch_host(int dr, int C, int64_t n_cap, const int64_t* nun_dev,
+                                   const int32_t* upts, const int32_t* code, const int32_t* elem,
+                                   const double* r, const double* dist, const double* values,
+                                   int32_t* hcode, int32_t* helem, double* hr, double* hdist,
+                                   double* hvalues, cudaStream_t st) {
+  int64_t b = (n_cap + 255) / 256;
+  if (b > 148 * 4) b = 148 * 4;
   if (b < 1) b = 1;
-  k_rest_gather<<<(unsigned)b, 256, 0, st>>>(dr, C, nun_dev, upts, code, elem, r, dist, values,
-                                             cap, packed);
+  k_rest_patch_host<<<(unsigned)b, 256, 0, st>>>(dr, C, nun_dev, upts, code, elem, r, dist,
+                                                 values, hcode, helem, hr, hdist, hvalues);
   return cudaGetLastError();
 }
 

@@ -477,65 +477,51 @@ class _SummedStats(Mapping):
 def _host_overlapped(S: EngineSetup, f: Field, x: torch.Tensor, out: dict, ws: dict,
                      sync: bool) -> dict:
     """One find with its download split in two: after round 1 every record
-    except the ~5% the rest phase revisits is final, so the full download runs
-    on a side stream under the rest kernels; the revisited records follow as
-    one small packed gather (fpx_rest_gather) scattered on the host."""
-    L = _C.lib()
+    except the ~5% the rest phase revisits is final, so the bulk download runs
+    on a side stream under the rest kernels; the revisited records are then
+    written straight into the (pinned, mapped) host arrays by a zero-copy
+    kernel (fpx_rest_patch_host).  No host thread writes those arrays: a
+    host-side scatter leaves their lines in the CPU caches, and the next
+    call's download into them then snoops (measured +2 ms per call)."""
     comp = torch.cuda.current_stream(S.device)
     side = _streams(S, 1)[0]
-    n, dr, C = int(x.shape[0]), S.ref_dim, f.components
-    W = 4 + dr + C
-    cap = max(4096, n // 16)
-    if ws.get("packed") is None or ws["packed"].shape[0] < cap + 1 or ws["packed"].shape[1] != W:
-        ws["packed"] = torch.empty((cap + 1, W), dtype=torch.float64, device=S.device)
-        ws["packed_host"] = torch.empty((cap + 1, W), dtype=torch.float64, pin_memory=True)
+    n = int(x.shape[0])
+    if ws.get("r1_event") is None:
         ws["r1_event"] = torch.cuda.Event()
+        ws["r1_event"].record(comp)  # torch creates the CUDA event on first record
     ev = ws["r1_event"]
     ws["x"].copy_(x, non_blocking=True)
-    gkey = (n, f.blocks.data_ptr(), C, out["code"].data_ptr(), out["values"].data_ptr())
+    gkey = (n, f.blocks.data_ptr(), f.components) + tuple(out[k].data_ptr() for k in _REC_KEYS)
     if S.options.graphs and ws.get("graph_key") != gkey:
-        # capture the single-stream device part once per buffers; a replay
-        # costs one launch instead of ~60 (the round-1 event is an external
-        # event node, so the side stream below can wait on it)
-        _host_device_part(S, f, out, ws, ev, cap)  # warm-up outside capture
+        # capture the device part once per buffers; a replay costs one launch
+        # instead of ~60.  The side-stream download forks from the round-1
+        # event inside the capture, so it is an edge of the graph.
+        _host_device_part(S, f, out, ws, ev, side)  # warm-up outside capture
         comp.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            st = _host_device_part(S, f, out, ws, ev, cap)
+            st = _host_device_part(S, f, out, ws, ev, side)
         ws.update(graph=g, graph_key=gkey, graph_stats=st)
     if S.options.graphs:
         ws["graph"].replay()
         st = ws["graph_stats"]
     else:
-        st = _host_device_part(S, f, out, ws, ev, cap)
-    # after round 1 every record but the rest points' is final: download them
-    # on the side stream (copies only: a kernel there would wait for an SM
-    # behind the persistent rest kernels) while the rest kernels run
-    side.wait_event(ev)
-    with torch.cuda.stream(side):
-        for k in ("values", "code", "elem", "r", "dist"):
-            out[k].copy_(ws[k], non_blocking=True)
-    comp.wait_stream(side)
+        st = _host_device_part(S, f, out, ws, ev, side)
     if not sync:
         raise ValueError("the overlapped host path completes on the host (sync=True)")
-    comp.synchronize()  # the host scatter below needs both downloads
-    ph = ws["packed_host"]
-    if int(ph[0, 0]) > cap:  # more revisited points than the gather holds
-        for k in ("values", "code", "elem", "r", "dist"):
-            out[k].copy_(ws[k])
-    else:
-        _C.check(L.fpx_scatter_packed_host(dr, C, ph.data_ptr(), cap, out["code"].data_ptr(),
-                                           out["elem"].data_ptr(), out["r"].data_ptr(),
-                                           out["dist"].data_ptr(), out["values"].data_ptr()),
-                 "fpx_scatter_packed_host")
+    comp.synchronize()
     out["stats"] = st
     return out
 
 
-def _host_device_part(S: EngineSetup, f: Field, out: dict, ws: dict, ev, cap: int):
-    """Single-stream device work of _host_overlapped (capturable): the find
-    (recording `ev` after round 1), the rank fill and rank download, the rest
-    gather and its download."""
+_REC_KEYS = ("values", "code", "elem", "r", "dist", "rank")
+
+
+def _host_device_part(S: EngineSetup, f: Field, out: dict, ws: dict, ev, side):
+    """Device work of _host_overlapped (capturable): the find (recording `ev`
+    after round 1), the bulk record download on `side` from that event on,
+    the rank fill and its download, and, once `side` is joined back, the
+    zero-copy patch of the rest points' records."""
     L = _C.lib()
     n, dr, C = int(ws["x"].shape[0]), S.ref_dim, f.components
     loc = dict(code=ws["code"], elem=ws["elem"], r=ws["r"], dist=ws["dist"], iters=None,
@@ -545,15 +531,25 @@ def _host_device_part(S: EngineSetup, f: Field, out: dict, ws: dict, ev, cap: in
         st = _find_into(S, ws["x"], loc, f)
     finally:
         L.fpx_set_round1_event(None)
+    # after round 1 every record but the rest points' is final: download them
+    # on the side stream (copies only: a kernel there would wait for an SM
+    # behind the persistent rest kernels) while the rest kernels run
+    side.wait_event(ev)
+    with torch.cuda.stream(side):
+        for k in ("values", "code", "elem", "r", "dist"):
+            out[k].copy_(ws[k], non_blocking=True)
     torch.where(loc["code"] != NOT_FOUND, torch.zeros_like(loc["elem"]),
                 torch.full_like(loc["elem"], -1), out=ws["rank"])
     out["rank"].copy_(ws["rank"], non_blocking=True)
+    torch.cuda.current_stream(S.device).wait_stream(side)
     wsf = _workspace(S, n, n)
-    _C.check(L.fpx_rest_gather(dr, C, n, _C.ptr(wsf), wsf.numel(), S.mesh_t, _C.ptr(ws["code"]),
-                               _C.ptr(ws["elem"]), _C.ptr(ws["r"]), _C.ptr(ws["dist"]),
-                               _C.ptr(ws["values"]), cap, _C.ptr(ws["packed"]),
-                               _C.stream_handle()), "fpx_rest_gather")
-    ws["packed_host"].copy_(ws["packed"], non_blocking=True)
+    _C.check(L.fpx_rest_patch_host(dr, C, n, _C.ptr(wsf), wsf.numel(), S.mesh_t,
+                                   _C.ptr(ws["code"]), _C.ptr(ws["elem"]), _C.ptr(ws["r"]),
+                                   _C.ptr(ws["dist"]), _C.ptr(ws["values"]),
+                                   out["code"].data_ptr(), out["elem"].data_ptr(),
+                                   out["r"].data_ptr(), out["dist"].data_ptr(),
+                                   out["values"].data_ptr(), _C.stream_handle()),
+             "fpx_rest_patch_host")
     return st
 
 
@@ -611,7 +607,7 @@ def find_and_interpolate_host(S: EngineSetup, field, x: torch.Tensor, *, chunks:
     chunks = max(1, min(chunks, n))
     bounds = [n * c // chunks for c in range(chunks + 1)]
     keys = ("values", "code", "rank", "elem", "r", "dist")
-    if chunks == 1 and fused:
+    if chunks == 1 and fused and all(out[k].is_pinned() for k in keys):
         return _host_overlapped(S, f, x, out, ws, sync)
     if chunks == 1:  # upload, find, download in order on the caller's stream
         ws["x"].copy_(x, non_blocking=True)

@@ -250,7 +250,12 @@ def test_host_pipeline_matches_device(chunks):
     field = toolkit.analytic_field("smooth", mesh)
     x = toolkit.uniform_points(20000, 3, seed=5, lo=-0.05, hi=1.05)
     vals, rec = engine.find_and_interpolate(S, field, torch.from_numpy(x).cuda())
-    out = engine.find_and_interpolate_host(S, field, torch.from_numpy(x), chunks=chunks)
+    # a call on other points first, into the same host buffers: the second
+    # call replays the captured device part on new inputs, and every record
+    # it returns must be of those inputs
+    x0 = toolkit.uniform_points(20000, 3, seed=6, lo=-0.05, hi=1.05)
+    out = engine.find_and_interpolate_host(S, field, torch.from_numpy(x0), chunks=chunks)
+    out = engine.find_and_interpolate_host(S, field, torch.from_numpy(x), chunks=chunks, out=out)
     code = rec.code.cpu()
     assert torch.equal(out["code"], code)
     assert torch.equal(out["rank"], rec.rank.cpu())
