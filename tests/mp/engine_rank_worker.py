@@ -14,17 +14,24 @@ sys.path.insert(0, ROOT)
 from paper_2501_12349_b200 import engine, toolkit, transport  # noqa: E402
 
 
+def mesh_of(name):
+    if name == "refined":  # SPEC acceptance 7: refined box, 8^3 -> 16^3 = 4096 hexes
+        return toolkit.generate_mesh(toolkit.MeshSpec("refined-box", 3, 4, 8, 0.02, 1))
+    return toolkit.kershaw_mesh(8, 4)
+
+
 def main():
     rank, size = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     out = sys.argv[1]
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=size)
     G = transport.RankGroup.from_torch()
-    mesh = toolkit.kershaw_mesh(8, 4)
+    mesh = mesh_of(os.environ.get("FPX_TEST_MESH", "kershaw"))
     field = toolkit.analytic_field("smooth", mesh)
     a, b = toolkit.partition_blocks(mesh.num_elements, size)[rank]
     S = engine.setup(torch.from_numpy(mesh.nodes[a:b]).cuda(), 4, 3, group=G, elem_offset=a)
-    x = toolkit.uniform_points(20000, 3, seed=50 + rank, lo=-0.03, hi=1.03)
+    npts = int(os.environ.get("FPX_TEST_NPTS", "20000"))
+    x = toolkit.uniform_points(npts, 3, seed=50 + rank, lo=-0.03, hi=1.03)
     F = engine.Field(torch.from_numpy(field[a:b]).cuda(), 4)
     vals, rec = engine.find_and_interpolate(S, F, x)
     v2 = engine.interpolate(S, F, rec)

@@ -24,19 +24,25 @@ def _port():
     return p
 
 
-def test_two_rank_engine_matches_single_rank(tmp_path):
-    size, port = 2, _port()
+@pytest.mark.parametrize("meshname,size,npts", [("kershaw", 2, 20000),
+                                                 ("refined", 4, 25000)])
+def test_multirank_engine_matches_single_rank(tmp_path, meshname, size, npts):
+    # refined/4: SPEC acceptance 7 (refined box >= 4096 elements, 10^5 points
+    # over the ranks, records and values identical to the single-rank run)
+    port = _port()
     procs, outs = [], []
     for rk in range(size):
         env = dict(os.environ, RANK=str(rk), WORLD_SIZE=str(size), MASTER_ADDR="127.0.0.1",
-                   MASTER_PORT=str(port))
+                   MASTER_PORT=str(port), FPX_TEST_MESH=meshname, FPX_TEST_NPTS=str(npts))
         outs.append(str(tmp_path / f"r{rk}.npz"))
         procs.append(subprocess.Popen([sys.executable, WORKER, outs[-1]], env=env,
                                       stdout=subprocess.PIPE, stderr=subprocess.STDOUT))
     for p in procs:
         o, _ = p.communicate(timeout=600)
         assert p.returncode == 0, o.decode()[-3000:]
-    mesh = toolkit.kershaw_mesh(8, 4)
+    sys.path.insert(0, os.path.dirname(WORKER))
+    from engine_rank_worker import mesh_of
+    mesh = mesh_of(meshname)
     field = toolkit.analytic_field("smooth", mesh)
     S = engine.setup(mesh)
     blocks = toolkit.partition_blocks(mesh.num_elements, size)
