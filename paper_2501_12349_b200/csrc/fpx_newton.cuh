@@ -239,6 +239,9 @@ __device__ __forceinline__ void eval_state_rt(const double* __restrict__ sX,
                                            const double* __restrict__ z,
                                            const double* __restrict__ scale, const double* r,
                                            const double* xs, NState& S, double* sb, const bool W2) {
+  // the second-derivative terms are always accumulated (a select per FMA
+  // cost more issue slots than the ~10% evaluations that do not need them);
+  // W2 only gates their use in S.Q
   // LAY 0: geometry staged in shared memory, rows padded to NP;
   // LAY 1: read in place from global memory ([d][N^dr]);
   // LAY 2: a per-lane shared slot holding [d][N^dr] unpadded.
@@ -257,7 +260,7 @@ __device__ __forceinline__ void eval_state_rt(const double* __restrict__ sX,
     for (int j = 0; j < N; ++j) {
       sb[(((a - 1) * 3 + 0) * N + j) * FPX_WARP] = v[j];
       sb[(((a - 1) * 3 + 1) * N + j) * FPX_WARP] = g[j];
-      if (W2) sb[(((a - 1) * 3 + 2) * N + j) * FPX_WARP] = h[j];
+      sb[(((a - 1) * 3 + 2) * N + j) * FPX_WARP] = h[j];
     }
   }
 #define SB(a, kind, j) sb[((((a)-1) * 3 + (kind)) * N + (j)) * FPX_WARP]
@@ -291,18 +294,18 @@ __device__ __forceinline__ void eval_state_rt(const double* __restrict__ sX,
             else p = make_double2(row[i], 0.0);
             s0 = fma(p.x, v0[i], s0);
             s1 = fma(p.x, g0[i], s1);
-            if (W2) s2 = fma(p.x, h0[i], s2);
+            s2 = fma(p.x, h0[i], s2);
             if (i + 1 < N) {
               s0 = fma(p.y, v0[i + 1], s0);
               s1 = fma(p.y, g0[i + 1], s1);
-              if (W2) s2 = fma(p.y, h0[i + 1], s2);
+              s2 = fma(p.y, h0[i + 1], s2);
             }
           }
           const double vj = SB(1, 0, j), gj = SB(1, 1, j);
           t00 = fma(s0, vj, t00);
           t10 = fma(s1, vj, t10);
           t01 = fma(s0, gj, t01);
-          if (W2) {
+          {
             const double hj = SB(1, 2, j);
             t20 = fma(s2, vj, t20);
             t11 = fma(s1, gj, t11);
@@ -314,7 +317,7 @@ __device__ __forceinline__ void eval_state_rt(const double* __restrict__ sX,
         G[0] = fma(t10, vk, G[0]);
         G[1] = fma(t01, vk, G[1]);
         G[2] = fma(t00, gk, G[2]);
-        if (W2) {
+        {
           const double hk = SB(2, 2, k);
           H2[0] = fma(t20, vk, H2[0]);
           H2[1] = fma(t02, vk, H2[1]);
@@ -334,13 +337,13 @@ __device__ __forceinline__ void eval_state_rt(const double* __restrict__ sX,
           const double p = row[i];
           s0 = fma(p, v0[i], s0);
           s1 = fma(p, g0[i], s1);
-          if (W2) s2 = fma(p, h0[i], s2);
+          s2 = fma(p, h0[i], s2);
         }
         const double vj = SB(1, 0, j), gj = SB(1, 1, j);
         xv = fma(s0, vj, xv);
         G[0] = fma(s1, vj, G[0]);
         G[1] = fma(s0, gj, G[1]);
-        if (W2) {
+        {
           const double hj = SB(1, 2, j);
           H2[0] = fma(s2, vj, H2[0]);
           H2[1] = fma(s0, hj, H2[1]);
@@ -353,7 +356,7 @@ __device__ __forceinline__ void eval_state_rt(const double* __restrict__ sX,
         const double p = Xc[i];
         xv = fma(p, v0[i], xv);
         G[0] = fma(p, g0[i], G[0]);
-        if (W2) H2[0] = fma(p, h0[i], H2[0]);
+        H2[0] = fma(p, h0[i], H2[0]);
       }
     }
 #undef SB
