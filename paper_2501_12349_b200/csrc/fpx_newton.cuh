@@ -1145,22 +1145,22 @@ __device__ __forceinline__ int seed_batch(const unsigned* js, int cnt, const dou
       }
     }
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-    for (int s = 0; s < 4; ++s) {
-      const double ob = __shfl_xor_sync(FPX_FULL, best[s], o);
-      const int oi = __shfl_xor_sync(FPX_FULL, bi[s], o);
-      if (ob < best[s] || (ob == best[s] && oi < bi[s])) {
-        best[s] = ob;
-        bi[s] = oi;
-      }
-    }
-  }
+  // warp argmin of (distance, index): distances are non-negative doubles, so
+  // their bit patterns order like the values; three redux.sync minima (high
+  // word, low word among the high-word winners, index among the exact ties)
   int mine = -1;
 #pragma unroll
-  for (int s = 0; s < 4; ++s)
-    if (s < cnt && (unsigned)lane == js[s]) mine = bi[s];
+  for (int s = 0; s < 4; ++s) {
+    if (s < cnt) {  // cnt is warp-uniform
+      const unsigned long long b = (unsigned long long)__double_as_longlong(best[s]);
+      const unsigned hi = (unsigned)(b >> 32), lo = (unsigned)b;
+      const bool c1 = hi == __reduce_min_sync(FPX_FULL, hi);
+      const unsigned ml = __reduce_min_sync(FPX_FULL, c1 ? lo : 0xffffffffu);
+      const bool c2 = c1 && lo == ml;
+      const unsigned mi = __reduce_min_sync(FPX_FULL, c2 ? (unsigned)bi[s] : 0xffffffffu);
+      if ((unsigned)lane == js[s]) mine = (int)mi;
+    }
+  }
   return mine;
 }
 
