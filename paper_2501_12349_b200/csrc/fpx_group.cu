@@ -66,6 +66,19 @@ __global__ void k_scatter_units(int64_t cap, const int64_t* __restrict__ n_dev,
 // into mapped pinned host arrays over PCIe, after the bulk download of the
 // round-1 records (engine.find_and_interpolate_host).  No host thread touches
 // those arrays, so the next download into them never snoops a CPU cache.
+// dst[0..len) = src[0..len) with 16-byte stores where dst allows: each store
+// is one PCIe write, and the write count bounds k_rest_patch_host
+__device__ __forceinline__ void store_row(double* dst, const double* src, int len) {
+  int a = 0;
+  if (len >= 2 && (reinterpret_cast<uintptr_t>(dst) & 15)) {
+    dst[0] = src[0];
+    a = 1;
+  }
+  for (; a + 1 < len; a += 2)
+    *reinterpret_cast<double2*>(dst + a) = make_double2(src[a], src[a + 1]);
+  if (a < len) dst[a] = src[a];
+}
+
 __global__ void k_rest_patch_host(int dr, int C, const int64_t* __restrict__ nun_dev,
                                   const int32_t* __restrict__ upts,
                                   const int32_t* __restrict__ code,
@@ -79,10 +92,9 @@ __global__ void k_rest_patch_host(int dr, int C, const int64_t* __restrict__ nun
     const int64_t k = upts[u];
     hcode[k] = code[k];
     helem[k] = elem[k];
-    for (int a = 0; a < dr; ++a) hr[k * dr + a] = r[k * dr + a];
+    store_row(hr + k * dr, r + k * dr, dr);
     hdist[k] = dist[k];
-    if (values)
-      for (int c = 0; c < C; ++c) hvalues[k * C + c] = values[k * C + c];
+    if (values) store_row(hvalues + k * C, values + k * C, C);
   }
 }
 
