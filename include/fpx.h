@@ -112,6 +112,7 @@ typedef struct fpx_mesh_t {
 #define FPX_STAT_REST_WARP_EVALS 12 /* rest kernel: map evaluations issued per warp */
 #define FPX_STAT_REST_W2_EVALS 13   /* ... of which with second derivatives */
 #define FPX_STAT_REST_LANE_EVALS 14 /* ... summed over the lanes that were iterating */
+#define FPX_STAT_REDO 15            /* candidates stopped by the abort rule (redo list) */
 #define FPX_STATS_LEN 16
 
 int fpx_abi_version(void);

@@ -19,7 +19,7 @@ ABI_VERSION = 3
 INTERIOR, BORDER, NOT_FOUND = 0, 1, 2
 STAT_NAMES = ["points", "box_tests", "newton", "iters", "rest_points", "r1_warp_evals",
               "r1_w2_evals", "evals", "newton_r1", "iters_r1", "evals_r1", "r1_items",
-              "rest_warp_evals", "rest_w2_evals", "rest_lane_evals", "spare"]
+              "rest_warp_evals", "rest_w2_evals", "rest_lane_evals", "redo"]
 STATS_LEN = len(STAT_NAMES)
 FREC = 32            # FPX_FREC: doubles per element filter record
 

@@ -181,9 +181,11 @@ struct FindWs {
   }
 };
 
-__global__ void k_find_totals(const int64_t* __restrict__ nun, int64_t* stats, int64_t n) {
+__global__ void k_find_totals(const int64_t* __restrict__ nun, const int64_t* __restrict__ nredo,
+                              int64_t* stats, int64_t n) {
   stats[FPX_STAT_POINTS] = n;
   stats[FPX_STAT_ROUND2_POINTS] = *nun;
+  stats[FPX_STAT_REDO] = *nredo;
 }
 
 
@@ -547,7 +549,7 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
                                    iters,
                                    field, C, values, w.counter, stats, st));
   g_launches += 1;
-  k_find_totals<<<1, 1, 0, st>>>(w.nun, stats, n);
+  k_find_totals<<<1, 1, 0, st>>>(w.nun, w.nredo, stats, n);
   FPX_CK(cudaGetLastError());
   return FPX_OK;
 }
