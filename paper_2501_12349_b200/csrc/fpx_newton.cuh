@@ -1040,6 +1040,19 @@ __device__ __forceinline__ bool mbar_test(uint64_t* mb, unsigned parity) {
   return ok != 0;
 }
 
+// Warp argmin of (d, i) over all lanes, d >= 0 (a distance; +inf allowed):
+// non-negative doubles order like their bit patterns, so three redux.sync
+// minima suffice -- the high word, the low word among the high-word winners,
+// the index among the exact ties.  Every lane gets the winning index.
+__device__ __forceinline__ int warp_argmin(double d, int i) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(d);
+  const unsigned hi = (unsigned)(b >> 32), lo = (unsigned)b;
+  const bool c1 = hi == __reduce_min_sync(FPX_FULL, hi);
+  const unsigned ml = __reduce_min_sync(FPX_FULL, c1 ? lo : 0xffffffffu);
+  const bool c2 = c1 && lo == ml;
+  return (int)__reduce_min_sync(FPX_FULL, c2 ? (unsigned)i : 0xffffffffu);
+}
+
 // Best-first ranked candidate lists of the rest points: the passing
 // entries of the hash list sorted by (v, e), FPX_RK per point
 // kept; beyond that the rest kernel scans the list itself.
@@ -1047,8 +1060,8 @@ __device__ __forceinline__ bool mbar_test(uint64_t* mb, unsigned parity) {
 template <int D>
 __global__ void __launch_bounds__(128)
     k_rest_lists(fpx_mesh_t m, const double* __restrict__ x, const int64_t* __restrict__ nun_dev,
-                 const int32_t* __restrict__ upts, int32_t* clist, int32_t* cnum, int32_t* nps,
-                 int32_t* hist) {
+                 const int32_t* __restrict__ upts, int32_t* clist, int16_t* cseed, int32_t* cnum,
+                 int32_t* nps, int32_t* hist) {
   // warp per rest point: lanes test the hash-list entries (one filter record
   // each), (v, e) of the passing ones go to shared memory, and the rank of
   // each is the number of passing entries before it in (v, e) order
@@ -1104,6 +1117,59 @@ __global__ void __launch_bounds__(128)
       atomicAdd(&hist[np < FPX_HMAX - 1 ? np : FPX_HMAX - 1], 1);
     }
     __syncwarp();
+    // Nearest node (the D7 seed) of every listed candidate of rank >= 1,
+    // stored for the rest kernel (cseed; -1 = not listed, it seeds itself).
+    // Fully listed points with several rest candidates are then reordered by
+    // that distance (ties keep the (v, e) order): the rest phase stops a
+    // point's other candidates once one is INTERIOR, so the owner should
+    // come early, and the affine best-first value ranks curved elements
+    // poorly (cfg-2: the owner was rank 1 for 54% of the rest points, 62%
+    // after the reorder).
+    const int nl = qe - qs <= L ? (np < FPX_RK ? np : FPX_RK) : 0;
+    if (lane < FPX_RK && (lane == 0 || lane >= nl)) cseed[u * FPX_RK + lane] = -1;
+    if (nl > 1) {
+      const int K = m.dr == 1 ? m.N : m.dr == 2 ? m.N * m.N : m.N * m.N * m.N;
+      for (int j = 1; j < nl; ++j) {
+        const double* X = m.nodes + (int64_t)clist[u * FPX_RK + j] * D * K;
+        double bd = INFINITY;
+        int bt = 0x7fffffff;
+        for (int t = lane; t < K; t += FPX_WARP) {
+          double dd = 0.0;
+#pragma unroll
+          for (int c = 0; c < D; ++c) {
+            const double tt = __dsub_rn(xs[c], __ldg(X + c * K + t));
+            dd = __fma_rn(tt, tt, dd);
+          }
+          if (dd < bd) {
+            bd = dd;
+            bt = t;
+          }
+        }
+        const int w = warp_argmin(bd, bt);  // node index; lane w % 32 holds it
+        bd = __shfl_sync(FPX_FULL, bd, w % FPX_WARP);
+        if (lane == 0) {
+          s_v[warp][j] = bd;
+          s_e[warp][j] = w;
+        }
+      }
+      __syncwarp();
+      if (lane >= 1 && lane < nl) {
+        const int e2 = clist[u * FPX_RK + lane];
+        const double dj = s_v[warp][lane];
+        int rk = lane;
+        if (np <= FPX_RK && np > 2) {  // the whole passing set is listed
+          rk = 1;
+          for (int j = 1; j < nl; ++j) {
+            const double di = s_v[warp][j];
+            rk += (di < dj || (di == dj && j < lane)) ? 1 : 0;
+          }
+        }
+        __syncwarp(__activemask());
+        clist[u * FPX_RK + rk] = e2;
+        cseed[u * FPX_RK + rk] = (int16_t)s_e[warp][lane];
+      }
+      __syncwarp();
+    }
   }
 }
 
@@ -1145,20 +1211,12 @@ __device__ __forceinline__ int seed_batch(const unsigned* js, int cnt, const dou
       }
     }
   }
-  // warp argmin of (distance, index): distances are non-negative doubles, so
-  // their bit patterns order like the values; three redux.sync minima (high
-  // word, low word among the high-word winners, index among the exact ties)
   int mine = -1;
 #pragma unroll
   for (int s = 0; s < 4; ++s) {
     if (s < cnt) {  // cnt is warp-uniform
-      const unsigned long long b = (unsigned long long)__double_as_longlong(best[s]);
-      const unsigned hi = (unsigned)(b >> 32), lo = (unsigned)b;
-      const bool c1 = hi == __reduce_min_sync(FPX_FULL, hi);
-      const unsigned ml = __reduce_min_sync(FPX_FULL, c1 ? lo : 0xffffffffu);
-      const bool c2 = c1 && lo == ml;
-      const unsigned mi = __reduce_min_sync(FPX_FULL, c2 ? (unsigned)bi[s] : 0xffffffffu);
-      if ((unsigned)lane == js[s]) mine = (int)mi;
+      const int mi = warp_argmin(best[s], bi[s]);
+      if ((unsigned)lane == js[s]) mine = mi;
     }
   }
   return mine;
@@ -1697,11 +1755,11 @@ template <int D, int DR, int N>
 __global__ void __launch_bounds__(128, 2)
     k_rest_l1(fpx_mesh_t m, const double* __restrict__ x, const int64_t* __restrict__ nun_dev,
               const int32_t* __restrict__ upts, const int32_t* __restrict__ clist,
-              const int32_t* __restrict__ cnum, const int32_t* __restrict__ nps,
-              const int32_t* __restrict__ perm, const int64_t* __restrict__ cum,
-              const int32_t* __restrict__ maxnp_dev, const int32_t* __restrict__ best,
-              const int4* __restrict__ pairs, int64_t pair_cap, const int64_t* __restrict__ npairs,
-              int abortable, int4* redo, int64_t* nredo, int32_t* found, int32_t* lock,
+              const int16_t* __restrict__ cseed, const int32_t* __restrict__ cnum,
+              const int32_t* __restrict__ nps, const int32_t* __restrict__ perm,
+              const int64_t* __restrict__ cum, const int32_t* __restrict__ maxnp_dev,
+              const int32_t* __restrict__ best, const int4* __restrict__ pairs, int64_t pair_cap,
+              const int64_t* __restrict__ npairs, int abortable, int4* redo, int64_t* nredo, int32_t* found, int32_t* lock,
               int32_t* code, int32_t* elem, double* r, double* dist, int32_t* iters,
               int64_t* counter, int64_t* stats) {
   using L = Lay<D, DR, N>;
@@ -1726,6 +1784,13 @@ __global__ void __launch_bounds__(128, 2)
   // in full)
   const bool redo_pass = maxnp_dev == nullptr;
   const int64_t gmax = redo_pass && *npairs > pair_cap ? pair_cap : *npairs;
+#ifdef FPX_DIAG
+  // development counters (FPX_DIAG builds; the caller allocates 16 + 80
+  // stats): pair outcomes by rank bucket -- [pass*16 + kind*5 + rank]
+  // counts, +32 their iterations; kind 0 stopped by the found flag,
+  // 1 INTERIOR, 2 other; 64.. aborted by R2 (+5 iterations)
+  int64_t* g_diag_base = stats + 16;
+#endif
   int64_t s_newton = 0, s_iters = 0, nev = 0, nev2 = 0, nlev = 0;
   int64_t u = 0, k = 0;
   double xs[3] = {0.0, 0.0, 0.0};
@@ -1806,7 +1871,22 @@ __global__ void __launch_bounds__(128, 2)
       if (en < 0) continue;
       e = en;
       cur.y = en;
-      phase = 1;  // needs its seed
+      const int sd = rank < FPX_RK ? cseed[u * FPX_RK + rank] : -1;
+      if (sd < 0) {
+        phase = 1;  // needs its seed
+        continue;
+      }
+      // seed found by k_rest_lists (the same D7 node search)
+      rc[0] = z[sd % N];
+      rc[1] = DR > 1 ? z[(sd / N) % N] : 0.0;
+      rc[2] = DR > 2 ? z[sd / (N * N)] : 0.0;
+#pragma unroll
+      for (int a = 0; a < 3; ++a) rn[a] = rc[a];
+      first = true;
+      held_prev = false;
+      it = 0;
+      alpha = P.alpha0;
+      phase = 3;
     }
     // seeds (D7) of the lanes that just got a pair, 4 at a time: the warp
     // reads each candidate's nodes with coalesced loads
@@ -1853,16 +1933,8 @@ __global__ void __launch_bounds__(128, 2)
         }
       }
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-        for (int s2 = 0; s2 < 4; ++s2) {
-          const double ob = __shfl_xor_sync(FPX_FULL, bst[s2], o);
-          const int oi = __shfl_xor_sync(FPX_FULL, bi[s2], o);
-          if (ob < bst[s2] || (ob == bst[s2] && oi < bi[s2])) {
-            bst[s2] = ob;
-            bi[s2] = oi;
-          }
-        }
+      for (int s2 = 0; s2 < 4; ++s2) {
+        if (s2 < cnt) bi[s2] = warp_argmin(bst[s2], bi[s2]);  // cnt is warp-uniform
       }
 #pragma unroll
       for (int s2 = 0; s2 < 4; ++s2) {
@@ -1912,6 +1984,11 @@ __global__ void __launch_bounds__(128, 2)
     if (!done && *(volatile int32_t*)&found[u]) {
       // another candidate of this point was INTERIOR meanwhile: its record
       // is final (an INTERIOR is unique up to shared faces), stop this one
+#ifdef FPX_DIAG
+      { const int rb = cur.w < 4 ? cur.w : 4;
+        atomicAdd((unsigned long long*)&g_diag_base[(redo_pass ? 16 : 0) + rb], 1ull);
+        atomicAdd((unsigned long long*)&g_diag_base[32 + (redo_pass ? 16 : 0) + rb], (unsigned long long)it); }
+#endif
       s_newton += 1;
       s_iters += it;
       phase = 0;
@@ -1940,6 +2017,11 @@ __global__ void __launch_bounds__(128, 2)
       else stash_state(stash, st);
     }
     if (done && aborted) {
+#ifdef FPX_DIAG
+      { const int rb = cur.w < 4 ? cur.w : 4;
+        atomicAdd((unsigned long long*)&g_diag_base[64 + rb], 1ull);
+        atomicAdd((unsigned long long*)&g_diag_base[64 + 5 + rb], (unsigned long long)it); }
+#endif
       s_newton += 1;
       s_iters += it;
       phase = 0;
@@ -1966,6 +2048,12 @@ __global__ void __launch_bounds__(128, 2)
         for (int a = 0; a < DR; ++a) r[k * DR + a] = rc[a];
       }
       if (iters) iters[k] += it;
+#ifdef FPX_DIAG
+      { const int rb = cur.w < 4 ? cur.w : 4;
+        const int kind = cd == kInterior ? 5 : 10;
+        atomicAdd((unsigned long long*)&g_diag_base[(redo_pass ? 16 : 0) + kind + rb], 1ull);
+        atomicAdd((unsigned long long*)&g_diag_base[32 + (redo_pass ? 16 : 0) + kind + rb], (unsigned long long)it); }
+#endif
       if (cd == kInterior) found[u] = 1;
       __threadfence();
       atomicExch(&lock[u], 0);
@@ -2562,7 +2650,8 @@ struct Rest {
   static constexpr int WPB = WPB0 > 16 ? 16 : (WPB0 < 1 ? 1 : WPB0);
   static cudaError_t run(const fpx_mesh_t& m, const double* x, int64_t nun_cap,
                          const int64_t* nun_dev, const int32_t* upts, const int32_t* clist,
-                         const int32_t* cnum, const int32_t* nps, const int32_t* perm,
+                         const int16_t* cseed, const int32_t* cnum, const int32_t* nps,
+                         const int32_t* perm,
                          const int64_t* cum, const int32_t* maxnp, const int32_t* best,
                          const int4* pairs, const int64_t* npairs, int4* redo, int64_t* nredo,
                          int32_t* found, int32_t* lock, int32_t* code, int32_t* elem, double* r,
@@ -2590,10 +2679,11 @@ struct Rest {
         const char* v = getenv("FPX_ABORT");
         return !(v && v[0] == '0');
       }();
-      fn<<<blocks, threads, smem, st>>>(m, x, nun_dev, upts, clist, cnum, nps, perm, cum, maxnp,
-                                        best, pairs, cap, npairs, abort_pass ? 1 : 0, redo, nredo,
-                                        found, lock, code, elem, r, dist, iters, counter, stats);
-      fn<<<blocks, threads, smem, st>>>(m, x, nun_dev, upts, clist, cnum, nps, perm, cum,
+      fn<<<blocks, threads, smem, st>>>(m, x, nun_dev, upts, clist, cseed, cnum, nps, perm, cum,
+                                        maxnp, best, pairs, cap, npairs, abort_pass ? 1 : 0, redo,
+                                        nredo, found, lock, code, elem, r, dist, iters, counter,
+                                        stats);
+      fn<<<blocks, threads, smem, st>>>(m, x, nun_dev, upts, clist, cseed, cnum, nps, perm, cum,
                                           nullptr, best, redo, cap, nredo, 0, nullptr, nullptr,
                                           found, lock, code, elem, r, dist, iters, counter + 1,
                                           stats);
@@ -2621,13 +2711,15 @@ struct Rest {
   }
   static cudaError_t lists(const fpx_mesh_t& m, const double* x, int64_t nun_cap,
                            const int64_t* nun_dev, const int32_t* upts, int32_t* clist,
+                           int16_t* cseed,
                            int32_t* cnum, int32_t* nps, int32_t* hist, int32_t* bstart,
                            int32_t* bcur, int32_t* perm, int64_t* cum, int32_t* maxnp,
                            int4* pairs, int64_t* npairs, cudaStream_t st) {
     int64_t b = (nun_cap + 3) / 4;
     if (b > 148 * 16) b = 148 * 16;
     if (b < 1) b = 1;
-    k_rest_lists<D><<<(unsigned)b, 128, 0, st>>>(m, x, nun_dev, upts, clist, cnum, nps, hist);
+    k_rest_lists<D><<<(unsigned)b, 128, 0, st>>>(m, x, nun_dev, upts, clist, cseed, cnum, nps,
+                                                 hist);
     k_rest_order<<<1, FPX_HMAX, 0, st>>>(hist, bstart, cum, maxnp, npairs);
     int64_t b2 = (nun_cap + 255) / 256;
     if (b2 > 148 * 8) b2 = 148 * 8;

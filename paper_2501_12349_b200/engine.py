@@ -361,12 +361,15 @@ def _find_local(S: EngineSetup, x: torch.Tensor, field: Field | None = None,
     return out, _SummedStats(parts)
 
 
+_DIAG_LEN = int(os.environ.get("FPX_DIAG_LEN", "0"))  # development builds (-DFPX_DIAG): 80
+
+
 def _find_into(S: EngineSetup, x: torch.Tensor, out: dict, field: Field | None,
                slot: int = 0) -> DeviceStats:
     """fpx_find on the current stream writing into caller-provided device
     slices (x contiguous); `slot` selects the workspace."""
     n = int(x.shape[0])
-    stats = torch.zeros(_C.STATS_LEN, dtype=torch.int64, device=S.device)
+    stats = torch.zeros(_C.STATS_LEN + _DIAG_LEN, dtype=torch.int64, device=S.device)
     if n == 0:
         return DeviceStats(stats)
     blocks, C = (field.blocks, int(field.blocks.shape[1])) if field is not None else (None, 0)
