@@ -1053,6 +1053,15 @@ __device__ __forceinline__ int warp_argmin(double d, int i) {
   return (int)__reduce_min_sync(FPX_FULL, c2 ? (unsigned)i : 0xffffffffu);
 }
 
+// Warp minimum of a non-negative double (bit patterns order like the values).
+__device__ __forceinline__ double warp_min_nonneg(double d) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(d);
+  const unsigned hi = __reduce_min_sync(FPX_FULL, (unsigned)(b >> 32));
+  const unsigned lo =
+      __reduce_min_sync(FPX_FULL, (unsigned)(b >> 32) == hi ? (unsigned)b : 0xffffffffu);
+  return __longlong_as_double((long long)(((unsigned long long)hi << 32) | lo));
+}
+
 // Best-first ranked candidate lists of the rest points: the passing
 // entries of the hash list sorted by (v, e), FPX_RK per point
 // kept; beyond that the rest kernel scans the list itself.
@@ -1131,7 +1140,7 @@ __global__ void __launch_bounds__(128)
       const int K = m.dr == 1 ? m.N : m.dr == 2 ? m.N * m.N : m.N * m.N * m.N;
       for (int j = 1; j < nl; ++j) {
         const double* X = m.nodes + (int64_t)clist[u * FPX_RK + j] * D * K;
-        double bd = INFINITY;
+        double bd = INFINITY, b2 = INFINITY;
         int bt = 0x7fffffff;
         for (int t = lane; t < K; t += FPX_WARP) {
           double dd = 0.0;
@@ -1141,27 +1150,36 @@ __global__ void __launch_bounds__(128)
             dd = __fma_rn(tt, tt, dd);
           }
           if (dd < bd) {
+            b2 = bd;
             bd = dd;
             bt = t;
+          } else if (dd < b2) {
+            b2 = dd;
           }
         }
         const int w = warp_argmin(bd, bt);  // node index; lane w % 32 holds it
-        bd = __shfl_sync(FPX_FULL, bd, w % FPX_WARP);
+        const bool own = lane == w % FPX_WARP;
+        const double d1 = __shfl_sync(FPX_FULL, bd, w % FPX_WARP);
+        // second-nearest node distance: breaks the ties of a shared (face,
+        // edge, corner) nearest node in favour of the element whose own
+        // nodes lie closer
+        const double d2 = warp_min_nonneg(own ? b2 : bd);
         if (lane == 0) {
-          s_v[warp][j] = bd;
+          s_v[warp][j] = d1;
+          s_v[warp][FPX_RK + j] = d2;
           s_e[warp][j] = w;
         }
       }
       __syncwarp();
       if (lane >= 1 && lane < nl) {
         const int e2 = clist[u * FPX_RK + lane];
-        const double dj = s_v[warp][lane];
+        const double dj = s_v[warp][lane], dj2 = s_v[warp][FPX_RK + lane];
         int rk = lane;
         if (np <= FPX_RK && np > 2) {  // the whole passing set is listed
           rk = 1;
           for (int j = 1; j < nl; ++j) {
-            const double di = s_v[warp][j];
-            rk += (di < dj || (di == dj && j < lane)) ? 1 : 0;
+            const double di = s_v[warp][j], di2 = s_v[warp][FPX_RK + j];
+            rk += (di < dj || (di == dj && (di2 < dj2 || (di2 == dj2 && j < lane)))) ? 1 : 0;
           }
         }
         __syncwarp(__activemask());
