@@ -1132,7 +1132,7 @@ __global__ void __launch_bounds__(128)
     // that distance (ties keep the (v, e) order): the rest phase stops a
     // point's other candidates once one is INTERIOR, so the owner should
     // come early, and the affine best-first value ranks curved elements
-    // poorly (cfg-2: the owner was rank 1 for 54% of the rest points, 62%
+    // poorly (cfg-2: the owner was rank 1 for 54% of the rest points, 64%
     // after the reorder).
     const int nl = qe - qs <= L ? (np < FPX_RK ? np : FPX_RK) : 0;
     if (lane < FPX_RK && (lane == 0 || lane >= nl)) cseed[u * FPX_RK + lane] = -1;
