@@ -242,18 +242,32 @@ def test_surface_mesh_find_eval(kind):
     assert np.all(code[np.abs(off) > 1e-8] == 1)
 
 
-@pytest.mark.parametrize("chunks", [1, 3])
-def test_host_pipeline_matches_device(chunks):
-    # find_and_interpolate_host (chunked, overlapped copies) == the device API
-    mesh = toolkit.kershaw_mesh(8, 4)
+def _host_case(kind):
+    if kind == "hex":
+        mesh = toolkit.kershaw_mesh(8, 4)
+        pts = lambda seed: toolkit.uniform_points(20000, 3, seed=seed, lo=-0.05, hi=1.05)
+    elif kind == "quad":
+        mesh = toolkit.box_mesh(2, 12, 5)
+        pts = lambda seed: toolkit.uniform_points(20000, 2, seed=seed, lo=-0.05, hi=1.05)
+    else:  # surface (d_r < d): the zero-copy patch with dr = 2 in 3D
+        mesh = toolkit.sphere_mesh(4, 4)
+        pts = lambda seed: toolkit.surface_points(mesh, 20000, seed=seed)[0]
+    return mesh, pts
+
+
+@pytest.mark.parametrize("chunks,kind", [(1, "hex"), (3, "hex"), (1, "quad"), (1, "surface")])
+def test_host_pipeline_matches_device(chunks, kind):
+    # find_and_interpolate_host (overlapped copies, zero-copy patch of the
+    # rest records; or chunked) == the device API
+    mesh, pts = _host_case(kind)
     S = engine.setup(mesh)
     field = toolkit.analytic_field("smooth", mesh)
-    x = toolkit.uniform_points(20000, 3, seed=5, lo=-0.05, hi=1.05)
+    x = pts(5)
     vals, rec = engine.find_and_interpolate(S, field, torch.from_numpy(x).cuda())
     # a call on other points first, into the same host buffers: the second
     # call replays the captured device part on new inputs, and every record
     # it returns must be of those inputs
-    x0 = toolkit.uniform_points(20000, 3, seed=6, lo=-0.05, hi=1.05)
+    x0 = pts(6)
     out = engine.find_and_interpolate_host(S, field, torch.from_numpy(x0), chunks=chunks)
     out = engine.find_and_interpolate_host(S, field, torch.from_numpy(x), chunks=chunks, out=out)
     code = rec.code.cpu()
