@@ -108,7 +108,10 @@ def run_reference(args):
 
 # ----------------------------------------------------------------- GPU arm
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons during the timed region."""
+    """nvidia-smi clocks and throttle reasons during the timed region: the
+    query loop runs every 10 ms, is live before the region starts (the
+    first row is awaited and dropped), and only rows stamped inside the
+    region are kept."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -117,24 +120,40 @@ class ClockSampler:
     def __init__(self, gpu):
         self.gpu = gpu
         self.p = None
+        self.rows = []
+        self.t0 = self.t1 = 0.0
+
+    def _read(self):
+        for line in self.p.stdout:
+            self.rows.append((time.perf_counter(), line))
 
     def __enter__(self):
+        import threading
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                       "--format=csv,noheader,nounits", "-lms", "10"],
                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+            t = time.perf_counter()
+            while not self.rows and time.perf_counter() - t < 10.0 and self.p.poll() is None:
+                time.sleep(0.005)
         except Exception:
             self.p = None
+        self.t0 = time.perf_counter()
         return self
 
     def __exit__(self, *a):
-        self.out = ""
+        self.t1 = time.perf_counter()
+        time.sleep(0.02)  # the row being sampled at the end of the region
         if self.p is not None:
             self.p.terminate()
             try:
-                self.out, _ = self.p.communicate(timeout=5)
+                self.p.wait(timeout=5)
+                self.th.join(timeout=5)
             except Exception:
-                self.out = ""
+                pass
+        self.out = "\n".join(l.strip() for t, l in self.rows if self.t0 <= t <= self.t1 + 0.02)
 
     def summary(self):
         rows = [r.split(", ") for r in (self.out or "").strip().splitlines() if r.strip()]
