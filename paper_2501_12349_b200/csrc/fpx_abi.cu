@@ -538,7 +538,7 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
   if (g_round1_done) FPX_CK(cudaEventRecord(g_round1_done, st));
   // --- rest: remaining candidates of the unresolved points
   FPX_CK(cudaMemsetAsync(w.hist, 0, sizeof(int32_t) * 2 * FPX_HMAX, st));
-  g_launches += 2;
+  g_launches += 3;  // k_rest_lists, k_rest_order, k_rest_scatter, k_rest_pairlist
   FPX_LAUNCH(fpx::launch_rest_lists(M, x, n, w.nun, w.upts, w.clist, w.cseed, w.cnum, w.nps, w.hist,
                                     w.bstart, w.bcur, w.perm, w.cum, w.maxnp, w.pairs, w.npairs,
                                     st));
@@ -550,6 +550,7 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
                                    r, dist,
                                    iters,
                                    field, C, values, w.counter, stats, st));
+  g_launches += field ? 2 : 1;  // k_rest_l1 pass 1 + redo pass (+ k_rest_values)
   g_launches += 1;
   k_find_totals<<<1, 1, 0, st>>>(w.nun, w.nredo, stats, n);
   FPX_CK(cudaGetLastError());
