@@ -131,8 +131,9 @@ int fpx_set_round1_event(void* ev);
 
 /* After fpx_find (same stream, same workspace): writes the records of the
  * points the rest phase settled straight into host record arrays (pinned,
- * mapped; zero-copy over PCIe).  Enqueue it after any bulk download into the
- * same arrays. */
+ * mapped; zero-copy over PCIe), in point order.  Enqueue it after any bulk
+ * download into the same arrays.  Uses the find's per-point scratch in `ws`
+ * (the records stay valid). */
 int fpx_rest_patch_host(int dr, int C, int64_t n, const void* ws, size_t ws_bytes,
                         const fpx_mesh_t* m, const int32_t* code, const int32_t* elem,
                         const double* r, const double* dist, const double* values,

@@ -79,17 +79,29 @@ __device__ __forceinline__ void store_row(double* dst, const double* src, int le
   if (a < len) dst[a] = src[a];
 }
 
-__global__ void k_rest_patch_host(int dr, int C, const int64_t* __restrict__ nun_dev,
-                                  const int32_t* __restrict__ upts,
-                                  const int32_t* __restrict__ code,
-                                  const int32_t* __restrict__ elem, const double* __restrict__ r,
-                                  const double* __restrict__ dist,
-                                  const double* __restrict__ values, int32_t* hcode,
-                                  int32_t* helem, double* hr, double* hdist, double* hvalues) {
+// flag[k] marks the rest points (k_rest_flag); the patch threads walk the
+// points in order, so the PCIe writes in flight land on neighbouring host
+// pages (IOMMU / DRAM locality), and clear the flags behind them.
+__global__ void k_rest_flag(const int64_t* __restrict__ nun_dev, const int32_t* __restrict__ upts,
+                            int32_t* flag) {
   const int64_t nun = *nun_dev;
   for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < nun;
-       u += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t k = upts[u];
+       u += (int64_t)gridDim.x * blockDim.x)
+    flag[upts[u]] = 1;
+}
+
+__global__ void k_rest_patch_host(int dr, int C, int64_t n, int32_t* flag,
+                                          const int32_t* __restrict__ code,
+                                          const int32_t* __restrict__ elem,
+                                          const double* __restrict__ r,
+                                          const double* __restrict__ dist,
+                                          const double* __restrict__ values, int32_t* hcode,
+                                          int32_t* helem, double* hr, double* hdist,
+                                          double* hvalues) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    if (!flag[k]) continue;
+    flag[k] = 0;
     hcode[k] = code[k];
     helem[k] = elem[k];
     store_row(hr + k * dr, r + k * dr, dr);
@@ -98,16 +110,19 @@ __global__ void k_rest_patch_host(int dr, int C, const int64_t* __restrict__ nun
   }
 }
 
-cudaError_t launch_rest_patch_host(int dr, int C, int64_t n_cap, const int64_t* nun_dev,
-                                   const int32_t* upts, const int32_t* code, const int32_t* elem,
-                                   const double* r, const double* dist, const double* values,
-                                   int32_t* hcode, int32_t* helem, double* hr, double* hdist,
-                                   double* hvalues, cudaStream_t st) {
-  int64_t b = (n_cap + 255) / 256;
-  if (b > 148 * 4) b = 148 * 4;
+cudaError_t launch_rest_patch_host(int dr, int C, int64_t n, const int64_t* nun_dev,
+                                           const int32_t* upts, int32_t* flag,
+                                           const int32_t* code, const int32_t* elem,
+                                           const double* r, const double* dist,
+                                           const double* values, int32_t* hcode, int32_t* helem,
+                                           double* hr, double* hdist, double* hvalues,
+                                           cudaStream_t st) {
+  int64_t b = (n + 255) / 256;
+  if (b > 148 * 8) b = 148 * 8;
   if (b < 1) b = 1;
-  k_rest_patch_host<<<(unsigned)b, 256, 0, st>>>(dr, C, nun_dev, upts, code, elem, r, dist,
-                                                 values, hcode, helem, hr, hdist, hvalues);
+  k_rest_flag<<<(unsigned)b, 256, 0, st>>>(nun_dev, upts, flag);
+  k_rest_patch_host<<<(unsigned)b, 256, 0, st>>>(dr, C, n, flag, code, elem, r, dist,
+                                                         values, hcode, helem, hr, hdist, hvalues);
   return cudaGetLastError();
 }
 

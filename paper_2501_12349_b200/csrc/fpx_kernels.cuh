@@ -59,11 +59,13 @@ cudaError_t launch_point_scatter(int64_t n, const int32_t* cellid, const int32_t
 cudaError_t launch_make_items(int64_t E, const int32_t* count, const uint64_t* packed_off,
                               Item* items, int64_t* nitems_dev, cudaStream_t st);
 // Zero-copy patch of the rest points' records into mapped host arrays.
-cudaError_t launch_rest_patch_host(int dr, int C, int64_t n_cap, const int64_t* nun_dev,
-                                   const int32_t* upts, const int32_t* code, const int32_t* elem,
-                                   const double* r, const double* dist, const double* values,
-                                   int32_t* hcode, int32_t* helem, double* hr, double* hdist,
-                                   double* hvalues, cudaStream_t st);
+cudaError_t launch_rest_patch_host(int dr, int C, int64_t n, const int64_t* nun_dev,
+                                           const int32_t* upts, int32_t* flag,
+                                           const int32_t* code, const int32_t* elem,
+                                           const double* r, const double* dist,
+                                           const double* values, int32_t* hcode, int32_t* helem,
+                                           double* hr, double* hdist, double* hvalues,
+                                           cudaStream_t st);
 cudaError_t launch_pack_counts(int64_t E, const int32_t* count, uint64_t* packed,
                                cudaStream_t st);
 cudaError_t launch_scatter_units(int64_t nunits_cap, const int64_t* nunits_dev,
