@@ -129,12 +129,13 @@ int fpx_profile_round1(void* ev_start, void* ev_stop);
  * points (fpx_rest_patch_host) still change.  NULL clears it. */
 int fpx_set_round1_event(void* ev);
 
-/* After fpx_find (same stream, same workspace): writes the records of the
- * points the rest phase settled straight into host record arrays (pinned,
- * mapped; zero-copy over PCIe), in point order.  Enqueue it after any bulk
- * download into the same arrays.  Uses the find's per-point scratch in `ws`
- * (the records stay valid). */
-int fpx_rest_patch_host(int dr, int C, int64_t n, const void* ws, size_t ws_bytes,
+/* After fpx_find (same stream, same workspace, same n): writes the records of
+ * the points the rest phase settled straight into host record arrays
+ * (pinned, mapped; zero-copy over PCIe), in point order.  Enqueue it after
+ * any bulk download into the same arrays.  It WRITES the find's per-point
+ * lock array in `ws` (reused as per-point flags; the records stay valid).
+ * FPX_EINVAL if `ws` was not last used by an fpx_find of n points on `m`. */
+int fpx_rest_patch_host(int dr, int C, int64_t n, void* ws, size_t ws_bytes,
                         const fpx_mesh_t* m, const int32_t* code, const int32_t* elem,
                         const double* r, const double* dist, const double* values,
                         int32_t* hcode, int32_t* helem, double* hr, double* hdist,
@@ -224,9 +225,6 @@ int fpx_invert_pairs(const fpx_mesh_t* m, int64_t npairs, const double* x, const
 int fpx_forward_map(const fpx_mesh_t* m, int64_t n, const int32_t* elem, const double* r,
                     double* x, double* G, double* H2, void* stream);
 
-/* Multi-rank routing helpers (engine Phase B, SPEC.md:407,417; PAPER.md:388-397):
- * global-grid cell owner of each point and the destination counts for an
- * all-to-allv: dest[n] in [-1, nranks), counts [nranks] (device int64). */
 /* Lagrangian particle step (Algorithm 1, ParticleRHS + Integrate +
  * ParticleBC): a = (u - v)/tau, AB2 update of x and v (forward Euler when
  * `first`), periodic wrap of axis c of the box (lo[d], hi[d] in host memory)
@@ -236,6 +234,9 @@ int fpx_particles_advance(int d, int64_t n, double* x, double* v, const double* 
                           double* v_prev, double* a_prev, double tau, double dt, int first,
                           const double* box, int periodic, void* stream);
 
+/* Multi-rank routing helpers (engine Phase B, SPEC.md:407,417; PAPER.md:388-397):
+ * global-grid cell owner of each point and the destination counts for an
+ * all-to-allv: dest[n] in [-1, nranks), counts [nranks] (device int64). */
 int fpx_route_count(int64_t n, const int32_t* dest, int nranks, int64_t* counts, void* stream);
 /* Stable pack by destination: perm[n] = position of point i in the send buffer
  * (-1 for dest < 0); offsets [nranks] = exclusive scan of counts. */

@@ -8,6 +8,9 @@
 
 #include <atomic>
 #include <cstdarg>
+#include <mutex>
+#include <unordered_map>
+#include <utility>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -33,6 +36,11 @@ thread_local std::string g_err;
 std::atomic<int64_t> g_launches{0};
 cudaEvent_t g_prof_start = nullptr, g_prof_stop = nullptr;
 thread_local cudaEvent_t g_round1_done = nullptr;
+
+// Layout of every find workspace at its last fpx_find (points, elements):
+// fpx_rest_patch_host re-carves the workspace and must see the same layout.
+std::mutex g_ws_mu;
+std::unordered_map<const void*, std::pair<int64_t, int64_t>> g_ws_layout;
 
 int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -281,7 +289,7 @@ int fpx_set_round1_event(void* ev) {
   return FPX_OK;
 }
 
-int fpx_rest_patch_host(int dr, int C, int64_t n, const void* ws, size_t ws_bytes,
+int fpx_rest_patch_host(int dr, int C, int64_t n, void* ws, size_t ws_bytes,
                         const fpx_mesh_t* m, const int32_t* code, const int32_t* elem,
                         const double* r, const double* dist, const double* values,
                         int32_t* hcode, int32_t* helem, double* hr, double* hdist,
@@ -298,7 +306,14 @@ int fpx_rest_patch_host(int dr, int C, int64_t n, const void* ws, size_t ws_byte
     if (at.type != cudaMemoryTypeHost || at.devicePointer != p)
       return fail(FPX_EINVAL, "rest patch: host array %p is not mapped pinned memory", p);
   }
-  Carver cv(const_cast<void*>(ws), ws_bytes);
+  {
+    std::lock_guard<std::mutex> g(g_ws_mu);
+    auto it = g_ws_layout.find(ws);
+    if (it == g_ws_layout.end() || it->second.first != n || it->second.second != m->E)
+      return fail(FPX_EINVAL, "rest patch: workspace was not last used by an fpx_find of %lld "
+                  "points on this mesh", (long long)n);
+  }
+  Carver cv(ws, ws_bytes);
   FindWs w;
   w.carve(cv, m->E, n);
   if (!cv.ok()) return fail(FPX_EINVAL, "rest patch: workspace too small");
@@ -486,6 +501,10 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
   if (!cv.ok()) return fail(FPX_EINVAL, "find workspace too small (%zu < %zu)", ws_bytes, cv.off);
   if (!m->frec) return fail(FPX_EINVAL, "mesh has no filter records (fpx_filter_records)");
   if (!m->nodes_pad) return fail(FPX_EINVAL, "mesh has no padded nodes (fpx_pad_nodes)");
+  {
+    std::lock_guard<std::mutex> g(g_ws_mu);
+    g_ws_layout[ws] = {n, E};
+  }
   const fpx_mesh_t& M = *m;
   // --- order the points by hash cell (counting sort)
   const int64_t nc = w.ncells;
@@ -500,11 +519,7 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
   FPX_LAUNCH(fpx::launch_point_scatter(n, w.cellid, w.cell_off, w.cell_cursor, w.order, st));
   // --- prefilter: hash list + AABB/OBB filter + best-first ranking
   FPX_CK(cudaMemsetAsync(w.g1.count, 0, sizeof(int32_t) * E, st));
-  static const int pf_mode = [] {
-    const char* v = getenv("FPX_PREFILTER");
-    return v && v[0] == '1' ? 1 : 0;
-  }();
-  FPX_LAUNCH(fpx::launch_prefilter(M, pf_mode, n, nc + 1, x, w.order, w.cellid, w.cell_off,
+  FPX_LAUNCH(fpx::launch_prefilter(M, n, nc + 1, x, w.order, w.cellid, w.cell_off,
                                    w.best, w.npass, code, elem, r, dist, iters,
                                    field ? values : nullptr, C, w.g1.count, stats, st));
   FPX_CK(cudaMemsetAsync(w.nun, 0, sizeof(int64_t), st));
@@ -514,29 +529,13 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
   g_launches += 3;
   FPX_CK(w.g1.build(E, n, nullptr, w.best, nullptr, st));
   if (g_prof_start) FPX_CK(cudaEventRecord(g_prof_start, st));
-  static const bool r1_items = [] {
-    const char* v = getenv("FPX_R1");
-    return v && v[0] == 'i';
-  }();
-  if (r1_items) {
-    FPX_LAUNCH(fpx::launch_newton_round1(M, n, x, w.g1.sorted, w.g1.items, w.g1.nitems,
-                                         w.g1.items_cap, w.npass, code, elem, r, dist, iters,
-                                         field, C, values, w.upts, nullptr, w.nun, stats, st));
-  } else {
-    FPX_CK(cudaMemsetAsync(w.chunk_ctr, 0, sizeof(int64_t), st));
-    // candidates held on a face twice in a row stop early (redo pass; see
-    // k_rest_l1).  FPX_ABORT=0, or the shared-slot rest variant, disable it.
-    static const bool abort_r1 = [] {
-      const char* v = getenv("FPX_ABORT");
-      const char* rv = getenv("FPX_REST");
-      return !(v && v[0] == '0') && !(rv && rv[0] == 's');
-    }();
-    FPX_LAUNCH(fpx::launch_newton_stream(M, n, x, w.g1.sorted, w.g1.packed_off, w.g1.count,
-                                         w.best, w.npass, code, elem, r, dist, iters, field, C,
-                                         values, w.upts, w.nun, w.chunk_ctr,
-                                         abort_r1 ? w.redo : nullptr, w.nredo, 2 * n + 1024,
-                                         stats, st));
-  }
+  FPX_CK(cudaMemsetAsync(w.chunk_ctr, 0, sizeof(int64_t), st));
+  // candidates held on a face twice in a row stop early and are redone in
+  // full only if their point ends without an INTERIOR (see k_rest_l1)
+  FPX_LAUNCH(fpx::launch_newton_stream(M, n, x, w.g1.sorted, w.g1.packed_off, w.g1.count,
+                                       w.best, w.npass, code, elem, r, dist, iters, field, C,
+                                       values, w.upts, w.nun, w.chunk_ctr, w.redo, w.nredo,
+                                       2 * n + 1024, stats, st));
   if (g_prof_stop) FPX_CK(cudaEventRecord(g_prof_stop, st));
   // external record: also a real event node when captured into a CUDA graph
   if (g_round1_done) FPX_CK(cudaEventRecord(g_round1_done, st));

@@ -794,107 +794,6 @@ __global__ void __launch_bounds__(256)
     atomicAdd((unsigned long long*)&stats[FPX_STAT_BOXTESTS], (unsigned long long)boxtests);
 }
 
-// Warp per hash cell: lanes over the cell's list (records in registers when
-// it fits one warp), the warp walks the cell's points and reduces the
-// best-first candidate with shuffles.  Preferable when cells hold few points
-// and long lists (fine hash grids).
-template <int D>
-__global__ void __launch_bounds__(128)
-    k_prefilter_cells(fpx_mesh_t m, int64_t ncells_tot, const double* __restrict__ x,
-                      const int32_t* __restrict__ order, const int32_t* __restrict__ cell_off,
-                      int32_t* best, int32_t* npass, int32_t* code, int32_t* elem, double* r,
-                      double* dist, int32_t* iters, double* values, int C, int32_t* elem_count,
-                      int64_t* stats) {
-  const int warp = threadIdx.x / FPX_WARP, lane = threadIdx.x % FPX_WARP;
-  const int64_t nc = ncells_tot - 1;  // last bucket: points outside the grid
-  int64_t boxtests = 0;
-  for (int64_t c = (int64_t)blockIdx.x * (blockDim.x / FPX_WARP) + warp; c < ncells_tot;
-       c += (int64_t)gridDim.x * (blockDim.x / FPX_WARP)) {
-    const int p0 = cell_off[c], p1 = cell_off[c + 1];
-    if (p0 == p1) continue;
-    if (c == nc) {
-      for (int p = p0 + lane; p < p1; p += FPX_WARP) {
-        const int64_t k = order[p];
-        best[k] = -1;
-        npass[k] = 0;
-        write_not_found(k, m.dr, code, elem, r, dist, iters, values, C);
-      }
-      continue;
-    }
-    const int s = m.offsets[c], L = m.offsets[c + 1] - s;
-    if (lane == 0) boxtests += (int64_t)L * (p1 - p0);
-    for (int q0 = 0; q0 < L || q0 == 0; q0 += FPX_WARP) {
-      // this chunk's records in registers (lane q holds entry q0 + q)
-      const bool have = q0 + lane < L;
-      const int e = have ? m.elems[s + q0 + lane] : 0;
-      const int64_t eo = have ? e : 0;
-      double bx[2 * D], cen[D], inv[D * D], fr[D + D * D];
-#pragma unroll
-      for (int t = 0; t < 2 * D; ++t) bx[t] = m.aabb[eo * 2 * D + t];
-#pragma unroll
-      for (int t = 0; t < D; ++t) cen[t] = m.obb_c[eo * D + t];
-#pragma unroll
-      for (int t = 0; t < D * D; ++t) inv[t] = m.obb_inv[eo * D * D + t];
-#pragma unroll
-      for (int t = 0; t < D + D * D; ++t) fr[t] = m.frame[eo * (D + D * D) + t];
-      const bool ok = m.obb_ok[eo] != 0;
-      const bool lastc = q0 + FPX_WARP >= L;
-      for (int pc = p0; pc < p1; pc += FPX_WARP) {
-        const int cnt = p1 - pc < FPX_WARP ? p1 - pc : FPX_WARP;
-        const int64_t kl = lane < cnt ? order[pc + lane] : 0;
-        double xl[D];
-#pragma unroll
-        for (int t = 0; t < D; ++t) xl[t] = lane < cnt ? x[kl * D + t] : 0.0;
-        // running (npass, best) of point pc + lane across chunks
-        int my_np = 0, my_b = -1;
-        double my_v = INFINITY;
-        if (q0 > 0 && lane < cnt) {
-          my_np = npass[kl];
-          my_b = best[kl];
-          my_v = my_b >= 0 ? bestfirst_value(D, m.frame + (int64_t)my_b * (D + D * D), xl)
-                           : INFINITY;
-        }
-        for (int pi = 0; pi < cnt; ++pi) {
-          double xx[D];
-#pragma unroll
-          for (int t = 0; t < D; ++t) xx[t] = __shfl_sync(FPX_FULL, xl[t], pi);
-          const bool pass = have && aabb_in(D, bx, xx) && (!ok || obb_in(D, cen, inv, xx));
-          double v = pass ? bestfirst_value(D, fr, xx) : INFINITY;
-          int be = pass ? e : 0x7fffffff;
-          const int np = __popc(__ballot_sync(FPX_FULL, pass));
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const double ov = __shfl_xor_sync(FPX_FULL, v, o);
-            const int oe = __shfl_xor_sync(FPX_FULL, be, o);
-            if (ov < v || (ov == v && oe < be)) {
-              v = ov;
-              be = oe;
-            }
-          }
-          if (lane == pi) {
-            my_np += np;
-            if (np > 0 && (v < my_v || (v == my_v && be < my_b) || my_b < 0)) {
-              my_v = v;
-              my_b = be;
-            }
-          }
-        }
-        if (lane < cnt) {
-          npass[kl] = my_np;
-          best[kl] = my_b;
-          if (lastc) {
-            if (my_b < 0) write_not_found(kl, m.dr, code, elem, r, dist, iters, values, C);
-            else atomicAdd(&elem_count[my_b], 1);
-          }
-        }
-      }
-      if (L == 0) break;
-    }
-  }
-  for (int o = 16; o > 0; o >>= 1) boxtests += __shfl_xor_sync(FPX_FULL, boxtests, o);
-  if (lane == 0 && boxtests)
-    atomicAdd((unsigned long long*)&stats[FPX_STAT_BOXTESTS], (unsigned long long)boxtests);
-}
 
 // Packed candidate-filter records (include/fpx.h, FPX_FREC): one 256-byte
 // row per element so the prefilter fetches a candidate in one round trip.
@@ -1023,24 +922,17 @@ cudaError_t launch_cell_of(int d, const double* grid, int n, int64_t npts, const
   k_cell_of<<<grid_for(npts, 256), 256, 0, st>>>(d, grid, n, npts, x, cell);
   return cudaGetLastError();
 }
-cudaError_t launch_prefilter(const fpx_mesh_t& m, int mode, int64_t n, int64_t ncells_tot,
+cudaError_t launch_prefilter(const fpx_mesh_t& m, int64_t n, int64_t ncells_tot,
                              const double* x, const int32_t* order, const int32_t* cellid,
                              const int32_t* cell_off, int32_t* best, int32_t* npass,
                              int32_t* code, int32_t* elem, double* r, double* dist,
                              int32_t* iters, double* values, int C, int32_t* elem_count,
                              int64_t* stats, cudaStream_t st) {
-  if (mode == 1) {
-    int64_t b = (ncells_tot + 3) / 4;
-    if (b > 148 * 64) b = 148 * 64;
-    if (b < 1) b = 1;
-    auto fn = m.d == 3 ? k_prefilter_cells<3> : k_prefilter_cells<2>;
-    fn<<<(unsigned)b, 128, 0, st>>>(m, ncells_tot, x, order, cell_off, best, npass, code, elem, r,
-                                    dist, iters, values, C, elem_count, stats);
-  } else {
-    auto fn = m.d == 3 ? k_prefilter_points<3> : k_prefilter_points<2>;
-    fn<<<grid_for(n, 256), 256, 0, st>>>(m, n, x, order, cellid, best, npass, code, elem, r, dist,
-                                         iters, values, C, elem_count, stats);
-  }
+  (void)ncells_tot;
+  (void)cell_off;
+  auto fn = m.d == 3 ? k_prefilter_points<3> : k_prefilter_points<2>;
+  fn<<<grid_for(n, 256), 256, 0, st>>>(m, n, x, order, cellid, best, npass, code, elem, r, dist,
+                                       iters, values, C, elem_count, stats);
   return cudaGetLastError();
 }
 cudaError_t launch_point_cells(const fpx_mesh_t& m, int64_t n, const double* x, int32_t* cellid,

@@ -44,8 +44,8 @@ cudaError_t launch_hash_sort(int64_t ncells, const int32_t* offsets, int32_t* el
                              int32_t* max_list, cudaStream_t st);
 cudaError_t launch_cell_of(int d, const double* grid, int n, int64_t npts, const double* x,
                            int64_t* cell, cudaStream_t st);
-// mode 0: thread per point (k_prefilter_points); 1: warp per cell.
-cudaError_t launch_prefilter(const fpx_mesh_t& m, int mode, int64_t n, int64_t ncells_tot,
+// thread per point in hash-cell order (k_prefilter_points)
+cudaError_t launch_prefilter(const fpx_mesh_t& m, int64_t n, int64_t ncells_tot,
                              const double* x, const int32_t* order, const int32_t* cellid,
                              const int32_t* cell_off, int32_t* best, int32_t* npass,
                              int32_t* code, int32_t* elem, double* r, double* dist,
@@ -75,13 +75,6 @@ cudaError_t launch_scatter_units(int64_t nunits_cap, const int64_t* nunits_dev,
 
 // Newton / eval (fpx_newton.cu, FMA allowed).
 bool newton_supported(int d, int dr, int N);
-cudaError_t launch_newton_round1(const fpx_mesh_t& m, int64_t n, const double* x,
-                                 const int32_t* sorted_pts, const Item* items,
-                                 const int64_t* nitems_dev, int64_t items_cap,
-                                 const int32_t* npass, int32_t* code, int32_t* elem, double* r,
-                                 double* dist, int32_t* iters, const double* field, int C,
-                                 double* values, int32_t* upts, int64_t* upair_cnt,
-                                 int64_t* nun_dev, int64_t* stats, cudaStream_t st);
 // Round 1 streamed (k_newton_stream): points sorted by best-first element
 // (sorted / packed_off / ecount from the element grouping).
 cudaError_t launch_newton_stream(const fpx_mesh_t& m, int64_t n, const double* x,

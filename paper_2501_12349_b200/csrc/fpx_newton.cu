@@ -44,19 +44,6 @@ static cudaError_t dispatch(int d, int dr, int N, A... args) {
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_newton_round1(const fpx_mesh_t& m, int64_t n, const double* x,
-                                 const int32_t* sorted_pts, const Item* items,
-                                 const int64_t* nitems_dev, int64_t items_cap,
-                                 const int32_t* npass, int32_t* code, int32_t* elem, double* r,
-                                 double* dist, int32_t* iters, const double* field, int C,
-                                 double* values, int32_t* upts, int64_t* upair_cnt,
-                                 int64_t* nun_dev, int64_t* stats, cudaStream_t st) {
-  (void)n;
-  return dispatch<Round1>(m.d, m.dr, m.N, m, x, sorted_pts, items, nitems_dev, items_cap, npass,
-                          code, elem, r, dist, iters, field, C, values, upts, upair_cnt, nun_dev,
-                          stats, st);
-}
-
 cudaError_t launch_newton_stream(const fpx_mesh_t& m, int64_t n, const double* x,
                                  const int32_t* sorted, const uint64_t* packed_off,
                                  const int32_t* ecount, const int32_t* best, const int32_t* npass,

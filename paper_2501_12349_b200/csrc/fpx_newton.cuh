@@ -795,94 +795,6 @@ __device__ __forceinline__ int64_t warp_sum64(int64_t v) {
   return v;
 }
 
-// Round 1: every found point's best-first candidate.  Final for INTERIOR or
-// single-candidate points (fused field evaluation); otherwise a tentative
-// BORDER record and the point joins the exhaustive round 2.
-template <int D, int DR, int N>
-__global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
-    k_newton_round1(fpx_mesh_t m, const double* __restrict__ x, const int32_t* __restrict__ sorted,
-                    const Item* __restrict__ items, const int64_t* __restrict__ nitems_dev,
-                    const int32_t* __restrict__ npass, int32_t* code, int32_t* elem, double* r,
-                    double* dist, int32_t* iters, const double* __restrict__ field, int C,
-                    double* values, int32_t* upts, int64_t* upair_cnt, int64_t* nun_dev,
-                    int64_t* stats) {
-  using L = Lay<D, DR, N>;
-  extern __shared__ __align__(16) double smem[];
-  double* z = smem;
-  double* scale = smem + N;
-  const int warp = threadIdx.x / FPX_WARP, lane = threadIdx.x % FPX_WARP;
-  const int wpb = blockDim.x / FPX_WARP;
-  const int fsz = field ? C * L::CS : 0;
-  constexpr int SCR = Scratch<DR, N>::SLOTS * FPX_WARP;
-  double* sX = smem + 2 * ((N + 1) & ~1) + warp * (L::GEO + SCR + fsz);
-  double* sb = sX + L::GEO + lane;
-  double* sU = sX + L::GEO + SCR;
-  if (threadIdx.x < N) {
-    z[threadIdx.x] = m.basis[FPX_BASIS_NODES(N, m.M) + threadIdx.x];
-    scale[threadIdx.x] = m.basis[FPX_BASIS_SCALE(N, m.M) + threadIdx.x];
-  }
-  __syncthreads();
-  const NewtonParams P = newton_of(m);
-  const int64_t nitems = *nitems_dev;
-  int64_t s_newton = 0, s_iters = 0, s_evals = 0, nev[2] = {0, 0}, s_items = 0;
-  for (int64_t w = (int64_t)blockIdx.x * wpb + warp; w < nitems; w += (int64_t)gridDim.x * wpb) {
-    const Item itm = items[w];
-    const int e = itm.elem;
-    ++s_items;
-    stage_block<DR, N>(sX, m.nodes + (int64_t)e * D * L::K, D, lane);
-    if (field) stage_block<DR, N>(sU, field + (int64_t)e * C * L::K, C, lane);
-    cp_async_wait_all();
-    __syncwarp();
-    const bool active = lane < itm.count;
-    const int pt = active ? sorted[itm.start + lane] : 0;
-    double xs[3] = {0.0, 0.0, 0.0};
-    if (active)
-#pragma unroll
-      for (int c = 0; c < D; ++c) xs[c] = x[(int64_t)pt * D + c];
-    NewtonOut o = newton_warp<D, DR, N>(sX, z, scale, xs, active, P, sb, nev);
-    if (active) {
-      s_newton += 1;
-      s_iters += o.iters;
-      const double epsd = DR < D ? eps_d_of(m, e) : 0.0;
-      const int cd = classify<D, DR>(o.r, o.dist, epsd);
-      const bool final = cd == kInterior || npass[pt] <= 1;
-      code[pt] = cd;
-      elem[pt] = e;
-#pragma unroll
-      for (int a = 0; a < DR; ++a) r[(int64_t)pt * DR + a] = o.r[a];
-      dist[pt] = o.dist;
-      if (iters) iters[pt] = o.iters;
-      if (final) {
-        if (field) {
-          double v[DR][N];
-          basis_values<DR, N>(z, scale, o.r, v);
-          for (int c = 0; c < C; ++c) values[(int64_t)pt * C + c] = contract_smem<DR, N>(sU + c * L::CS, v);
-          ++s_evals;
-        }
-      } else {
-        const int slot = (int)atomicAdd((unsigned long long*)nun_dev, 1ull);
-        upts[slot] = pt;
-        if (upair_cnt) upair_cnt[slot] = npass[pt] - 1;
-      }
-    }
-    __syncwarp();
-  }
-  s_newton = warp_sum64(s_newton);
-  s_iters = warp_sum64(s_iters);
-  s_evals = warp_sum64(s_evals);
-  if (lane == 0) {
-    atomicAdd((unsigned long long*)&stats[FPX_STAT_NEWTON], (unsigned long long)s_newton);
-    atomicAdd((unsigned long long*)&stats[FPX_STAT_ITERS], (unsigned long long)s_iters);
-    atomicAdd((unsigned long long*)&stats[FPX_STAT_EVALS], (unsigned long long)s_evals);
-    atomicAdd((unsigned long long*)&stats[FPX_STAT_NEWTON_R1], (unsigned long long)s_newton);
-    atomicAdd((unsigned long long*)&stats[FPX_STAT_ITERS_R1], (unsigned long long)s_iters);
-    atomicAdd((unsigned long long*)&stats[FPX_STAT_EVALS_R1], (unsigned long long)s_evals);
-    atomicAdd((unsigned long long*)&stats[FPX_STAT_R1_WARP_EVALS], (unsigned long long)nev[0]);
-    atomicAdd((unsigned long long*)&stats[FPX_STAT_R1_W2_EVALS], (unsigned long long)nev[1]);
-    atomicAdd((unsigned long long*)&stats[FPX_STAT_R1_ITEMS], (unsigned long long)s_items);
-  }
-}
-
 // Round 2 (and fpx_invert_pairs): Newton per explicit (point, element) pair.
 template <int D, int DR, int N>
 __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
@@ -1250,421 +1162,6 @@ __device__ __forceinline__ bool held_on_face(const double* r, const double* J) {
   return held;
 }
 
-// Per-point slot: geometry [D][N^DR] | axis-1.. basis values | Newton stash,
-// odd stride in doubles (the 16 points of a warp hit distinct bank pairs).
-template <int D, int DR, int N>
-struct PairLay {
-  static constexpr int K = Pow<DR, N>::K;
-  static constexpr int BAS = (DR - 1) * 3 * N;   // v, d1, d2 of axes 1..DR-1
-  static constexpr int STASH = D * K + BAS;      // 16 doubles
-  static constexpr int SS = (D * K + BAS + 16) | 1;
-};
-
-// Forward map + Newton state at r for one point evaluated by a lane pair:
-// lane `part` takes the rows q = part, part + 2, ... of every coordinate,
-// the per-coordinate partial sums are added across the pair (xor 1, the same
-// order on both lanes, so both hold bitwise identical states).  sp: the
-// point's slot; its basis block is written by lane 0 of the pair.
-template <int D, int DR, int N, int G, bool W2>
-__device__ __forceinline__ void eval_state_pair(const double* __restrict__ sp,
-                                                const double* __restrict__ z,
-                                                const double* __restrict__ scale, const double* r,
-                                                const double* xs, NState& S, int part) {
-  using PL = PairLay<D, DR, N>;
-  constexpr int K = PL::K, R = K / N;
-  double* sbas = const_cast<double*>(sp) + D * K;
-  double v0[N], g0[N], h0[N];
-  lagrange<N, W2>(z, scale, r[0], v0, g0, h0);
-  __syncwarp();
-#pragma unroll
-  for (int a = 1; a < DR; ++a) {
-    if (part == 0) {
-      double v[N], g[N], h[N];
-      lagrange<N, W2>(z, scale, r[a], v, g, h);
-#pragma unroll
-      for (int j = 0; j < N; ++j) {
-        sbas[((a - 1) * 3 + 0) * N + j] = v[j];
-        sbas[((a - 1) * 3 + 1) * N + j] = g[j];
-        if (W2) sbas[((a - 1) * 3 + 2) * N + j] = h[j];
-      }
-    }
-  }
-  __syncwarp();
-#define PSB(a, kind, j) sbas[(((a)-1) * 3 + (kind)) * N + (j)]
-  double X[D], GG[D][3], HH[D][6];
-#pragma unroll
-  for (int c = 0; c < D; ++c) {
-    const double* Xc = sp + c * K;
-    double xv = 0.0, g_0 = 0.0, g_1 = 0.0, g_2 = 0.0;
-    double h00 = 0.0, h11 = 0.0, h22 = 0.0, h01 = 0.0, h02 = 0.0, h12 = 0.0;
-#pragma unroll 3
-    for (int q = part; q < R; q += G) {
-      const double* row = Xc + q * N;
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-#pragma unroll
-      for (int i = 0; i < N; ++i) {
-        const double p = row[i];
-        s0 = fma(p, v0[i], s0);
-        s1 = fma(p, g0[i], s1);
-        if (W2) s2 = fma(p, h0[i], s2);
-      }
-      if constexpr (DR == 3) {
-        const int j = q % N, k = q / N;
-        const double vj = PSB(1, 0, j), gj = PSB(1, 1, j), vk = PSB(2, 0, k), gk = PSB(2, 1, k);
-        const double wvv = vj * vk, wgv = gj * vk, wvg = vj * gk;
-        xv = fma(s0, wvv, xv);
-        g_0 = fma(s1, wvv, g_0);
-        g_1 = fma(s0, wgv, g_1);
-        g_2 = fma(s0, wvg, g_2);
-        if (W2) {
-          h00 = fma(s2, wvv, h00);
-          h11 = fma(s0, PSB(1, 2, j) * vk, h11);
-          h22 = fma(s0, vj * PSB(2, 2, k), h22);
-          h01 = fma(s1, wgv, h01);
-          h02 = fma(s1, wvg, h02);
-          h12 = fma(s0, gj * gk, h12);
-        }
-      } else if constexpr (DR == 2) {
-        const double vj = PSB(1, 0, q), gj = PSB(1, 1, q);
-        xv = fma(s0, vj, xv);
-        g_0 = fma(s1, vj, g_0);
-        g_1 = fma(s0, gj, g_1);
-        if (W2) {
-          h00 = fma(s2, vj, h00);
-          h11 = fma(s0, PSB(1, 2, q), h11);
-          h01 = fma(s1, gj, h01);
-        }
-      } else {
-        xv = s0;
-        g_0 = s1;
-        if (W2) h00 = s2;
-      }
-    }
-    X[c] = xv;
-    GG[c][0] = g_0;
-    GG[c][1] = g_1;
-    GG[c][2] = g_2;
-    HH[c][0] = h00;
-    HH[c][1] = h11;
-    HH[c][2] = h22;
-    HH[c][3] = h01;
-    HH[c][4] = h02;
-    HH[c][5] = h12;
-  }
-#undef PSB
-  // group sums (xor butterfly: every lane adds the same numbers in the same
-  // order, so the group holds bitwise identical states)
-#pragma unroll
-  for (int o = 1; o < G; o <<= 1) {
-#pragma unroll
-    for (int c = 0; c < D; ++c) {
-      X[c] += __shfl_xor_sync(FPX_FULL, X[c], o);
-#pragma unroll
-      for (int a = 0; a < DR; ++a) GG[c][a] += __shfl_xor_sync(FPX_FULL, GG[c][a], o);
-      if (W2) {
-#pragma unroll
-        for (int t = 0; t < 6; ++t) {
-          if (DR < 3 && (t == 2 || t >= 4)) continue;
-          if (DR < 2 && t != 0) continue;
-          HH[c][t] += __shfl_xor_sync(FPX_FULL, HH[c][t], o);
-        }
-      }
-    }
-  }
-  S.f = 0.0;
-#pragma unroll
-  for (int t = 0; t < 3; ++t) S.J[t] = 0.0;
-#pragma unroll
-  for (int t = 0; t < 6; ++t) {
-    S.H0[t] = 0.0;
-    S.Q[t] = 0.0;
-  }
-#pragma unroll
-  for (int c = 0; c < D; ++c) {
-    const double dx = xs[c] - X[c];
-    S.f = fma(dx, dx, S.f);
-#pragma unroll
-    for (int a = 0; a < DR; ++a) S.J[a] = fma(-GG[c][a], dx, S.J[a]);
-    S.H0[0] = fma(GG[c][0], GG[c][0], S.H0[0]);
-    if (DR > 1) {
-      S.H0[1] = fma(GG[c][1], GG[c][1], S.H0[1]);
-      S.H0[3] = fma(GG[c][0], GG[c][1], S.H0[3]);
-    }
-    if (DR > 2) {
-      S.H0[2] = fma(GG[c][2], GG[c][2], S.H0[2]);
-      S.H0[4] = fma(GG[c][0], GG[c][2], S.H0[4]);
-      S.H0[5] = fma(GG[c][1], GG[c][2], S.H0[5]);
-    }
-    if (W2) {
-#pragma unroll
-      for (int t = 0; t < 6; ++t) S.Q[t] = fma(dx, HH[c][t], S.Q[t]);
-    }
-  }
-}
-
-template <int D, int DR, int N, int G, int WPB>
-__global__ void __launch_bounds__(WPB * 32, 1)
-    k_rest_pairs(fpx_mesh_t m, const double* __restrict__ x, const int64_t* __restrict__ nun_dev,
-                 const int32_t* __restrict__ upts, const int32_t* __restrict__ clist,
-                 const int32_t* __restrict__ cnum, int32_t* code, int32_t* elem, double* r,
-                 double* dist, int32_t* iters, int64_t* counter, int64_t* stats) {
-  using PL = PairLay<D, DR, N>;
-  constexpr int K = PL::K;
-  constexpr int PPW = FPX_WARP / G;  // points per warp
-  extern __shared__ __align__(16) double smem[];
-  double* z = smem;
-  double* scale = smem + N;
-  const int warp = threadIdx.x / FPX_WARP, lane = threadIdx.x % FPX_WARP;
-  const int pslot = lane / G, part = lane % G, glead = lane & ~(G - 1);
-  double* slots = smem + 2 * ((N + 1) & ~1) + (size_t)warp * PPW * PL::SS;
-  double* mine = slots + pslot * PL::SS;
-  double* stash = mine + PL::STASH;
-  uint64_t* mbars =
-      reinterpret_cast<uint64_t*>(smem + 2 * ((N + 1) & ~1) + (size_t)WPB * PPW * PL::SS) +
-      warp * PPW;
-  if (threadIdx.x < N) {
-    z[threadIdx.x] = m.basis[FPX_BASIS_NODES(N, m.M) + threadIdx.x];
-    scale[threadIdx.x] = m.basis[FPX_BASIS_SCALE(N, m.M) + threadIdx.x];
-  }
-  for (int t = lane; t < PPW * PL::SS; t += FPX_WARP) slots[t] = 0.0;
-  if (lane < PPW) mbar_init(&mbars[lane], FPX_WARP);
-  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  __syncthreads();
-  const NewtonParams P = newton_of(m);
-  const int64_t nun = *nun_dev;
-  int64_t s_newton = 0, s_iters = 0, nev = 0, nev2 = 0, nlev = 0;
-  // point state (identical on both lanes of the pair)
-  bool have_point = false, point_done = false;
-  int64_t u = 0, k = 0;
-  double xs[3] = {0.0, 0.0, 0.0};
-  int bc = -1, be = -1, it_tot = 0, rank = 0, nlist = 0, te = -1, qs = 0, qe = 0;
-  bool over = false;
-  double bd = INFINITY, br[3] = {0.0, 0.0, 0.0}, tv = -INFINITY;
-  // 0 needs a candidate, 1 copy requested, 2 copy in flight, 3 iterating,
-  // 4 no work left
-  int phase = 0;
-  unsigned parity = 0;
-  int e = -1, it = 0;
-  bool first = true;
-  double rc[3] = {0.0, 0.0, 0.0}, rn[3] = {0.0, 0.0, 0.0};
-  double alpha = 1.0, fcur = 0.0, pred = 0.0, smax = 0.0;
-  NState st;
-  while (true) {
-    // (a) points without a candidate pick the next one (or finish)
-    if (phase == 0) {
-      while (true) {
-        if (!have_point) {
-          int64_t uu = 0;
-          if (part == 0) uu = (int64_t)atomicAdd((unsigned long long*)counter, 1ull);
-          u = __shfl_sync(__activemask(), uu, glead);
-          if (u >= nun) {
-            phase = 4;
-            break;
-          }
-          k = upts[u];
-#pragma unroll
-          for (int c = 0; c < D; ++c) xs[c] = x[k * D + c];
-          bc = code[k];
-          be = elem[k];
-          bd = dist[k];
-#pragma unroll
-          for (int a = 0; a < DR; ++a) br[a] = r[k * DR + a];
-          it_tot = iters ? iters[k] : 0;
-          const int cn = cnum[u];
-          nlist = cn < 0 ? -cn : cn;
-          over = cn < 0;
-          rank = 1;  // rank 0 is round 1's candidate
-          if (over) {
-            FRec R;
-            load_frec(m.frec, be, R);
-            tv = frec_bestfirst<D>(R, xs);
-            te = be;
-            int ax[3];
-            const int64_t cell = cell_of(D, m.grid, m.ncell, xs, ax);
-            qs = m.offsets[cell];
-            qe = m.offsets[cell + 1];
-          }
-          have_point = true;
-          point_done = false;
-        }
-        e = -1;
-        if (!point_done) {
-          if (rank < nlist) {
-            e = clist[u * FPX_RK + rank++];
-            if (over) {
-              FRec R;
-              load_frec(m.frec, e, R);
-              tv = frec_bestfirst<D>(R, xs);
-              te = e;
-            }
-          } else if (over) {
-            double bv = INFINITY;
-            int bb = 0x7fffffff;
-            for (int q = qs; q < qe; ++q) {
-              const int ee = m.elems[q];
-              FRec R;
-              load_frec(m.frec, ee, R);
-              if (!frec_passes<D>(R, xs)) continue;
-              const double v = frec_bestfirst<D>(R, xs);
-              if (bf_less(tv, te, v, ee) && bf_less(v, ee, bv, bb)) {
-                bv = v;
-                bb = ee;
-              }
-            }
-            if (bb != 0x7fffffff) {
-              e = bb;
-              tv = bv;
-              te = bb;
-            }
-          }
-        }
-        if (e >= 0) {
-          phase = 1;
-          break;
-        }
-        // the point is complete (its field value is evaluated afterwards)
-        if (part == 0) {
-          code[k] = bc;
-          elem[k] = be;
-          dist[k] = bd;
-          if (iters) iters[k] = it_tot;
-#pragma unroll
-          for (int a = 0; a < DR; ++a) r[k * DR + a] = br[a];
-        }
-        have_point = false;
-      }
-    }
-    // (b) the warp copies the requested candidates into their slots
-    for (unsigned req = __ballot_sync(FPX_FULL, phase == 1 && part == 0); req; req &= req - 1) {
-      const int j = __ffs(req) - 1;
-      const int ej = __shfl_sync(FPX_FULL, e, j);
-      const double* src = m.nodes + (int64_t)ej * D * K;
-      double* dst = slots + (j / G) * PL::SS;
-      for (int t = lane; t < D * K; t += FPX_WARP) cp_async8(dst + t, src + t);
-      cp_async_arrive_noinc(&mbars[j / G]);
-    }
-    if (phase == 1) phase = 2;
-    // (c) points whose copy landed get their seed (warp-cooperative, D7)
-    const bool landed = phase == 2 && mbar_test(&mbars[pslot], parity);
-    if (landed) parity ^= 1u;
-    for (unsigned rdy = __ballot_sync(FPX_FULL, landed && part == 0); rdy;) {
-      unsigned js[4];
-      const double* sj[4];
-      double xj[4][3];
-      int cnt = 0;
-#pragma unroll
-      for (int s2 = 0; s2 < 4; ++s2) {
-        js[s2] = rdy ? (unsigned)(__ffs(rdy) - 1) : 0u;
-        if (rdy) {
-          rdy &= rdy - 1;
-          cnt = s2 + 1;
-        }
-        sj[s2] = slots + (js[s2] / G) * PL::SS;
-#pragma unroll
-        for (int c = 0; c < D; ++c) xj[s2][c] = __shfl_sync(FPX_FULL, xs[c], js[s2]);
-      }
-      int bi = seed_batch<D, DR, N, false>(js, cnt, sj, xj, lane);
-      bi = __shfl_sync(FPX_FULL, bi, glead);  // the group leader holds the seed
-      if (bi >= 0 && landed) {
-        rc[0] = z[bi % N];
-        rc[1] = DR > 1 ? z[(bi / N) % N] : 0.0;
-        rc[2] = DR > 2 ? z[bi / (N * N)] : 0.0;
-      }
-    }
-    if (landed) {
-#pragma unroll
-      for (int a = 0; a < 3; ++a) rn[a] = rc[a];
-      first = true;
-      it = 0;
-      alpha = P.alpha0;
-      phase = 3;
-    }
-    if (!__any_sync(FPX_FULL, phase != 4)) break;
-    if (!__any_sync(FPX_FULL, phase == 3)) continue;  // copies in flight
-    // (d) one map evaluation for every point of the warp
-    const bool w2 = __any_sync(FPX_FULL, phase == 3 && on_boundary<DR>(rn));
-    ++nev;
-    nev2 += w2 ? 1 : 0;
-    nlev += (phase == 3 && part == 0) ? 1 : 0;
-    if (w2) eval_state_pair<D, DR, N, G, true>(mine, z, scale, rn, xs, st, part);
-    else eval_state_pair<D, DR, N, G, false>(mine, z, scale, rn, xs, st, part);
-    if (phase != 3) continue;
-    // (e) the point's trust-region Newton update (newton_warp, D8)
-    bool done = false;
-    if (first) {
-      first = false;
-    } else {
-      const double decr = fcur - st.f;
-      if (decr >= P.accept * pred) {
-        if (decr >= P.keep * pred) alpha *= P.grow;
-#pragma unroll
-        for (int a = 0; a < DR; ++a) rc[a] = rn[a];
-      } else {
-        alpha *= P.shrink;
-#pragma unroll
-        for (int t = 0; t < 3; ++t) st.J[t] = stash[t];
-#pragma unroll
-        for (int t = 0; t < 6; ++t) {
-          st.H0[t] = stash[3 + t];
-          st.Q[t] = stash[9 + t];
-        }
-        st.f = fcur;
-      }
-      if (smax < P.tol) done = true;
-      else if (it >= P.max_iters) done = true;
-    }
-    if (!done) {
-      fcur = st.f;
-      const bool go = propose_step<DR>(st, rc, it, alpha, rn, pred, smax);
-      ++it;
-      if (!go) {
-        done = true;
-      } else if (part == 0) {
-#pragma unroll
-        for (int t = 0; t < 3; ++t) stash[t] = st.J[t];
-#pragma unroll
-        for (int t = 0; t < 6; ++t) {
-          stash[3 + t] = st.H0[t];
-          stash[9 + t] = st.Q[t];
-        }
-      }
-    }
-    if (done) {
-      const double dd = sqrt(st.f);
-      if (part == 0) {
-        s_newton += 1;
-        s_iters += it;
-      }
-      it_tot += it;
-      const double epsd = DR < D ? eps_d_of(m, e) : 0.0;
-      const int cd = classify<D, DR>(rc, dd, epsd);
-      bool take;
-      if (cd == kInterior) take = bc != kInterior || e < be;
-      else take = bc != kInterior && (dd < bd || (dd == bd && e < be));
-      if (take) {
-        bc = cd;
-        be = e;
-        bd = dd;
-#pragma unroll
-        for (int a = 0; a < DR; ++a) br[a] = rc[a];
-      }
-      if (bc == kInterior) point_done = true;
-      phase = 0;
-    }
-  }
-  s_newton = warp_sum64(s_newton);
-  s_iters = warp_sum64(s_iters);
-  nlev = warp_sum64(nlev);
-  if (lane == 0) {
-    atomicAdd((unsigned long long*)&stats[FPX_STAT_NEWTON], (unsigned long long)s_newton);
-    atomicAdd((unsigned long long*)&stats[FPX_STAT_ITERS], (unsigned long long)s_iters);
-    atomicAdd((unsigned long long*)&stats[FPX_STAT_REST_WARP_EVALS], (unsigned long long)nev);
-    atomicAdd((unsigned long long*)&stats[FPX_STAT_REST_W2_EVALS], (unsigned long long)nev2);
-    atomicAdd((unsigned long long*)&stats[FPX_STAT_REST_LANE_EVALS], (unsigned long long)nlev);
-  }
-}
-
-
 // Block-wide inclusive sum over FPX_HMAX threads (one value per thread).
 __device__ __forceinline__ int64_t block_incl_sum(int64_t v, int64_t* ws) {
   const int lane = threadIdx.x % FPX_WARP, warp = threadIdx.x / FPX_WARP;
@@ -1802,13 +1299,6 @@ __global__ void __launch_bounds__(128, 2)
   // in full)
   const bool redo_pass = maxnp_dev == nullptr;
   const int64_t gmax = redo_pass && *npairs > pair_cap ? pair_cap : *npairs;
-#ifdef FPX_DIAG
-  // development counters (FPX_DIAG builds; the caller allocates 16 + 80
-  // stats): pair outcomes by rank bucket -- [pass*16 + kind*5 + rank]
-  // counts, +32 their iterations; kind 0 stopped by the found flag,
-  // 1 INTERIOR, 2 other; 64.. aborted by R2 (+5 iterations)
-  int64_t* g_diag_base = stats + 16;
-#endif
   int64_t s_newton = 0, s_iters = 0, nev = 0, nev2 = 0, nlev = 0;
   int64_t u = 0, k = 0;
   double xs[3] = {0.0, 0.0, 0.0};
@@ -2002,11 +1492,6 @@ __global__ void __launch_bounds__(128, 2)
     if (!done && *(volatile int32_t*)&found[u]) {
       // another candidate of this point was INTERIOR meanwhile: its record
       // is final (an INTERIOR is unique up to shared faces), stop this one
-#ifdef FPX_DIAG
-      { const int rb = cur.w < 4 ? cur.w : 4;
-        atomicAdd((unsigned long long*)&g_diag_base[(redo_pass ? 16 : 0) + rb], 1ull);
-        atomicAdd((unsigned long long*)&g_diag_base[32 + (redo_pass ? 16 : 0) + rb], (unsigned long long)it); }
-#endif
       s_newton += 1;
       s_iters += it;
       phase = 0;
@@ -2035,11 +1520,6 @@ __global__ void __launch_bounds__(128, 2)
       else stash_state(stash, st);
     }
     if (done && aborted) {
-#ifdef FPX_DIAG
-      { const int rb = cur.w < 4 ? cur.w : 4;
-        atomicAdd((unsigned long long*)&g_diag_base[64 + rb], 1ull);
-        atomicAdd((unsigned long long*)&g_diag_base[64 + 5 + rb], (unsigned long long)it); }
-#endif
       s_newton += 1;
       s_iters += it;
       phase = 0;
@@ -2066,12 +1546,6 @@ __global__ void __launch_bounds__(128, 2)
         for (int a = 0; a < DR; ++a) r[k * DR + a] = rc[a];
       }
       if (iters) iters[k] += it;
-#ifdef FPX_DIAG
-      { const int rb = cur.w < 4 ? cur.w : 4;
-        const int kind = cd == kInterior ? 5 : 10;
-        atomicAdd((unsigned long long*)&g_diag_base[(redo_pass ? 16 : 0) + kind + rb], 1ull);
-        atomicAdd((unsigned long long*)&g_diag_base[32 + (redo_pass ? 16 : 0) + kind + rb], (unsigned long long)it); }
-#endif
       if (cd == kInterior) found[u] = 1;
       __threadfence();
       atomicExch(&lock[u], 0);
@@ -2090,7 +1564,7 @@ __global__ void __launch_bounds__(128, 2)
   }
 }
 
-// Field values of the rest points (after k_rest_pairs settled their
+// Field values of the rest points (after k_rest_l1 settled their
 // records): thread per point, NaN for NOT_FOUND (D12).
 template <int DR, int N>
 __global__ void k_rest_values(const double* __restrict__ fbasis, int M,
@@ -2566,28 +2040,6 @@ inline size_t newton_smem(int geo, int fsz, int N, int wpb) {
 }
 
 template <int D, int DR, int N>
-struct Round1 {
-  static cudaError_t run(const fpx_mesh_t& m, const double* x, const int32_t* sorted,
-                         const Item* items, const int64_t* nitems_dev, int64_t items_cap,
-                         const int32_t* npass, int32_t* code, int32_t* elem, double* r,
-                         double* dist, int32_t* iters, const double* field, int C, double* values,
-                         int32_t* upts, int64_t* upair_cnt, int64_t* nun_dev, int64_t* stats,
-                         cudaStream_t st) {
-    using L = Lay<D, DR, N>;
-    const int threads = 128;
-    const size_t smem = newton_smem(L::GEO + Scratch<DR, N>::SLOTS * FPX_WARP,
-                                    field ? C * L::CS : 0, N, threads / FPX_WARP);
-    auto fn = k_newton_round1<D, DR, N>;
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    unsigned blocks = persistent_blocks((const void*)fn, threads, smem, items_cap);
-    fn<<<blocks, threads, smem, st>>>(m, x, sorted, items, nitems_dev, npass, code, elem, r, dist,
-                                      iters, field, C, values, upts, upair_cnt, nun_dev, stats);
-    return cudaGetLastError();
-  }
-};
-
-template <int D, int DR, int N>
 struct Stream {
   static constexpr int S = 3;
   static cudaError_t run(const fpx_mesh_t& m, const double* x, const int32_t* sorted,
@@ -2610,17 +2062,12 @@ struct Stream {
     auto fn = k_newton_stream<D, DR, N, S>;
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    static const int chunk_env = [] {
-      const char* v = getenv("FPX_R1_CHUNK");
-      const int c = v ? atoi(v) : 0;
-      return c < 0 ? 0 : c;
-    }();
     // chunk: FPX_CHUNK_DEFAULT points, shrunk when the stream is too short to
     // give every resident warp a chunk (a sparse stream - about one point per
     // element - keeps at most S lanes of a warp busy, so its latency is the
     // per-warp point count, not the total)
-    int chunk = chunk_env;
-    if (chunk == 0) {
+    int chunk;
+    {
       const int64_t warps = (int64_t)persistent_blocks((const void*)fn, threads, smem,
                                                        INT64_C(1) << 40) * wpb;
       const int64_t want = (n_cap + warps - 1) / (warps > 0 ? warps : 1);
@@ -2655,17 +2102,8 @@ struct Pairs {
   }
 };
 
-#ifndef FPX_REST_G
-#define FPX_REST_G 4
-#endif
 template <int D, int DR, int N>
 struct Rest {
-  using PL = PairLay<D, DR, N>;
-  static constexpr int G = FPX_REST_G;  // lanes per point
-  // warps per block (32/G points each) whose slots fit ~220 KB
-  static constexpr size_t WARP_BYTES = (size_t)(FPX_WARP / G) * (PL::SS * 8 + 8);
-  static constexpr int WPB0 = (int)((220 * 1024 - 256) / WARP_BYTES);
-  static constexpr int WPB = WPB0 > 16 ? 16 : (WPB0 < 1 ? 1 : WPB0);
   static cudaError_t run(const fpx_mesh_t& m, const double* x, int64_t nun_cap,
                          const int64_t* nun_dev, const int32_t* upts, const int32_t* clist,
                          const int16_t* cseed, const int32_t* cnum, const int32_t* nps,
@@ -2675,50 +2113,25 @@ struct Rest {
                          int32_t* found, int32_t* lock, int32_t* code, int32_t* elem, double* r,
                          double* dist, int32_t* iters, const double* field, int C,
                          double* values, int64_t* counter, int64_t* stats, cudaStream_t st) {
-    static const bool l1 = [] {
-      const char* v = getenv("FPX_REST");
-      return !(v && v[0] == 's');
-    }();
-    cudaError_t err;
-    if (l1) {
-      const int threads = 128;
-      const size_t smem = (size_t)(2 * ((N + 1) & ~1) + 4 * Scratch<DR, N>::SLOTS * FPX_WARP) * 8;
-      auto fn = k_rest_l1<D, DR, N>;
-      if (smem > 48 * 1024)
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      unsigned blocks = persistent_blocks((const void*)fn, threads, smem,
-                                          (nun_cap + FPX_WARP - 1) / FPX_WARP);
-      const int64_t cap = 2 * nun_cap + 1024;
-      // Pass 1 stops candidates held on a face (descent direction leaving
-      // it) for two consecutive iterations; pass 2 redoes every stopped
-      // candidate (of round 1 and of pass 1) in full for points still without
-      // an INTERIOR.  Exact either way; FPX_ABORT=0 disables both.
-      static const bool abort_pass = [] {
-        const char* v = getenv("FPX_ABORT");
-        return !(v && v[0] == '0');
-      }();
-      fn<<<blocks, threads, smem, st>>>(m, x, nun_dev, upts, clist, cseed, cnum, nps, perm, cum,
-                                        maxnp, best, pairs, cap, npairs, abort_pass ? 1 : 0, redo,
-                                        nredo, found, lock, code, elem, r, dist, iters, counter,
-                                        stats);
-      fn<<<blocks, threads, smem, st>>>(m, x, nun_dev, upts, clist, cseed, cnum, nps, perm, cum,
-                                          nullptr, best, redo, cap, nredo, 0, nullptr, nullptr,
-                                          found, lock, code, elem, r, dist, iters, counter + 1,
-                                          stats);
-      err = cudaGetLastError();
-    } else {
-      const int threads = WPB * FPX_WARP;
-      const size_t smem = (size_t)(2 * ((N + 1) & ~1)) * 8 + (size_t)WPB * WARP_BYTES;
-      if (smem > 227 * 1024) return cudaErrorInvalidValue;
-      auto fn = k_rest_pairs<D, DR, N, G, WPB>;
-      if (smem > 48 * 1024)
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      unsigned blocks = persistent_blocks((const void*)fn, threads, smem,
-                                          (nun_cap * G + FPX_WARP - 1) / FPX_WARP);
-      fn<<<blocks, threads, smem, st>>>(m, x, nun_dev, upts, clist, cnum, code, elem, r, dist,
-                                        iters, counter, stats);
-      err = cudaGetLastError();
-    }
+    const int threads = 128;
+    const size_t smem = (size_t)(2 * ((N + 1) & ~1) + 4 * Scratch<DR, N>::SLOTS * FPX_WARP) * 8;
+    auto fn = k_rest_l1<D, DR, N>;
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    unsigned blocks = persistent_blocks((const void*)fn, threads, smem,
+                                        (nun_cap + FPX_WARP - 1) / FPX_WARP);
+    const int64_t cap = 2 * nun_cap + 1024;
+    // Pass 1 stops candidates held on a face (descent direction leaving it)
+    // for two consecutive iterations; pass 2 redoes every stopped candidate
+    // (of round 1 and of pass 1) in full for points still without an
+    // INTERIOR.  The records are those of the full solves either way.
+    fn<<<blocks, threads, smem, st>>>(m, x, nun_dev, upts, clist, cseed, cnum, nps, perm, cum,
+                                      maxnp, best, pairs, cap, npairs, 1, redo, nredo, found,
+                                      lock, code, elem, r, dist, iters, counter, stats);
+    fn<<<blocks, threads, smem, st>>>(m, x, nun_dev, upts, clist, cseed, cnum, nps, perm, cum,
+                                      nullptr, best, redo, cap, nredo, 0, nullptr, nullptr,
+                                      found, lock, code, elem, r, dist, iters, counter + 1, stats);
+    cudaError_t err = cudaGetLastError();
     if (err != cudaSuccess || !field) return err;
     int64_t b = (nun_cap + 127) / 128;
     if (b > 148 * 8) b = 148 * 8;

@@ -18,8 +18,6 @@ from __future__ import annotations
 from dataclasses import dataclass, field as dfield
 
 from collections.abc import Mapping
-import os
-
 import numpy as np
 import torch
 
@@ -44,14 +42,10 @@ class EngineOptions:
     newton: NewtonSettings = dfield(default_factory=NewtonSettings)
     eps_d: float | None = None        # absolute surface threshold; None -> relative
     eps_d_rel: float = 1e-10
-    # finds of >= split_min points run as `split` concurrent slices (perf only;
-    # FPX_SPLIT overrides)
-    split: int = dfield(default_factory=lambda: int(os.environ.get("FPX_SPLIT", "1")))
-    split_min: int = 1 << 18
-    # host-buffer API: replay its device part as a CUDA graph (FPX_GRAPHS=0: off)
-    graphs: bool = dfield(default_factory=lambda: os.environ.get("FPX_GRAPHS", "1") != "0")
-    # local cells per axis = hash_refine * SPEC rule (perf only; FPX_HASH_REFINE overrides)
-    hash_refine: int = dfield(default_factory=lambda: int(os.environ.get("FPX_HASH_REFINE", "3")))
+    # host-buffer API: replay its device part as a CUDA graph
+    graphs: bool = True
+    # local cells per axis = hash_refine * SPEC rule (perf only; results do not depend on it)
+    hash_refine: int = 3
 
 
 @dataclass
@@ -340,40 +334,21 @@ def _find_local(S: EngineSetup, x: torch.Tensor, field: Field | None = None,
     if n == 0:
         return out, _stats_dict(np.zeros(_C.STATS_LEN, np.int64))
     x = x.contiguous()
-    k = S.options.split if n >= S.options.split_min else 1
-    if k <= 1:
-        return out, _find_into(S, x, out, field)
-    # k slices on k side streams: the slices' kernels overlap, so the tail
-    # of one slice's Newton kernels runs under the next slice's bulk work
-    comp = torch.cuda.current_stream(dev)
-    start = torch.cuda.Event()
-    start.record(comp)
-    bounds = [n * c // k for c in range(k + 1)]
-    parts = []
-    for c, sc in enumerate(_streams(S, k)):
-        a_, b_ = bounds[c], bounds[c + 1]
-        sc.wait_event(start)
-        with torch.cuda.stream(sc):
-            sl = {key: (v[a_:b_] if v is not None else None) for key, v in out.items()}
-            parts.append(_find_into(S, x[a_:b_], sl, field, slot=c))
-    for sc in _streams(S, k):
-        comp.wait_stream(sc)
-    return out, _SummedStats(parts)
-
-
-_DIAG_LEN = int(os.environ.get("FPX_DIAG_LEN", "0"))  # development builds (-DFPX_DIAG): 80
+    return out, _find_into(S, x, out, field)
 
 
 def _find_into(S: EngineSetup, x: torch.Tensor, out: dict, field: Field | None,
-               slot: int = 0) -> DeviceStats:
+               slot: int = 0, ws: torch.Tensor | None = None) -> DeviceStats:
     """fpx_find on the current stream writing into caller-provided device
-    slices (x contiguous); `slot` selects the workspace."""
+    slices (x contiguous); `slot` selects the shared workspace unless the
+    caller owns one (`ws`, e.g. a captured graph's)."""
     n = int(x.shape[0])
-    stats = torch.zeros(_C.STATS_LEN + _DIAG_LEN, dtype=torch.int64, device=S.device)
+    stats = torch.zeros(_C.STATS_LEN, dtype=torch.int64, device=S.device)
     if n == 0:
         return DeviceStats(stats)
     blocks, C = (field.blocks, int(field.blocks.shape[1])) if field is not None else (None, 0)
-    ws = _workspace(S, n, n, slot)
+    if ws is None:
+        ws = _workspace(S, n, n, slot)
     _C.check(_C.lib().fpx_find(
         S.mesh_t, n, _C.ptr(x), _C.ptr(out["code"]), _C.ptr(out["elem"]), _C.ptr(out["r"]),
         _C.ptr(out["dist"]), _C.ptr(out.get("iters")), _C.ptr(blocks), C,
@@ -494,7 +469,8 @@ def _host_overlapped(S: EngineSetup, f: Field, x: torch.Tensor, out: dict, ws: d
         ws["r1_event"].record(comp)  # torch creates the CUDA event on first record
     ev = ws["r1_event"]
     ws["x"].copy_(x, non_blocking=True)
-    gkey = (n, f.blocks.data_ptr(), f.components) + tuple(out[k].data_ptr() for k in _REC_KEYS)
+    gkey = (n, f.blocks.data_ptr(), f.components) + tuple(out[k].data_ptr() for k in _REC_KEYS) \
+        + tuple(ws[k].data_ptr() for k in ("x", "values", "code", "elem", "r", "dist"))
     if S.options.graphs and ws.get("graph_key") != gkey:
         # capture the device part once per buffers; a replay costs one launch
         # instead of ~60.  The side-stream download forks from the round-1
@@ -507,7 +483,8 @@ def _host_overlapped(S: EngineSetup, f: Field, x: torch.Tensor, out: dict, ws: d
         ws.update(graph=g, graph_key=gkey, graph_stats=st)
     if S.options.graphs:
         ws["graph"].replay()
-        st = ws["graph_stats"]
+        # a snapshot per call: the graph rewrites its counter buffer each replay
+        st = DeviceStats(ws["graph_stats"]._t.clone())
     else:
         st = _host_device_part(S, f, out, ws, ev, side)
     if not sync:
@@ -529,9 +506,15 @@ def _host_device_part(S: EngineSetup, f: Field, out: dict, ws: dict, ev, side):
     n, dr, C = int(ws["x"].shape[0]), S.ref_dim, f.components
     loc = dict(code=ws["code"], elem=ws["elem"], r=ws["r"], dist=ws["dist"], iters=None,
                values=ws["values"])
+    # the pipeline owns its find workspace: a captured graph keeps its
+    # pointer, so it must not be the shared one other calls may reallocate
+    need = L.fpx_find_workspace_bytes(S.mesh_t, n, n)
+    if ws.get("find_ws") is None or ws["find_ws"].numel() < need:
+        ws["find_ws"] = torch.empty(need, dtype=torch.uint8, device=S.device)
+    wsf = ws["find_ws"]
     L.fpx_set_round1_event(ev.cuda_event)
     try:
-        st = _find_into(S, ws["x"], loc, f)
+        st = _find_into(S, ws["x"], loc, f, ws=wsf)
     finally:
         L.fpx_set_round1_event(None)
     # after round 1 every record but the rest points' is final: download them
@@ -545,7 +528,6 @@ def _host_device_part(S: EngineSetup, f: Field, out: dict, ws: dict, ev, side):
                 torch.full_like(loc["elem"], -1), out=ws["rank"])
     out["rank"].copy_(ws["rank"], non_blocking=True)
     torch.cuda.current_stream(S.device).wait_stream(side)
-    wsf = _workspace(S, n, n)
     _C.check(L.fpx_rest_patch_host(dr, C, n, _C.ptr(wsf), wsf.numel(), S.mesh_t,
                                    _C.ptr(ws["code"]), _C.ptr(ws["elem"]), _C.ptr(ws["r"]),
                                    _C.ptr(ws["dist"]), _C.ptr(ws["values"]),
