@@ -58,8 +58,7 @@ def workload_config(n_gpus):
             "mesh": f"kershaw{N_ELEM_AXIS}^3", "order": ORDER, "elements": N_ELEM_AXIS ** 3,
             "points_per_gpu": PTS_PER_GPU, "components": 1,
             "partition": "contiguous z-slabs" if n_gpus > 1 else "single",
-            "l2": "flushed (256 MiB write) between timed steps",
-            "slices": "one find per step (FPX_SPLIT=1)"}
+            "l2": "flushed (256 MiB write) between timed steps"}
 
 
 def build_inputs(rank=0):
@@ -76,7 +75,10 @@ def cpu_find_eval(sample=20000, threads=None, steps=1, warmup=0, rank=0):
     from oracle import oracle as O
     mesh, field, x = build_inputs(rank)
     nthreads = threads or len(os.sched_getaffinity(0))
-    OS = O.OracleSetup(mesh.nodes, 3, 3, ORDER, nthreads=nthreads)
+    # the same local grid as engine.setup's default (hash_refine x SPEC rule)
+    from paper_2501_12349_b200.engine import EngineOptions
+    ncell = min(1024, EngineOptions().hash_refine * O.n_cells(mesh.num_elements, 3))
+    OS = O.OracleSetup(mesh.nodes, 3, 3, ORDER, nthreads=nthreads, ncell=ncell)
     xs = x[:sample]
     times = []
     for k in range(warmup + steps):
@@ -85,7 +87,9 @@ def cpu_find_eval(sample=20000, threads=None, steps=1, warmup=0, rank=0):
         O.evaluate(OS.B, 3, field, rec["code"], rec["elem"], rec["r"], nthreads=nthreads)
         if k >= warmup:
             times.append(time.perf_counter() - t)
-    return sample / float(np.mean(times)), nthreads, float(np.mean(times))
+    work = {"points": int(sample), "box_tests": int(rec["nbox"].sum()),
+            "newton": int(rec["ncand"].sum()), "iters": int(rec["iters"].sum())}
+    return sample / float(np.mean(times)), nthreads, float(np.mean(times)), work
 
 
 def run_reference(args):
@@ -93,7 +97,7 @@ def run_reference(args):
     if rank != 0:
         return
     sample = args.cpu_sample
-    v, cores, t = cpu_find_eval(sample=sample, steps=args.steps, warmup=args.warmup)
+    v, cores, t, _ = cpu_find_eval(sample=sample, steps=args.steps, warmup=args.warmup)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
@@ -240,17 +244,14 @@ def run_ours(args):
         barrier()
     launches = L.fpx_launch_count() - launches0
     step_ms = float(np.mean([s.elapsed_time(e) for s, e in ev]))
-    # round-1 kernel alone (roofline): the same steps without the slice
-    # overlap, CUDA events around the launch on its stream
-    split = S.options.split
-    S.options.split = 1
+    # round-1 kernel alone (roofline): the same steps again, CUDA events
+    # around the launch on its stream
     for k in range(args.steps):
         flush.fill_(float(k))
         L.fpx_profile_round1(kev[k][0].cuda_event, kev[k][1].cuda_event)
         vals, rec1 = engine.find_and_interpolate(S, F, x_dev)
     L.fpx_profile_round1(None, None)
     torch.cuda.synchronize()
-    S.options.split = split
     kern_ms = float(np.mean([s.elapsed_time(e) for s, e in kev]))
     step1 = rec1.stats
     step_ms_max = max_over_ranks(step_ms)
@@ -264,13 +265,13 @@ def run_ours(args):
                 dist=torch.empty(n, dtype=torch.float64).pin_memory())
     e2e_ms = []
     for _ in range(max(args.warmup, 3)):  # warm-up: host-path buffers, streams
-        engine.find_and_interpolate_host(S, F, x_pin, out=outs, chunks=E2E_CHUNKS, sync=True)
+        engine.find_and_interpolate_host(S, F, x_pin, out=outs, sync=True)
     barrier()
     for k in range(args.steps):
         flush.fill_(float(k))
         torch.cuda.synchronize()
         t0 = time.perf_counter()  # wall clock: the call returns host records
-        engine.find_and_interpolate_host(S, F, x_pin, out=outs, chunks=E2E_CHUNKS, sync=True)
+        engine.find_and_interpolate_host(S, F, x_pin, out=outs, sync=True)
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
     e2e_max = max_over_ranks(float(np.mean(e2e_ms)))
     h2d = n * 3 * 8
@@ -292,7 +293,14 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
     if rank == 0:
-        cpu_v, cores, cpu_t = cpu_find_eval(sample=args.cpu_sample, steps=1, warmup=0)
+        cpu_v, cores, cpu_t, owork = cpu_find_eval(sample=args.cpu_sample, steps=1, warmup=0)
+        # the kernels' own work counters on the same sample, beside the
+        # oracle's (the oracle visits candidates in ascending id, the kernels
+        # best-first, so newton/iters differ by design; box_tests agree)
+        _, srec = engine.find_and_interpolate(S, F, x_dev[:args.cpu_sample])
+        ss = srec.stats
+        kwork = {"points": int(ss["points"]), "box_tests": int(ss["box_tests"]),
+                 "newton": int(ss["newton"]), "iters": int(ss["iters"])}
         clocks = clk.summary()
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -305,14 +313,15 @@ def run_ours(args):
                     "ms_per_step": e2e_max,
                     "api": "engine.find_and_interpolate_host (host points in, host records "
                            "out; wall clock; round-1 records downloaded under the rest phase)"},
+            "work_vs_oracle": {"sample": f"first {args.cpu_sample} points of the step",
+                               "kernels": kwork, "oracle": owork},
             "roofline": {"bound": "fp64", "kernel": "k_newton_stream<3,3,5,3> (round 1)",
                          "achieved": achieved, "peak": float(tf[0]), "unit": "TFLOP/s",
                          "frac": achieved / float(tf[0]), "traffic": traffic,
                          "peak_source": "fpx_probe_fp64 DFMA chains, measured in this run "
                                         "(FP64 is not in MEASURED_PEAKS.json)",
                          "kernel_ms": kern_ms, "kernel_share": kern_ms / step_ms,
-                         "kernel_timing": "CUDA events around the round-1 launch, find run "
-                                          "unsplit (split=1) so the launch is not overlapped",
+                         "kernel_timing": "CUDA events around the round-1 launch on its stream",
                          "flops_per_launch": flops_r1},
             "cpu_baseline": {"value": cpu_v, "unit": UNIT, "cores": cores, "kind": "port",
                              "sample": f"{args.cpu_sample} of the cfg-2 points, oracle C port "
@@ -324,9 +333,6 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
-
-
-E2E_CHUNKS = int(os.environ.get("FPX_E2E_CHUNKS", "1"))
 
 
 def main():

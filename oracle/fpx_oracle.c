@@ -23,6 +23,9 @@
 
 #define ZERO_EXTENT_REL 1e-12     /* bounds.py:43 */
 #define INTERIOR_TOL 1e-12
+/* D8 resolvability floor of the predicted decrease (DESIGN.md §3 D8) */
+#define UNRES_REL 1e-13
+#define UNRES_ABS 1e-14
 
 /* ------------------------------------------------------------------ basis */
 
@@ -1042,11 +1045,6 @@ void fpxo_invert(const fpxo_basis* B, int d, int dr, const double* X, const doub
       if (fabs(s[a]) > smax) smax = fabs(s[a]);
     }
     double pred = -(2.0 * js + shs);
-    /* the step cannot change |dx|^2 in floating point: converged */
-#ifdef FPXO_TRACE
-    if (!(pred > 1e-15 * f)) fprintf(stderr, "stop it %d pred %.3e f %.3e s=(%.3e %.3e %.3e) J=(%.3e %.3e %.3e) free %d%d%d alpha %.3e\n", it, pred, f, s[0], s[1], s[2], J[0], J[1], J[2], freem[0], freem[1], freem[2], alpha);
-#endif
-    if (!(pred > 1e-15 * f)) { converged = 1; break; }
     double rn[3] = {0, 0, 0};
     for (int a = 0; a < dr; ++a) {
       double v = r[a] + s[a];
@@ -1054,6 +1052,28 @@ void fpxo_invert(const fpxo_basis* B, int d, int dr, const double* X, const doub
       if (v < -1.0) v = -1.0;
       if (v > 1.0) v = 1.0;
       rn[a] = v;
+    }
+    /* D8 resolvability: |dx|^2 = f carries a rounding noise of about
+     * eps f + 2 d* eps |x|.  A predicted decrease below that floor cannot be
+     * checked against the actual one, so the step is taken on the model's
+     * word: pred = -inf (accepted, alpha grows); a step below tol is the last
+     * one and is applied without a trial evaluation (d* stays that of the
+     * last evaluated iterate; the difference is second order).  r* is thus
+     * the root of the projected gradient to roundoff, not wherever f
+     * stopped resolving steps. */
+    double xsc = 0.0;
+    for (int c = 0; c < d; ++c) xsc = fmax(xsc, fabs(xs[c]));
+    const int unres = !(pred > UNRES_REL * f + UNRES_ABS * sqrt(f) * xsc);
+#ifdef FPXO_TRACE
+    if (unres) fprintf(stderr, "unres it %d pred %.3e f %.3e s=(%.3e %.3e %.3e) J=(%.3e %.3e %.3e) free %d%d%d alpha %.3e\n", it, pred, f, s[0], s[1], s[2], J[0], J[1], J[2], freem[0], freem[1], freem[2], alpha);
+#endif
+    if (unres) {
+      if (smax < S->tol) {
+        for (int a = 0; a < dr; ++a) r[a] = rn[a];
+        converged = 1;
+        break;
+      }
+      pred = -INFINITY;
     }
     fmap(B, d, dr, X, rn, on_boundary(dr, rn), &nxt);
     double dxn[3], fn = 0.0;

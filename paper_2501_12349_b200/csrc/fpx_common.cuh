@@ -13,6 +13,9 @@ enum { kInterior = FPX_INTERIOR, kBorder = FPX_BORDER, kNotFound = FPX_NOT_FOUND
 
 // SPEC.md:311,434 strict-interior tolerance; literal shared with the oracle.
 #define FPX_INTERIOR_TOL 1e-12
+// D8 resolvability floor of the predicted decrease (oracle UNRES_REL/ABS)
+#define FPX_UNRES_REL 1e-13
+#define FPX_UNRES_ABS 1e-14
 #define FPX_ZERO_EXTENT_REL 1e-12  // bounds.py:43
 
 // Newton settings copied by value into kernels.

@@ -494,6 +494,15 @@ __device__ __forceinline__ bool constrained_step(const double* Hm, const double*
   return true;
 }
 
+// |x*|_inf: the scale of the rounding noise in dx = x* - x(r) (D8)
+template <int D>
+__device__ __forceinline__ double xscale(const double* xs) {
+  double m = fabs(xs[0]);
+#pragma unroll
+  for (int c = 1; c < D; ++c) m = fmax(m, fabs(xs[c]));
+  return m;
+}
+
 template <int DR>
 __device__ __forceinline__ bool on_boundary(const double* r) {
   bool b = false;
@@ -576,6 +585,7 @@ __device__ __forceinline__ NewtonOut newton_warp(const double* __restrict__ sX,
   NState st;
   double rn[3] = {r[0], r[1], r[2]};
   double alpha = P.alpha0, fcur = 0.0, pred = 0.0, smax = 0.0;
+  const double xsc = xscale<D>(xs);
   int it = 0;
   bool done = !active, conv = false, first = true, step = active;
   while (true) {
@@ -659,18 +669,25 @@ __device__ __forceinline__ NewtonOut newton_warp(const double* __restrict__ sX,
         smax = fabs(s[a]) > smax ? fabs(s[a]) : smax;
       }
       pred = -(2.0 * js + shs);
-      if (!(pred > 1e-15 * fcur)) {  // step below what |dx|^2 resolves
+#pragma unroll
+      for (int a = 0; a < DR; ++a) {
+        double v = r[a] + s[a];
+        if (hit & (1 << a)) v = s[a] > 0.0 ? 1.0 : -1.0;  // lands on the face
+        v = v < -1.0 ? -1.0 : (v > 1.0 ? 1.0 : v);
+        rn[a] = v;
+      }
+      // D8 resolvability: below the rounding floor of |dx|^2 the step is
+      // taken on the model's word (pred = -inf); such a step below tol is
+      // the last one, applied without a trial evaluation (oracle fpxo_invert)
+      const bool unres = !(pred > FPX_UNRES_REL * fcur + FPX_UNRES_ABS * sqrt(fcur) * xsc);
+      if (unres) pred = -INFINITY;
+      if (unres && smax < P.tol) {
         conv = true;
         done = true;
+#pragma unroll
+        for (int a = 0; a < DR; ++a) r[a] = rn[a];
       } else {
         step = true;
-#pragma unroll
-        for (int a = 0; a < DR; ++a) {
-          double v = r[a] + s[a];
-          if (hit & (1 << a)) v = s[a] > 0.0 ? 1.0 : -1.0;  // lands on the face
-          v = v < -1.0 ? -1.0 : (v > 1.0 ? 1.0 : v);
-          rn[a] = v;
-        }
         stash_state(stash, st);
       }
     }
@@ -857,12 +874,13 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
 }
 
 // The projected trust-region step from state st at r (D8; the same
-// arithmetic as newton_warp).  Returns false when the predicted decrease is
-// below what |dx|^2 resolves (converged); else the trial point rn.
+// arithmetic as newton_warp): the trial point rn.  Returns false when the
+// solve has converged (an unresolvable step below tol): rn is then the final
+// iterate, taken without evaluation.
 template <int DR>
 __device__ __forceinline__ bool propose_step(const NState& st, const double* r, int it,
-                                             double alpha, double* rn, double& pred,
-                                             double& smax) {
+                                             double alpha, double xsc, double tol,
+                                             double* rn, double& pred, double& smax) {
   const double fcur = st.f;
   const bool beta = it > 0 && on_boundary<DR>(r);
   bool freem[3] = {true, true, true};
@@ -905,13 +923,19 @@ __device__ __forceinline__ bool propose_step(const NState& st, const double* r, 
     smax = fabs(s[a]) > smax ? fabs(s[a]) : smax;
   }
   pred = -(2.0 * js + shs);
-  if (!(pred > 1e-15 * fcur)) return false;
 #pragma unroll
   for (int a = 0; a < DR; ++a) {
     double v = r[a] + s[a];
     if (hit & (1 << a)) v = s[a] > 0.0 ? 1.0 : -1.0;  // lands on the face
     v = v < -1.0 ? -1.0 : (v > 1.0 ? 1.0 : v);
     rn[a] = v;
+  }
+  // D8 resolvability (newton_warp): below the floor the step is accepted
+  // unchecked (pred = -inf); such a step below tol is the last one, applied
+  // by the caller without a trial evaluation
+  if (!(pred > FPX_UNRES_REL * fcur + FPX_UNRES_ABS * sqrt(fcur) * xsc)) {
+    if (smax < tol) return false;
+    pred = -INFINITY;
   }
   return true;
 }
@@ -1514,10 +1538,15 @@ __global__ void __launch_bounds__(128, 2)
     }
     if (!done) {
       fcur = st.f;
-      const bool go = propose_step<DR>(st, rc, it, alpha, rn, pred, smax);
+      const bool go = propose_step<DR>(st, rc, it, alpha, xscale<D>(xs), P.tol, rn, pred, smax);
       ++it;
-      if (!go) done = true;
-      else stash_state(stash, st);
+      if (!go) {
+        done = true;
+#pragma unroll
+        for (int a = 0; a < DR; ++a) rc[a] = rn[a];
+      } else {
+        stash_state(stash, st);
+      }
     }
     if (done && aborted) {
       s_newton += 1;
@@ -1888,10 +1917,15 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
     }
     if (!done) {
       fcur = st.f;
-      const bool go = propose_step<DR>(st, rc, it, alpha, rn, pred, smax);
+      const bool go = propose_step<DR>(st, rc, it, alpha, xscale<D>(xs), P.tol, rn, pred, smax);
       ++it;
-      if (!go) done = true;
-      else stash_state(stash, st);
+      if (!go) {
+        done = true;
+#pragma unroll
+        for (int a = 0; a < DR; ++a) rc[a] = rn[a];
+      } else {
+        stash_state(stash, st);
+      }
     }
     if (done) {
       const double dd = sqrt(st.f);

@@ -4,10 +4,13 @@ Contract (north_star):
   * setup: AABB / OBB / hash boxes bit-identical to the oracle fed the same
     basis constants; the CSR local map identical;
   * find: codes bit-exact; elements bit-exact except points within 1e-10 of
-    a shared face (either owner accepted); INTERIOR r to 1e-12; BORDER
-    compared by d* (1e-10 rel) with r* to 1e-6 (the distance is flat at a
-    boundary minimum, so r* is only defined to ~sqrt(eps));
-  * eval: 1e-10 relative at INTERIOR records (1e-6 at BORDER ones).
+    a shared face (either owner accepted); r* to 1e-12 and d* to 1e-12
+    relative (1e-14 absolute) for every found record.  A BORDER minimum
+    outside an element can be worse conditioned than that: there r* is held
+    to 8x its own roundoff sensitivity kappa (r_sensitivity), which no
+    implementation in another arithmetic order can beat (the oracle built
+    with and without FMA differs by up to 3e-12 at cfg-2 exterior points);
+  * eval: 1e-10 relative for every found record.
 """
 import numpy as np
 import pytest
@@ -19,6 +22,10 @@ from paper_2501_12349_b200.basis import BasisConstants, ReferenceBasis, build_ba
 
 pytestmark = pytest.mark.gpu
 
+R_TOL = 1e-12       # north_star: reference coordinates
+V_RTOL = 1e-10      # north_star: interpolated values (relative)
+_SYM = ((0, 3, 4), (3, 1, 5), (4, 5, 2))
+
 
 def oracle_for(S, nodes, **kw):
     bc = BasisConstants.of(S.basis, S.envelope)
@@ -26,7 +33,46 @@ def oracle_for(S, nodes, **kw):
     return O.OracleSetup(nodes, S.phys_dim, S.ref_dim, S.order, B=B, ncell=S.ncell, **kw)
 
 
-def assert_find_parity(S, OS, x, field=None, rtol_val=1e-10):
+def r_sensitivity(OS, x, elem, r, dist):
+    """Roundoff sensitivity kappa of a minimiser r* of |x* - x(r)|^2 / 2 on
+    its free axes F.  The gradient J = -G^T dx is computed with an error of
+    about eps (|G_F| |dx rounding| + d* |dG rounding|): x(r) and G(r) are
+    sums of |X|-sized node values times Lagrange factors, so
+      kappa = eps |H_FF^-1|_2 (|G_F|_2 max(1, |x*|) + d* Lambda'_F |X|_inf),
+    with H = G^T G - sum_c dx_c d2x_c the exact Hessian and Lambda'_F the
+    largest Lebesgue sum of a first derivative along a free axis.  Checked
+    against long-double roots: both implementations lie within 0.4 kappa
+    of the true minimiser."""
+    d, dr = OS.d, OS.dr
+    eps = 2.220446049250313e-16
+    out = np.zeros(len(elem))
+    for k in range(len(elem)):
+        rk = np.asarray(r[k], float)
+        F = [a for a in range(dr) if abs(rk[a]) < 1.0]
+        if not F:
+            continue
+        X = OS.nodes[elem[k]]
+        xx, G, H2 = O.forward_map(OS.B, d, dr, X, rk, second=True)
+        dx = x[k] - xx
+        H = G.T @ G
+        for a in range(dr):
+            for b in range(dr):
+                H[a, b] -= dx @ H2[:, _SYM[a][b]]
+        try:
+            Hi = np.linalg.inv(H[np.ix_(F, F)])
+        except np.linalg.LinAlgError:
+            out[k] = np.inf
+            continue
+        v, d1, _ = O.lagrange(OS.B, rk)
+        lam, lamd = np.abs(v).sum(axis=1), np.abs(d1).sum(axis=1)
+        lp = max(lamd[a] * np.prod([lam[b] for b in range(dr) if b != a]) for a in F)
+        out[k] = eps * np.linalg.norm(Hi, 2) * (
+            np.linalg.norm(G[:, F], 2) * max(1.0, np.abs(x[k]).max())
+            + dist[k] * lp * np.abs(X).max())
+    return out
+
+
+def assert_find_parity(S, OS, x, field=None, rtol_val=V_RTOL):
     if field is not None:
         vals, rec = engine.find_and_interpolate(S, field, x)
     else:
@@ -55,24 +101,37 @@ def assert_find_parity(S, OS, x, field=None, rtol_val=1e-10):
                       f"{orec['dist'][i]:.3e})" for i in idx[:6])
     same = ~diff
     inter = same & (code == 0)
+    report = {"n": len(code), "interior": int(inter.sum()), "r_err_interior": 0.0,
+              "r_err_border": 0.0, "border_kappa_bound": 0}
     if inter.any():
-        assert np.max(np.abs(r[inter] - orec["r"][inter])) < 1e-12
-        assert np.max(np.abs(dist[inter] - orec["dist"][inter])) < 1e-12
+        report["r_err_interior"] = float(np.max(np.abs(r[inter] - orec["r"][inter])))
+        assert report["r_err_interior"] < R_TOL
+        assert np.max(np.abs(dist[inter] - orec["dist"][inter])) < R_TOL
     bord = same & (code == 1)
     if bord.any():
-        np.testing.assert_allclose(dist[bord], orec["dist"][bord], rtol=1e-10, atol=1e-12)
-        # r* of a boundary minimum is defined only to ~sqrt(eps): d* is flat there
-        assert np.max(np.abs(r[bord] - orec["r"][bord])) < 1e-6
+        # d* = |x* - x(r*)|: 1e-12 relative, or the absolute rounding of x(r)
+        np.testing.assert_allclose(dist[bord], orec["dist"][bord], rtol=R_TOL, atol=1e-14)
+        err = np.max(np.abs(r[bord] - orec["r"][bord]), axis=1)
+        report["r_err_border"] = float(err.max())
+        over = err >= R_TOL
+        if over.any():
+            bi = np.nonzero(bord)[0][over]
+            kap = r_sensitivity(OS, x[bi], orec["elem"][bi], orec["r"][bi], orec["dist"][bi])
+            report["border_kappa_bound"] = int(over.sum())
+            report["max_err_over_kappa"] = float(np.max(err[over] / kap))
+            worst = np.argmax(err[over] / kap)
+            assert np.all(err[over] < 8 * kap), (
+                f"BORDER r* off by {err[over][worst]:.3e} > 8 kappa = {8 * kap[worst]:.3e} "
+                f"at x={x[bi[worst]].tolist()}")
     nf = code == 2
     assert np.all(elem[nf] == -1) and np.all(np.isnan(dist[nf]))
     if field is not None:
         v = vals.cpu().numpy()
         ov = O.evaluate(OS.B, S.ref_dim, field, orec["code"], orec["elem"], orec["r"])
-        f = (code == 0) & same
+        f = (code != 2) & same
         np.testing.assert_allclose(v[f], ov[f], rtol=rtol_val, atol=1e-12)
-        b = (code == 1) & same
-        np.testing.assert_allclose(v[b], ov[b], rtol=1e-6, atol=1e-8)
         assert np.all(np.isnan(v[nf]))
+    rec.report = report
     return rec, orec
 
 
@@ -205,26 +264,37 @@ def test_bounds_api_matches_reference_goldens():
             assert np.array_equal(b2.upper, gd[f"fb_p{p}_hi2"][k])
 
 
-def test_cfg2_full_size_properties():
-    """cfg-2 size (32^3 hexes p=4, 10^6 points): size-independent properties
-    -- every point of [0,1]^3 is found, INTERIOR records reproduce x* through
-    the coordinate field, and a sample agrees with the oracle."""
+def test_cfg2_full_size_vs_oracle():
+    """cfg-2 at full size (Kershaw 32^3 hexes, p=4, 10^6 uniform points, the
+    bench workload): every record against the oracle under the full contract
+    (codes and elements bit-exact up to shared faces, r* 1e-12, values 1e-10),
+    plus size-independent properties: every point of [0,1]^3 is found and
+    the coordinate field reproduces x*."""
     m = toolkit.kershaw_mesh(32, 4)
     S = engine.setup(m)
+    OS = oracle_for(S, m.nodes, nthreads=0)
     x = toolkit.uniform_points(1_000_000, 3, seed=7)
-    f = toolkit.analytic_field("coordinates", m)
-    v, rec = engine.find_and_interpolate(S, f, x)
+    rec, orec = assert_find_parity(S, OS, x, toolkit.analytic_field("smooth", m))
     code = rec.code.cpu().numpy()
     assert np.all(code != 2)
+    print("cfg2 parity report:", rec.report)
+    v = engine.interpolate(S, toolkit.analytic_field("coordinates", m), rec).cpu().numpy()
     inter = code == 0
     assert inter.mean() > 0.999
-    assert np.max(np.abs(v.cpu().numpy()[inter] - x[inter])) < 1e-10
+    assert np.max(np.abs(v[inter] - x[inter])) < 1e-10
+
+
+def test_cfg2_exterior_border_records():
+    """BORDER records at the headline mesh: points up to 0.05 outside the
+    unit cube, compared with the oracle under the full contract."""
+    m = toolkit.kershaw_mesh(32, 4)
+    S = engine.setup(m)
     OS = oracle_for(S, m.nodes, nthreads=0)
-    sub = x[::50]
-    orec = OS.find(sub)
-    assert np.array_equal(code[::50], orec["code"])
-    same = rec.elem.cpu().numpy()[::50] == orec["elem"]
-    assert same.mean() > 0.999
+    x = toolkit.uniform_points(200_000, 3, seed=17, lo=-0.05, hi=1.05)
+    rec, orec = assert_find_parity(S, OS, x, toolkit.analytic_field("smooth", m))
+    print("cfg2 exterior parity report:", rec.report, rec.counts())
+    c = rec.counts()
+    assert c["BORDER"] > 3000 and c["NOT_FOUND"] > 0
 
 
 @pytest.mark.parametrize("kind", ["sphere", "torus"])
@@ -273,11 +343,14 @@ def test_host_pipeline_matches_device(chunks, kind):
     code = rec.code.cpu()
     assert torch.equal(out["code"], code)
     assert torch.equal(out["rank"], rec.rank.cpu())
-    inter = code == 0
-    assert torch.equal(out["elem"][inter], rec.elem.cpu()[inter])
-    assert torch.allclose(out["r"][inter], rec.r.cpu()[inter], rtol=0, atol=1e-12)
+    # every found record (the zero-copy patch rewrites the rest points, many
+    # of which end BORDER): same element, r*, d* and value as the device API
+    found = code != 2
+    assert torch.equal(out["elem"], rec.elem.cpu())
+    assert torch.allclose(out["r"][found], rec.r.cpu()[found], rtol=0, atol=1e-12)
+    assert torch.allclose(out["dist"][found], rec.dist.cpu()[found], rtol=1e-12, atol=1e-15)
     v, vd = out["values"], vals.cpu()
-    assert torch.allclose(v[inter], vd[inter], rtol=1e-10, atol=1e-12)
+    assert torch.allclose(v[found], vd[found], rtol=1e-10, atol=1e-12)
     assert torch.isnan(v[code == 2]).all()
     assert out["stats"]["points"] == x.shape[0]
 
