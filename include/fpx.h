@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define FPX_ABI_VERSION 3
+#define FPX_ABI_VERSION 4
 
 /* error codes */
 #define FPX_OK 0
@@ -216,9 +216,12 @@ int fpx_findpts_eval(int dr, int Nf, const double* fbasis, int C, int64_t E,
                      const double* r, double* values, void* ws, size_t ws_bytes, void* stream);
 
 /* invmap.invert_point batched over explicit (point, element) pairs
- * (SPEC.md:298-307): r [npairs][dr], dist, iters, converged. */
+ * (SPEC.md:298-307): r [npairs][dr], dist, iters, converged.  r0
+ * [npairs][dr] is the initial guess (SPEC.md:298 r0), or NULL for the D7
+ * seed (nearest GLL node). */
 int fpx_invert_pairs(const fpx_mesh_t* m, int64_t npairs, const double* x, const int32_t* elem,
-                     double* r, double* dist, int32_t* iters, int32_t* converged, void* stream);
+                     const double* r0, double* r, double* dist, int32_t* iters,
+                     int32_t* converged, void* stream);
 
 /* invmap.forward_map batched: x [n][d], G [n][d][dr],
  * H2 [n][d][6] (optional; symmetric order rr,ss,tt,rs,rt,st). */

@@ -964,8 +964,20 @@ int fpxo_diag_abort_it = -1;
 int fpxo_diag_abort_it2 = -1;   /* first iteration held for the 2nd consecutive time */
 double fpxo_diag_abort_f = 0.0;  /* |dx|^2 when the rule first fired */
 
+void fpxo_invert_from(const fpxo_basis* B, int d, int dr, const double* X, const double* xs,
+                      const fpxo_newton* S, const double* r0, double* r_out, double* dist,
+                      int* iters, int* conv);
+
 void fpxo_invert(const fpxo_basis* B, int d, int dr, const double* X, const double* xs,
                  const fpxo_newton* S, double* r_out, double* dist, int* iters, int* conv) {
+  fpxo_invert_from(B, d, dr, X, xs, S, NULL, r_out, dist, iters, conv);
+}
+
+/* invert_point with an explicit initial guess r0 (NULL -> the
+ * D7 nearest-node seed), clamped to [-1, 1]. */
+void fpxo_invert_from(const fpxo_basis* B, int d, int dr, const double* X, const double* xs,
+                      const fpxo_newton* S, const double* r0, double* r_out, double* dist,
+                      int* iters, int* conv) {
   fpxo_diag_abort_it = -1;
   fpxo_diag_abort_it2 = -1;
   int held_prev = 0;
@@ -983,6 +995,8 @@ void fpxo_invert(const fpxo_basis* B, int d, int dr, const double* X, const doub
   r[0] = B->z[bi % N];
   if (dr > 1) r[1] = B->z[(bi / N) % N];
   if (dr > 2) r[2] = B->z[bi / (N * N)];
+  if (r0)
+    for (int a = 0; a < dr; ++a) r[a] = fmin(1.0, fmax(-1.0, r0[a]));
   fmap_t cur, nxt;
   fmap(B, d, dr, X, r, on_boundary(dr, r), &cur);
   double dx[3], f = 0.0;

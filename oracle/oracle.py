@@ -96,6 +96,8 @@ def lib():
         L.fpxo_forward_map.argtypes = [C.POINTER(Basis), C.c_int, C.c_int, P, P, P, P, P]
         L.fpxo_invert.argtypes = [C.POINTER(Basis), C.c_int, C.c_int, P, P,
                                   C.POINTER(Newton), P, P, P, P]
+        L.fpxo_invert_from.argtypes = [C.POINTER(Basis), C.c_int, C.c_int, P, P,
+                                       C.POINTER(Newton), P, P, P, P, P]
         L.fpxo_find.argtypes = [C.POINTER(Mesh), C.c_int64, P, P, P, P, P, P, P, P, C.c_int]
         L.fpxo_eval.argtypes = [C.POINTER(Basis), C.c_int, C.c_int, P, C.c_int64, P, P, P, P,
                                 C.c_int]
@@ -306,11 +308,13 @@ def evaluate(Bf, dr, field, code, elem, r, nthreads=0):
     return out
 
 
-def invert(B, d, dr, X, xs, newton=None):
+def invert(B, d, dr, X, xs, newton=None, r0=None):
     X = _f64(X); xs = _f64(xs)
     r = np.zeros(3); dist = np.zeros(1); it = np.zeros(1, np.int32); cv = np.zeros(1, np.int32)
     S = newton or default_newton()
-    lib().fpxo_invert(C.byref(B), d, dr, _p(X), _p(xs), C.byref(S), _p(r), _p(dist), _p(it), _p(cv))
+    r0a = None if r0 is None else _f64(np.resize(np.asarray(r0, float), 3))
+    lib().fpxo_invert_from(C.byref(B), d, dr, _p(X), _p(xs), C.byref(S),
+                           _p(r0a) if r0a is not None else None, _p(r), _p(dist), _p(it), _p(cv))
     return r[:dr].copy(), float(dist[0]), int(it[0]), bool(cv[0])
 
 

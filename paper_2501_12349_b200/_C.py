@@ -14,7 +14,7 @@ import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FPX_LIB") or os.path.join(HERE, "lib", "libfpx_sm100.so")
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 INTERIOR, BORDER, NOT_FOUND = 0, 1, 2
 STAT_NAMES = ["points", "box_tests", "newton", "iters", "rest_points", "r1_warp_evals",
@@ -84,7 +84,7 @@ def lib():
         "fpx_find": ([C.POINTER(MeshT), i64, P, P, P, P, P, P, P, i32, P, P, i64, P, sz, P], i32),
         "fpx_eval_workspace_bytes": ([i64, i64], sz),
         "fpx_findpts_eval": ([i32, i32, P, i32, i64, P, i64, P, P, P, P, P, sz, P], i32),
-        "fpx_invert_pairs": ([C.POINTER(MeshT), i64, P, P, P, P, P, P, P], i32),
+        "fpx_invert_pairs": ([C.POINTER(MeshT), i64, P, P, P, P, P, P, P, P], i32),
         "fpx_forward_map": ([C.POINTER(MeshT), i64, P, P, P, P, P, P], i32),
         "fpx_route_count": ([i64, P, i32, P, P], i32),
         "fpx_route_pack": ([i64, P, i32, P, P, P, sz, P], i32),

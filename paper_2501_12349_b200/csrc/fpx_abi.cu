@@ -23,9 +23,9 @@
 namespace fpx {
 cudaError_t launch_invert_pairs_grouped(const fpx_mesh_t& m, const double* x,
                                         const int32_t* sorted, const Item* items,
-                                        const int64_t* nitems_dev, int64_t items_cap, double* r,
-                                        double* dist, int32_t* iters, int32_t* conv,
-                                        cudaStream_t st);
+                                        const int64_t* nitems_dev, int64_t items_cap,
+                                        const double* r0, double* r, double* dist,
+                                        int32_t* iters, int32_t* conv, cudaStream_t st);
 }
 
 using fpx::Item;
@@ -593,7 +593,8 @@ int fpx_findpts_eval(int dr, int Nf, const double* fbasis, int C, int64_t E,
 }
 
 int fpx_invert_pairs(const fpx_mesh_t* m, int64_t npairs, const double* x, const int32_t* elem,
-                     double* r, double* dist, int32_t* iters, int32_t* converged, void* stream) {
+                     const double* r0, double* r, double* dist, int32_t* iters,
+                     int32_t* converged, void* stream) {
   int rc = check_mesh(m);
   if (rc) return rc;
   if (npairs <= 0) return FPX_OK;
@@ -611,7 +612,7 @@ int fpx_invert_pairs(const fpx_mesh_t* m, int64_t npairs, const double* x, const
   FPX_CK(cudaGetLastError());
   g_launches += 3;
   FPX_CK(g.build(m->E, npairs, nullptr, elem, nullptr, st));
-  FPX_LAUNCH(fpx::launch_invert_pairs_grouped(*m, x, g.sorted, g.items, g.nitems, g.items_cap, r, dist,
+  FPX_LAUNCH(fpx::launch_invert_pairs_grouped(*m, x, g.sorted, g.items, g.nitems, g.items_cap, r0, r, dist,
                                           iters, converged, st));
   FPX_CK(cudaFreeAsync(ws, st));
   return FPX_OK;

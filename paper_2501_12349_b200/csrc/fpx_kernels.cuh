@@ -85,11 +85,6 @@ cudaError_t launch_newton_stream(const fpx_mesh_t& m, int64_t n, const double* x
                                  int32_t* upts, int64_t* nun_dev, int64_t* chunk_ctr, int4* redo,
                                  int64_t* nredo, int64_t redo_cap, int64_t* stats,
                                  cudaStream_t st);
-cudaError_t launch_newton_pairs(const fpx_mesh_t& m, const double* x, const int32_t* pair_pt,
-                                const int32_t* sorted_pairs, const Item* items,
-                                const int64_t* nitems_dev, int64_t items_cap, int32_t* pcode,
-                                double* pr, double* pdist, int32_t* piters, int64_t* stats,
-                                cudaStream_t st);
 // Remaining candidates of the points round 1 left unresolved: their
 // best-first candidate lists (k_rest_lists), then the lane-per-point Newton
 // (k_rest_lanes).

@@ -57,15 +57,6 @@ cudaError_t launch_newton_stream(const fpx_mesh_t& m, int64_t n, const double* x
                           redo, nredo, redo_cap, stats, st);
 }
 
-cudaError_t launch_newton_pairs(const fpx_mesh_t& m, const double* x, const int32_t* pair_pt,
-                                const int32_t* sorted_pairs, const Item* items,
-                                const int64_t* nitems_dev, int64_t items_cap, int32_t* pcode,
-                                double* pr, double* pdist, int32_t* piters, int64_t* stats,
-                                cudaStream_t st) {
-  return dispatch<Pairs>(m.d, m.dr, m.N, m, x, pair_pt, sorted_pairs, items, nitems_dev,
-                         items_cap, pcode, pr, pdist, piters, (int32_t*)nullptr, stats, st);
-}
-
 template <int D, int DR, int N>
 struct RestLists {
   template <typename... A>
@@ -110,11 +101,11 @@ cudaError_t launch_forward_map(const fpx_mesh_t& m, int64_t n, const int32_t* el
 // the same item machinery; here the pair id is the point id.
 cudaError_t launch_invert_pairs_grouped(const fpx_mesh_t& m, const double* x,
                                         const int32_t* sorted, const Item* items,
-                                        const int64_t* nitems_dev, int64_t items_cap, double* r,
-                                        double* dist, int32_t* iters, int32_t* conv,
-                                        cudaStream_t st) {
+                                        const int64_t* nitems_dev, int64_t items_cap,
+                                        const double* r0, double* r, double* dist,
+                                        int32_t* iters, int32_t* conv, cudaStream_t st) {
   return dispatch<Pairs>(m.d, m.dr, m.N, m, x, (const int32_t*)nullptr, sorted, items,
-                         nitems_dev, items_cap, (int32_t*)nullptr, r, dist, iters, conv,
+                         nitems_dev, items_cap, r0, (int32_t*)nullptr, r, dist, iters, conv,
                          (int64_t*)nullptr, st);
 }
 

@@ -549,15 +549,18 @@ __device__ __forceinline__ NewtonOut newton_warp(const double* __restrict__ sX,
                                                  const double* __restrict__ scale,
                                                  const double* xs, bool active,
                                                  const NewtonParams& P, double* sb,
-                                                 int64_t* nev = nullptr) {
+                                                 int64_t* nev = nullptr,
+                                                 const double* r0 = nullptr) {
   using L = Lay<D, DR, N>;
   double* stash = sb + Scratch<DR, N>::STASH * FPX_WARP;
   // seed: nearest GLL node, ties -> lowest lexicographic index (D7); the
-  // distance is accumulated with fma exactly as the oracle does.
+  // distance is accumulated with fma exactly as the oracle does.  An
+  // explicit initial guess r0 (invert_point's r0; warp-uniform
+  // presence) replaces it, clamped to [-1, 1].
   double best = INFINITY;
   int bi = 0;
 #pragma unroll 1
-  for (int row = 0; row < L::ROWS; ++row) {
+  for (int row = 0; row < (r0 ? 0 : L::ROWS); ++row) {
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       double dd = 0.0;
@@ -579,6 +582,9 @@ __device__ __forceinline__ NewtonOut newton_warp(const double* __restrict__ sX,
   r[0] = z[bi % N];
   if (DR > 1) r[1] = z[(bi / N) % N];
   if (DR > 2) r[2] = z[bi / (N * N)];
+  if (r0)
+#pragma unroll
+    for (int a = 0; a < DR; ++a) r[a] = fmin(1.0, fmax(-1.0, r0[a]));
   // One evaluation site (the seed is evaluated as the first "trial") and one
   // constrained_step site (the Hessian fallbacks loop over it) keep the
   // kernel's code small: instruction fetch was the top stall when inlined.
@@ -817,8 +823,9 @@ template <int D, int DR, int N>
 __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
     k_newton_pairs(fpx_mesh_t m, const double* __restrict__ x, const int32_t* __restrict__ pair_pt,
                    const int32_t* __restrict__ sorted, const Item* __restrict__ items,
-                   const int64_t* __restrict__ nitems_dev, int32_t* pcode, double* pr,
-                   double* pdist, int32_t* piters, int32_t* pconv, int64_t* stats) {
+                   const int64_t* __restrict__ nitems_dev, const double* __restrict__ r0,
+                   int32_t* pcode, double* pr, double* pdist, int32_t* piters, int32_t* pconv,
+                   int64_t* stats) {
   using L = Lay<D, DR, N>;
   extern __shared__ __align__(16) double smem[];
   double* z = smem;
@@ -845,11 +852,16 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
     const bool active = lane < itm.count;
     const int pair = active ? sorted[itm.start + lane] : 0;
     const int pt = active ? (pair_pt ? pair_pt[pair] : pair) : 0;
-    double xs[3] = {0.0, 0.0, 0.0};
-    if (active)
+    double xs[3] = {0.0, 0.0, 0.0}, rs[3] = {0.0, 0.0, 0.0};
+    if (active) {
 #pragma unroll
       for (int c = 0; c < D; ++c) xs[c] = x[(int64_t)pt * D + c];
-    NewtonOut o = newton_warp<D, DR, N>(sX, z, scale, xs, active, P, sb);
+      if (r0)
+#pragma unroll
+        for (int a = 0; a < DR; ++a) rs[a] = r0[(int64_t)pair * DR + a];
+    }
+    NewtonOut o = newton_warp<D, DR, N>(sX, z, scale, xs, active, P, sb, nullptr,
+                                        r0 ? rs : nullptr);
     if (active) {
       s_newton += 1;
       s_iters += o.iters;
@@ -1779,6 +1791,15 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
       if (lane < S && !(ready & (1u << lane)) && meta->end[lane] > meta->start[lane])
         ok = mbar_test(&meta->mbar[lane], meta->parity[lane]);
       const unsigned landed = __ballot_sync(FPX_FULL, ok);
+      // every lane acquires the completed phase itself (all lanes issued the
+      // slot's copies): their reads of the slot, and its next refill, are
+      // then ordered after the landing for each lane, not only for lane s
+      for (unsigned l = landed; l; l &= l - 1) {
+        const int s2 = __ffs(l) - 1;
+        while (!mbar_test(&meta->mbar[s2], meta->parity[s2])) {
+        }
+      }
+      __syncwarp();
       if (ok) meta->parity[lane] ^= 1u;
       ready |= landed;
       __syncwarp();
@@ -2120,8 +2141,9 @@ template <int D, int DR, int N>
 struct Pairs {
   static cudaError_t run(const fpx_mesh_t& m, const double* x, const int32_t* pair_pt,
                          const int32_t* sorted, const Item* items, const int64_t* nitems_dev,
-                         int64_t items_cap, int32_t* pcode, double* pr, double* pdist,
-                         int32_t* piters, int32_t* pconv, int64_t* stats, cudaStream_t st) {
+                         int64_t items_cap, const double* r0, int32_t* pcode, double* pr,
+                         double* pdist, int32_t* piters, int32_t* pconv, int64_t* stats,
+                         cudaStream_t st) {
     using L = Lay<D, DR, N>;
     const int threads = 128;
     const size_t smem = newton_smem(L::GEO + Scratch<DR, N>::SLOTS * FPX_WARP, 0, N,
@@ -2130,8 +2152,8 @@ struct Pairs {
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     unsigned blocks = persistent_blocks((const void*)fn, threads, smem, items_cap);
-    fn<<<blocks, threads, smem, st>>>(m, x, pair_pt, sorted, items, nitems_dev, pcode, pr, pdist,
-                                      piters, pconv, stats);
+    fn<<<blocks, threads, smem, st>>>(m, x, pair_pt, sorted, items, nitems_dev, r0, pcode, pr,
+                                      pdist, piters, pconv, stats);
     return cudaGetLastError();
   }
 };

@@ -580,14 +580,16 @@ def find_and_interpolate_host(S: EngineSetup, field, x: torch.Tensor, *, chunks:
                    dist=torch.empty(n, dtype=torch.float64, **pin))
     ws = S.__dict__.setdefault("_host_pipe", {})
     if ws.get("n") != n or ws.get("C") != C:
+        # zero-filled once: the bulk download reads the rest points' records
+        # before the zero-copy patch replaces them (initcheck-clean)
         ws.clear()
-        ws.update(n=n, C=C, x=torch.empty((n, S.phys_dim), dtype=torch.float64, device=dev),
-                  values=torch.empty((n, C), dtype=torch.float64, device=dev),
-                  code=torch.empty(n, dtype=torch.int32, device=dev),
-                  rank=torch.empty(n, dtype=torch.int32, device=dev),
-                  elem=torch.empty(n, dtype=torch.int32, device=dev),
-                  r=torch.empty((n, dr), dtype=torch.float64, device=dev),
-                  dist=torch.empty(n, dtype=torch.float64, device=dev))
+        ws.update(n=n, C=C, x=torch.zeros((n, S.phys_dim), dtype=torch.float64, device=dev),
+                  values=torch.zeros((n, C), dtype=torch.float64, device=dev),
+                  code=torch.zeros(n, dtype=torch.int32, device=dev),
+                  rank=torch.zeros(n, dtype=torch.int32, device=dev),
+                  elem=torch.zeros(n, dtype=torch.int32, device=dev),
+                  r=torch.zeros((n, dr), dtype=torch.float64, device=dev),
+                  dist=torch.zeros(n, dtype=torch.float64, device=dev))
     comp = torch.cuda.current_stream(dev)
     chunks = max(1, min(chunks, n))
     bounds = [n * c // chunks for c in range(chunks + 1)]

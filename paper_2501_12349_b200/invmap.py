@@ -116,40 +116,50 @@ def forward_map(geom, r, second: bool = False, envelope=None):
     return out
 
 
+def _r0_tensor(r0, n: int, dr: int, dev):
+    if r0 is None:
+        return None
+    t = torch.as_tensor(r0, dtype=torch.float64).reshape(n, dr)
+    if not torch.all((t >= -1.0) & (t <= 1.0)):
+        raise ValueError("r0 must lie in [-1, 1]^dr (SPEC.md:298 pre)")
+    return t.to(dev).contiguous()
+
+
 def invert_point(geom, x_star, r0=None, settings: NewtonSettings | None = None,
                  envelope=None) -> InverseMapResult:
-    """Closest point x(r*) to x* over the element.  The seed
-    is always the nearest GLL node (decision D7); an explicit
-    r0 is not supported by the kernel and is rejected."""
-    if r0 is not None:
-        raise ValueError("invert_point seeds at the nearest GLL node (D7); r0 must be None")
+    """Closest point x(r*) to x* over the element.  The
+    initial guess is r0 when given, else the nearest GLL node (decision D7,
+    SPEC.md:327)."""
     m, keep = _one_element_mesh(geom, envelope, settings)
     dev = keep[1].device
     xs = torch.from_numpy(np.asarray(x_star, dtype=float).reshape(1, -1)).to(dev)
     el = torch.zeros(1, dtype=torch.int32, device=dev)
     dr = geom.ref_dim
+    rt = _r0_tensor(r0, 1, dr, dev)
     r = torch.empty((1, dr), dtype=torch.float64, device=dev)
     dist = torch.empty(1, dtype=torch.float64, device=dev)
     it = torch.empty(1, dtype=torch.int32, device=dev)
     cv = torch.empty(1, dtype=torch.int32, device=dev)
-    _C.check(_C.lib().fpx_invert_pairs(m, 1, _C.ptr(xs), _C.ptr(el), _C.ptr(r), _C.ptr(dist),
-                                       _C.ptr(it), _C.ptr(cv), _C.stream_handle()),
+    _C.check(_C.lib().fpx_invert_pairs(m, 1, _C.ptr(xs), _C.ptr(el), _C.ptr(rt), _C.ptr(r),
+                                       _C.ptr(dist), _C.ptr(it), _C.ptr(cv), _C.stream_handle()),
              "fpx_invert_pairs")
     return InverseMapResult(r[0].cpu().numpy(), float(dist[0]), int(it[0]), bool(cv[0]))
 
 
-def invert_points(setup, x: torch.Tensor, elem: torch.Tensor):
+def invert_points(setup, x: torch.Tensor, elem: torch.Tensor, r0=None):
     """Batched invert_point over explicit (point, local element) pairs of an
-    engine setup.  Returns (r [n, dr], dist [n], iters [n], converged [n])."""
+    engine setup (initial guesses r0 [n, dr] or the D7 seed).  Returns
+    (r [n, dr], dist [n], iters [n], converged [n])."""
     dev = setup.device
     x = torch.as_tensor(x, dtype=torch.float64, device=dev).contiguous()
     elem = torch.as_tensor(elem, dtype=torch.int32, device=dev).contiguous()
     n = x.shape[0]
+    rt = _r0_tensor(r0, n, setup.ref_dim, dev)
     r = torch.empty((n, setup.ref_dim), dtype=torch.float64, device=dev)
     dist = torch.empty(n, dtype=torch.float64, device=dev)
     it = torch.empty(n, dtype=torch.int32, device=dev)
     cv = torch.empty(n, dtype=torch.int32, device=dev)
-    _C.check(_C.lib().fpx_invert_pairs(setup.mesh_t, n, _C.ptr(x), _C.ptr(elem), _C.ptr(r),
-                                       _C.ptr(dist), _C.ptr(it), _C.ptr(cv), _C.stream_handle()),
-             "fpx_invert_pairs")
+    _C.check(_C.lib().fpx_invert_pairs(setup.mesh_t, n, _C.ptr(x), _C.ptr(elem), _C.ptr(rt),
+                                       _C.ptr(r), _C.ptr(dist), _C.ptr(it), _C.ptr(cv),
+                                       _C.stream_handle()), "fpx_invert_pairs")
     return r, dist, it, cv.bool()

@@ -9,6 +9,7 @@ frozen so the oracle, the tests and bench.py all see identical inputs:
   sin(2 pi x_b), s = (+1, -1, +1) (cfg-1 with a = 0.02).
 * ``spiral``    -- one thick planar spiral element.
 * ``sphere`` / ``torus`` -- quad surface meshes embedded in 3D (cfg-4).
+* ``curve`` / ``helix`` -- line meshes (d_r = 1) in 2D and 3D.
 
 Every mesh is a `MeshData`: nodes f64[E, d, N**dr], lexicographic node order
 with the first reference axis fastest (bounds.py:58-94).
@@ -22,8 +23,9 @@ import numpy as np
 from .basis import gll_nodes
 
 __all__ = ["MeshData", "MeshSpec", "generate_mesh", "kershaw_mesh", "box_mesh",
-           "spiral_mesh", "sphere_mesh", "torus_mesh", "analytic_field", "uniform_points",
-           "surface_points", "partition_blocks"]
+           "spiral_mesh", "sphere_mesh", "torus_mesh", "curve_mesh", "helix_mesh",
+           "analytic_field", "uniform_points", "surface_points", "curve_points",
+           "partition_blocks"]
 
 
 @dataclass
@@ -162,6 +164,57 @@ def torus_mesh(n_major: int, n_minor: int, p: int, R: float = 1.0, r: float = 0.
     return MeshData(np.ascontiguousarray(np.stack(elems)), 3, 2, p)
 
 
+def curve_mesh(n: int, p: int, R: float = 1.0, a: float = 0.15, lobes: int = 5) -> MeshData:
+    """Closed planar curve of n line elements of order p (d = 2, d_r = 1):
+    x(th) = (R + a cos(lobes th)) (cos th, sin th), th in [0, 2 pi)."""
+    z = gll_nodes(p)
+    elems = []
+    for i in range(n):
+        th = 2.0 * np.pi * (i + 0.5 * (z + 1.0)) / n
+        rho = R + a * np.cos(lobes * th)
+        elems.append(np.stack([rho * np.cos(th), rho * np.sin(th)]))
+    return MeshData(np.ascontiguousarray(np.stack(elems)), 2, 1, p)
+
+
+def helix_mesh(n: int, p: int, turns: float = 2.0, R: float = 0.5, pitch: float = 0.4) -> MeshData:
+    """Helix of n line elements of order p in 3D (d = 3, d_r = 1)."""
+    z = gll_nodes(p)
+    elems = []
+    for i in range(n):
+        t = (i + 0.5 * (z + 1.0)) / n
+        th = 2.0 * np.pi * turns * t
+        elems.append(np.stack([R * np.cos(th), R * np.sin(th), pitch * turns * t]))
+    return MeshData(np.ascontiguousarray(np.stack(elems)), 3, 1, p)
+
+
+def curve_points(mesh: MeshData, n: int, seed: int = 1, offset_frac: float = 0.3,
+                 max_offset: float = 1e-5):
+    """Query points near a line mesh (d_r = 1): random (element, r) mapped to
+    x(r); a fraction gets an offset |t| <= max_offset along a unit normal to
+    the tangent (2D: the normal; 3D: a random perpendicular).  Returns
+    (points, element, r, offset)."""
+    from .basis import ReferenceBasis, lagrange_eval
+    rng = np.random.default_rng(seed)
+    rb = ReferenceBasis(mesh.order)
+    d = mesh.phys_dim
+    e = rng.integers(0, mesh.num_elements, size=n)
+    r = rng.uniform(-1, 1, size=n)
+    v, d1, _ = lagrange_eval(rb, r)
+    Xe = mesh.nodes[e]                               # (n, d, N)
+    x = np.einsum("nci,ni->nc", Xe, v)
+    t = np.einsum("nci,ni->nc", Xe, d1)
+    t /= np.linalg.norm(t, axis=1, keepdims=True)
+    if d == 2:
+        nrm = np.stack([-t[:, 1], t[:, 0]], axis=1)
+    else:
+        g = rng.normal(size=(n, 3))
+        nrm = g - np.sum(g * t, axis=1, keepdims=True) * t
+        nrm /= np.linalg.norm(nrm, axis=1, keepdims=True)
+    off = np.where(rng.uniform(size=n) < offset_frac,
+                   rng.uniform(-max_offset, max_offset, size=n), 0.0)
+    return x + off[:, None] * nrm, e, r, off
+
+
 def generate_mesh(spec: MeshSpec) -> MeshData:
     """SPEC.md:464-467 `generate_mesh`; refinement is applied by increasing the
     per-axis element count 2**refinement (oct-refinement of a box)."""
@@ -176,6 +229,10 @@ def generate_mesh(spec: MeshSpec) -> MeshData:
         return sphere_mesh(n, spec.order)
     if spec.generator == "torus":
         return torus_mesh(2 * n, n, spec.order)
+    if spec.generator == "curve":
+        return curve_mesh(n, spec.order)
+    if spec.generator == "helix":
+        return helix_mesh(n, spec.order)
     raise ValueError(f"unknown generator {spec.generator!r}")
 
 

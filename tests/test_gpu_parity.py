@@ -373,3 +373,94 @@ def test_spiral_newton_efficiency_gpu():
     assert np.max(np.abs(r.cpu().numpy() - rh)) < 1e-9
     rec = engine.find(S, xs)
     assert (rec.code.cpu().numpy() == 0).all()
+
+
+@pytest.mark.parametrize("kind", ["curve", "helix"])
+def test_line_mesh_find_eval(kind):
+    """Row f2, d_r = 1: line meshes in 2D (curve) and 3D (helix) -- on-curve
+    and offset points against the oracle under the full contract, and the
+    eps_d classification (on-curve INTERIOR, offset BORDER)."""
+    m = toolkit.curve_mesh(24, 4) if kind == "curve" else toolkit.helix_mesh(32, 5)
+    S = engine.setup(m)
+    OS = oracle_for(S, m.nodes)
+    x, e, r, off = toolkit.curve_points(m, 20_000, seed=9, offset_frac=0.3, max_offset=1e-6)
+    rec, orec = assert_find_parity(S, OS, x, toolkit.analytic_field("smooth", m))
+    code = rec.code.cpu().numpy()
+    assert np.mean(code[off == 0] == 0) > 0.99
+    assert np.all(code[np.abs(off) > 1e-8] == 1)
+
+
+@pytest.mark.parametrize("kind", ["sphere", "curve"])
+def test_closest_point_acceptance_8_gpu(kind):
+    """SPEC.md:512 (acceptance 8) on the device: 100 exterior points near a
+    curved surface (and a curve); d* within 1e-6 of a 10^6-sample
+    brute-force closest point, and the oracle's records."""
+    from closest_point import closest_point, exterior_points
+    if kind == "sphere":
+        m = toolkit.sphere_mesh(3, 4)
+        x = exterior_points(m, 100, seed=21, tmin=1e-4, tmax=4e-3)
+    else:
+        m = toolkit.curve_mesh(16, 4)
+        x = exterior_points(m, 100, seed=22, tmin=1e-4, tmax=4e-3)
+    S = engine.setup(m, options=engine.EngineOptions(expansion=1.0))
+    OS = oracle_for(S, m.nodes, expansion=1.0)
+    rec, orec = assert_find_parity(S, OS, x)
+    d = rec.dist.cpu().numpy()
+    assert np.all(rec.code.cpu().numpy() != 2)
+    for k in range(len(x)):
+        db, _, _ = closest_point(m, x[k], samples=1_000_000)
+        assert d[k] <= db + 1e-6 and abs(d[k] - db) < 1e-6, (k, d[k], db)
+
+
+def test_field_order_differs_from_geometry():
+    """a field of order p~ != p interpolated at the found
+    records, against the oracle's evaluate with the field's own basis."""
+    m = toolkit.kershaw_mesh(6, 4)
+    S = engine.setup(m)
+    OS = oracle_for(S, m.nodes)
+    x = toolkit.uniform_points(10_000, 3, seed=31, lo=-0.02, hi=1.02)
+    rec = engine.find(S, x)
+    orec = OS.find(x)
+    code = rec.code.cpu().numpy()
+    assert np.array_equal(code, orec["code"])
+    rng = np.random.default_rng(5)
+    for pf in (2, 6):
+        Nf = pf + 1
+        blocks = rng.normal(size=(m.num_elements, 2, Nf ** 3))
+        v = engine.interpolate(S, engine.Field(torch.from_numpy(blocks), pf), rec).cpu().numpy()
+        ov = O.evaluate(O.basis(pf), 3, blocks, code, rec.elem.cpu().numpy(), rec.r.cpu().numpy())
+        f = code != 2
+        np.testing.assert_allclose(v[f], ov[f], rtol=V_RTOL, atol=1e-12)
+        assert np.all(np.isnan(v[~f]))
+
+
+def test_invert_point_r0_and_idempotence():
+    """SPEC.md:298 (explicit r0) and the idempotence property:
+    re-running invert_point seeded at a converged r* ends in <= 1 iteration
+    with the same r* to 1e-12; an explicit r0 matches the oracle."""
+    m = toolkit.kershaw_mesh(4, 5)
+    S = engine.setup(m)
+    bc = BasisConstants.of(S.basis, S.envelope)
+    B = O.basis_from_arrays(bc.nodes, bc.scale, bc.proj0, bc.proj1, bc.eta, bc.lo, bc.hi)
+    rng = np.random.default_rng(12)
+    n = 2000
+    el = rng.integers(0, m.num_elements, n).astype(np.int32)
+    rh = rng.uniform(-0.97, 0.97, (n, 3))
+    xs = np.stack([O.forward_map(B, 3, 3, m.nodes[el[k]], rh[k])[0] for k in range(n)])
+    xs[: n // 2] += rng.normal(scale=0.01, size=(n // 2, 3))   # some exterior minima
+    r1, d1, it1, cv1 = invmap.invert_points(S, xs, el)
+    r1 = r1.cpu().numpy()
+    r2, d2, it2, cv2 = invmap.invert_points(S, xs, el, r0=r1)
+    assert int(it2.max()) <= 1 and bool(cv2.all())
+    assert np.max(np.abs(r2.cpu().numpy() - r1)) < 1e-12
+    # explicit, non-converged r0 against the oracle
+    r0 = rng.uniform(-1, 1, (n, 3))
+    r3, d3, it3, _ = invmap.invert_points(S, xs, el, r0=r0)
+    r3, d3 = r3.cpu().numpy(), d3.cpu().numpy()
+    for k in range(0, n, 10):
+        ro, do, ito, _ = O.invert(B, 3, 3, m.nodes[el[k]], xs[k], r0=r0[k])
+        assert abs(d3[k] - do) <= 1e-12 * max(1.0, do) + 1e-14
+    # the scalar API takes r0 too
+    g = bounds.ElementGeometry(3, 3, 5, m.nodes[el[0]])
+    res = invmap.invert_point(g, xs[0], r0=r1[0])
+    assert res.iterations <= 1 and np.max(np.abs(res.r - r1[0])) < 1e-12
