@@ -593,7 +593,7 @@ static int center_frame(const fpxo_basis* B, int d, int dr, const double* X,
 int64_t fpxo_element_boxes(const fpxo_basis* B, int d, int dr, int64_t E,
                            const double* nodes, double expansion, double* aabb,
                            double* obb_c, double* obb_inv, double* hbox,
-                           uint8_t* obb_ok, int32_t* status) {
+                           uint8_t* obb_ok, int32_t* status, double* frame) {
   int N = B->N;
   int K = dr == 1 ? N : (dr == 2 ? N * N : N * N * N);
   int64_t bad = 0;
@@ -649,6 +649,12 @@ int64_t fpxo_element_boxes(const fpxo_basis* B, int d, int dr, int64_t E,
       }
       obb_ok[e] = 0;
       if (status[e] == 0) status[e] = 2;
+    }
+    if (frame) {  /* centre frame (x_c, M^-1; zero when unusable): the D7' seed */
+      double* fr = frame + e * (d + d * d);
+      for (int c = 0; c < d; ++c) fr[c] = xc[c];
+      for (int c = 0; c < d; ++c)
+        for (int b = 0; b < d; ++b) fr[d + c * d + b] = ok ? Mi[c][b] : 0.0;
     }
   }
   return bad;
@@ -958,19 +964,13 @@ static int on_boundary(int dr, const double* r) {
 
 /* invert_point with the frozen
  * mechanics of decision D8. */
-/* Diagnostic (tests only): the first iteration at which the current iterate
- * was on a face with the descent direction leaving through it (-1: never). */
-int fpxo_diag_abort_it = -1;
-int fpxo_diag_abort_it2 = -1;   /* first iteration held for the 2nd consecutive time */
-double fpxo_diag_abort_f = 0.0;  /* |dx|^2 when the rule first fired */
-
-void fpxo_invert_from(const fpxo_basis* B, int d, int dr, const double* X, const double* xs,
-                      const fpxo_newton* S, const double* r0, double* r_out, double* dist,
-                      int* iters, int* conv);
+static void invert_core(const fpxo_basis* B, int d, int dr, const double* X, const double* xs,
+                        const fpxo_newton* S, const double* r0, int abort_r2, double* r_out,
+                        double* dist, int* iters, int* conv, int* aborted);
 
 void fpxo_invert(const fpxo_basis* B, int d, int dr, const double* X, const double* xs,
                  const fpxo_newton* S, double* r_out, double* dist, int* iters, int* conv) {
-  fpxo_invert_from(B, d, dr, X, xs, S, NULL, r_out, dist, iters, conv);
+  invert_core(B, d, dr, X, xs, S, NULL, 0, r_out, dist, iters, conv, NULL);
 }
 
 /* invert_point with an explicit initial guess r0 (NULL -> the
@@ -978,15 +978,23 @@ void fpxo_invert(const fpxo_basis* B, int d, int dr, const double* X, const doub
 void fpxo_invert_from(const fpxo_basis* B, int d, int dr, const double* X, const double* xs,
                       const fpxo_newton* S, const double* r0, double* r_out, double* dist,
                       int* iters, int* conv) {
-  fpxo_diag_abort_it = -1;
-  fpxo_diag_abort_it2 = -1;
+  invert_core(B, d, dr, X, xs, S, r0, 0, r_out, dist, iters, conv, NULL);
+}
+
+/* The trust-region solve.  abort_r2: stop (*aborted = 1) when the iterate is
+ * held on a face -- on it, with the descent direction -J leaving through it
+ * -- at two consecutive iterations (it >= 1; rule R2, DESIGN.md §3 D7'). */
+static void invert_core(const fpxo_basis* B, int d, int dr, const double* X, const double* xs,
+                        const fpxo_newton* S, const double* r0, int abort_r2, double* r_out,
+                        double* dist, int* iters, int* conv, int* aborted) {
   int held_prev = 0;
+  if (aborted) *aborted = 0;
   int N = B->N;
   int K = dr == 1 ? N : (dr == 2 ? N * N : N * N * N);
   /* seed: nearest GLL node, ties -> lowest lexicographic index (D7) */
   double best = INFINITY;
   int bi = 0;
-  for (int n = 0; n < K; ++n) {
+  for (int n = 0; n < (r0 ? 0 : K); ++n) {
     double dd = 0.0;
     for (int c = 0; c < d; ++c) { double t = xs[c] - X[c * K + n]; dd = fma(t, t, dd); }
     if (dd < best) { best = dd; bi = n; }
@@ -1021,10 +1029,12 @@ void fpxo_invert_from(const fpxo_basis* B, int d, int dr, const double* X, const
     int freem[3] = {1, 1, 1};
     for (int a = 0; a < dr; ++a)
       if ((r[a] == 1.0 && J[a] < 0.0) || (r[a] == -1.0 && J[a] > 0.0)) freem[a] = 0;
-    {
-      const int held = it >= 1 && !(freem[0] && freem[1] && freem[2]);
-      if (fpxo_diag_abort_it < 0 && held) { fpxo_diag_abort_it = it; fpxo_diag_abort_f = f; }
-      if (fpxo_diag_abort_it2 < 0 && held && held_prev) fpxo_diag_abort_it2 = it;
+    if (abort_r2 && it >= 1) {
+      const int held = !(freem[0] && freem[1] && freem[2]);
+      if (held && held_prev) {
+        if (aborted) *aborted = 1;
+        break;
+      }
       held_prev = held;
     }
     double s[3] = {0, 0, 0};
@@ -1121,6 +1131,39 @@ static int classify(int d, int dr, const double* r, double dist, double eps_d) {
   return FPXO_INTERIOR;
 }
 
+/* One candidate's solve, decision D7': for volume elements
+ * with a centre frame, first from the affine seed r0 = clamp(J_c^-1 (x* -
+ * x_c)) with the abort rule R2; that result stands if it is INTERIOR (the
+ * unique zero of the injective element map, whatever the seed).  Otherwise
+ * -- aborted or BORDER -- the solve from the D7 nearest-node seed (SPEC.md:
+ * 327) is the candidate's result.  Surfaces and lines use D7 only.  The
+ * seed is formed with separate multiply and add exactly as the kernels do. */
+static void candidate_solve(const fpxo_mesh* m, int32_t e, const double* xs, double* rr,
+                            double* dd, int* it, int* cv) {
+  int d = m->d, dr = m->dr, N = m->B->N;
+  int K = dr == 1 ? N : (dr == 2 ? N * N : N * N * N);
+  const double* X = m->nodes + (int64_t)e * d * K;
+  if (m->frame && d == dr) {
+    const double* fr = m->frame + (int64_t)e * (d + d * d);
+    double r0[3] = {0, 0, 0}, dx[3];
+    for (int c = 0; c < d; ++c) dx[c] = xs[c] - fr[c];
+    for (int a = 0; a < d; ++a) {
+      double y = 0.0;
+      for (int b = 0; b < d; ++b) y = y + fr[d + a * d + b] * dx[b];
+      r0[a] = isfinite(y) ? fmin(1.0, fmax(-1.0, y)) : 0.0;
+    }
+    int ab = 0, it1 = 0;
+    invert_core(m->B, d, dr, X, xs, &m->newton, r0, 1, rr, dd, &it1, cv, &ab);
+    int inside = !ab;
+    for (int a = 0; a < dr; ++a) inside &= fabs(rr[a]) < 1.0 - INTERIOR_TOL;
+    if (inside) { *it = it1; return; }
+    invert_core(m->B, d, dr, X, xs, &m->newton, NULL, 0, rr, dd, it, cv, NULL);
+    *it += it1;
+    return;
+  }
+  invert_core(m->B, d, dr, X, xs, &m->newton, NULL, 0, rr, dd, it, cv, NULL);
+}
+
 /* engine.find Phase A: candidates from
  * the local map in ascending element id, AABB then OBB filter, Newton,
  * first INTERIOR wins, else min-d* BORDER (ties -> lower id), else
@@ -1130,8 +1173,8 @@ static int classify(int d, int dr, const double* r, double dist, double eps_d) {
 void fpxo_find(const fpxo_mesh* m, int64_t n, const double* x, int32_t* code, int32_t* elem,
                double* r, double* dist, int32_t* iters, int32_t* ncand, int32_t* nbox,
                int nthreads) {
-  int d = m->d, dr = m->dr, N = m->B->N;
-  int K = dr == 1 ? N : (dr == 2 ? N * N : N * N * N);
+  int d = m->d, dr = m->dr;
+  
 #ifdef _OPENMP
   if (nthreads > 0) omp_set_num_threads(nthreads);
 #endif
@@ -1150,7 +1193,7 @@ void fpxo_find(const fpxo_mesh* m, int64_t n, const double* x, int32_t* code, in
                                           m->obb_inv + (int64_t)e * d * d, xs)) continue;
         double rr[3], dd;
         int it, cv;
-        fpxo_invert(m->B, d, dr, m->nodes + (int64_t)e * d * K, xs, &m->newton, rr, &dd, &it, &cv);
+        candidate_solve(m, e, xs, rr, &dd, &it, &cv);
         tot += it;
         ++nc;
         double eps_d = 0.0;

@@ -59,6 +59,7 @@ typedef struct {
   fpxo_newton newton;
   double eps_d_abs;             /* >= 0: absolute eps_d (surfaces) */
   double eps_d_rel;             /* used when eps_d_abs < 0: rel * AABB diagonal */
+  const double* frame;          /* [E][d + d*d] centre frame (x_c, J_c^-1) or NULL (pure D7) */
 } fpxo_mesh;
 
 #endif

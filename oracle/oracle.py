@@ -58,6 +58,7 @@ class Mesh(C.Structure):
         ("obb_inv", C.c_void_p), ("obb_ok", C.c_void_p), ("grid", C.c_void_p),
         ("ncell", C.c_int), ("offsets", C.c_void_p), ("elems", C.c_void_p),
         ("newton", Newton), ("eps_d_abs", C.c_double), ("eps_d_rel", C.c_double),
+        ("frame", C.c_void_p),
     ]
 
 
@@ -85,7 +86,7 @@ def lib():
         L.fpxo_envelope_violation.restype = C.c_double
         L.fpxo_coord_bounds.argtypes = [C.POINTER(Basis), C.c_int, C.c_int, P, P, P]
         L.fpxo_element_boxes.argtypes = [C.POINTER(Basis), C.c_int, C.c_int, C.c_int64, P,
-                                         C.c_double, P, P, P, P, P, P]
+                                         C.c_double, P, P, P, P, P, P, P]
         L.fpxo_element_boxes.restype = C.c_int64
         L.fpxo_contains.argtypes = [C.c_int, C.c_int64, P, P, P, P, P, P]
         L.fpxo_hash_grid.argtypes = [C.c_int, C.c_int64, P, C.c_int, P]
@@ -196,10 +197,11 @@ def element_boxes(B, d, dr, nodes, expansion=0.10):
     E = nodes.shape[0]
     out = dict(aabb=np.zeros((E, 2, d)), obb_c=np.zeros((E, d)), obb_inv=np.zeros((E, d, d)),
                hbox=np.zeros((E, 2, d)), obb_ok=np.zeros(E, np.uint8),
-               status=np.zeros(E, np.int32))
+               status=np.zeros(E, np.int32), frame=np.zeros((E, d + d * d)))
     bad = lib().fpxo_element_boxes(C.byref(B), d, dr, E, _p(nodes), float(expansion),
                                    _p(out["aabb"]), _p(out["obb_c"]), _p(out["obb_inv"]),
-                                   _p(out["hbox"]), _p(out["obb_ok"]), _p(out["status"]))
+                                   _p(out["hbox"]), _p(out["obb_ok"]), _p(out["status"]),
+                                   _p(out["frame"]))
     out["degenerate"] = int(bad)
     return out
 
@@ -253,7 +255,10 @@ class OracleSetup:
     """Oracle counterpart of engine.setup: boxes, hash and the mesh struct."""
 
     def __init__(self, nodes, d, dr, p, expansion=0.10, B=None, ncell=None,
-                 newton=None, eps_d_abs=-1.0, eps_d_rel=1e-10, nthreads=0):
+                 newton=None, eps_d_abs=-1.0, eps_d_rel=1e-10, nthreads=0, seeds="D7'"):
+        """seeds: "D7'" (default; affine-frame seed first for volume
+        elements, then the nearest node -- the kernels' rule) or "D7" (the
+        SPEC's nearest-node seed only)."""
         self.nodes = _f64(nodes)
         self.d, self.dr, self.p = d, dr, p
         self.B = B if B is not None else basis(p)
@@ -283,6 +288,9 @@ class OracleSetup:
         m.newton = newton or default_newton()
         m.eps_d_abs = eps_d_abs
         m.eps_d_rel = eps_d_rel
+        if seeds not in ("D7'", "D7"):
+            raise ValueError(f"seeds must be D7' or D7, got {seeds!r}")
+        m.frame = bx["frame"].ctypes.data if seeds == "D7'" else None
         self.nthreads = nthreads
 
     def find(self, x, nthreads=None):

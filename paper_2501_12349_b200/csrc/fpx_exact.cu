@@ -618,44 +618,33 @@ __device__ __forceinline__ bool cell_meets_obb(int d, const double* grid, int i,
   return true;
 }
 
-__global__ void k_hash_count(int d, int64_t E, const double* __restrict__ box,
-                             const double* __restrict__ obb_c, const double* __restrict__ obb_inv,
-                             const uint8_t* __restrict__ obb_ok, const double* __restrict__ grid,
-                             int n, int32_t* cnt) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
-       e += (int64_t)gridDim.x * blockDim.x) {
+// Warp per element, lanes over the flattened cell range of its hash box
+// (SPEC.md:230-238 build_local_map; D5b culling): at cfg-2 a box spans ~170
+// cells of the refined grid, so a thread-per-element loop ran one wave of
+// long serial trips (7 ms); here every lane tests ~5 cells.
+// fill == nullptr: count pass (cnt[cell] += 1); else fill pass.
+__global__ void __launch_bounds__(256)
+    k_hash_cells(int d, int64_t E, const double* __restrict__ box,
+                 const double* __restrict__ obb_c, const double* __restrict__ obb_inv,
+                 const uint8_t* __restrict__ obb_ok, const double* __restrict__ grid, int n,
+                 int32_t* cnt, const int32_t* __restrict__ offsets, int32_t* elems) {
+  const int lane = threadIdx.x % 32;
+  const int64_t w0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
+  const int64_t nw = (int64_t)gridDim.x * blockDim.x / 32;
+  for (int64_t e = w0; e < E; e += nw) {
     int a[3], b[3];
     box_cells(d, grid, n, box + e * 2 * d, a, b);
+    const int ni = b[0] - a[0] + 1, nj = b[1] - a[1] + 1, nk = b[2] - a[2] + 1;
+    const int tot = ni * nj * nk;
     const bool cull = obb_ok && obb_ok[e];
-    for (int k = a[2]; k <= b[2]; ++k)
-      for (int j = a[1]; j <= b[1]; ++j)
-        for (int i = a[0]; i <= b[0]; ++i) {
-          if (cull && !cell_meets_obb(d, grid, i, j, k, obb_c + e * d, obb_inv + e * d * d))
-            continue;
-          atomicAdd(&cnt[i + (int64_t)n * (j + (int64_t)n * k)], 1);
-        }
-  }
-}
-
-__global__ void k_hash_fill(int d, int64_t E, const double* __restrict__ box,
-                            const double* __restrict__ obb_c, const double* __restrict__ obb_inv,
-                            const uint8_t* __restrict__ obb_ok, const double* __restrict__ grid,
-                            int n, const int32_t* __restrict__ offsets, int32_t* cursor,
-                            int32_t* elems) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    int a[3], b[3];
-    box_cells(d, grid, n, box + e * 2 * d, a, b);
-    const bool cull = obb_ok && obb_ok[e];
-    for (int k = a[2]; k <= b[2]; ++k)
-      for (int j = a[1]; j <= b[1]; ++j)
-        for (int i = a[0]; i <= b[0]; ++i) {
-          if (cull && !cell_meets_obb(d, grid, i, j, k, obb_c + e * d, obb_inv + e * d * d))
-            continue;
-          int64_t cell = i + (int64_t)n * (j + (int64_t)n * k);
-          int slot = atomicAdd(&cursor[cell], 1);
-          elems[offsets[cell] + slot] = (int32_t)e;
-        }
+    for (int t = lane; t < tot; t += 32) {
+      const int i = a[0] + t % ni, j = a[1] + (t / ni) % nj, k = a[2] + t / (ni * nj);
+      if (cull && !cell_meets_obb(d, grid, i, j, k, obb_c + e * d, obb_inv + e * d * d))
+        continue;
+      const int64_t cell = i + (int64_t)n * (j + (int64_t)n * k);
+      const int slot = atomicAdd(&cnt[cell], 1);
+      if (elems) elems[offsets[cell] + slot] = (int32_t)e;
+    }
   }
 }
 
@@ -901,15 +890,16 @@ cudaError_t launch_hash_grid(int d, int64_t E, const double* box, int ncell, dou
 cudaError_t launch_hash_count(int d, int64_t E, const double* box, const double* obb_c,
                               const double* obb_inv, const uint8_t* obb_ok, const double* grid,
                               int n, int32_t* cnt, cudaStream_t st) {
-  k_hash_count<<<grid_for(E, 256), 256, 0, st>>>(d, E, box, obb_c, obb_inv, obb_ok, grid, n, cnt);
+  k_hash_cells<<<grid_for(E * 32, 256), 256, 0, st>>>(d, E, box, obb_c, obb_inv, obb_ok, grid,
+                                                      n, cnt, nullptr, nullptr);
   return cudaGetLastError();
 }
 cudaError_t launch_hash_fill(int d, int64_t E, const double* box, const double* obb_c,
                              const double* obb_inv, const uint8_t* obb_ok, const double* grid,
                              int n, const int32_t* offsets, int32_t* cursor, int32_t* elems,
                              cudaStream_t st) {
-  k_hash_fill<<<grid_for(E, 256), 256, 0, st>>>(d, E, box, obb_c, obb_inv, obb_ok, grid, n,
-                                                offsets, cursor, elems);
+  k_hash_cells<<<grid_for(E * 32, 256), 256, 0, st>>>(d, E, box, obb_c, obb_inv, obb_ok, grid,
+                                                      n, cursor, offsets, elems);
   return cudaGetLastError();
 }
 cudaError_t launch_hash_sort(int64_t ncells, const int32_t* offsets, int32_t* elems,

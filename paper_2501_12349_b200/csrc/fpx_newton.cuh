@@ -503,6 +503,23 @@ __device__ __forceinline__ double xscale(const double* xs) {
   return m;
 }
 
+// D7' seed of a volume element: r0 = clamp(J_c^-1 (x* - x_c)) from its centre
+// frame fr = (x_c[D], J_c^-1[D][D]) (zero matrix when the frame is unusable),
+// with separate multiply and add in the oracle's order (candidate_solve).
+template <int D>
+__device__ __forceinline__ void affine_seed(const double* fr, const double* xs, double* r0) {
+  double dx[3];
+#pragma unroll
+  for (int c = 0; c < D; ++c) dx[c] = __dsub_rn(xs[c], fr[c]);
+#pragma unroll
+  for (int a = 0; a < D; ++a) {
+    double y = 0.0;
+#pragma unroll
+    for (int b = 0; b < D; ++b) y = __dadd_rn(y, __dmul_rn(fr[D + a * D + b], dx[b]));
+    r0[a] = isfinite(y) ? fmin(1.0, fmax(-1.0, y)) : 0.0;
+  }
+}
+
 template <int DR>
 __device__ __forceinline__ bool on_boundary(const double* r) {
   bool b = false;
@@ -1338,9 +1355,13 @@ __global__ void __launch_bounds__(128, 2)
   int64_t s_newton = 0, s_iters = 0, nev = 0, nev2 = 0, nlev = 0;
   int64_t u = 0, k = 0;
   double xs[3] = {0.0, 0.0, 0.0};
-  int phase = 0;  // 0 needs a pair, 3 iterating, 4 done
+  int phase = 0;  // 0 needs a pair, 1 needs its D7 seed, 3 iterating, 4 done
   int e = 0, it = 0;
   bool held_prev = false;
+  // D7': pass 1 solves volume candidates from the affine seed (with R2);
+  // d7 marks a solve from the nearest-node seed (redo pass, surfaces, or a
+  // pass-1 pair restarted in place when the redo list is full)
+  bool d7 = false;
   int4 cur = make_int4(0, 0, 0, 0);  // the pair being solved
   bool first = true;
   double rc[3] = {0.0, 0.0, 0.0}, rn[3] = {0.0, 0.0, 0.0};
@@ -1415,6 +1436,22 @@ __global__ void __launch_bounds__(128, 2)
       if (en < 0) continue;
       e = en;
       cur.y = en;
+      d7 = redo_pass || DR < D;
+      if (!d7) {
+        double fr[D + D * D];
+        const double* gfr = m.frec + (int64_t)e * FPX_FREC + 3 * D + D * D;
+#pragma unroll
+        for (int t = 0; t < D + D * D; ++t) fr[t] = __ldg(gfr + t);
+        affine_seed<D>(fr, xs, rc);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) rn[a] = rc[a];
+        first = true;
+        held_prev = false;
+        it = 0;
+        alpha = P.alpha0;
+        phase = 3;
+        continue;
+      }
       const int sd = rank < FPX_RK ? cseed[u * FPX_RK + rank] : -1;
       if (sd < 0) {
         phase = 1;  // needs its seed
@@ -1524,7 +1561,6 @@ __global__ void __launch_bounds__(128, 2)
       if (smax < P.tol) done = true;
       else if (it >= P.max_iters) done = true;
     }
-    bool aborted = false;
     if (!done && *(volatile int32_t*)&found[u]) {
       // another candidate of this point was INTERIOR meanwhile: its record
       // is final (an INTERIOR is unique up to shared faces), stop this one
@@ -1533,18 +1569,25 @@ __global__ void __launch_bounds__(128, 2)
       phase = 0;
       continue;
     }
-    if (!done && abortable && it >= 1) {
+    if (!done && abortable && !d7 && it >= 1) {
       // held on a face (descent direction leaving it) for two consecutive
-      // iterations: this candidate is most likely not the owner.  Stop; the
-      // pair is redone in full (second pass) only if its point ends without
-      // an INTERIOR.
+      // iterations (rule R2): this candidate is most likely not the owner.
+      // Stop; under D7' the pair is redone from the D7 seed (redo pass) if
+      // its point ends without an INTERIOR -- at once, in place, when the
+      // redo list is full.
       const bool held = held_on_face<DR>(rc, st.J);
       if (held && held_prev) {
         const int64_t slot = (int64_t)atomicAdd((unsigned long long*)nredo, 1ull);
+        s_newton += 1;
+        s_iters += it;
         if (slot < pair_cap) {
           redo[slot] = cur;
-          aborted = done = true;
+          phase = 0;
+        } else {
+          d7 = true;
+          phase = 1;
         }
+        continue;
       }
       held_prev = held;
     }
@@ -1560,16 +1603,25 @@ __global__ void __launch_bounds__(128, 2)
         stash_state(stash, st);
       }
     }
-    if (done && aborted) {
-      s_newton += 1;
-      s_iters += it;
-      phase = 0;
-    } else if (done) {
+    if (done) {
       const double dd = sqrt(st.f);
       s_newton += 1;
       s_iters += it;
       const double epsd = DR < D ? eps_d_of(m, e) : 0.0;
       const int cd = classify<D, DR>(rc, dd, epsd);
+      if (!d7 && cd != kInterior) {
+        // D7': a BORDER result from the affine seed is replaced by the
+        // solve from the D7 seed (redo pass; in place when the list is full)
+        const int64_t slot = (int64_t)atomicAdd((unsigned long long*)nredo, 1ull);
+        if (slot < pair_cap) {
+          redo[slot] = cur;
+          phase = 0;
+        } else {
+          d7 = true;
+          phase = 1;
+        }
+        continue;
+      }
       // D6 merge into the point's record under its lock
       while (atomicCAS(&lock[u], 0, 1) != 0) {
       }
@@ -1684,6 +1736,8 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
   double* scale = smem + N;
   const int warp = threadIdx.x / FPX_WARP, lane = threadIdx.x % FPX_WARP;
   const int wpb = blockDim.x / FPX_WARP;
+  // slot: geometry [D][ROWS][NP] | field [C][ROWS][NP] | frame (x_c, J_c^-1)
+  const int frame_off = L::GEO + (field ? C * L::CS : 0);
   double* slots = smem + 2 * ((N + 1) & ~1) + (size_t)warp * (S * slot_stride + SCR * FPX_WARP);
   double* sb = slots + S * slot_stride + lane;
   double* stash = sb + Scratch<DR, N>::STASH * FPX_WARP;
@@ -1773,6 +1827,10 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
           cp_async8(sl + L::GEO + c * L::CS + row * L::NP + i, gu + t);
         }
       }
+      if constexpr (DR == D) {  // the affine frame (x_c, J_c^-1) for the seeds
+        if (lane < D + D * D)
+          cp_async8(sl + frame_off + lane, m.frec + (int64_t)e * FPX_FREC + 3 * D + D * D + lane);
+      }
       cp_async_arrive_noinc(&meta->mbar[s]);
       __syncwarp();
       if (lane == 0) {
@@ -1827,7 +1885,23 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
           if (meta->start[s2] <= p && p < meta->end[s2]) myslot = s2;
 #pragma unroll
         for (int c = 0; c < D; ++c) xs[c] = x[(int64_t)pt * D + c];
-        phase = 1;
+        if constexpr (DR == D) {
+          // seed (decision D7'): the affine prediction of the element's
+          // centre frame; an INTERIOR result is final (the unique zero of the
+          // injective element map), a BORDER or aborted one is recomputed
+          // from the D7 nearest-node seed by the redo pass.  On cfg-2 it
+          // halves the owner's Newton iterations (3.0 -> 1.7).
+          affine_seed<D>(slots + myslot * slot_stride + frame_off, xs, rc);
+#pragma unroll
+          for (int a = 0; a < 3; ++a) rn[a] = rc[a];
+          first = true;
+          held_prev = false;
+          it = 0;
+          alpha = P.alpha0;
+          phase = 2;
+        } else {
+          phase = 1;
+        }
       }
       q += take;
       if (q >= alen && bclaimed) {  // chunk A consumed: B becomes A
@@ -1846,7 +1920,8 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
       }
     }
     // ---- cooperative seeds (D7) of the lanes that just got a point
-    for (unsigned sd = __ballot_sync(FPX_FULL, phase == 1); sd;) {
+    // (surfaces and lines; volume elements seed from their frame above)
+    for (unsigned sd = DR < D ? __ballot_sync(FPX_FULL, phase == 1) : 0u; sd;) {
       unsigned js[4];
       const double* sj[4];
       double xj[4][3];
@@ -1955,6 +2030,24 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
       s_iters += it;
       const double epsd = DR < D ? eps_d_of(m, e) : 0.0;
       const int cd = classify<D, DR>(rc, dd, epsd);
+      if (DR == D && cd != kInterior && redo) {
+        // a solve from the affine seed that ends BORDER is not final: like
+        // an aborted one it goes to the redo pass, which recomputes it from
+        // the D7 seed if the point finds no INTERIOR (at most one round-1
+        // entry per point: the list cannot overflow)
+        const int64_t rs = (int64_t)atomicAdd((unsigned long long*)nredo, 1ull);
+        const int slot = (int)atomicAdd((unsigned long long*)nun_dev, 1ull);
+        upts[slot] = pt;
+        redo[rs] = make_int4(pt, e, slot, 0);
+        code[pt] = kBorder;  // placeholder: any computed record replaces it
+        elem[pt] = e;
+        dist[pt] = INFINITY;
+#pragma unroll
+        for (int a = 0; a < DR; ++a) r[(int64_t)pt * DR + a] = rc[a];
+        if (iters) iters[pt] = it;
+        phase = 0;
+        continue;
+      }
       const bool final = cd == kInterior || npass[pt] <= 1;
       code[pt] = cd;
       elem[pt] = e;
@@ -2105,7 +2198,7 @@ struct Stream {
                          int4* redo, int64_t* nredo, int64_t redo_cap, int64_t* stats,
                          cudaStream_t st) {
     using L = Lay<D, DR, N>;
-    int ss = L::GEO + (field ? C * L::CS : 0);
+    int ss = L::GEO + (field ? C * L::CS : 0) + (DR == D ? D + D * D : 0);
     ss = (ss + 13) / 16 * 16 + 2;  // slot stride = 16 bytes mod 128: distinct bank groups
     const size_t per_warp =
         (size_t)(S * ss + Scratch<DR, N>::SLOTS * FPX_WARP) * 8 + sizeof(StreamMeta<S>);

@@ -149,6 +149,8 @@ def test_setup_bitexact_and_hash_identical(mesh_fn):
         assert np.array_equal(getattr(S, k).cpu().numpy(), OS.boxes[k]), k
     for k in ("obb_c", "obb_inv"):
         assert np.array_equal(getattr(S, k).cpu().numpy()[ok], OS.boxes[k][ok]), k
+    # the centre frame seeds D7' (affine seed): bit-identical
+    assert np.array_equal(S.frame.cpu().numpy(), OS.boxes["frame"])
     assert np.array_equal(S.offsets.cpu().numpy(), OS.offsets)
     assert np.array_equal(S.elems.cpu().numpy(), OS.elems)
 
