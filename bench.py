@@ -52,6 +52,28 @@ def f_eval(N, C=1):
     return 3 * 8 * N + 2 * C * (N ** 3 + N ** 2 + N)
 
 
+F_SEED_AFFINE = 2 * 3 * 3 + 3   # D7' seed: J_c^-1 (x* - x_c) (3x3 mat-vec + 3 subtractions)
+
+
+def round1_flops(st, N):
+    """Algorithmic FP64 work of the round-1 kernel: every lane evaluation of
+    the map (basis, x + G contraction, step algebra = F_iter), the affine
+    seed of every solve, the fused field evaluation of every final point."""
+    return st["r1_lane_evals"] * f_iter(N) + st["newton_r1"] * F_SEED_AFFINE \
+        + st["evals_r1"] * f_eval(N)
+
+
+def step_flops(st, N):
+    """Whole find+eval step: round 1, the rest kernels' lane evaluations
+    (each rest solve counted with a nearest-node seed, 8 N^3: an upper bound,
+    pass-1 solves seed from the frame), 30 flops per box test, and the field
+    evaluation of every found point."""
+    rest_solves = st["newton"] - st["newton_r1"]
+    return round1_flops(st, N) + st["rest_lane_evals"] * f_iter(N) \
+        + rest_solves * f_seed(N) + 30 * st["box_tests"] \
+        + (st["evals"] - st["evals_r1"]) * f_eval(N)
+
+
 def workload_config(n_gpus):
     return {"workload": f"cfg-2: Kershaw hex {N_ELEM_AXIS}^3 p={ORDER}, "
                         f"{PTS_PER_GPU} uniform pts/GPU, find+eval (C=1)",
@@ -279,8 +301,7 @@ def run_ours(args):
     # --- roofline of the dominant kernel (round-1 Newton, FP64-bound)
     st = dict(stats[-1])
     N = ORDER + 1
-    flops_r1 = (step1["newton_r1"] * (f_seed(N) + f_iter(N)) + step1["iters_r1"] * f_iter(N)
-                + step1["evals_r1"] * f_eval(N))
+    flops_r1 = round1_flops(step1, N)
     tf = np.zeros(1)
     _C.check(L.fpx_probe_fp64(tf.ctypes.data, _C.stream_handle()), "fpx_probe_fp64")
     achieved = flops_r1 / (kern_ms * 1e-3) / 1e12
@@ -288,8 +309,7 @@ def run_ours(args):
     tpath = os.path.join(ROOT, "profiles", "newton_stream_dram.json")
     if os.path.exists(tpath):
         traffic = json.load(open(tpath)).get("bytes_per_launch")
-    flops_all = (st["newton"] * (f_seed(N) + f_iter(N)) + st["iters"] * f_iter(N)
-                 + st["evals"] * f_eval(N))
+    flops_all = step_flops(st, N)
     if world > 1:
         dist.barrier()
     if rank == 0:

@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define FPX_ABI_VERSION 4
+#define FPX_ABI_VERSION 5
 
 /* error codes */
 #define FPX_OK 0
@@ -112,8 +112,9 @@ typedef struct fpx_mesh_t {
 #define FPX_STAT_REST_WARP_EVALS 12 /* rest kernel: map evaluations issued per warp */
 #define FPX_STAT_REST_W2_EVALS 13   /* ... of which with second derivatives */
 #define FPX_STAT_REST_LANE_EVALS 14 /* ... summed over the lanes that were iterating */
-#define FPX_STAT_REDO 15            /* candidates stopped by the abort rule (redo list) */
-#define FPX_STATS_LEN 16
+#define FPX_STAT_REDO 15            /* candidates handed to the redo pass (R2 abort or D7') */
+#define FPX_STAT_R1_LANE_EVALS 16   /* round-1 map evaluations summed over iterating lanes */
+#define FPX_STATS_LEN 17
 
 int fpx_abi_version(void);
 const char* fpx_last_error(void);

@@ -14,12 +14,12 @@ import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FPX_LIB") or os.path.join(HERE, "lib", "libfpx_sm100.so")
-ABI_VERSION = 4
+ABI_VERSION = 5
 
 INTERIOR, BORDER, NOT_FOUND = 0, 1, 2
 STAT_NAMES = ["points", "box_tests", "newton", "iters", "rest_points", "r1_warp_evals",
               "r1_w2_evals", "evals", "newton_r1", "iters_r1", "evals_r1", "r1_items",
-              "rest_warp_evals", "rest_w2_evals", "rest_lane_evals", "redo"]
+              "rest_warp_evals", "rest_w2_evals", "rest_lane_evals", "redo", "r1_lane_evals"]
 STATS_LEN = len(STAT_NAMES)
 FREC = 32            # FPX_FREC: doubles per element filter record
 

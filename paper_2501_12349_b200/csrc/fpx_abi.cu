@@ -145,7 +145,6 @@ struct FindWs {
   int32_t *best, *npass, *upts, *clist, *cnum, *found, *lock, *nps, *perm, *hist, *bstart, *bcur,
       *maxnp;
   int64_t *cum, *npairs, *nredo;
-  int16_t* cseed;
   int4 *pairs, *redo;
   int64_t *nun, *counter, *chunk_ctr;
   Group g1;
@@ -169,7 +168,6 @@ struct FindWs {
     npass = c.take<int32_t>(n);
     upts = c.take<int32_t>(n);
     clist = c.take<int32_t>(n * FPX_RK);
-    cseed = c.take<int16_t>(n * FPX_RK);  // nearest node of each listed candidate
     cnum = c.take<int32_t>(n);
     found = c.take<int32_t>(n);
     lock = c.take<int32_t>(n);
@@ -542,12 +540,12 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
   // --- rest: remaining candidates of the unresolved points
   FPX_CK(cudaMemsetAsync(w.hist, 0, sizeof(int32_t) * 2 * FPX_HMAX, st));
   g_launches += 3;  // k_rest_lists, k_rest_order, k_rest_scatter, k_rest_pairlist
-  FPX_LAUNCH(fpx::launch_rest_lists(M, x, n, w.nun, w.upts, w.clist, w.cseed, w.cnum, w.nps, w.hist,
+  FPX_LAUNCH(fpx::launch_rest_lists(M, x, n, w.nun, w.upts, w.clist, w.cnum, w.nps, w.hist,
                                     w.bstart, w.bcur, w.perm, w.cum, w.maxnp, w.pairs, w.npairs,
                                     st));
   FPX_CK(cudaMemsetAsync(w.found, 0, sizeof(int32_t) * n, st));
   FPX_CK(cudaMemsetAsync(w.lock, 0, sizeof(int32_t) * n, st));
-  FPX_LAUNCH(fpx::launch_find_rest(M, x, n, w.nun, w.upts, w.clist, w.cseed, w.cnum, w.nps, w.perm,
+  FPX_LAUNCH(fpx::launch_find_rest(M, x, n, w.nun, w.upts, w.clist, w.cnum, w.nps, w.perm,
                                    w.cum, w.maxnp, w.best, w.pairs, w.npairs, w.redo, w.nredo,
                                    w.found, w.lock, code, elem,
                                    r, dist,

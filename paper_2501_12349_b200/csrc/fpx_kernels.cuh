@@ -90,13 +90,11 @@ cudaError_t launch_newton_stream(const fpx_mesh_t& m, int64_t n, const double* x
 // (k_rest_lanes).
 cudaError_t launch_rest_lists(const fpx_mesh_t& m, const double* x, int64_t nun_cap,
                               const int64_t* nun_dev, const int32_t* upts, int32_t* clist,
-                              int16_t* cseed,
                               int32_t* cnum, int32_t* nps, int32_t* hist, int32_t* bstart,
                               int32_t* bcur, int32_t* perm, int64_t* cum, int32_t* maxnp,
                               int4* pairs, int64_t* npairs, cudaStream_t st);
 cudaError_t launch_find_rest(const fpx_mesh_t& m, const double* x, int64_t nun_cap,
                              const int64_t* nun_dev, const int32_t* upts, const int32_t* clist,
-                             const int16_t* cseed,
                              const int32_t* cnum, const int32_t* nps, const int32_t* perm,
                              const int64_t* cum, const int32_t* maxnp, const int32_t* best,
                              const int4* pairs, const int64_t* npairs, int4* redo,

@@ -65,17 +65,15 @@ struct RestLists {
 
 cudaError_t launch_rest_lists(const fpx_mesh_t& m, const double* x, int64_t nun_cap,
                               const int64_t* nun_dev, const int32_t* upts, int32_t* clist,
-                              int16_t* cseed,
                               int32_t* cnum, int32_t* nps, int32_t* hist, int32_t* bstart,
                               int32_t* bcur, int32_t* perm, int64_t* cum, int32_t* maxnp,
                               int4* pairs, int64_t* npairs, cudaStream_t st) {
-  return dispatch<RestLists>(m.d, m.dr, m.N, m, x, nun_cap, nun_dev, upts, clist, cseed, cnum, nps, hist,
+  return dispatch<RestLists>(m.d, m.dr, m.N, m, x, nun_cap, nun_dev, upts, clist, cnum, nps, hist,
                              bstart, bcur, perm, cum, maxnp, pairs, npairs, st);
 }
 
 cudaError_t launch_find_rest(const fpx_mesh_t& m, const double* x, int64_t nun_cap,
                              const int64_t* nun_dev, const int32_t* upts, const int32_t* clist,
-                             const int16_t* cseed,
                              const int32_t* cnum, const int32_t* nps, const int32_t* perm,
                              const int64_t* cum, const int32_t* maxnp, const int32_t* best,
                              const int4* pairs, const int64_t* npairs, int4* redo,
@@ -83,7 +81,7 @@ cudaError_t launch_find_rest(const fpx_mesh_t& m, const double* x, int64_t nun_c
                              int32_t* lock, int32_t* code, int32_t* elem, double* r, double* dist,
                              int32_t* iters, const double* field, int C, double* values,
                              int64_t* counter, int64_t* stats, cudaStream_t st) {
-  return dispatch<Rest>(m.d, m.dr, m.N, m, x, nun_cap, nun_dev, upts, clist, cseed, cnum, nps, perm, cum,
+  return dispatch<Rest>(m.d, m.dr, m.N, m, x, nun_cap, nun_dev, upts, clist, cnum, nps, perm, cum,
                         maxnp, best, pairs, npairs, redo, nredo, found, lock, code, elem, r, dist,
                         iters, field, C,
                         values,

@@ -970,20 +970,16 @@ __device__ __forceinline__ bool propose_step(const NState& st, const double* r, 
 }
 
 // ---------------------------------------------------------------- rest kernel
-// Points left unresolved by round 1 (a BORDER record with more than one
-// passing candidate, ~5% of the points) visit their remaining candidates in
+// Points left unresolved by round 1 (~5%: their best-first candidate ended
+// BORDER or was stopped by rule R2) visit their remaining candidates in
 // best-first order, stop at the first INTERIOR and otherwise keep the D6
 // winner.  These (point, candidate) pairs hit ~1 pair per element, so the
-// element-major mapping of round 1 would run warps with one live lane.
-// Instead every lane owns one point and a private shared-memory slot for
-// its current candidate's geometry: the lanes run their own Newton solves in
-// lockstep (one warp-uniform map evaluation per pass, as in round 1), and a
-// lane whose candidate finished picks its next candidate (or point) at once,
-// so no lane waits for the slowest one.  The warp cooperates on the
-// irregular parts: the geometry copies (cp.async, completion on the owning
-// lane's mbarrier, polled without blocking) and the nearest-node seeds.
-// Slot stride is odd in doubles, so the 32 lanes' 8-byte loads at equal
-// offsets fall into distinct bank pairs.
+// element-major mapping of round 1 would run warps with one live lane:
+// k_rest_l1 gives every lane one pair and reads that element's geometry in
+// place through L1 (mesh.nodes_pad).  Pass 1 solves from the affine seed
+// (D7', rule R2); a BORDER or aborted result goes to the redo list, whose
+// pairs the second launch solves from the nearest-node seed (D7, the
+// warp-cooperative node search) only if their point found no INTERIOR.
 
 __device__ __forceinline__ void mbar_init(uint64_t* mb, unsigned count) {
   const unsigned a = (unsigned)__cvta_generic_to_shared(mb);
@@ -1034,7 +1030,7 @@ __device__ __forceinline__ double warp_min_nonneg(double d) {
 template <int D>
 __global__ void __launch_bounds__(128)
     k_rest_lists(fpx_mesh_t m, const double* __restrict__ x, const int64_t* __restrict__ nun_dev,
-                 const int32_t* __restrict__ upts, int32_t* clist, int16_t* cseed, int32_t* cnum,
+                 const int32_t* __restrict__ upts, int32_t* clist, int32_t* cnum,
                  int32_t* nps, int32_t* hist) {
   // warp per rest point: lanes test the hash-list entries (one filter record
   // each), (v, e) of the passing ones go to shared memory, and the rank of
@@ -1091,68 +1087,6 @@ __global__ void __launch_bounds__(128)
       atomicAdd(&hist[np < FPX_HMAX - 1 ? np : FPX_HMAX - 1], 1);
     }
     __syncwarp();
-    // Nearest node (the D7 seed) of every listed candidate of rank >= 1,
-    // stored for the rest kernel (cseed; -1 = not listed, it seeds itself).
-    // Fully listed points with several rest candidates are then reordered by
-    // that distance (ties keep the (v, e) order): the rest phase stops a
-    // point's other candidates once one is INTERIOR, so the owner should
-    // come early, and the affine best-first value ranks curved elements
-    // poorly (cfg-2: the owner was rank 1 for 54% of the rest points, 64%
-    // after the reorder).
-    const int nl = qe - qs <= L ? (np < FPX_RK ? np : FPX_RK) : 0;
-    if (lane < FPX_RK && (lane == 0 || lane >= nl)) cseed[u * FPX_RK + lane] = -1;
-    if (nl > 1) {
-      const int K = m.dr == 1 ? m.N : m.dr == 2 ? m.N * m.N : m.N * m.N * m.N;
-      for (int j = 1; j < nl; ++j) {
-        const double* X = m.nodes + (int64_t)clist[u * FPX_RK + j] * D * K;
-        double bd = INFINITY, b2 = INFINITY;
-        int bt = 0x7fffffff;
-        for (int t = lane; t < K; t += FPX_WARP) {
-          double dd = 0.0;
-#pragma unroll
-          for (int c = 0; c < D; ++c) {
-            const double tt = __dsub_rn(xs[c], __ldg(X + c * K + t));
-            dd = __fma_rn(tt, tt, dd);
-          }
-          if (dd < bd) {
-            b2 = bd;
-            bd = dd;
-            bt = t;
-          } else if (dd < b2) {
-            b2 = dd;
-          }
-        }
-        const int w = warp_argmin(bd, bt);  // node index; lane w % 32 holds it
-        const bool own = lane == w % FPX_WARP;
-        const double d1 = __shfl_sync(FPX_FULL, bd, w % FPX_WARP);
-        // second-nearest node distance: breaks the ties of a shared (face,
-        // edge, corner) nearest node in favour of the element whose own
-        // nodes lie closer
-        const double d2 = warp_min_nonneg(own ? b2 : bd);
-        if (lane == 0) {
-          s_v[warp][j] = d1;
-          s_v[warp][FPX_RK + j] = d2;
-          s_e[warp][j] = w;
-        }
-      }
-      __syncwarp();
-      if (lane >= 1 && lane < nl) {
-        const int e2 = clist[u * FPX_RK + lane];
-        const double dj = s_v[warp][lane], dj2 = s_v[warp][FPX_RK + lane];
-        int rk = lane;
-        if (np <= FPX_RK && np > 2) {  // the whole passing set is listed
-          rk = 1;
-          for (int j = 1; j < nl; ++j) {
-            const double di = s_v[warp][j], di2 = s_v[warp][FPX_RK + j];
-            rk += (di < dj || (di == dj && (di2 < dj2 || (di2 == dj2 && j < lane)))) ? 1 : 0;
-          }
-        }
-        __syncwarp(__activemask());
-        clist[u * FPX_RK + rk] = e2;
-        cseed[u * FPX_RK + rk] = (int16_t)s_e[warp][lane];
-      }
-      __syncwarp();
-    }
   }
 }
 
@@ -1323,7 +1257,7 @@ template <int D, int DR, int N>
 __global__ void __launch_bounds__(128, 2)
     k_rest_l1(fpx_mesh_t m, const double* __restrict__ x, const int64_t* __restrict__ nun_dev,
               const int32_t* __restrict__ upts, const int32_t* __restrict__ clist,
-              const int16_t* __restrict__ cseed, const int32_t* __restrict__ cnum,
+              const int32_t* __restrict__ cnum,
               const int32_t* __restrict__ nps, const int32_t* __restrict__ perm,
               const int64_t* __restrict__ cum, const int32_t* __restrict__ maxnp_dev,
               const int32_t* __restrict__ best, const int4* __restrict__ pairs, int64_t pair_cap,
@@ -1452,22 +1386,7 @@ __global__ void __launch_bounds__(128, 2)
         phase = 3;
         continue;
       }
-      const int sd = rank < FPX_RK ? cseed[u * FPX_RK + rank] : -1;
-      if (sd < 0) {
-        phase = 1;  // needs its seed
-        continue;
-      }
-      // seed found by k_rest_lists (the same D7 node search)
-      rc[0] = z[sd % N];
-      rc[1] = DR > 1 ? z[(sd / N) % N] : 0.0;
-      rc[2] = DR > 2 ? z[sd / (N * N)] : 0.0;
-#pragma unroll
-      for (int a = 0; a < 3; ++a) rn[a] = rc[a];
-      first = true;
-      held_prev = false;
-      it = 0;
-      alpha = P.alpha0;
-      phase = 3;
+      phase = 1;  // needs its D7 seed
     }
     // seeds (D7) of the lanes that just got a pair, 4 at a time: the warp
     // reads each candidate's nodes with coalesced loads
@@ -1772,7 +1691,7 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
   double xs[3] = {0.0, 0.0, 0.0}, rc[3] = {0.0, 0.0, 0.0}, rn[3] = {0.0, 0.0, 0.0};
   double alpha = 1.0, fcur = 0.0, pred = 0.0, smax = 0.0;
   NState st;
-  int64_t s_newton = 0, s_iters = 0, s_evals = 0, nev = 0, nev2 = 0, s_chunks = 0;
+  int64_t s_newton = 0, s_iters = 0, s_evals = 0, nev = 0, nev2 = 0, s_chunks = 0, nlev = 0;
   // first chunk
   {
     int64_t c = 0;
@@ -1964,6 +1883,7 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
     const bool w2 = __any_sync(FPX_FULL, phase == 2 && on_boundary<DR>(rn));
     ++nev;
     nev2 += w2 ? 1 : 0;
+    nlev += phase == 2 ? 1 : 0;
     eval_state_rt<D, DR, N, 0>(sX, z, scale, rn, xs, st, sb, w2);
     if (phase != 2) continue;
     // ---- this lane's trust-region Newton update (newton_warp, D8)
@@ -2073,6 +1993,7 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
   s_newton = warp_sum64(s_newton);
   s_iters = warp_sum64(s_iters);
   s_evals = warp_sum64(s_evals);
+  nlev = warp_sum64(nlev);
   if (lane == 0) {
     atomicAdd((unsigned long long*)&stats[FPX_STAT_NEWTON], (unsigned long long)s_newton);
     atomicAdd((unsigned long long*)&stats[FPX_STAT_ITERS], (unsigned long long)s_iters);
@@ -2083,6 +2004,7 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
     atomicAdd((unsigned long long*)&stats[FPX_STAT_R1_WARP_EVALS], (unsigned long long)nev);
     atomicAdd((unsigned long long*)&stats[FPX_STAT_R1_W2_EVALS], (unsigned long long)nev2);
     atomicAdd((unsigned long long*)&stats[FPX_STAT_R1_ITEMS], (unsigned long long)s_chunks);
+    atomicAdd((unsigned long long*)&stats[FPX_STAT_R1_LANE_EVALS], (unsigned long long)nlev);
   }
 }
 
@@ -2255,7 +2177,7 @@ template <int D, int DR, int N>
 struct Rest {
   static cudaError_t run(const fpx_mesh_t& m, const double* x, int64_t nun_cap,
                          const int64_t* nun_dev, const int32_t* upts, const int32_t* clist,
-                         const int16_t* cseed, const int32_t* cnum, const int32_t* nps,
+                         const int32_t* cnum, const int32_t* nps,
                          const int32_t* perm,
                          const int64_t* cum, const int32_t* maxnp, const int32_t* best,
                          const int4* pairs, const int64_t* npairs, int4* redo, int64_t* nredo,
@@ -2274,10 +2196,10 @@ struct Rest {
     // for two consecutive iterations; pass 2 redoes every stopped candidate
     // (of round 1 and of pass 1) in full for points still without an
     // INTERIOR.  The records are those of the full solves either way.
-    fn<<<blocks, threads, smem, st>>>(m, x, nun_dev, upts, clist, cseed, cnum, nps, perm, cum,
+    fn<<<blocks, threads, smem, st>>>(m, x, nun_dev, upts, clist, cnum, nps, perm, cum,
                                       maxnp, best, pairs, cap, npairs, 1, redo, nredo, found,
                                       lock, code, elem, r, dist, iters, counter, stats);
-    fn<<<blocks, threads, smem, st>>>(m, x, nun_dev, upts, clist, cseed, cnum, nps, perm, cum,
+    fn<<<blocks, threads, smem, st>>>(m, x, nun_dev, upts, clist, cnum, nps, perm, cum,
                                       nullptr, best, redo, cap, nredo, 0, nullptr, nullptr,
                                       found, lock, code, elem, r, dist, iters, counter + 1, stats);
     cudaError_t err = cudaGetLastError();
@@ -2291,14 +2213,13 @@ struct Rest {
   }
   static cudaError_t lists(const fpx_mesh_t& m, const double* x, int64_t nun_cap,
                            const int64_t* nun_dev, const int32_t* upts, int32_t* clist,
-                           int16_t* cseed,
                            int32_t* cnum, int32_t* nps, int32_t* hist, int32_t* bstart,
                            int32_t* bcur, int32_t* perm, int64_t* cum, int32_t* maxnp,
                            int4* pairs, int64_t* npairs, cudaStream_t st) {
     int64_t b = (nun_cap + 3) / 4;
     if (b > 148 * 16) b = 148 * 16;
     if (b < 1) b = 1;
-    k_rest_lists<D><<<(unsigned)b, 128, 0, st>>>(m, x, nun_dev, upts, clist, cseed, cnum, nps,
+    k_rest_lists<D><<<(unsigned)b, 128, 0, st>>>(m, x, nun_dev, upts, clist, cnum, nps,
                                                  hist);
     k_rest_order<<<1, FPX_HMAX, 0, st>>>(hist, bstart, cum, maxnp, npairs);
     int64_t b2 = (nun_cap + 255) / 256;

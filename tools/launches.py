@@ -1,5 +1,5 @@
 """Summarise an ncu launch list (gpu__time_duration.sum CSV): the kernels of
-the last bench step (from the last k_point_cells launch)."""
+the longest find of the run (a full bench step)."""
 import csv
 import sys
 
@@ -13,9 +13,13 @@ for r in rows:
         d = dict(zip(hdr, r))
         if d.get('Metric Name') == 'gpu__time_duration.sum':
             out.append((d['Kernel Name'], float(d['Metric Value'])))
-start = [i for i, o in enumerate(out) if 'k_point_cells' in o[0]][-1]
+# the finds of the run start at k_point_cells; report the longest one (the
+# full-size bench step, not the small work-counter sample that follows it)
+starts = [i for i, o in enumerate(out) if 'k_point_cells' in o[0]] + [len(out)]
+spans = [(sum(ns for _, ns in out[a:b]), a, b) for a, b in zip(starts, starts[1:])]
+_, start, stop = max(spans)
 tot = 0.0
-for name, ns in out[start:]:
+for name, ns in out[start:stop]:
     if 'dfma_probe' in name or 'at::' in name:
         continue
     tot += ns
