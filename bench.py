@@ -1,6 +1,7 @@
 """findpts+eval throughput benchmark (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload cfg2|cfg3|cfg4]
 
 Workload (BASELINE.json configs[1]): 3D Kershaw-deformed
 hex mesh 32^3 elements, p=4 (eps_y = eps_z = 0.3), field sin(pi x)cos(pi y)e^z,
@@ -16,6 +17,9 @@ through the public API with host points copied in and values + records
 copied out inside the timed region; roofline of the dominant kernel
 (k_newton_stream, FP64-bound); cpu_baseline = the oracle port on the host
 cores over a bounded sample.
+--workload cfg3 (Kershaw 64^3, p=7, 10^7 points, mesh replicated on the GPU)
+and cfg4 (cubed sphere 6*32^2 quads, p=4, 10^6 on/near-surface points) run the
+same step on the other BASELINE configs; cfg2 stays the default.
 --impl reference: the reference's CPU path (the C oracle port; the reference
 package itself has no find/eval code) on all host cores.
 """
@@ -33,80 +37,128 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-N_ELEM_AXIS = 32
-ORDER = 4
-PTS_PER_GPU = 1_000_000
 METRIC = "findpts+eval points/sec (3D hex, p=4, 1M pts/GPU) at 1/2/4/8 B200"
 UNIT = "points/s"
 
-# Algorithmic FP64 work per unit (frozen; N = p+1, d = dr = 3).
-def f_iter(N):   # one Newton iteration: 3 basis evals + x,G contraction + 3x3 solve
-    return 3 * 13 * N + 2 * 3 * (2 * N ** 3 + 3 * N ** 2 + 4 * N) + 130
+
+class Workload:
+    """One benchmark configuration (BASELINE.json configs).
+    cfg2 is the headline (BASELINE metric); cfg3/cfg4 are the other
+    single-GPU-sized configs, run with --workload."""
+
+    def __init__(self, key, gen, n_axis, order, pts, dr, metric, desc, points="uniform"):
+        self.key, self.gen, self.n_axis, self.order = key, gen, n_axis, order
+        self.pts, self.dr, self.metric, self.desc, self.points = pts, dr, metric, desc, points
+
+    def mesh(self):
+        from paper_2501_12349_b200 import toolkit
+        if self.gen == "kershaw":
+            return toolkit.kershaw_mesh(self.n_axis, self.order)
+        return toolkit.sphere_mesh(self.n_axis, self.order)
+
+    def field(self, mesh):
+        from paper_2501_12349_b200 import toolkit
+        return toolkit.analytic_field("smooth", mesh)
+
+    def query(self, mesh, n, rank):
+        from paper_2501_12349_b200 import toolkit
+        if self.points == "uniform":
+            return toolkit.uniform_points(n, 3, seed=1000 + rank)
+        return toolkit.surface_points(mesh, n, seed=1000 + rank)[0]
+
+    def config(self, n_gpus):
+        E = self.n_axis ** 3 if self.gen == "kershaw" else 6 * self.n_axis ** 2
+        return {"workload": f"{self.key}: {self.desc}, {self.pts} pts/GPU, find+eval (C=1)",
+                "mesh": f"{self.gen}{self.n_axis}" + ("^3" if self.gen == "kershaw" else ""),
+                "order": self.order, "elements": E, "points_per_gpu": self.pts,
+                "components": 1,
+                "partition": "contiguous z-slabs" if n_gpus > 1 else "single",
+                "l2": "flushed (256 MiB write) between timed steps"}
 
 
-def f_seed(N):   # nearest-node seed over N^3 nodes
-    return 8 * N ** 3
+WORKLOADS = {
+    "cfg2": Workload("cfg-2", "kershaw", 32, 4, 1_000_000, 3, METRIC,
+                     "Kershaw hex 32^3 p=4 (eps 0.3)"),
+    "cfg3": Workload("cfg-3", "kershaw", 64, 7, 10_000_000, 3,
+                     "findpts+eval points/sec (3D hex 64^3, p=7, 1e7 pts) on B200",
+                     "Kershaw hex 64^3 p=7 (eps 0.3), replicated mesh"),
+    "cfg4": Workload("cfg-4", "sphere", 32, 4, 1_000_000, 2,
+                     "surface findpts+eval points/sec (cubed sphere, p=4, 1e6 pts) on B200",
+                     "cubed-sphere quads 6*32^2 p=4 in 3D", points="surface"),
+}
+W = WORKLOADS["cfg2"]
 
 
-def f_eval(N, C=1):
-    return 3 * 8 * N + 2 * C * (N ** 3 + N ** 2 + N)
+# Algorithmic FP64 work per unit (SURVEY.md §8d, frozen; N = p+1; the
+# contraction term generalises 2N^3+3N^2+4N (d_r = 3) to d_r = 2 and 1).
+def _contr(N, dr):
+    return {3: 2 * N ** 3 + 3 * N ** 2 + 4 * N, 2: 2 * N ** 2 + 3 * N, 1: 2 * N}[dr]
+
+
+def f_iter(N, d=3, dr=3):  # one Newton iteration: basis evals + x,G contraction + solve
+    return dr * 13 * N + 2 * d * _contr(N, dr) + 130
+
+
+def f_seed(N, dr=3):   # nearest-node seed over N^dr nodes
+    return 8 * N ** dr
+
+
+def f_eval(N, C=1, dr=3):
+    return dr * 8 * N + 2 * C * sum(N ** k for k in range(1, dr + 1))
 
 
 F_SEED_AFFINE = 2 * 3 * 3 + 3   # D7' seed: J_c^-1 (x* - x_c) (3x3 mat-vec + 3 subtractions)
 
 
-def round1_flops(st, N):
+def round1_flops(st, N, d=3, dr=3):
     """Algorithmic FP64 work of the round-1 kernel: every lane evaluation of
-    the map (basis, x + G contraction, step algebra = F_iter), the affine
-    seed of every solve, the fused field evaluation of every final point."""
-    return st["r1_lane_evals"] * f_iter(N) + st["newton_r1"] * F_SEED_AFFINE \
-        + st["evals_r1"] * f_eval(N)
+    the map (basis, x + G contraction, step algebra = F_iter), the seed of
+    every solve (affine for volumes, nearest node for d_r < d), the fused
+    field evaluation of every final point."""
+    seed = F_SEED_AFFINE if dr == d else f_seed(N, dr)
+    return st["r1_lane_evals"] * f_iter(N, d, dr) + st["newton_r1"] * seed \
+        + st["evals_r1"] * f_eval(N, 1, dr)
 
 
-def step_flops(st, N):
+def step_flops(st, N, d=3, dr=3):
     """Whole find+eval step: round 1, the rest kernels' lane evaluations
-    (each rest solve counted with a nearest-node seed, 8 N^3: an upper bound,
-    pass-1 solves seed from the frame), 30 flops per box test, and the field
-    evaluation of every found point."""
+    (each rest solve counted with a nearest-node seed, 8 N^dr: an upper
+    bound, pass-1 solves seed from the frame), 30 flops per box test, and the
+    field evaluation of every found point."""
     rest_solves = st["newton"] - st["newton_r1"]
-    return round1_flops(st, N) + st["rest_lane_evals"] * f_iter(N) \
-        + rest_solves * f_seed(N) + 30 * st["box_tests"] \
-        + (st["evals"] - st["evals_r1"]) * f_eval(N)
+    return round1_flops(st, N, d, dr) + st["rest_lane_evals"] * f_iter(N, d, dr) \
+        + rest_solves * f_seed(N, dr) + 30 * st["box_tests"] \
+        + (st["evals"] - st["evals_r1"]) * f_eval(N, 1, dr)
 
 
 def workload_config(n_gpus):
-    return {"workload": f"cfg-2: Kershaw hex {N_ELEM_AXIS}^3 p={ORDER}, "
-                        f"{PTS_PER_GPU} uniform pts/GPU, find+eval (C=1)",
-            "mesh": f"kershaw{N_ELEM_AXIS}^3", "order": ORDER, "elements": N_ELEM_AXIS ** 3,
-            "points_per_gpu": PTS_PER_GPU, "components": 1,
-            "partition": "contiguous z-slabs" if n_gpus > 1 else "single",
-            "l2": "flushed (256 MiB write) between timed steps"}
+    return W.config(n_gpus)
 
 
-def build_inputs(rank=0):
-    from paper_2501_12349_b200 import toolkit
-    mesh = toolkit.kershaw_mesh(N_ELEM_AXIS, ORDER)
-    field = toolkit.analytic_field("smooth", mesh)
-    x = toolkit.uniform_points(PTS_PER_GPU, 3, seed=1000 + rank)
+def build_inputs(rank=0, n=None):
+    mesh = W.mesh()
+    field = W.field(mesh)
+    x = W.query(mesh, n or W.pts, rank)
     return mesh, field, x
 
 
 # ----------------------------------------------------------------- CPU arm
-def cpu_find_eval(sample=20000, threads=None, steps=1, warmup=0, rank=0):
+def cpu_find_eval(sample=20000, threads=None, steps=1, warmup=0, rank=0, inputs=None):
     """The oracle port (oracle/fpx_oracle.c, OpenMP) on the host cores."""
     from oracle import oracle as O
-    mesh, field, x = build_inputs(rank)
+    mesh, field, x = inputs or build_inputs(rank, sample)
     nthreads = threads or len(os.sched_getaffinity(0))
     # the same local grid as engine.setup's default (hash_refine x SPEC rule)
     from paper_2501_12349_b200.engine import EngineOptions
-    ncell = min(1024, EngineOptions().hash_refine * O.n_cells(mesh.num_elements, 3))
-    OS = O.OracleSetup(mesh.nodes, 3, 3, ORDER, nthreads=nthreads, ncell=ncell)
+    d = mesh.phys_dim
+    ncell = min(1024, EngineOptions().hash_refine * O.n_cells(mesh.num_elements, d))
+    OS = O.OracleSetup(mesh.nodes, d, W.dr, W.order, nthreads=nthreads, ncell=ncell)
     xs = x[:sample]
     times = []
     for k in range(warmup + steps):
         t = time.perf_counter()
         rec = OS.find(xs, nthreads=nthreads)
-        O.evaluate(OS.B, 3, field, rec["code"], rec["elem"], rec["r"], nthreads=nthreads)
+        O.evaluate(OS.B, W.dr, field, rec["code"], rec["elem"], rec["r"], nthreads=nthreads)
         if k >= warmup:
             times.append(time.perf_counter() - t)
     work = {"points": int(sample), "box_tests": int(rec["nbox"].sum()),
@@ -120,13 +172,13 @@ def run_reference(args):
         return
     sample = args.cpu_sample
     v, cores, t, _ = cpu_find_eval(sample=sample, steps=args.steps, warmup=args.warmup)
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
+    line = {"impl": "reference", "metric": W.metric, "value": v, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(args.gpus),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"{sample} of the {PTS_PER_GPU} cfg-2 points per step "
+                             "sample": f"{sample} of the {W.pts} {W.key} points per step "
                                        "(oracle C port, OpenMP over points, setup excluded)"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -217,11 +269,11 @@ def run_ours(args):
     nodes = mesh.nodes[a:b]
     fblk = torch.from_numpy(np.ascontiguousarray(field[a:b])).to(dev)
     t0 = time.perf_counter()
-    S = engine.setup(torch.from_numpy(np.ascontiguousarray(nodes)).to(dev), ORDER, 3,
+    S = engine.setup(torch.from_numpy(np.ascontiguousarray(nodes)).to(dev), W.order, W.dr,
                      group=group, elem_offset=a)
     torch.cuda.synchronize()
     setup_ms = (time.perf_counter() - t0) * 1e3
-    F = engine.Field(fblk, ORDER)
+    F = engine.Field(fblk, W.order)
     x_dev = torch.from_numpy(x_host).to(dev)
     x_pin = torch.from_numpy(x_host).pin_memory()
     n = x_host.shape[0]
@@ -283,7 +335,7 @@ def run_ours(args):
                 code=torch.empty(n, dtype=torch.int32).pin_memory(),
                 elem=torch.empty(n, dtype=torch.int32).pin_memory(),
                 rank=torch.empty(n, dtype=torch.int32).pin_memory(),
-                r=torch.empty((n, 3), dtype=torch.float64).pin_memory(),
+                r=torch.empty((n, W.dr), dtype=torch.float64).pin_memory(),
                 dist=torch.empty(n, dtype=torch.float64).pin_memory())
     e2e_ms = []
     for _ in range(max(args.warmup, 3)):  # warm-up: host-path buffers, streams
@@ -296,24 +348,26 @@ def run_ours(args):
         engine.find_and_interpolate_host(S, F, x_pin, out=outs, sync=True)
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
     e2e_max = max_over_ranks(float(np.mean(e2e_ms)))
-    h2d = n * 3 * 8
-    d2h = n * (8 + 4 + 4 + 4 + 24 + 8)
+    d = mesh.phys_dim
+    h2d = n * d * 8
+    d2h = n * (8 + 4 + 4 + 4 + 8 * W.dr + 8)
     # --- roofline of the dominant kernel (round-1 Newton, FP64-bound)
     st = dict(stats[-1])
-    N = ORDER + 1
-    flops_r1 = round1_flops(step1, N)
+    N = W.order + 1
+    flops_r1 = round1_flops(step1, N, d, W.dr)
     tf = np.zeros(1)
     _C.check(L.fpx_probe_fp64(tf.ctypes.data, _C.stream_handle()), "fpx_probe_fp64")
     achieved = flops_r1 / (kern_ms * 1e-3) / 1e12
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "newton_stream_dram.json")
-    if os.path.exists(tpath):
-        traffic = json.load(open(tpath)).get("bytes_per_launch")
-    flops_all = step_flops(st, N)
+    if os.path.exists(tpath):  # ncu dram bytes of the same launch, per workload
+        traffic = json.load(open(tpath)).get(W.key, {}).get("bytes_per_launch")
+    flops_all = step_flops(st, N, d, W.dr)
     if world > 1:
         dist.barrier()
     if rank == 0:
-        cpu_v, cores, cpu_t, owork = cpu_find_eval(sample=args.cpu_sample, steps=1, warmup=0)
+        cpu_v, cores, cpu_t, owork = cpu_find_eval(sample=args.cpu_sample, steps=1, warmup=0,
+                                                   inputs=(mesh, field, x_host))
         # the kernels' own work counters on the same sample, beside the
         # oracle's (the oracle visits candidates in ascending id, the kernels
         # best-first, so newton/iters differ by design; box_tests agree)
@@ -323,7 +377,7 @@ def run_ours(args):
                  "newton": int(ss["newton"]), "iters": int(ss["iters"])}
         clocks = clk.summary()
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "metric": W.metric, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": step_ms_max,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded Kershaw mesh + uniform points)",
@@ -335,7 +389,8 @@ def run_ours(args):
                            "out; wall clock; round-1 records downloaded under the rest phase)"},
             "work_vs_oracle": {"sample": f"first {args.cpu_sample} points of the step",
                                "kernels": kwork, "oracle": owork},
-            "roofline": {"bound": "fp64", "kernel": "k_newton_stream<3,3,5,3> (round 1)",
+            "roofline": {"bound": "fp64",
+                         "kernel": f"k_newton_stream<{d},{W.dr},{N},S> (round 1)",
                          "achieved": achieved, "peak": float(tf[0]), "unit": "TFLOP/s",
                          "frac": achieved / float(tf[0]), "traffic": traffic,
                          "peak_source": "fpx_probe_fp64 DFMA chains, measured in this run "
@@ -344,7 +399,7 @@ def run_ours(args):
                          "kernel_timing": "CUDA events around the round-1 launch on its stream",
                          "flops_per_launch": flops_r1},
             "cpu_baseline": {"value": cpu_v, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"{args.cpu_sample} of the cfg-2 points, oracle C port "
+                             "sample": f"{args.cpu_sample} of the {W.key} points, oracle C port "
                                        "(OpenMP over points), setup excluded"},
             "clocks": clocks, "gpu_launches": int(launches),
             "work": {"setup_ms": setup_ms, "step_flops": flops_all,
@@ -362,7 +417,12 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=50000)
+    ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS),
+                    help="cfg2 = the BASELINE headline (default); cfg3 / cfg4 = the other "
+                         "BASELINE configs that fit one GPU")
     args = ap.parse_args()
+    global W
+    W = WORKLOADS[args.workload]
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
