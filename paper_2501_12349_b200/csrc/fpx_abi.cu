@@ -145,7 +145,8 @@ struct FindWs {
   int32_t *best, *npass, *upts, *clist, *cnum, *found, *lock, *nps, *perm, *hist, *bstart, *bcur,
       *maxnp;
   int64_t *cum, *npairs, *nredo;
-  int4 *pairs, *redo;
+  int4 *pairs, *redo, *umeta;
+  double* ux;
   int64_t *nun, *counter, *chunk_ctr;
   Group g1;
   // point ordering by hash cell
@@ -185,6 +186,8 @@ struct FindWs {
     nun = c.take<int64_t>(1);
     counter = c.take<int64_t>(2);
     chunk_ctr = c.take<int64_t>(1);
+    ux = c.take<double>(3 * n);
+    umeta = c.take<int4>(n);
     g1.carve(c, E, n);
   }
 };
@@ -526,14 +529,15 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
   // --- round 1: group by best-first element, Newton, fused eval
   g_launches += 3;
   FPX_CK(w.g1.build(E, n, nullptr, w.best, nullptr, st));
+  FPX_LAUNCH(fpx::launch_stream_units(n, E, w.g1.packed_off, w.g1.sorted, w.best, w.g1.count, x,
+                                      M.d, w.ux, w.umeta, st));
   if (g_prof_start) FPX_CK(cudaEventRecord(g_prof_start, st));
   FPX_CK(cudaMemsetAsync(w.chunk_ctr, 0, sizeof(int64_t), st));
   // candidates held on a face twice in a row stop early and are redone in
   // full only if their point ends without an INTERIOR (see k_rest_l1)
-  FPX_LAUNCH(fpx::launch_newton_stream(M, n, x, w.g1.sorted, w.g1.packed_off, w.g1.count,
-                                       w.best, w.npass, code, elem, r, dist, iters, field, C,
-                                       values, w.upts, w.nun, w.chunk_ctr, w.redo, w.nredo,
-                                       2 * n + 1024, stats, st));
+  FPX_LAUNCH(fpx::launch_newton_stream(M, n, w.ux, w.umeta, w.g1.packed_off, w.npass, code,
+                                       elem, r, dist, iters, field, C, values, w.upts, w.nun,
+                                       w.chunk_ctr, w.redo, w.nredo, 2 * n + 1024, stats, st));
   if (g_prof_stop) FPX_CK(cudaEventRecord(g_prof_stop, st));
   // external record: also a real event node when captured into a CUDA graph
   if (g_round1_done) FPX_CK(cudaEventRecord(g_round1_done, st));

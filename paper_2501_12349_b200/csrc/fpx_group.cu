@@ -62,6 +62,33 @@ __global__ void k_scatter_units(int64_t cap, const int64_t* __restrict__ n_dev,
   }
 }
 
+// Stream-ordered unit records of round 1 (k_newton_stream): for stream
+// position g, the point's coordinates ux[g] and umeta[g] = (point, element,
+// end of the element's group).  The round-1 loader and lane refill then read
+// one record each instead of the dependent sorted -> best -> packed_off chain.
+__global__ void k_stream_units(int64_t E, const uint64_t* __restrict__ packed_off,
+                               const int32_t* __restrict__ sorted, const int32_t* __restrict__ best,
+                               const int32_t* __restrict__ ecount, const double* __restrict__ x,
+                               int d, double* ux, int4* umeta) {
+  const int64_t nu = (int64_t)(packed_off[E] & 0xffffffffull);
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < nu;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int pt = sorted[g];
+    const int e = best[pt];
+    const int64_t gend = (int64_t)(packed_off[e] & 0xffffffffull) + ecount[e];
+    for (int c = 0; c < d; ++c) ux[g * d + c] = x[(int64_t)pt * d + c];
+    umeta[g] = make_int4(pt, e, (int)gend, 0);
+  }
+}
+
+cudaError_t launch_stream_units(int64_t n_cap, int64_t E, const uint64_t* packed_off,
+                                const int32_t* sorted, const int32_t* best, const int32_t* ecount,
+                                const double* x, int d, double* ux, int4* umeta, cudaStream_t st) {
+  k_stream_units<<<grid_of(n_cap, 256), 256, 0, st>>>(E, packed_off, sorted, best, ecount, x, d,
+                                                      ux, umeta);
+  return cudaGetLastError();
+}
+
 // Zero-copy patch of host records: the rest points' records written straight
 // into mapped pinned host arrays over PCIe, after the bulk download of the
 // round-1 records (engine.find_and_interpolate_host).  No host thread touches

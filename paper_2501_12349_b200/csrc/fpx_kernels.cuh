@@ -75,16 +75,19 @@ cudaError_t launch_scatter_units(int64_t nunits_cap, const int64_t* nunits_dev,
 
 // Newton / eval (fpx_newton.cu, FMA allowed).
 bool newton_supported(int d, int dr, int N);
-// Round 1 streamed (k_newton_stream): points sorted by best-first element
-// (sorted / packed_off / ecount from the element grouping).
-cudaError_t launch_newton_stream(const fpx_mesh_t& m, int64_t n, const double* x,
-                                 const int32_t* sorted, const uint64_t* packed_off,
-                                 const int32_t* ecount, const int32_t* best, const int32_t* npass,
-                                 int32_t* code, int32_t* elem, double* r, double* dist,
-                                 int32_t* iters, const double* field, int C, double* values,
-                                 int32_t* upts, int64_t* nun_dev, int64_t* chunk_ctr, int4* redo,
-                                 int64_t* nredo, int64_t redo_cap, int64_t* stats,
-                                 cudaStream_t st);
+// Stream-ordered unit records (x and (point, element, group end)) of round 1.
+cudaError_t launch_stream_units(int64_t n_cap, int64_t E, const uint64_t* packed_off,
+                                const int32_t* sorted, const int32_t* best, const int32_t* ecount,
+                                const double* x, int d, double* ux, int4* umeta, cudaStream_t st);
+// Round 1 streamed (k_newton_stream): points in best-first element order as
+// stream records (ux / umeta from launch_stream_units; packed_off[E] = count).
+cudaError_t launch_newton_stream(const fpx_mesh_t& m, int64_t n, const double* ux,
+                                 const int4* umeta, const uint64_t* packed_off,
+                                 const int32_t* npass, int32_t* code, int32_t* elem, double* r,
+                                 double* dist, int32_t* iters, const double* field, int C,
+                                 double* values, int32_t* upts, int64_t* nun_dev,
+                                 int64_t* chunk_ctr, int4* redo, int64_t* nredo, int64_t redo_cap,
+                                 int64_t* stats, cudaStream_t st);
 // Remaining candidates of the points round 1 left unresolved: their
 // best-first candidate lists (k_rest_lists), then the lane-per-point Newton
 // (k_rest_lanes).

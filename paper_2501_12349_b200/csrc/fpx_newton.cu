@@ -44,17 +44,16 @@ static cudaError_t dispatch(int d, int dr, int N, A... args) {
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_newton_stream(const fpx_mesh_t& m, int64_t n, const double* x,
-                                 const int32_t* sorted, const uint64_t* packed_off,
-                                 const int32_t* ecount, const int32_t* best, const int32_t* npass,
-                                 int32_t* code, int32_t* elem, double* r, double* dist,
-                                 int32_t* iters, const double* field, int C, double* values,
-                                 int32_t* upts, int64_t* nun_dev, int64_t* chunk_ctr, int4* redo,
-                                 int64_t* nredo, int64_t redo_cap, int64_t* stats,
-                                 cudaStream_t st) {
-  return dispatch<Stream>(m.d, m.dr, m.N, m, x, sorted, packed_off, ecount, best, npass, code,
-                          elem, r, dist, iters, field, C, values, upts, nun_dev, chunk_ctr, n,
-                          redo, nredo, redo_cap, stats, st);
+cudaError_t launch_newton_stream(const fpx_mesh_t& m, int64_t n, const double* ux,
+                                 const int4* umeta, const uint64_t* packed_off,
+                                 const int32_t* npass, int32_t* code, int32_t* elem, double* r,
+                                 double* dist, int32_t* iters, const double* field, int C,
+                                 double* values, int32_t* upts, int64_t* nun_dev,
+                                 int64_t* chunk_ctr, int4* redo, int64_t* nredo, int64_t redo_cap,
+                                 int64_t* stats, cudaStream_t st) {
+  return dispatch<Stream>(m.d, m.dr, m.N, m, ux, umeta, packed_off, npass, code, elem, r, dist,
+                          iters, field, C, values, upts, nun_dev, chunk_ctr, n, redo, nredo,
+                          redo_cap, stats, st);
 }
 
 template <int D, int DR, int N>

@@ -757,11 +757,16 @@ __device__ __forceinline__ double contract_smem(const double* __restrict__ sU,
       double t = 0.0;
 #pragma unroll
       for (int j = 0; j < N; ++j) {
-        const double* row = sU + (j + N * k) * NP;
-        double s = 0.0;
+        const double* row = sU + (j + N * k) * NP;  // 16-byte aligned, NP even
+        double s = 0.0, s1 = 0.0;
 #pragma unroll
-        for (int i = 0; i < N; ++i) s = fma(row[i], v[0][i], s);
-        t = fma(s, v[1][j], t);
+        for (int i = 0; i + 1 < N; i += 2) {
+          const double2 p = *reinterpret_cast<const double2*>(row + i);
+          s = fma(p.x, v[0][i], s);
+          s1 = fma(p.y, v[0][i + 1], s1);
+        }
+        if (N % 2) s = fma(row[N - 1], v[0][N - 1], s);
+        t = fma(s + s1, v[1][j], t);
       }
       q = fma(t, v[2][k], q);
     }
@@ -780,6 +785,51 @@ __device__ __forceinline__ double contract_smem(const double* __restrict__ sU,
     double s = 0.0;
 #pragma unroll
     for (int i = 0; i < N; ++i) s = fma(sU[i], v[0][i], s);
+    return s;
+  }
+}
+
+// Field value at r from a lexicographic unpadded block [K] (a slot's staged
+// field in shared memory, or global memory): generic loads.
+template <int DR, int N>
+__device__ __forceinline__ double contract_flat(const double* __restrict__ U,
+                                               const double (*v)[N]) {
+  if constexpr (DR == 3) {
+    double q = 0.0;
+#pragma unroll
+    for (int k = 0; k < N; ++k) {
+      double t = 0.0;
+#pragma unroll
+      for (int j = 0; j < N; ++j) {
+        const double* row = U + N * (j + N * k);
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int i = 0; i < N; i += 2) {
+          s0 = fma(row[i], v[0][i], s0);
+          if (i + 1 < N) s1 = fma(row[i + 1], v[0][i + 1], s1);
+        }
+        t = fma(s0 + s1, v[1][j], t);
+      }
+      q = fma(t, v[2][k], q);
+    }
+    return q;
+  } else if constexpr (DR == 2) {
+    double t = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; i += 2) {
+        s0 = fma(U[j * N + i], v[0][i], s0);
+        if (i + 1 < N) s1 = fma(U[j * N + i + 1], v[0][i + 1], s1);
+      }
+      t = fma(s0 + s1, v[1][j], t);
+    }
+    return t;
+  } else {
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < N; ++i) s = fma(U[i], v[0][i], s);
     return s;
   }
 }
@@ -988,6 +1038,25 @@ __device__ __forceinline__ void mbar_init(uint64_t* mb, unsigned count) {
 __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* mb) {
   const unsigned a = (unsigned)__cvta_generic_to_shared(mb);
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(a) : "memory");
+}
+// One elected lane: expect `bytes` on the slot's mbarrier (its single
+// arrival), then 1D TMA bulk copies global -> shared that complete_tx on it.
+// The proxy fence orders the lanes' earlier generic reads of the slot before
+// the async-proxy refill.
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* mb, unsigned bytes) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(mb);
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(a), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* gsrc, unsigned bytes,
+                                         uint64_t* mb) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(sdst);
+  const unsigned b = (unsigned)__cvta_generic_to_shared(mb);
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(d),
+      "l"(gsrc), "r"(bytes), "r"(b)
+      : "memory");
 }
 __device__ __forceinline__ bool mbar_test(uint64_t* mb, unsigned parity) {
   const unsigned a = (unsigned)__cvta_generic_to_shared(mb);
@@ -1631,51 +1700,74 @@ __global__ void k_rest_values(const double* __restrict__ fbasis, int M,
 #define FPX_CHUNK_DEFAULT 64
 #endif
 
+// L1 prefetch of a claimed chunk's stream records (ux, umeta): the lanes
+// that take its units later read them from L1 instead of a DRAM round trip.
+__device__ __forceinline__ void prefetch_lines(const void* p, size_t bytes, int lane) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(127);
+  const uintptr_t b = reinterpret_cast<uintptr_t>(p) + bytes;
+  for (uintptr_t q = a + (uintptr_t)lane * 128; q < b; q += 32 * 128)
+    asm volatile("prefetch.L1 [%0];\n" ::"l"(q));
+}
+template <int D>
+__device__ __forceinline__ void prefetch_chunk(const double* ux, const int4* umeta, int64_t c0,
+                                               int len, int lane) {
+  prefetch_lines(ux + c0 * D, (size_t)len * D * sizeof(double), lane);
+  prefetch_lines(umeta + c0, (size_t)len * sizeof(int4), lane);
+}
+
 template <int S>
 struct StreamMeta {
   uint64_t mbar[S];
-  int elem[S], start[S], end[S];
+  int elem[S], start[S], end[S], fsh[S];
   unsigned parity[S];
 };
 
 template <int D, int DR, int N, int S>
 __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
-    k_newton_stream(fpx_mesh_t m, const double* __restrict__ x, const int32_t* __restrict__ sorted,
-                    const uint64_t* __restrict__ packed_off, const int32_t* __restrict__ ecount,
-                    const int32_t* __restrict__ best, const int32_t* __restrict__ npass,
+    k_newton_stream(fpx_mesh_t m, const double* __restrict__ ux, const int4* __restrict__ umeta,
+                    const uint64_t* __restrict__ packed_off, const int32_t* __restrict__ npass,
                     int32_t* code, int32_t* elem, double* r, double* dist, int32_t* iters,
                     const double* __restrict__ field, int C, double* values, int32_t* upts,
-                    int64_t* nun_dev, int64_t* chunk_ctr, int slot_stride, int chunk,
-                    int4* redo, int64_t* nredo, int64_t redo_cap, int64_t* stats) {
+                    int64_t* nun_dev, int64_t* chunk_ctr, int slot_stride, int nslot,
+                    int fstage, int chunk, int4* redo, int64_t* nredo, int64_t redo_cap,
+                    int64_t* stats) {
   using L = Lay<D, DR, N>;
   constexpr int K = L::K;
   constexpr int SCR = Scratch<DR, N>::SLOTS;
+  constexpr int FRAME = DR == D ? D + D * D : 0;  // affine frame doubles per slot
   extern __shared__ __align__(16) double smem[];
   double* z = smem;
   double* scale = smem + N;
   const int warp = threadIdx.x / FPX_WARP, lane = threadIdx.x % FPX_WARP;
   const int wpb = blockDim.x / FPX_WARP;
-  // slot: geometry [D][ROWS][NP] | field [C][ROWS][NP] | frame (x_c, J_c^-1)
-  const int frame_off = L::GEO + (field ? C * L::CS : 0);
-  double* slots = smem + 2 * ((N + 1) & ~1) + (size_t)warp * (S * slot_stride + SCR * FPX_WARP);
-  double* sb = slots + S * slot_stride + lane;
+  // slot (nslot <= S of them per warp): geometry [D][ROWS][NP] (= the
+  // mesh.nodes_pad block) | frame (x_c, J_c^-1) | field [C][K] from the
+  // 16-byte boundary below the element's block (when fstage)
+  constexpr int frame_off = L::GEO;
+  constexpr int field_off = L::GEO + ((FRAME + 1) & ~1);
+  double* slots =
+      smem + 2 * ((N + 1) & ~1) + (size_t)warp * (nslot * slot_stride + SCR * FPX_WARP);
+  double* sb = slots + nslot * slot_stride + lane;
   double* stash = sb + Scratch<DR, N>::STASH * FPX_WARP;
   StreamMeta<S>* meta =
       reinterpret_cast<StreamMeta<S>*>(smem + 2 * ((N + 1) & ~1) +
-                                       (size_t)wpb * (S * slot_stride + SCR * FPX_WARP)) +
+                                       (size_t)wpb * (nslot * slot_stride + SCR * FPX_WARP)) +
       warp;
   if (threadIdx.x < N) {
     z[threadIdx.x] = m.basis[FPX_BASIS_NODES(N, m.M) + threadIdx.x];
     scale[threadIdx.x] = m.basis[FPX_BASIS_SCALE(N, m.M) + threadIdx.x];
   }
-  for (int t = lane; t < S * slot_stride; t += FPX_WARP) slots[t] = 0.0;
+  for (int t = lane; t < nslot * slot_stride; t += FPX_WARP) slots[t] = 0.0;
   if (lane < S) {
-    mbar_init(&meta->mbar[lane], FPX_WARP);
+    mbar_init(&meta->mbar[lane], 1);
+    meta->fsh[lane] = 0;
     meta->parity[lane] = 0;
     meta->start[lane] = meta->end[lane] = 0;
     meta->elem[lane] = -1;
   }
   asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  // the zero fill (generic proxy) before the bulk copies (async proxy)
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   __syncthreads();
   const NewtonParams P = newton_of(m);
   const int64_t nu = (int64_t)(packed_off[m.E] & 0xffffffffull);
@@ -1701,6 +1793,7 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
     else {
       a0 = c;
       alen = (int)(nu - c < chunk ? nu - c : chunk);
+      prefetch_chunk<D>(ux, umeta, a0, alen, lane);
       ++s_chunks;
     }
   }
@@ -1719,40 +1812,38 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
         }
         b0 = c;
         blen = (int)(nu - c < chunk ? nu - c : chunk);
+        prefetch_chunk<D>(ux, umeta, b0, blen, lane);
         bclaimed = true;
         ++s_chunks;
       }
-      const int s = nord % S;
+      const int s = nord % nslot;
       const bool busy = __any_sync(FPX_FULL, phase != 0 && myslot == s);
       if (busy || meta->end[s] > q) break;  // slot still has lanes or unassigned units
       const int64_t g = ld < alen ? a0 + ld : b0 + (ld - alen);
-      const int e = best[sorted[g]];
-      const int64_t gend = (int64_t)(packed_off[e] & 0xffffffffull) + ecount[e];
+      const int4 um = umeta[g];
+      const int e = um.y;
+      const int64_t gend = um.z;
       const int64_t cend = ld < alen ? a0 + alen : b0 + blen;
       const int lend = ld + (int)((gend < cend ? gend : cend) - g);
       __syncwarp();
-      double* sl = slots + s * slot_stride;
-      const double* gx = m.nodes + (int64_t)e * D * K;
-      for (int t = lane; t < D * K; t += FPX_WARP) {
-        const int c = t / K, qq = t - c * K;
-        const int row = qq / N, i = qq - row * N;
-        cp_async8(sl + c * L::CS + row * L::NP + i, gx + t);
-      }
-      if (field) {
-        const double* gu = field + (int64_t)e * C * K;
-        for (int t = lane; t < C * K; t += FPX_WARP) {
-          const int c = t / K, qq = t - c * K;
-          const int row = qq / N, i = qq - row * N;
-          cp_async8(sl + L::GEO + c * L::CS + row * L::NP + i, gu + t);
-        }
-      }
-      if constexpr (DR == D) {  // the affine frame (x_c, J_c^-1) for the seeds
-        if (lane < D + D * D)
-          cp_async8(sl + frame_off + lane, m.frec + (int64_t)e * FPX_FREC + 3 * D + D * D + lane);
-      }
-      cp_async_arrive_noinc(&meta->mbar[s]);
-      __syncwarp();
       if (lane == 0) {
+        // one elected lane stages the element with TMA bulk copies: the
+        // padded geometry block, the affine frame (seeds), the field block
+        double* sl = slots + s * slot_stride;
+        const unsigned gb = L::GEO * 8, fb = FRAME * 8;
+        uintptr_t ua = 0;
+        unsigned ub = 0;
+        if (fstage) {
+          const uintptr_t u0 = reinterpret_cast<uintptr_t>(field + (int64_t)e * C * K);
+          ua = u0 & ~uintptr_t(15);
+          ub = (unsigned)(((u0 + (uintptr_t)C * K * 8 + 15) & ~uintptr_t(15)) - ua);
+          meta->fsh[s] = (int)((u0 - ua) / 8);
+        }
+        uint64_t* mb = &meta->mbar[s];
+        mbar_expect_tx(mb, gb + fb + ub);
+        bulk_g2s(sl, m.nodes_pad + (int64_t)e * L::GEO, gb, mb);
+        if (FRAME) bulk_g2s(sl + frame_off, m.frec + (int64_t)e * FPX_FREC + 3 * D + D * D, fb, mb);
+        if (ub) bulk_g2s(sl + field_off, reinterpret_cast<const double*>(ua), ub, mb);
         meta->elem[s] = e;
         meta->start[s] = ld;
         meta->end[s] = lend;
@@ -1798,12 +1889,12 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
       if (phase == 0 && rk < take) {
         const int p = q + rk;
         const int64_t g = p < alen ? a0 + p : b0 + (p - alen);
-        pt = sorted[g];
+        pt = umeta[g].x;
 #pragma unroll
         for (int s2 = 0; s2 < S; ++s2)
           if (meta->start[s2] <= p && p < meta->end[s2]) myslot = s2;
 #pragma unroll
-        for (int c = 0; c < D; ++c) xs[c] = x[(int64_t)pt * D + c];
+        for (int c = 0; c < D; ++c) xs[c] = ux[g * D + c];
         if constexpr (DR == D) {
           // seed (decision D7'): the affine prediction of the element's
           // centre frame; an INTERIOR result is final (the unique zero of the
@@ -1979,8 +2070,10 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
         if (field) {
           double v[DR][N];
           basis_values<DR, N>(z, scale, rc, v);
+          const double* fu = fstage ? sX + field_off + meta->fsh[myslot]
+                                    : field + (int64_t)e * C * K;
           for (int c = 0; c < C; ++c)
-            values[(int64_t)pt * C + c] = contract_smem<DR, N>(sX + L::GEO + c * L::CS, v);
+            values[(int64_t)pt * C + c] = contract_flat<DR, N>(fu + c * K, v);
           ++s_evals;
         }
       } else {
@@ -2112,24 +2205,47 @@ inline size_t newton_smem(int geo, int fsz, int N, int wpb) {
 template <int D, int DR, int N>
 struct Stream {
   static constexpr int S = 3;
-  static cudaError_t run(const fpx_mesh_t& m, const double* x, const int32_t* sorted,
-                         const uint64_t* packed_off, const int32_t* ecount, const int32_t* best,
-                         const int32_t* npass, int32_t* code, int32_t* elem, double* r,
+  static cudaError_t run(const fpx_mesh_t& m, const double* ux, const int4* umeta,
+                         const uint64_t* packed_off, const int32_t* npass, int32_t* code,
+                         int32_t* elem, double* r,
                          double* dist, int32_t* iters, const double* field, int C, double* values,
                          int32_t* upts, int64_t* nun_dev, int64_t* chunk_ctr, int64_t n_cap,
                          int4* redo, int64_t* nredo, int64_t redo_cap, int64_t* stats,
                          cudaStream_t st) {
     using L = Lay<D, DR, N>;
-    int ss = L::GEO + (field ? C * L::CS : 0) + (DR == D ? D + D * D : 0);
-    ss = (ss + 13) / 16 * 16 + 2;  // slot stride = 16 bytes mod 128: distinct bank groups
-    const size_t per_warp =
-        (size_t)(S * ss + Scratch<DR, N>::SLOTS * FPX_WARP) * 8 + sizeof(StreamMeta<S>);
-    int wpb = 4;
-    while (wpb > 1 && (size_t)wpb * per_warp + 256 > 220 * 1024) --wpb;
-    if ((size_t)wpb * per_warp + 256 > 227 * 1024) return cudaErrorInvalidValue;
-    const int threads = wpb * FPX_WARP;
-    const size_t smem = (size_t)(2 * ((N + 1) & ~1)) * 8 + (size_t)wpb * per_warp;
+    constexpr int FRAME = DR == D ? D + D * D : 0;
     auto fn = k_newton_stream<D, DR, N, S>;
+    // Slot configuration: the deepest ring (3 slots, field staged) that
+    // still fits 8 resident warps per SM; at high order (p = 7: 16.5 KB per
+    // slot) fewer slots and the field read from global memory at the final
+    // evaluation instead, for more resident warps.
+    int best_warps = -1, nslot = S, fstage = 0, ss = 0, wpb = 4;
+    size_t smem = 0;
+    for (int cfg = 0; cfg < 4; ++cfg) {
+      const int ns = cfg < 2 ? 3 : 2;
+      const int fs = (cfg % 2 == 0 && field) ? 1 : 0;
+      if (cfg % 2 == 0 && !field) continue;
+      int sst = L::GEO + ((FRAME + 1) & ~1) + (fs ? C * L::K + 2 : 0);
+      sst = (sst + 13) / 16 * 16 + 2;  // slot stride = 16 bytes mod 128: distinct bank groups
+      const size_t per_warp =
+          (size_t)(ns * sst + Scratch<DR, N>::SLOTS * FPX_WARP) * 8 + sizeof(StreamMeta<S>);
+      for (int w = 4; w >= 1; --w) {  // warps per CTA
+        const size_t sm = (size_t)(2 * ((N + 1) & ~1)) * 8 + (size_t)w * per_warp;
+        if (sm > 227 * 1024) continue;
+        int warps_sm = (int)((228 * 1024) / (sm + 1024)) * w;
+        if (warps_sm > 8) warps_sm = 8;  // 242 registers: at most 8 warps per SM
+        if (warps_sm > best_warps) {
+          best_warps = warps_sm;
+          nslot = ns;
+          fstage = fs;
+          ss = sst;
+          wpb = w;
+          smem = sm;
+        }
+      }
+    }
+    if (best_warps < 0) return cudaErrorInvalidValue;
+    const int threads = wpb * FPX_WARP;
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     // chunk: FPX_CHUNK_DEFAULT points, shrunk when the stream is too short to
@@ -2145,9 +2261,9 @@ struct Stream {
     }
     unsigned blocks = persistent_blocks((const void*)fn, threads, smem,
                                         (n_cap + chunk - 1) / chunk);
-    fn<<<blocks, threads, smem, st>>>(m, x, sorted, packed_off, ecount, best, npass, code, elem, r,
-                                      dist, iters, field, C, values, upts, nun_dev, chunk_ctr, ss,
-                                      chunk, redo, nredo, redo_cap, stats);
+    fn<<<blocks, threads, smem, st>>>(m, ux, umeta, packed_off, npass, code, elem, r, dist,
+                                      iters, field, C, values, upts, nun_dev, chunk_ctr, ss,
+                                      nslot, fstage, chunk, redo, nredo, redo_cap, stats);
     return cudaGetLastError();
   }
 };
