@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define FPX_ABI_VERSION 5
+#define FPX_ABI_VERSION 6
 
 /* error codes */
 #define FPX_OK 0
@@ -130,17 +130,28 @@ int fpx_profile_round1(void* ev_start, void* ev_stop);
  * points (fpx_rest_patch_host) still change.  NULL clears it. */
 int fpx_set_round1_event(void* ev);
 
-/* After fpx_find (same stream, same workspace, same n): writes the records of
- * the points the rest phase settled straight into host record arrays
- * (pinned, mapped; zero-copy over PCIe), in point order.  Enqueue it after
- * any bulk download into the same arrays.  It WRITES the find's per-point
- * lock array in `ws` (reused as per-point flags; the records stay valid).
- * FPX_EINVAL if `ws` was not last used by an fpx_find of n points on `m`. */
-int fpx_rest_patch_host(int dr, int C, int64_t n, void* ws, size_t ws_bytes,
-                        const fpx_mesh_t* m, const int32_t* code, const int32_t* elem,
-                        const double* r, const double* dist, const double* values,
-                        int32_t* hcode, int32_t* helem, double* hr, double* hdist,
-                        double* hvalues, void* stream);
+/* (ABI 6) The next fpx_find calls on this thread take their n points in k
+ * contiguous chunks [n*c/k, n*(c+1)/k): chunk c may be read once events[c]
+ * (cudaEvent_t) has completed.  The find waits on each event on its stream
+ * just before sorting and filtering that chunk, so the host-to-device copy
+ * of chunk c+1 overlaps the prefilter of chunk c.  k <= 1 or NULL clears. */
+int fpx_set_upload_events(int k, void* const* events);
+
+/* After a host-mode fpx_find (fpx_set_round1_event set; same stream, same
+ * workspace, same n): writes the records of the points in [k0, k1) that the
+ * rest phase settled straight into host record arrays (pinned, mapped;
+ * zero-copy over PCIe), in point order.  Enqueue it after any bulk download
+ * of the same range into the same arrays; ranges may be patched as their
+ * downloads land (ABI 6).  It clears the per-point flags the find left in
+ * the lock array of `ws`.  FPX_EINVAL if `ws` was not last used by an
+ * fpx_find of n points on `m`, or for a bad range.
+ * Replaces: the record copy-back of engine.find_and_interpolate_host
+ * (SPEC.md:423-426 find_and_interpolate, host arrays). */
+int fpx_rest_patch_host(int dr, int C, int64_t n, int64_t k0, int64_t k1, void* ws,
+                        size_t ws_bytes, const fpx_mesh_t* m, const int32_t* code,
+                        const int32_t* elem, const double* r, const double* dist,
+                        const double* values, int32_t* hcode, int32_t* helem, double* hr,
+                        double* hdist, double* hvalues, void* stream);
 
 /* FP64 FMA throughput probe (TFLOP/s): a DFMA-chain kernel over all SMs,
  * timed with CUDA events on `stream` (synchronising).  Roofline denominator. */
@@ -237,15 +248,6 @@ int fpx_forward_map(const fpx_mesh_t* m, int64_t n, const int32_t* elem, const d
 int fpx_particles_advance(int d, int64_t n, double* x, double* v, const double* u,
                           double* v_prev, double* a_prev, double tau, double dt, int first,
                           const double* box, int periodic, void* stream);
-
-/* Multi-rank routing helpers (engine Phase B):
- * global-grid cell owner of each point and the destination counts for an
- * all-to-allv: dest[n] in [-1, nranks), counts [nranks] (device int64). */
-int fpx_route_count(int64_t n, const int32_t* dest, int nranks, int64_t* counts, void* stream);
-/* Stable pack by destination: perm[n] = position of point i in the send buffer
- * (-1 for dest < 0); offsets [nranks] = exclusive scan of counts. */
-int fpx_route_pack(int64_t n, const int32_t* dest, int nranks, const int64_t* offsets,
-                   int64_t* perm, void* ws, size_t ws_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -14,7 +14,7 @@ import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FPX_LIB") or os.path.join(HERE, "lib", "libfpx_sm100.so")
-ABI_VERSION = 5
+ABI_VERSION = 6
 
 INTERIOR, BORDER, NOT_FOUND = 0, 1, 2
 STAT_NAMES = ["points", "box_tests", "newton", "iters", "rest_points", "r1_warp_evals",
@@ -73,8 +73,9 @@ def lib():
         "fpx_filter_records": ([i32, i64, P, P, P, P, P, P, P], i32),
         "fpx_pad_nodes": ([i32, i32, i32, i64, P, P, P], i32),
         "fpx_set_round1_event": ([P], i32),
-        "fpx_rest_patch_host": ([i32, i32, i64, P, C.c_size_t, C.POINTER(MeshT), P, P, P, P, P,
-                                 P, P, P, P, P, P], i32),
+        "fpx_rest_patch_host": ([i32, i32, i64, i64, i64, P, C.c_size_t, C.POINTER(MeshT), P, P,
+                                 P, P, P, P, P, P, P, P, P], i32),
+        "fpx_set_upload_events": ([i32, P], i32),
         "fpx_particles_advance": ([i32, i64, P, P, P, P, P, f64, f64, i32, P, i32, P], i32),
         "fpx_bound_function": ([i32, i32, i32, i64, P, P, P, P, P], i32),
         "fpx_hash_workspace_bytes": ([i32, i64, i32], sz),
@@ -86,8 +87,6 @@ def lib():
         "fpx_findpts_eval": ([i32, i32, P, i32, i64, P, i64, P, P, P, P, P, sz, P], i32),
         "fpx_invert_pairs": ([C.POINTER(MeshT), i64, P, P, P, P, P, P, P, P], i32),
         "fpx_forward_map": ([C.POINTER(MeshT), i64, P, P, P, P, P, P], i32),
-        "fpx_route_count": ([i64, P, i32, P, P], i32),
-        "fpx_route_pack": ([i64, P, i32, P, P, P, sz, P], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -103,11 +102,10 @@ def exported_symbols():
     """Names declared in include/fpx.h (checked by the CPU test suite)."""
     return ["fpx_abi_version", "fpx_last_error", "fpx_launch_count", "fpx_profile_round1",
             "fpx_probe_fp64", "fpx_supported", "fpx_setup_bounds", "fpx_filter_records", "fpx_pad_nodes",
-            "fpx_particles_advance", "fpx_set_round1_event", "fpx_rest_patch_host",
+            "fpx_particles_advance", "fpx_set_round1_event", "fpx_rest_patch_host", "fpx_set_upload_events",
             "fpx_bound_function", "fpx_hash_workspace_bytes", "fpx_hash_build", "fpx_cell_of",
             "fpx_find_workspace_bytes", "fpx_find", "fpx_eval_workspace_bytes",
-            "fpx_findpts_eval", "fpx_invert_pairs", "fpx_forward_map", "fpx_route_count",
-            "fpx_route_pack"]
+            "fpx_findpts_eval", "fpx_invert_pairs", "fpx_forward_map"]
 
 
 def check(rc: int, what: str) -> None:

@@ -36,6 +36,10 @@ thread_local std::string g_err;
 std::atomic<int64_t> g_launches{0};
 cudaEvent_t g_prof_start = nullptr, g_prof_stop = nullptr;
 thread_local cudaEvent_t g_round1_done = nullptr;
+// fpx_set_upload_events: the points arrive in k chunks, chunk c ready at ev[c]
+constexpr int kMaxUpload = 16;
+thread_local int g_upload_k = 0;
+thread_local cudaEvent_t g_upload_ev[kMaxUpload];
 
 // Layout of every find workspace at its last fpx_find (points, elements):
 // fpx_rest_patch_host re-carves the workspace and must see the same layout.
@@ -206,33 +210,6 @@ __global__ void k_count_elems(int64_t n, const int32_t* __restrict__ elem, int32
     atomicAdd(&count[elem[k]], 1);
 }
 
-__global__ void k_route_count(int64_t n, const int32_t* __restrict__ dest, int nranks,
-                              int64_t* counts) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    const int d = dest[k];
-    if (d >= 0 && d < nranks) atomicAdd((unsigned long long*)&counts[d], 1ull);
-  }
-}
-
-__global__ void k_route_flags(int64_t n, const int32_t* __restrict__ dest, int rank,
-                              int64_t* flags) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x)
-    flags[k] = dest[k] == rank ? 1 : 0;
-}
-
-__global__ void k_route_place(int64_t n, const int32_t* __restrict__ dest, int rank,
-                              const int64_t* __restrict__ pos, const int64_t* __restrict__ offsets,
-                              int64_t* perm) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x) {
-    const int d = dest[k];
-    if (d == rank) perm[k] = offsets[rank] + pos[k];
-    else if (d < 0 && rank == 0) perm[k] = -1;
-  }
-}
-
 // 8 independent DFMA chains per thread (fpx_probe_fp64).
 __global__ void __launch_bounds__(256) k_dfma_probe(double* out, int iters, double a, double b) {
   double x[8];
@@ -290,7 +267,19 @@ int fpx_set_round1_event(void* ev) {
   return FPX_OK;
 }
 
-int fpx_rest_patch_host(int dr, int C, int64_t n, void* ws, size_t ws_bytes,
+int fpx_set_upload_events(int k, void* const* events) {
+  if (k <= 1 || !events) {
+    g_upload_k = 0;
+    return FPX_OK;
+  }
+  if (k > kMaxUpload) return fail(FPX_EINVAL, "upload events: k=%d > %d", k, kMaxUpload);
+  for (int c = 0; c < k; ++c) g_upload_ev[c] = reinterpret_cast<cudaEvent_t>(events[c]);
+  g_upload_k = k;
+  return FPX_OK;
+}
+
+int fpx_rest_patch_host(int dr, int C, int64_t n, int64_t k0, int64_t k1, void* ws,
+                        size_t ws_bytes,
                         const fpx_mesh_t* m, const int32_t* code, const int32_t* elem,
                         const double* r, const double* dist, const double* values,
                         int32_t* hcode, int32_t* helem, double* hr, double* hdist,
@@ -299,6 +288,7 @@ int fpx_rest_patch_host(int dr, int C, int64_t n, void* ws, size_t ws_bytes,
   if (rc) return rc;
   if (!hcode || !helem || !hr || !hdist || (values && !hvalues))
     return fail(FPX_EINVAL, "rest patch: null host array");
+  if (k0 < 0 || k1 > n || k0 > k1) return fail(FPX_EINVAL, "rest patch: bad range");
   // the host arrays must be device-accessible (pinned, hence mapped)
   const void* hp[5] = {hcode, helem, hr, hdist, values ? (const void*)hvalues : (const void*)hcode};
   for (const void* p : hp) {
@@ -311,19 +301,19 @@ int fpx_rest_patch_host(int dr, int C, int64_t n, void* ws, size_t ws_bytes,
     std::lock_guard<std::mutex> g(g_ws_mu);
     auto it = g_ws_layout.find(ws);
     if (it == g_ws_layout.end() || it->second.first != n || it->second.second != m->E)
-      return fail(FPX_EINVAL, "rest patch: workspace was not last used by an fpx_find of %lld "
-                  "points on this mesh", (long long)n);
+      return fail(FPX_EINVAL, "rest patch: workspace was not last used by a host-mode fpx_find "
+                  "of %lld points on this mesh", (long long)n);
   }
   Carver cv(ws, ws_bytes);
   FindWs w;
   w.carve(cv, m->E, n);
   if (!cv.ok()) return fail(FPX_EINVAL, "rest patch: workspace too small");
-  // point order (the find left its per-point locks at 0: reused as flags):
+  // point order over the flags the host-mode find left in its lock array:
   // the PCIe writes in flight land on neighbouring host pages, 708 -> 505 us
   // per 10^6 points against walking the rest list
-  g_launches += 1;
-  FPX_LAUNCH(fpx::launch_rest_patch_host(dr, C, n, w.nun, w.upts, w.lock, code, elem, r, dist,
-                                         values, hcode, helem, hr, hdist, hvalues, S(stream)));
+  if (k1 > k0)
+    FPX_LAUNCH(fpx::launch_rest_patch_host(dr, C, k0, k1, w.lock, code, elem, r, dist, values,
+                                           hcode, helem, hr, hdist, hvalues, S(stream)));
   return FPX_OK;
 }
 
@@ -507,22 +497,35 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
     g_ws_layout[ws] = {n, E};
   }
   const fpx_mesh_t& M = *m;
-  // --- order the points by hash cell (counting sort)
+  // --- order the points by hash cell (counting sort), then the prefilter:
+  // hash list + AABB/OBB filter + best-first ranking.  With upload events
+  // (host path) the points arrive in k chunks and each chunk is sorted and
+  // filtered as soon as it has landed, under the next chunk's copy.
   const int64_t nc = w.ncells;
-  FPX_CK(cudaMemsetAsync(w.cell_count, 0, sizeof(int32_t) * (nc + 2), st));
-  FPX_LAUNCH(fpx::launch_point_cells(M, n, x, w.cellid, w.cell_count, st));
-  {
-    size_t tb3 = w.scan3_bytes;
-    FPX_CK(cub::DeviceScan::ExclusiveSum(w.scan3_temp, tb3, w.cell_count, w.cell_off,
-                                         (int)(nc + 2), st));
-  }
-  FPX_CK(cudaMemsetAsync(w.cell_cursor, 0, sizeof(int32_t) * (nc + 2), st));
-  FPX_LAUNCH(fpx::launch_point_scatter(n, w.cellid, w.cell_off, w.cell_cursor, w.order, st));
-  // --- prefilter: hash list + AABB/OBB filter + best-first ranking
   FPX_CK(cudaMemsetAsync(w.g1.count, 0, sizeof(int32_t) * E, st));
-  FPX_LAUNCH(fpx::launch_prefilter(M, n, nc + 1, x, w.order, w.cellid, w.cell_off,
-                                   w.best, w.npass, code, elem, r, dist, iters,
-                                   field ? values : nullptr, C, w.g1.count, stats, st));
+  const int nchunk = g_upload_k > 1 ? g_upload_k : 1;
+  for (int ck = 0; ck < nchunk; ++ck) {
+    const int64_t a = n * ck / nchunk, nn = n * (ck + 1) / nchunk - a;
+    if (nchunk > 1) FPX_CK(cudaStreamWaitEvent(st, g_upload_ev[ck], 0));
+    if (nn == 0) continue;
+    const double* xa = x + a * M.d;
+    FPX_CK(cudaMemsetAsync(w.cell_count, 0, sizeof(int32_t) * (nc + 2), st));
+    FPX_LAUNCH(fpx::launch_point_cells(M, nn, xa, w.cellid + a, w.cell_count, st));
+    {
+      size_t tb3 = w.scan3_bytes;
+      FPX_CK(cub::DeviceScan::ExclusiveSum(w.scan3_temp, tb3, w.cell_count, w.cell_off,
+                                           (int)(nc + 2), st));
+    }
+    FPX_CK(cudaMemsetAsync(w.cell_cursor, 0, sizeof(int32_t) * (nc + 2), st));
+    // cell-ordered point copies for the prefilter: in buffers that are free
+    // until later phases (ux: round-1 stream records; perm: rest order)
+    FPX_LAUNCH(fpx::launch_point_scatter(nn, a, M.d, xa, w.cellid + a, w.cell_off,
+                                         w.cell_cursor, w.order + a, w.ux + a * M.d,
+                                         w.perm + a, st));
+    FPX_LAUNCH(fpx::launch_prefilter(M, nn, w.ux + a * M.d, w.order + a, w.perm + a, w.best,
+                                     w.npass, code, elem, r, dist, iters,
+                                     field ? values : nullptr, C, w.g1.count, stats, st));
+  }
   FPX_CK(cudaMemsetAsync(w.nun, 0, sizeof(int64_t), st));
   FPX_CK(cudaMemsetAsync(w.counter, 0, 2 * sizeof(int64_t), st));
   FPX_CK(cudaMemsetAsync(w.nredo, 0, sizeof(int64_t), st));
@@ -556,6 +559,9 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
                                    iters,
                                    field, C, values, w.counter, stats, st));
   g_launches += field ? 2 : 1;  // k_rest_l1 pass 1 + redo pass (+ k_rest_values)
+  if (g_round1_done) {  // host mode: flag the rest points for fpx_rest_patch_host
+    FPX_LAUNCH(fpx::launch_rest_flag(n, w.nun, w.upts, w.lock, st));
+  }
   g_launches += 1;
   k_find_totals<<<1, 1, 0, st>>>(w.nun, w.nredo, stats, n);
   FPX_CK(cudaGetLastError());
@@ -639,41 +645,6 @@ int fpx_particles_advance(int d, int64_t n, double* x, double* v, const double* 
   const double unit[6] = {0, 0, 0, 1, 1, 1};
   FPX_LAUNCH(fpx::launch_particles_advance(d, n, x, v, u, v_prev, a_prev, tau, dt, first,
                                            box ? box : unit, periodic, S(stream)));
-  return FPX_OK;
-}
-
-int fpx_route_count(int64_t n, const int32_t* dest, int nranks, int64_t* counts, void* stream) {
-  if (nranks < 1) return fail(FPX_EINVAL, "route: nranks < 1");
-  cudaStream_t st = S(stream);
-  FPX_CK(cudaMemsetAsync(counts, 0, sizeof(int64_t) * nranks, st));
-  if (n <= 0) return FPX_OK;
-  g_launches += 1;
-  k_route_count<<<grid1(n), 256, 0, st>>>(n, dest, nranks, counts);
-  FPX_CK(cudaGetLastError());
-  return FPX_OK;
-}
-
-int fpx_route_pack(int64_t n, const int32_t* dest, int nranks, const int64_t* offsets,
-                   int64_t* perm, void* ws, size_t ws_bytes, void* stream) {
-  if (nranks < 1) return fail(FPX_EINVAL, "route: nranks < 1");
-  if (n <= 0) return FPX_OK;
-  cudaStream_t st = S(stream);
-  Carver cv(ws, ws_bytes);
-  int64_t* flags = cv.take<int64_t>(n);
-  int64_t* pos = cv.take<int64_t>(n);
-  size_t tb = scan_temp_i64(n);
-  void* temp = cv.take<char>(tb);
-  if (!ws) return fail(FPX_EINVAL, "route: workspace required (%zu bytes)", cv.off + 256);
-  if (!cv.ok()) return fail(FPX_EINVAL, "route workspace too small (%zu < %zu)", ws_bytes, cv.off);
-  for (int rk = 0; rk < nranks; ++rk) {
-    g_launches += 2;
-    k_route_flags<<<grid1(n), 256, 0, st>>>(n, dest, rk, flags);
-    FPX_CK(cudaGetLastError());
-    size_t t2 = tb;
-    FPX_CK(cub::DeviceScan::ExclusiveSum(temp, t2, flags, pos, (int)n, st));
-    k_route_place<<<grid1(n), 256, 0, st>>>(n, dest, rk, pos, offsets, perm);
-    FPX_CK(cudaGetLastError());
-  }
   return FPX_OK;
 }
 

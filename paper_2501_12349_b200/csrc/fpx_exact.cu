@@ -702,14 +702,20 @@ __global__ void k_point_cells(fpx_mesh_t m, int64_t n, const double* __restrict_
   }
 }
 
-__global__ void k_point_scatter(int64_t n, const int32_t* __restrict__ cellid,
+// Counting-sort scatter of the points by hash cell; also writes the
+// cell-ordered copies the prefilter reads (coordinates, cell id), so its
+// per-point start is one load instead of order -> cellid -> x.
+__global__ void k_point_scatter(int64_t n, int64_t base, int d, const double* __restrict__ x,
+                                const int32_t* __restrict__ cellid,
                                 const int32_t* __restrict__ cell_off, int32_t* cursor,
-                                int32_t* order) {
+                                int32_t* order, double* xo, int32_t* co) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * blockDim.x) {
     const int c = cellid[k];
-    const int slot = atomicAdd(&cursor[c], 1);
-    order[cell_off[c] + slot] = (int32_t)k;
+    const int64_t pos = cell_off[c] + atomicAdd(&cursor[c], 1);
+    order[pos] = (int32_t)(base + k);
+    co[pos] = c;
+    for (int a = 0; a < d; ++a) xo[pos * d + a] = x[k * d + a];
   }
 }
 
@@ -747,58 +753,104 @@ __device__ __forceinline__ void frec_range(const double* __restrict__ frec, int6
 }
 
 //
-// Thread per point, points in hash-cell order: the lanes of a warp share one
-// or two cells' lists, so the element records they read are the same
-// (broadcast) and the loop trip counts agree.  The record is loaded in
-// stages: the AABB (48 B), the OBB and its flag only if the AABB passes, the
-// affine frame only if the OBB passes.  (A lane-per-(point, entry) variant
-// with a segmented warp reduction measured 447 us against 332 us: its
-// lanes gather 32 different records per load instead of broadcasting.)
+// kPfLanes lanes per point, points in hash-cell order: lane j of a point
+// tests list entries j, j + kPfLanes, ...; the (count, best) of the lanes are
+// combined with two shuffles.  Consecutive points share one or two cells'
+// lists, so the records a warp reads at one time are few (L1 broadcast),
+// and each lane's chain of dependent record loads is a quarter of the
+// list: the kernel is bound by that chain's latency (thread per point:
+// 343 us, long_scoreboard 25 per issue).  The record is loaded in stages:
+// the AABB (48 B), the OBB and its flag only if the AABB passes, the affine
+// frame only if the OBB passes.  (A lane-per-(point, entry) variant with a
+// segmented warp reduction measured 447 us: its lanes gather 32 different
+// records per load instead of broadcasting.)
+#ifndef FPX_PF_LANES
+#define FPX_PF_LANES 2
+#endif
+#ifndef FPX_PF_TRIP
+#define FPX_PF_TRIP 2
+#endif
+constexpr int kPfLanes = FPX_PF_LANES;
+constexpr int kPfTrip = FPX_PF_TRIP;  // list entries per loop trip (AABB loads in flight)
+
 template <int D>
 __global__ void __launch_bounds__(256)
-    k_prefilter_points(fpx_mesh_t m, int64_t n, const double* __restrict__ x,
-                       const int32_t* __restrict__ order, const int32_t* __restrict__ cellid,
+    k_prefilter_points(fpx_mesh_t m, int64_t n, const double* __restrict__ xo,
+                       const int32_t* __restrict__ order, const int32_t* __restrict__ co,
                        int32_t* best, int32_t* npass, int32_t* code, int32_t* elem, double* r,
                        double* dist, int32_t* iters, double* values, int C, int32_t* elem_count,
                        int64_t* stats) {
   int64_t nc = 1;
   for (int c = 0; c < D; ++c) nc *= m.ncell;
   int64_t boxtests = 0;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t k = order[t];
-    const int64_t cell = cellid[k];
+  const int sub = threadIdx.x % kPfLanes;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x / kPfLanes;
+  // whole warps iterate together (the shuffles below need every lane)
+  const int64_t nround = (n + stride - 1) / stride;
+  int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kPfLanes;
+  for (int64_t it = 0; it < nround; ++it, t += stride) {
+    const bool valid = t < n;
+    const int64_t k = valid ? order[t] : 0;
+    const int64_t cell = valid ? co[t] : nc;
     double xx[D];
 #pragma unroll
-    for (int c = 0; c < D; ++c) xx[c] = x[k * D + c];
-    int cnt = 0, bst = -1;
+    for (int c = 0; c < D; ++c) xx[c] = valid ? xo[t * D + c] : 0.0;
+    int cnt = 0, bst = INT_MAX;
     double bval = INFINITY;
     if (cell < nc) {
       const int s = m.offsets[cell], e1 = m.offsets[cell + 1];
-      boxtests += e1 - s;
-      int en = s < e1 ? m.elems[s] : 0;  // list entry prefetched one ahead
-      for (int q = s; q < e1; ++q) {
-        const int e = en;
-        if (q + 1 < e1) en = m.elems[q + 1];
-        double R[FPX_FREC];
-        frec_range<D, 0, 2 * D>(m.frec, e, R);
-        if (!aabb_in(D, R, xx)) continue;
-        frec_range<D, 2 * D, 3 * D + D * D>(m.frec, e, R);
-        frec_range<D, FPX_FREC - 1, FPX_FREC>(m.frec, e, R);
-        if (!(R[FPX_FREC - 1] == 0.0 || obb_in(D, R + 2 * D, R + 3 * D, xx))) continue;
-        frec_range<D, 3 * D + D * D, 4 * D + 2 * D * D>(m.frec, e, R);
-        ++cnt;
-        const double v = bestfirst_value(D, R + 3 * D + D * D, xx);
-        if (v < bval) {  // strict: ties keep the lower (earlier) id
-          bval = v;
-          bst = e;
+      if (sub == 0) boxtests += e1 - s;
+      // kPfTrip entries per trip (q, q + kPfLanes, ...): their AABB loads in flight
+      for (int q = s + sub; q < e1; q += kPfTrip * kPfLanes) {
+        int ee[kPfTrip];
+        bool in[kPfTrip];
+        double R[kPfTrip][FPX_FREC];
+#pragma unroll
+        for (int h = 0; h < kPfTrip; ++h) {
+          const bool ok = q + h * kPfLanes < e1;
+          ee[h] = ok ? m.elems[q + h * kPfLanes] : -1;
+        }
+#pragma unroll
+        for (int h = 0; h < kPfTrip; ++h)
+          frec_range<D, 0, 2 * D>(m.frec, ee[h] < 0 ? ee[0] : ee[h], R[h]);
+#pragma unroll
+        for (int h = 0; h < kPfTrip; ++h) in[h] = ee[h] >= 0 && aabb_in(D, R[h], xx);
+#pragma unroll
+        for (int h = 0; h < kPfTrip; ++h) {  // list order
+          if (!in[h]) continue;
+          frec_range<D, 2 * D, 3 * D + D * D>(m.frec, ee[h], R[h]);
+          frec_range<D, FPX_FREC - 1, FPX_FREC>(m.frec, ee[h], R[h]);
+          if (!(R[h][FPX_FREC - 1] == 0.0 || obb_in(D, R[h] + 2 * D, R[h] + 3 * D, xx))) continue;
+          frec_range<D, 3 * D + D * D, 4 * D + 2 * D * D>(m.frec, ee[h], R[h]);
+          ++cnt;
+          const double v = bestfirst_value(D, R[h] + 3 * D + D * D, xx);
+          if (v < bval) {  // strict: ties keep the lower (earlier) id
+            bval = v;
+            bst = ee[h];
+          }
         }
       }
     }
-    best[k] = bst;
-    npass[k] = cnt;
-    if (bst < 0) write_not_found(k, m.dr, code, elem, r, dist, iters, values, C);
-    else atomicAdd(&elem_count[bst], 1);
+    // (v, e)-lexicographic minimum over the point's lanes == the first
+    // minimum in list order (lists ascend in element id)
+#pragma unroll
+    for (int o = 1; o < kPfLanes; o <<= 1) {
+      const int co = __shfl_xor_sync(FPX_FULL, cnt, o);
+      const double vo = __shfl_xor_sync(FPX_FULL, bval, o);
+      const int eo = __shfl_xor_sync(FPX_FULL, bst, o);
+      cnt += co;
+      if (bf_less(vo, eo, bval, bst)) {
+        bval = vo;
+        bst = eo;
+      }
+    }
+    if (valid && sub == 0) {
+      if (cnt == 0) bst = -1;
+      best[k] = bst;
+      npass[k] = cnt;
+      if (bst < 0) write_not_found(k, m.dr, code, elem, r, dist, iters, values, C);
+      else atomicAdd(&elem_count[bst], 1);
+    }
   }
   for (int o = 16; o > 0; o >>= 1) boxtests += __shfl_xor_sync(FPX_FULL, boxtests, o);
   if ((threadIdx.x & 31) == 0 && boxtests)
@@ -934,17 +986,14 @@ cudaError_t launch_cell_of(int d, const double* grid, int n, int64_t npts, const
   k_cell_of<<<grid_for(npts, 256), 256, 0, st>>>(d, grid, n, npts, x, cell);
   return cudaGetLastError();
 }
-cudaError_t launch_prefilter(const fpx_mesh_t& m, int64_t n, int64_t ncells_tot,
-                             const double* x, const int32_t* order, const int32_t* cellid,
-                             const int32_t* cell_off, int32_t* best, int32_t* npass,
-                             int32_t* code, int32_t* elem, double* r, double* dist,
-                             int32_t* iters, double* values, int C, int32_t* elem_count,
-                             int64_t* stats, cudaStream_t st) {
-  (void)ncells_tot;
-  (void)cell_off;
+cudaError_t launch_prefilter(const fpx_mesh_t& m, int64_t n, const double* xo,
+                             const int32_t* order, const int32_t* co, int32_t* best,
+                             int32_t* npass, int32_t* code, int32_t* elem, double* r,
+                             double* dist, int32_t* iters, double* values, int C,
+                             int32_t* elem_count, int64_t* stats, cudaStream_t st) {
   auto fn = m.d == 3 ? k_prefilter_points<3> : k_prefilter_points<2>;
-  fn<<<grid_for(n, 256), 256, 0, st>>>(m, n, x, order, cellid, best, npass, code, elem, r, dist,
-                                       iters, values, C, elem_count, stats);
+  fn<<<grid_for(n * kPfLanes, 256), 256, 0, st>>>(m, n, xo, order, co, best, npass, code, elem,
+                                                   r, dist, iters, values, C, elem_count, stats);
   return cudaGetLastError();
 }
 cudaError_t launch_point_cells(const fpx_mesh_t& m, int64_t n, const double* x, int32_t* cellid,
@@ -952,9 +1001,11 @@ cudaError_t launch_point_cells(const fpx_mesh_t& m, int64_t n, const double* x, 
   k_point_cells<<<grid_for(n, 256), 256, 0, st>>>(m, n, x, cellid, cell_count);
   return cudaGetLastError();
 }
-cudaError_t launch_point_scatter(int64_t n, const int32_t* cellid, const int32_t* cell_off,
-                                 int32_t* cursor, int32_t* order, cudaStream_t st) {
-  k_point_scatter<<<grid_for(n, 256), 256, 0, st>>>(n, cellid, cell_off, cursor, order);
+cudaError_t launch_point_scatter(int64_t n, int64_t base, int d, const double* x,
+                                 const int32_t* cellid, const int32_t* cell_off, int32_t* cursor,
+                                 int32_t* order, double* xo, int32_t* co, cudaStream_t st) {
+  k_point_scatter<<<grid_for(n, 256), 256, 0, st>>>(n, base, d, x, cellid, cell_off, cursor,
+                                                    order, xo, co);
   return cudaGetLastError();
 }
 }  // namespace fpx

@@ -117,15 +117,13 @@ __global__ void k_rest_flag(const int64_t* __restrict__ nun_dev, const int32_t* 
     flag[upts[u]] = 1;
 }
 
-__global__ void k_rest_patch_host(int dr, int C, int64_t n, int32_t* flag,
-                                          const int32_t* __restrict__ code,
-                                          const int32_t* __restrict__ elem,
-                                          const double* __restrict__ r,
-                                          const double* __restrict__ dist,
-                                          const double* __restrict__ values, int32_t* hcode,
-                                          int32_t* helem, double* hr, double* hdist,
-                                          double* hvalues) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+__global__ void k_rest_patch_host(int dr, int C, int64_t k0, int64_t k1, int32_t* flag,
+                                  const int32_t* __restrict__ code,
+                                  const int32_t* __restrict__ elem, const double* __restrict__ r,
+                                  const double* __restrict__ dist,
+                                  const double* __restrict__ values, int32_t* hcode,
+                                  int32_t* helem, double* hr, double* hdist, double* hvalues) {
+  for (int64_t k = k0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < k1;
        k += (int64_t)gridDim.x * blockDim.x) {
     if (!flag[k]) continue;
     flag[k] = 0;
@@ -137,19 +135,22 @@ __global__ void k_rest_patch_host(int dr, int C, int64_t n, int32_t* flag,
   }
 }
 
-cudaError_t launch_rest_patch_host(int dr, int C, int64_t n, const int64_t* nun_dev,
-                                           const int32_t* upts, int32_t* flag,
-                                           const int32_t* code, const int32_t* elem,
-                                           const double* r, const double* dist,
-                                           const double* values, int32_t* hcode, int32_t* helem,
-                                           double* hr, double* hdist, double* hvalues,
-                                           cudaStream_t st) {
-  int64_t b = (n + 255) / 256;
+cudaError_t launch_rest_flag(int64_t n, const int64_t* nun_dev, const int32_t* upts,
+                             int32_t* flag, cudaStream_t st) {
+  k_rest_flag<<<grid_of(n, 256), 256, 0, st>>>(nun_dev, upts, flag);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rest_patch_host(int dr, int C, int64_t k0, int64_t k1, int32_t* flag,
+                                   const int32_t* code, const int32_t* elem, const double* r,
+                                   const double* dist, const double* values, int32_t* hcode,
+                                   int32_t* helem, double* hr, double* hdist, double* hvalues,
+                                   cudaStream_t st) {
+  int64_t b = (k1 - k0 + 255) / 256;
   if (b > 148 * 8) b = 148 * 8;
   if (b < 1) b = 1;
-  k_rest_flag<<<(unsigned)b, 256, 0, st>>>(nun_dev, upts, flag);
-  k_rest_patch_host<<<(unsigned)b, 256, 0, st>>>(dr, C, n, flag, code, elem, r, dist,
-                                                         values, hcode, helem, hr, hdist, hvalues);
+  k_rest_patch_host<<<(unsigned)b, 256, 0, st>>>(dr, C, k0, k1, flag, code, elem, r, dist,
+                                                 values, hcode, helem, hr, hdist, hvalues);
   return cudaGetLastError();
 }
 

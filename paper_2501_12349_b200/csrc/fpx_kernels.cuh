@@ -45,27 +45,27 @@ cudaError_t launch_hash_sort(int64_t ncells, const int32_t* offsets, int32_t* el
 cudaError_t launch_cell_of(int d, const double* grid, int n, int64_t npts, const double* x,
                            int64_t* cell, cudaStream_t st);
 // thread per point in hash-cell order (k_prefilter_points)
-cudaError_t launch_prefilter(const fpx_mesh_t& m, int64_t n, int64_t ncells_tot,
-                             const double* x, const int32_t* order, const int32_t* cellid,
-                             const int32_t* cell_off, int32_t* best, int32_t* npass,
-                             int32_t* code, int32_t* elem, double* r, double* dist,
-                             int32_t* iters, double* values, int C, int32_t* elem_count,
-                             int64_t* stats, cudaStream_t st);
+cudaError_t launch_prefilter(const fpx_mesh_t& m, int64_t n, const double* xo,
+                             const int32_t* order, const int32_t* co, int32_t* best,
+                             int32_t* npass, int32_t* code, int32_t* elem, double* r,
+                             double* dist, int32_t* iters, double* values, int C,
+                             int32_t* elem_count, int64_t* stats, cudaStream_t st);
 cudaError_t launch_point_cells(const fpx_mesh_t& m, int64_t n, const double* x, int32_t* cellid,
                                int32_t* cell_count, cudaStream_t st);
-cudaError_t launch_point_scatter(int64_t n, const int32_t* cellid, const int32_t* cell_off,
-                                 int32_t* cursor, int32_t* order, cudaStream_t st);
+cudaError_t launch_point_scatter(int64_t n, int64_t base, int d, const double* x,
+                                 const int32_t* cellid, const int32_t* cell_off, int32_t* cursor,
+                                 int32_t* order, double* xo, int32_t* co, cudaStream_t st);
 // Element grouping (fpx_group.cu): count -> packed scan -> items + scatter.
 cudaError_t launch_make_items(int64_t E, const int32_t* count, const uint64_t* packed_off,
                               Item* items, int64_t* nitems_dev, cudaStream_t st);
 // Zero-copy patch of the rest points' records into mapped host arrays.
-cudaError_t launch_rest_patch_host(int dr, int C, int64_t n, const int64_t* nun_dev,
-                                           const int32_t* upts, int32_t* flag,
-                                           const int32_t* code, const int32_t* elem,
-                                           const double* r, const double* dist,
-                                           const double* values, int32_t* hcode, int32_t* helem,
-                                           double* hr, double* hdist, double* hvalues,
-                                           cudaStream_t st);
+cudaError_t launch_rest_flag(int64_t n, const int64_t* nun_dev, const int32_t* upts,
+                             int32_t* flag, cudaStream_t st);
+cudaError_t launch_rest_patch_host(int dr, int C, int64_t k0, int64_t k1, int32_t* flag,
+                                   const int32_t* code, const int32_t* elem, const double* r,
+                                   const double* dist, const double* values, int32_t* hcode,
+                                   int32_t* helem, double* hr, double* hdist, double* hvalues,
+                                   cudaStream_t st);
 cudaError_t launch_pack_counts(int64_t E, const int32_t* count, uint64_t* packed,
                                cudaStream_t st);
 cudaError_t launch_scatter_units(int64_t nunits_cap, const int64_t* nunits_dev,

@@ -1702,17 +1702,23 @@ __global__ void k_rest_values(const double* __restrict__ fbasis, int M,
 
 // L1 prefetch of a claimed chunk's stream records (ux, umeta): the lanes
 // that take its units later read them from L1 instead of a DRAM round trip.
-__device__ __forceinline__ void prefetch_lines(const void* p, size_t bytes, int lane) {
-  const uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(127);
-  const uintptr_t b = reinterpret_cast<uintptr_t>(p) + bytes;
-  for (uintptr_t q = a + (uintptr_t)lane * 128; q < b; q += 32 * 128)
+// One line per lane, no loop (a chunk is <= FPX_CHUNK_DEFAULT = 64 units:
+// <= 13 lines of ux, <= 9 of umeta): the loader sits in the hot loop, whose
+// instruction footprint matters.
+__device__ __forceinline__ void prefetch_chunk3(const void* p0, size_t b0, const void* p1,
+                                                size_t b1, int lane) {
+  const uintptr_t a0 = reinterpret_cast<uintptr_t>(p0) & ~uintptr_t(127);
+  const uintptr_t a1 = reinterpret_cast<uintptr_t>(p1) & ~uintptr_t(127);
+  const int n0 = (int)((reinterpret_cast<uintptr_t>(p0) + b0 - a0 + 127) / 128);
+  const uintptr_t q = lane < n0 ? a0 + (uintptr_t)lane * 128 : a1 + (uintptr_t)(lane - n0) * 128;
+  if (q < (lane < n0 ? reinterpret_cast<uintptr_t>(p0) + b0 : reinterpret_cast<uintptr_t>(p1) + b1))
     asm volatile("prefetch.L1 [%0];\n" ::"l"(q));
 }
 template <int D>
 __device__ __forceinline__ void prefetch_chunk(const double* ux, const int4* umeta, int64_t c0,
                                                int len, int lane) {
-  prefetch_lines(ux + c0 * D, (size_t)len * D * sizeof(double), lane);
-  prefetch_lines(umeta + c0, (size_t)len * sizeof(int4), lane);
+  prefetch_chunk3(ux + c0 * D, (size_t)len * D * sizeof(double), umeta + c0,
+                  (size_t)len * sizeof(int4), lane);
 }
 
 template <int S>
@@ -1816,7 +1822,7 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
         bclaimed = true;
         ++s_chunks;
       }
-      const int s = nord % nslot;
+      const int s = nslot == 3 ? nord % 3 : nord & 1;
       const bool busy = __any_sync(FPX_FULL, phase != 0 && myslot == s);
       if (busy || meta->end[s] > q) break;  // slot still has lanes or unassigned units
       const int64_t g = ld < alen ? a0 + ld : b0 + (ld - alen);

@@ -18,6 +18,7 @@ from __future__ import annotations
 from dataclasses import dataclass, field as dfield
 
 from collections.abc import Mapping
+import ctypes
 import numpy as np
 import torch
 
@@ -452,41 +453,56 @@ class _SummedStats(Mapping):
         return _C.STATS_LEN
 
 
+_UPLOAD_CHUNKS = 2     # host path: points uploaded in chunks, each filtered as it lands
+_DOWNLOAD_PIECES = 8   # host path: records downloaded in point ranges ...
+_EARLY_PIECES = 4      # ... the first ones under the rest kernels (then patched)
+
+
 def _host_overlapped(S: EngineSetup, f: Field, x: torch.Tensor, out: dict, ws: dict,
                      sync: bool) -> dict:
-    """One find with its download split in two: after round 1 every record
-    except the ~5% the rest phase revisits is final, so the bulk download runs
-    on a side stream under the rest kernels; the revisited records are then
-    written straight into the (pinned, mapped) host arrays by a zero-copy
-    kernel (fpx_rest_patch_host).  No host thread writes those arrays: a
-    host-side scatter leaves their lines in the CPU caches, and the next
-    call's download into them then snoops (measured +2 ms per call)."""
+    """One find with its host copies overlapped (captured once per buffer set
+    as a CUDA graph; a replay is one launch):
+      * the points go up in _UPLOAD_CHUNKS chunks on a copy stream, and the
+        find sorts and prefilters each chunk as soon as it has landed
+        (fpx_set_upload_events), under the next chunk's copy;
+      * after round 1 every record except the ~5% the rest phase revisits
+        is final, so the first _EARLY_PIECES of _DOWNLOAD_PIECES point ranges
+        of the records go down on a second copy stream under the rest
+        kernels (about what the link moves in that time), the other ranges
+        once the find is complete;
+      * the early ranges' revisited records are written straight into the
+        (pinned, mapped) host arrays by a zero-copy kernel
+        (fpx_rest_patch_host) while the late ranges download.
+    No host thread writes the output arrays: a host-side scatter leaves
+    their lines in the CPU caches, and the next call's download into them
+    then snoops (measured +2 ms per call)."""
     comp = torch.cuda.current_stream(S.device)
-    side = _streams(S, 1)[0]
+    up, dn = _streams(S, 2)
     n = int(x.shape[0])
-    if ws.get("r1_event") is None:
-        ws["r1_event"] = torch.cuda.Event()
-        ws["r1_event"].record(comp)  # torch creates the CUDA event on first record
-    ev = ws["r1_event"]
-    ws["x"].copy_(x, non_blocking=True)
-    gkey = (n, f.blocks.data_ptr(), f.components) + tuple(out[k].data_ptr() for k in _REC_KEYS) \
-        + tuple(ws[k].data_ptr() for k in ("x", "values", "code", "elem", "r", "dist"))
+    if ws.get("events") is None:
+        evs = {k: [torch.cuda.Event() for _ in range(m)] for k, m in
+               (("r1", 1), ("start", 1), ("up", _UPLOAD_CHUNKS), ("dn", _DOWNLOAD_PIECES),
+                ("rank", 1))}
+        for lst in evs.values():  # torch creates the CUDA event on first record
+            for e in lst:
+                e.record(comp)
+        ws["events"] = evs
+    gkey = (n, x.data_ptr(), f.blocks.data_ptr(), f.components) + \
+        tuple(out[k].data_ptr() for k in _REC_KEYS) + \
+        tuple(ws[k].data_ptr() for k in ("x", "values", "code", "elem", "r", "dist"))
     if S.options.graphs and ws.get("graph_key") != gkey:
-        # capture the device part once per buffers; a replay costs one launch
-        # instead of ~60.  The side-stream download forks from the round-1
-        # event inside the capture, so it is an edge of the graph.
-        _host_device_part(S, f, out, ws, ev, side)  # warm-up outside capture
+        _host_device_part(S, f, x, out, ws, up, dn)  # warm-up outside capture
         comp.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            st = _host_device_part(S, f, out, ws, ev, side)
+            st = _host_device_part(S, f, x, out, ws, up, dn)
         ws.update(graph=g, graph_key=gkey, graph_stats=st)
     if S.options.graphs:
         ws["graph"].replay()
         # a snapshot per call: the graph rewrites its counter buffer each replay
         st = DeviceStats(ws["graph_stats"]._t.clone())
     else:
-        st = _host_device_part(S, f, out, ws, ev, side)
+        st = _host_device_part(S, f, x, out, ws, up, dn)
     if not sync:
         raise ValueError("the overlapped host path completes on the host (sync=True)")
     comp.synchronize()
@@ -497,12 +513,11 @@ def _host_overlapped(S: EngineSetup, f: Field, x: torch.Tensor, out: dict, ws: d
 _REC_KEYS = ("values", "code", "elem", "r", "dist", "rank")
 
 
-def _host_device_part(S: EngineSetup, f: Field, out: dict, ws: dict, ev, side):
-    """Device work of _host_overlapped (capturable): the find (recording `ev`
-    after round 1), the bulk record download on `side` from that event on,
-    the rank fill and its download, and, once `side` is joined back, the
-    zero-copy patch of the rest points' records."""
+def _host_device_part(S: EngineSetup, f: Field, x: torch.Tensor, out: dict, ws: dict, up, dn):
+    """Device work of _host_overlapped (capturable; see there)."""
     L = _C.lib()
+    comp = torch.cuda.current_stream(S.device)
+    ev = ws["events"]
     n, dr, C = int(ws["x"].shape[0]), S.ref_dim, f.components
     loc = dict(code=ws["code"], elem=ws["elem"], r=ws["r"], dist=ws["dist"], iters=None,
                values=ws["values"])
@@ -512,29 +527,58 @@ def _host_device_part(S: EngineSetup, f: Field, out: dict, ws: dict, ev, side):
     if ws.get("find_ws") is None or ws["find_ws"].numel() < need:
         ws["find_ws"] = torch.empty(need, dtype=torch.uint8, device=S.device)
     wsf = ws["find_ws"]
-    L.fpx_set_round1_event(ev.cuda_event)
+    # chunked upload on `up`
+    K = _UPLOAD_CHUNKS
+    ev["start"][0].record(comp)
+    up.wait_event(ev["start"][0])
+    with torch.cuda.stream(up):
+        for c in range(K):
+            a, b = n * c // K, n * (c + 1) // K
+            ws["x"][a:b].copy_(x[a:b], non_blocking=True)
+            ev["up"][c].record(up)
+    handles = (ctypes.c_void_p * K)(*[e.cuda_event for e in ev["up"]])
+    L.fpx_set_upload_events(K, ctypes.cast(handles, ctypes.c_void_p))
+    L.fpx_set_round1_event(ev["r1"][0].cuda_event)
     try:
         st = _find_into(S, ws["x"], loc, f, ws=wsf)
     finally:
         L.fpx_set_round1_event(None)
-    # after round 1 every record but the rest points' is final: download them
-    # on the side stream (copies only: a kernel there would wait for an SM
-    # behind the persistent rest kernels) while the rest kernels run
-    side.wait_event(ev)
-    with torch.cuda.stream(side):
-        for k in ("values", "code", "elem", "r", "dist"):
-            out[k].copy_(ws[k], non_blocking=True)
+        L.fpx_set_upload_events(0, None)
+    # after round 1 every record but the rest points' is final: download the
+    # early ranges on `dn` (copies only: a kernel there would wait for an SM
+    # behind the persistent rest kernels) while the rest runs, the late ones
+    # (and the rank column) once the find is complete
+    Pn, Pe = _DOWNLOAD_PIECES, _EARLY_PIECES
+    rng = [(n * j // Pn, n * (j + 1) // Pn) for j in range(Pn)]
+    dn.wait_event(ev["r1"][0])
+    with torch.cuda.stream(dn):
+        for j in range(Pe):
+            a, b = rng[j]
+            for k in ("values", "code", "elem", "r", "dist"):
+                out[k][a:b].copy_(ws[k][a:b], non_blocking=True)
+            ev["dn"][j].record(dn)
     torch.where(loc["code"] != NOT_FOUND, torch.zeros_like(loc["elem"]),
                 torch.full_like(loc["elem"], -1), out=ws["rank"])
-    out["rank"].copy_(ws["rank"], non_blocking=True)
-    torch.cuda.current_stream(S.device).wait_stream(side)
-    _C.check(L.fpx_rest_patch_host(dr, C, n, _C.ptr(wsf), wsf.numel(), S.mesh_t,
-                                   _C.ptr(ws["code"]), _C.ptr(ws["elem"]), _C.ptr(ws["r"]),
-                                   _C.ptr(ws["dist"]), _C.ptr(ws["values"]),
-                                   out["code"].data_ptr(), out["elem"].data_ptr(),
-                                   out["r"].data_ptr(), out["dist"].data_ptr(),
-                                   out["values"].data_ptr(), _C.stream_handle()),
-             "fpx_rest_patch_host")
+    ev["rank"][0].record(comp)
+    dn.wait_event(ev["rank"][0])
+    with torch.cuda.stream(dn):
+        for j in range(Pe, Pn):
+            a, b = rng[j]
+            for k in ("values", "code", "elem", "r", "dist"):
+                out[k][a:b].copy_(ws[k][a:b], non_blocking=True)
+        out["rank"].copy_(ws["rank"], non_blocking=True)
+    # the early ranges' rest records, each as soon as its download has landed
+    for j in range(Pe):
+        a, b = rng[j]
+        comp.wait_event(ev["dn"][j])
+        _C.check(L.fpx_rest_patch_host(dr, C, n, a, b, _C.ptr(wsf), wsf.numel(), S.mesh_t,
+                                       _C.ptr(ws["code"]), _C.ptr(ws["elem"]), _C.ptr(ws["r"]),
+                                       _C.ptr(ws["dist"]), _C.ptr(ws["values"]),
+                                       out["code"].data_ptr(), out["elem"].data_ptr(),
+                                       out["r"].data_ptr(), out["dist"].data_ptr(),
+                                       out["values"].data_ptr(), _C.stream_handle()),
+                 "fpx_rest_patch_host")
+    comp.wait_stream(dn)
     return st
 
 

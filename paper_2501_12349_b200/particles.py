@@ -79,8 +79,8 @@ def _migrate(S: engine.EngineSetup, st: ParticleState) -> None:
     G = S.group
     rows = torch.cat([st.x, st.v, st.v_prev, st.a_prev], dim=1)
     dest = st.records.rank.long()
-    sends = [rows[dest == k] for k in range(G.size)]
-    recv = torch.cat(transport.exchange(G, sends), dim=0)
+    order = torch.argsort(dest, stable=True)   # rows grouped by owner rank
+    recv, _ = transport.exchange_packed(G, rows[order], torch.bincount(dest, minlength=G.size))
     d = st.x.shape[1]
     st.x, st.v = recv[:, :d].contiguous(), recv[:, d:2 * d].contiguous()
     st.v_prev, st.a_prev = recv[:, 2 * d:3 * d].contiguous(), recv[:, 3 * d:].contiguous()

@@ -9,7 +9,12 @@ the winner rule D6 merges them: INTERIOR > BORDER > smaller d* > smaller
 find_and_interpolate the remote rank also evaluates the field at its record
 and returns the value with it (2 all-to-alls in total).
 
-The data movement is torch device ops around NCCL all-to-alls; the search
+Everything stays on the device: the (point, destination) pairs are
+enumerated destination-major with one nonzero over the candidate bitmasks,
+each exchange is one counts all-to-all plus one payload all-to-all with a
+single host read of the split sizes (transport.exchange_packed), and the D6
+merge is one vectorised compare-and-replace pass per source rank (each
+origin point has at most one reply per source), with no sorts.  The search
 itself is engine._find_local (the fpx_find kernels).
 """
 from __future__ import annotations
@@ -44,6 +49,23 @@ def _candidate_masks(S, x: torch.Tensor) -> torch.Tensor:
     return m & ~(1 << S.group.rank)
 
 
+def _pack_by_dest(masks: torch.Tensor, P: int):
+    """(row, destination) pairs of a candidate-rank bitmask per row, in
+    destination-major order: returns (rows, counts[P]) on the device."""
+    bits = (masks[None, :] >> torch.arange(P, device=masks.device)[:, None]) & 1
+    dst, rows = torch.nonzero(bits, as_tuple=True)
+    return rows, torch.bincount(dst, minlength=P)
+
+
+def d6_better(cc, cd, ck, ce, bc, bd, bk, be):
+    """Candidate (code, dist, rank, elem) beats the current record under the
+    winner rule D6 (lexicographic; NaN distances count as +inf)."""
+    cd = torch.nan_to_num(cd, nan=float("inf"))
+    bd = torch.nan_to_num(bd, nan=float("inf"))
+    return (cc < bc) | ((cc == bc) & ((cd < bd) | ((cd == bd) & (
+        (ck < bk) | ((ck == bk) & (ce < be))))))
+
+
 def phase_b(S, x: torch.Tensor, loc: dict, stats: dict, field) -> "E.FindRecords":
     G = S.group
     P, me = G.size, G.rank
@@ -57,83 +79,52 @@ def phase_b(S, x: torch.Tensor, loc: dict, stats: dict, field) -> "E.FindRecords
     r = loc["r"].clone()
     dist = loc["dist"].clone()
     values = loc["values"].clone() if field is not None else None
-    # --- route BORDER / NOT_FOUND points to their candidate ranks
+    # --- route BORDER / NOT_FOUND points to their candidate ranks (D11)
     todo = torch.nonzero(code != INTERIOR).flatten()
     masks = _candidate_masks(S, x[todo]) if todo.numel() else \
         torch.zeros(0, dtype=torch.int64, device=dev)
-    sends, send_idx = [], []
-    for k in range(P):
-        sel = todo[((masks >> k) & 1).bool()] if k != me else todo[:0]
-        send_idx.append(sel)
-        payload = torch.cat([x[sel], sel.to(torch.float64)[:, None]], dim=1)
-        sends.append(payload)
-    recv = transport.exchange(G, sends)
-    counts_in = [t.shape[0] for t in recv]
-    xr = torch.cat(recv, dim=0) if sum(counts_in) else torch.zeros((0, d + 1), dtype=torch.float64,
-                                                                    device=dev)
+    rows, counts = _pack_by_dest(masks, P)
+    src_idx = todo[rows]
+    payload = torch.cat([x[src_idx], src_idx.to(torch.float64)[:, None]], dim=1)
+    xr, counts_in = transport.exchange_packed(G, payload, counts)
     # --- remote Phase A on the received points
     rloc, rstats = E._find_local(S, xr[:, :d].contiguous(), field)
     rcode = rloc["code"]
     relem = torch.where(rcode != NOT_FOUND, rloc["elem"] + S.elem_offset, rloc["elem"])
     cols = [rcode.to(torch.float64)[:, None], relem.to(torch.float64)[:, None], rloc["r"],
-            rloc["dist"][:, None], xr[:, d:d + 1]]
+            rloc["dist"][:, None]]
     if field is not None:
-        cols.insert(4, rloc["values"])
+        cols.append(rloc["values"])
+    cols.append(xr[:, d:d + 1])
     reply = torch.cat(cols, dim=1)
-    backs, o = [], 0
-    for c in counts_in:
-        backs.append(reply[o:o + c])
-        o += c
-    got = transport.exchange(G, backs)
-    # --- merge at the origin (D6): candidates = local record + replies
-    width = 4 + dr + C
-    cand = [torch.cat([code.to(torch.float64)[:, None], rank.to(torch.float64)[:, None],
-                       elem.to(torch.float64)[:, None], r, dist[:, None]]
-                      + ([values] if field is not None else []), dim=1)]
-    cand_pt = [torch.arange(n, device=dev)]
-    for k, g in enumerate(got):
-        if g.shape[0] == 0:
+    got, counts_back = transport.exchange_packed(G, reply, counts_in)
+    # --- D6 merge at the origin: one pass per source rank, in rank order
+    # (a point has at most one reply per source, so a pass is conflict-free)
+    o = 0
+    for k, cnt in enumerate(counts_back):
+        g = got[o:o + cnt]
+        o += cnt
+        if cnt == 0:
             continue
-        keep = g[:, 0] != NOT_FOUND
-        g = g[keep]
-        rk = torch.full((g.shape[0], 1), float(k), dtype=torch.float64, device=dev)
-        row = torch.cat([g[:, 0:1], rk, g[:, 1:2], g[:, 2:2 + dr], g[:, 2 + dr:3 + dr]]
-                        + ([g[:, 3 + dr:3 + dr + C]] if field is not None else []), dim=1)
-        cand.append(row)
-        cand_pt.append(g[:, -1].to(torch.int64))
-    allc = torch.cat(cand, dim=0)
-    allp = torch.cat(cand_pt)
-    assert allc.shape[1] == width
-    # lexicographic (point, code, dist, rank, elem) via stable sorts, least
-    # significant key first; NaN distances (NOT_FOUND) sort last.
-    dkey = torch.nan_to_num(allc[:, 3 + dr], nan=float("inf"))
-    order = torch.arange(allc.shape[0], device=dev)
-    for key in (allc[:, 2], allc[:, 1], dkey, allc[:, 0], allp.to(torch.float64)):
-        idx = torch.sort(key[order], stable=True).indices
-        order = order[idx]
-    first = torch.ones(order.numel(), dtype=torch.bool, device=dev)
-    ps = allp[order]
-    first[1:] = ps[1:] != ps[:-1]
-    win = order[first]
-    wp = allp[win]
-    best = allc[win]
-    out_code = torch.empty(n, dtype=torch.int32, device=dev)
-    out_code[wp] = best[:, 0].to(torch.int32)
-    out_rank = torch.empty(n, dtype=torch.int32, device=dev)
-    out_rank[wp] = best[:, 1].to(torch.int32)
-    out_elem = torch.empty(n, dtype=torch.int32, device=dev)
-    out_elem[wp] = best[:, 2].to(torch.int32)
-    out_r = torch.empty((n, dr), dtype=torch.float64, device=dev)
-    out_r[wp] = best[:, 3:3 + dr]
-    out_d = torch.empty(n, dtype=torch.float64, device=dev)
-    out_d[wp] = best[:, 3 + dr]
-    rec = E.FindRecords(out_code, out_rank, out_elem, out_r, out_d, None,
+        t = g[:, -1].to(torch.int64)
+        gc = g[:, 0].to(torch.int32)
+        ge = g[:, 1].to(torch.int32)
+        gd = g[:, 2 + dr]
+        gk = torch.full_like(gc, k)
+        win = d6_better(gc, gd, gk, ge, code[t], dist[t], rank[t], elem[t]) & (gc != NOT_FOUND)
+        t = t[win]
+        code[t] = gc[win]
+        rank[t] = gk[win]
+        elem[t] = ge[win]
+        r[t] = g[win][:, 2:2 + dr]
+        dist[t] = gd[win]
+        if field is not None:
+            values[t] = g[win][:, 3 + dr:3 + dr + C]
+    rec = E.FindRecords(code, rank, elem, r, dist, None,
                         {**stats, "remote_points": int(sum(counts_in)),
                          "remote_newton": rstats.get("newton", 0)})
     if field is not None:
-        vals = torch.empty((n, C), dtype=torch.float64, device=dev)
-        vals[wp] = best[:, 4 + dr:4 + dr + C]
-        rec.values = vals
+        rec.values = values
     return rec
 
 
@@ -152,25 +143,21 @@ def interpolate_routed(S, field, records: "E.FindRecords") -> torch.Tensor:
     if mine.numel():
         out[mine] = E._eval_local(S, field, records.code[mine], records.elem[mine] - S.elem_offset,
                                   records.r[mine])
-    sends, idxs = [], []
-    for k in range(P):
-        sel = torch.nonzero(found & (records.rank == k)).flatten() if k != me else \
-            torch.zeros(0, dtype=torch.int64, device=dev)
-        idxs.append(sel)
-        sends.append(torch.cat([sel.to(torch.float64)[:, None],
-                                records.elem[sel].to(torch.float64)[:, None], records.r[sel]], 1))
-    recv = transport.exchange(G, sends)
-    backs = []
-    for g in recv:
-        if g.shape[0]:
-            el = g[:, 1].to(torch.int32) - S.elem_offset
-            cd = torch.zeros(g.shape[0], dtype=torch.int32, device=dev)
-            v = E._eval_local(S, field, cd, el, g[:, 2:2 + dr].contiguous())
-        else:
-            v = torch.zeros((0, C), dtype=torch.float64, device=dev)
-        backs.append(torch.cat([g[:, 0:1], v], 1))
-    got = transport.exchange(G, backs)
-    for g in got:
-        if g.shape[0]:
-            out[g[:, 0].to(torch.int64)] = g[:, 1:]
+    remote = torch.nonzero(found & (records.rank != me)).flatten()
+    dst = records.rank[remote].to(torch.int64)
+    order = torch.argsort(dst, stable=True)
+    sel = remote[order]
+    counts = torch.bincount(dst, minlength=P)
+    payload = torch.cat([sel.to(torch.float64)[:, None],
+                         records.elem[sel].to(torch.float64)[:, None], records.r[sel]], 1)
+    g, counts_in = transport.exchange_packed(G, payload, counts)
+    if g.shape[0]:
+        el = g[:, 1].to(torch.int32) - S.elem_offset
+        cd = torch.zeros(g.shape[0], dtype=torch.int32, device=dev)
+        v = E._eval_local(S, field, cd, el, g[:, 2:2 + dr].contiguous())
+    else:
+        v = torch.zeros((0, C), dtype=torch.float64, device=dev)
+    back, _ = transport.exchange_packed(G, torch.cat([g[:, 0:1], v], 1), counts_in)
+    if back.shape[0]:
+        out[back[:, 0].to(torch.int64)] = back[:, 1:]
     return out

@@ -187,37 +187,47 @@ def build_global_map(group, boxes: torch.Tensor, domain_lo, domain_hi,
     P = group.size
     if P > 32:
         raise ValueError("global map bitmask supports up to 32 ranks")
-    cells = _overlapped_cells(grid, boxes.detach().cpu().numpy())
+    cells = _overlapped_cells(grid, boxes.detach())
     owner = cells % P
-    per_dest = [cells[owner == k] for k in range(P)]
-    got = transport.exchange(group, [torch.from_numpy(c.astype(np.int64)) for c in per_dest])
+    order = torch.argsort(owner, stable=True)
+    counts = torch.bincount(owner, minlength=P)
+    got, rc = transport.exchange_packed(group, cells[order], counts)
     nc = n ** d
-    local = np.zeros(nc, np.int32)
-    for src, arr in enumerate(got):
-        a = arr.numpy()
-        local[a] |= np.int32(1 << src)
-    mask = transport.allreduce_bitor(group, torch.from_numpy(local))
+    local = torch.zeros(nc, dtype=torch.int32, device=cells.device)
+    src = torch.repeat_interleave(torch.arange(P, device=cells.device),
+                                  torch.as_tensor(rc, device=cells.device))
+    # (cell, source) pairs are unique per source: adding the bits is an OR
+    local.index_put_((got,), (1 << src).to(torch.int32), accumulate=True)
+    mask = transport.allreduce_bitor(group, local)
     dev = boxes.device
     return GlobalMapShard(grid, P, mask.to(dev), torch.from_numpy(grid.packed()).to(dev))
 
 
-def _overlapped_cells(grid: CartesianGrid, boxes: np.ndarray) -> np.ndarray:
-    """Unique global cells overlapped by any of the boxes."""
+def _overlapped_cells(grid: CartesianGrid, boxes: torch.Tensor) -> torch.Tensor:
+    """Unique global cells overlapped by any of the boxes [E, 2, d], on the
+    boxes' device: per-box cell ranges (the IEEE operations of
+    box_cell_range), expanded into cell ids with one repeat_interleave."""
     n, d = grid.cells, grid.dim
-    out = []
-    for lo, hi in boxes:
-        a, b = box_cell_range(grid, lo, hi)
-        rng = [np.arange(a[c], b[c] + 1) for c in range(d)]
-        mesh = np.meshgrid(*rng, indexing="ij")
-        idx = np.zeros(mesh[0].shape, np.int64)
-        mul = 1
-        for c in range(d):
-            idx += mesh[c] * mul
-            mul *= n
-        out.append(idx.ravel())
-    if not out:
-        return np.zeros(0, np.int64)
-    return np.unique(np.concatenate(out))
+    dev = boxes.device
+    if boxes.shape[0] == 0:
+        return torch.zeros(0, dtype=torch.int64, device=dev)
+    lo = torch.as_tensor(np.asarray(grid.lower, float), device=dev)
+    h = torch.as_tensor(np.asarray(grid.cell_size, float), device=dev)
+    qa = torch.floor((boxes[:, 0, :d] - lo) / h).clamp_(0, n - 1).to(torch.int64)
+    qb = torch.floor((boxes[:, 1, :d] - lo) / h).clamp_(0, n - 1).to(torch.int64)
+    ext = qb - qa + 1
+    cnt = ext.prod(dim=1)
+    eidx = torch.repeat_interleave(torch.arange(boxes.shape[0], device=dev), cnt)
+    start = torch.cumsum(cnt, 0) - cnt
+    rem = torch.arange(eidx.numel(), device=dev) - start[eidx]
+    idx = torch.zeros_like(rem)
+    mul = 1
+    for c in range(d):
+        e_c = ext[eidx, c]
+        idx += (qa[eidx, c] + rem % e_c) * mul
+        rem = rem // e_c
+        mul *= n
+    return torch.unique(idx)
 
 
 def lookup_global(gmap: GlobalMapShard, x) -> list[int]:

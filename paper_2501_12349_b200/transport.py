@@ -54,45 +54,33 @@ def exchange(group: RankGroup, sends: list[torch.Tensor]) -> list[torch.Tensor]:
         raise ValueError(f"exchange needs {P} per-destination tensors, got {len(sends)}")
     if P == 1:
         return [sends[0]]
-    home = sends[0].device
-    sends = [s.to(group.device) for s in sends]
-    ref = sends[0]
-    dev, tail = ref.device, tuple(ref.shape[1:])
-    w = int(np.prod(tail)) if tail else 1
-    counts = torch.tensor([s.shape[0] for s in sends], dtype=torch.int64, device=dev)
-    rcounts = torch.empty_like(counts)
-    _a2a(group, rcounts, counts, [1] * P, [1] * P)
-    sc = counts.tolist()
-    rc = rcounts.tolist()
-    flat = torch.cat([s.reshape(-1) for s in sends]) if sum(sc) else \
-        torch.empty(0, dtype=ref.dtype, device=dev)
-    recv = torch.empty(sum(rc) * w, dtype=ref.dtype, device=dev)
-    _a2a(group, recv, flat, [c * w for c in rc], [c * w for c in sc])
-    out, o = [], 0
-    for c in rc:
-        out.append(recv[o:o + c * w].reshape((c,) + tail).to(home))
-        o += c * w
-    return out
+    counts = [int(s.shape[0]) for s in sends]
+    recv, rc = exchange_packed(group, torch.cat(sends, dim=0), counts)
+    return list(torch.split(recv, rc, dim=0))
 
 
-def exchange_packed(group: RankGroup, payload: torch.Tensor, counts: list[int]):
+def exchange_packed(group: RankGroup, payload: torch.Tensor, counts):
     """All-to-all of a buffer already packed by destination (rows grouped in
-    rank order, `counts[k]` rows for rank k).  Returns (recv, recv_counts)."""
+    rank order, `counts[k]` rows for rank k; a list or a device tensor).
+    One counts all-to-all, one host read of the send and receive counts
+    together (NCCL needs the splits on the host: buffer sizing only), one
+    payload all-to-all.  Returns (recv, recv_counts)."""
     P = group.size
     if P == 1:
-        return payload, counts
+        return payload, [int(c) for c in (counts.tolist() if torch.is_tensor(counts) else counts)]
     home = payload.device
     payload = payload.to(group.device)
     dev = payload.device
     tail = tuple(payload.shape[1:])
     w = int(np.prod(tail)) if tail else 1
-    ct = torch.tensor(counts, dtype=torch.int64, device=dev)
+    ct = torch.as_tensor(counts, dtype=torch.int64).to(dev)
     rct = torch.empty_like(ct)
     _a2a(group, rct, ct, [1] * P, [1] * P)
-    rc = rct.tolist()
+    both = torch.cat([ct, rct]).tolist()
+    sc, rc = both[:P], both[P:]
     recv = torch.empty((sum(rc),) + tail, dtype=payload.dtype, device=dev)
-    _a2a(group, recv.reshape(-1), payload.reshape(-1), [c * w for c in rc],
-         [c * w for c in counts])
+    _a2a(group, recv.reshape(-1), payload.reshape(-1).contiguous(), [c * w for c in rc],
+         [c * w for c in sc])
     return recv.to(home), rc
 
 

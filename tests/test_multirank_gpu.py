@@ -11,6 +11,7 @@ import pytest
 import torch
 
 from paper_2501_12349_b200 import engine, toolkit
+from test_gpu_parity import check_records, oracle_for
 
 pytestmark = pytest.mark.gpu
 WORKER = os.path.join(os.path.dirname(__file__), "mp", "engine_rank_worker.py")
@@ -45,6 +46,7 @@ def test_multirank_engine_matches_single_rank(tmp_path, meshname, size, npts):
     mesh = mesh_of(meshname)
     field = toolkit.analytic_field("smooth", mesh)
     S = engine.setup(mesh)
+    OS = oracle_for(S, mesh.nodes)
     blocks = toolkit.partition_blocks(mesh.num_elements, size)
     for out in outs:
         got = np.load(out)
@@ -62,6 +64,13 @@ def test_multirank_engine_matches_single_rank(tmp_path, meshname, size, npts):
         np.testing.assert_allclose(got["values"][same], v[same], rtol=1e-10, atol=1e-12)
         np.testing.assert_allclose(got["ivalues"][same], v[same], rtol=1e-10, atol=1e-12)
         assert np.all(np.isnan(got["values"][~f]))
+        # and against the oracle's full-mesh records of the same points: the
+        # whole parity contract (codes, elements but on shared faces, r*, d*,
+        # values; the routed interpolate as well)
+        check_records(OS, got["x"], got["code"], got["elem"], got["r"], got["dist"],
+                      got["values"], field)
+        check_records(OS, got["x"], got["code"], got["elem"], got["r"], got["dist"],
+                      got["ivalues"], field)
 
 
 def test_two_rank_particle_migration():
