@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 from . import _C
-from .basis import BasisConstants, BasisEnvelope
+from .basis import BasisConstants, BasisEnvelope, ReferenceBasis, eval_tensor_product, lagrange_eval
 
 __all__ = [
     "GeometryError",
@@ -28,6 +28,7 @@ __all__ = [
     "FunctionBounds2D",
     "bound_function_1d",
     "bound_function_2d",
+    "center_map_and_jacobian",
     "element_aabb",
     "element_obb",
     "aabb_contains",
@@ -230,6 +231,25 @@ def bound_function_2d(envelope: BasisEnvelope, values) -> FunctionBounds2D:
     return FunctionBounds2D(envelope.interval_points, lo, hi)
 
 
+def center_map_and_jacobian(geom: ElementGeometry, basis: ReferenceBasis):
+    """x(0) (d,) and the Jacobian dx/dr(0) (d, d_r) of the element map at the
+    reference centre (bounds.py:97-107): the nodes contracted with the
+    centre Lagrange values, with axis a's factor replaced by the first
+    derivatives for column a.  Host-side scalar helper (numpy), like
+    aabb_contains; the setup kernel forms the same frame for every element
+    on the GPU (k_setup_bounds)."""
+    v, g, _ = lagrange_eval(basis, 0.0, second=False)
+    dr = geom.ref_dim
+    val = v[None, :]
+    x_c = eval_tensor_product(geom.nodes, [val] * dr)[0]
+    jac = np.empty((geom.phys_dim, dr))
+    for a in range(dr):
+        f = [val] * dr
+        f[a] = g[None, :]
+        jac[:, a] = eval_tensor_product(geom.nodes, f)[0]
+    return x_c, jac
+
+
 def _single(geom: ElementGeometry, envelope: BasisEnvelope, expansion: float):
     dev = _C.require_cuda()
     nodes = torch.from_numpy(geom.nodes[None]).to(dev)
@@ -238,7 +258,8 @@ def _single(geom: ElementGeometry, envelope: BasisEnvelope, expansion: float):
 
 def element_aabb(geom: ElementGeometry, envelope: BasisEnvelope,
                  expansion: float = DEFAULT_EXPANSION) -> Aabb:
-    """Axis-aligned bounding box (bounds.py:292-297)."""
+    """Axis-aligned bounding box (bounds.py:292-297).  Runs the setup kernel
+    on the GPU (FpxNativeError without a CUDA device: no CPU fallback)."""
     out = _single(geom, envelope, expansion)
     if int(out["status"][0]) == 1:
         raise DegenerateElementError("element has zero extent on every axis")
@@ -248,7 +269,8 @@ def element_aabb(geom: ElementGeometry, envelope: BasisEnvelope,
 
 def element_obb(geom: ElementGeometry, envelope: BasisEnvelope,
                 expansion: float = DEFAULT_EXPANSION) -> Obb:
-    """Oriented bounding box from the centre frame (bounds.py:366-384)."""
+    """Oriented bounding box from the centre frame (bounds.py:366-384).  Runs
+    the setup kernel on the GPU (FpxNativeError without a CUDA device)."""
     out = _single(geom, envelope, expansion)
     if int(out["status"][0]) == 1:
         raise DegenerateElementError("element has zero extent on every axis")

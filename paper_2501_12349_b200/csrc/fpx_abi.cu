@@ -547,7 +547,8 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
   // --- rest: remaining candidates of the unresolved points
   FPX_CK(cudaMemsetAsync(w.hist, 0, sizeof(int32_t) * 2 * FPX_HMAX, st));
   g_launches += 3;  // k_rest_lists, k_rest_order, k_rest_scatter, k_rest_pairlist
-  FPX_LAUNCH(fpx::launch_rest_lists(M, x, n, w.nun, w.upts, w.clist, w.cnum, w.nps, w.hist,
+  FPX_LAUNCH(fpx::launch_rest_lists(M, x, n, w.nun, w.upts, w.best, w.clist, w.cnum, w.nps,
+                                    w.hist,
                                     w.bstart, w.bcur, w.perm, w.cum, w.maxnp, w.pairs, w.npairs,
                                     st));
   FPX_CK(cudaMemsetAsync(w.found, 0, sizeof(int32_t) * n, st));

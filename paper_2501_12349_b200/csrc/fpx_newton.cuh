@@ -1099,8 +1099,8 @@ __device__ __forceinline__ double warp_min_nonneg(double d) {
 template <int D>
 __global__ void __launch_bounds__(128)
     k_rest_lists(fpx_mesh_t m, const double* __restrict__ x, const int64_t* __restrict__ nun_dev,
-                 const int32_t* __restrict__ upts, int32_t* clist, int32_t* cnum,
-                 int32_t* nps, int32_t* hist) {
+                 const int32_t* __restrict__ upts, const int32_t* __restrict__ best,
+                 int32_t* clist, int32_t* cnum, int32_t* nps, int32_t* hist) {
   // warp per rest point: lanes test the hash-list entries (one filter record
   // each), (v, e) of the passing ones go to shared memory, and the rank of
   // each is the number of passing entries before it in (v, e) order
@@ -1126,6 +1126,9 @@ __global__ void __launch_bounds__(128)
       s_e[warp][q] = pass ? e : -1;
     }
     __syncwarp();
+    // rank 0 is the candidate round 1 solved (the prefilter's choice);
+    // the others follow in (v, e) order
+    const int e0 = best[k];
     int np = 0;
     for (int q = lane; q < L; q += FPX_WARP) {
       const int e = s_e[warp][q];
@@ -1133,9 +1136,12 @@ __global__ void __launch_bounds__(128)
       ++np;
       const double v = s_v[warp][q];
       int rank = 0;
-      for (int j = 0; j < L; ++j) {
-        const int ej = s_e[warp][j];
-        rank += (ej >= 0 && bf_less(s_v[warp][j], ej, v, e)) ? 1 : 0;
+      if (e != e0) {
+        rank = 1;
+        for (int j = 0; j < L; ++j) {
+          const int ej = s_e[warp][j];
+          rank += (ej >= 0 && ej != e0 && bf_less(s_v[warp][j], ej, v, e)) ? 1 : 0;
+        }
       }
       if (rank < FPX_RK) clist[u * FPX_RK + rank] = e;
     }
@@ -1426,7 +1432,7 @@ __global__ void __launch_bounds__(128, 2)
         int want = rank - nlist;
         for (int q = m.offsets[cell]; q < m.offsets[cell + 1]; ++q) {
           const int ee = m.elems[q];
-          if (all && ee == te) continue;
+          if (ee == best[k]) continue;  // round 1's candidate (rank 0)
           load_frec(m.frec, ee, R);
           if (!frec_passes<D>(R, xs)) continue;
           if (!all && !bf_less(tv, te, frec_bestfirst<D>(R, xs), ee)) continue;
@@ -2334,14 +2340,15 @@ struct Rest {
     return cudaGetLastError();
   }
   static cudaError_t lists(const fpx_mesh_t& m, const double* x, int64_t nun_cap,
-                           const int64_t* nun_dev, const int32_t* upts, int32_t* clist,
+                           const int64_t* nun_dev, const int32_t* upts, const int32_t* best,
+                           int32_t* clist,
                            int32_t* cnum, int32_t* nps, int32_t* hist, int32_t* bstart,
                            int32_t* bcur, int32_t* perm, int64_t* cum, int32_t* maxnp,
                            int4* pairs, int64_t* npairs, cudaStream_t st) {
     int64_t b = (nun_cap + 3) / 4;
     if (b > 148 * 16) b = 148 * 16;
     if (b < 1) b = 1;
-    k_rest_lists<D><<<(unsigned)b, 128, 0, st>>>(m, x, nun_dev, upts, clist, cnum, nps,
+    k_rest_lists<D><<<(unsigned)b, 128, 0, st>>>(m, x, nun_dev, upts, best, clist, cnum, nps,
                                                  hist);
     k_rest_order<<<1, FPX_HMAX, 0, st>>>(hist, bstart, cum, maxnp, npairs);
     int64_t b2 = (nun_cap + 255) / 256;
