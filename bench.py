@@ -386,7 +386,9 @@ def run_ours(args):
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "ms_per_step": e2e_max,
                     "api": "engine.find_and_interpolate_host (host points in, host records "
-                           "out; wall clock; round-1 records downloaded under the rest phase)"},
+                           "out; wall clock; points up in chunks under the prefilter, "
+                           "records down in ranges from round 1 on, rest records patched "
+                           "per range)"},
             "work_vs_oracle": {"sample": f"first {args.cpu_sample} points of the step",
                                "kernels": kwork, "oracle": owork},
             "roofline": {"bound": "fp64",

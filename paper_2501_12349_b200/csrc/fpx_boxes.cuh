@@ -79,29 +79,35 @@ __device__ __forceinline__ bool candidate_passes_t(const fpx_mesh_t& m, int e, c
   return true;
 }
 
-// Packed filter record of element e (mesh.frec, FPX_FREC doubles, 16-byte
-// vector loads: one round trip for the whole record).
-struct FRec {
-  double v[FPX_FREC];
-};
-__device__ __forceinline__ void load_frec(const double* __restrict__ frec, int64_t e, FRec& R) {
+// Doubles [A, B) of element e's filter record (16-byte loads).
+template <int D, int A, int B>
+__device__ __forceinline__ void frec_range(const double* __restrict__ frec, int64_t e, double* v) {
   const double2* p = reinterpret_cast<const double2*>(frec + e * FPX_FREC);
 #pragma unroll
-  for (int i = 0; i < FPX_FREC / 2; ++i) {
+  for (int i = A / 2; i < (B + 1) / 2; ++i) {
     const double2 t = __ldg(p + i);
-    R.v[2 * i] = t.x;
-    R.v[2 * i + 1] = t.y;
+    v[2 * i] = t.x;
+    v[2 * i + 1] = t.y;
   }
 }
-// aabb_in, then obb_in unless the OBB frame is singular (decision D4).
+
+// The candidate filter (D4) with the record loaded in stages: the AABB
+// (48 B), the OBB and its flag only if the AABB passes, the affine frame
+// only if the OBB passes (then *v = the best-first value).
 template <int D>
-__device__ __forceinline__ bool frec_passes(const FRec& R, const double* x) {
-  if (!aabb_in(D, R.v, x)) return false;
-  return R.v[FPX_FREC - 1] == 0.0 || obb_in(D, R.v + 2 * D, R.v + 3 * D, x);
-}
-template <int D>
-__device__ __forceinline__ double frec_bestfirst(const FRec& R, const double* x) {
-  return bestfirst_value(D, R.v + 3 * D + D * D, x);
+__device__ __forceinline__ bool frec_filter(const double* __restrict__ frec, int64_t e,
+                                            const double* x, double* v) {
+  double R[FPX_FREC];
+  frec_range<D, 0, 2 * D>(frec, e, R);
+  if (!aabb_in(D, R, x)) return false;
+  frec_range<D, 2 * D, 3 * D + D * D>(frec, e, R);
+  frec_range<D, FPX_FREC - 1, FPX_FREC>(frec, e, R);
+  if (!(R[FPX_FREC - 1] == 0.0 || obb_in(D, R + 2 * D, R + 3 * D, x))) return false;
+  if (v) {
+    frec_range<D, 3 * D + D * D, 4 * D + 2 * D * D>(frec, e, R);
+    *v = bestfirst_value(D, R + 3 * D + D * D, x);
+  }
+  return true;
 }
 
 // (v, e) lexicographic order of the best-first ranking (ties -> lower id).

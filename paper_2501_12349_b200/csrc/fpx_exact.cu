@@ -740,38 +740,23 @@ __device__ __forceinline__ void write_not_found(int64_t k, int dr, int32_t* code
 // The rest kernel re-derives the further best-first candidates of the ~5%
 // of points round 1 leaves unresolved, so nothing else is stored.
 
-// Doubles [A, B) of element e's filter record (16-byte loads).
-template <int D, int A, int B>
-__device__ __forceinline__ void frec_range(const double* __restrict__ frec, int64_t e, double* v) {
-  const double2* p = reinterpret_cast<const double2*>(frec + e * FPX_FREC);
-#pragma unroll
-  for (int i = A / 2; i < (B + 1) / 2; ++i) {
-    const double2 t = __ldg(p + i);
-    v[2 * i] = t.x;
-    v[2 * i + 1] = t.y;
-  }
-}
-
 //
 // kPfLanes lanes per point, points in hash-cell order: lane j of a point
-// tests list entries j, j + kPfLanes, ...; the (count, best) of the lanes are
-// combined with two shuffles.  Consecutive points share one or two cells'
-// lists, so the records a warp reads at one time are few (L1 broadcast),
-// and each lane's chain of dependent record loads is a quarter of the
-// list: the kernel is bound by that chain's latency (thread per point:
-// 343 us, long_scoreboard 25 per issue).  The record is loaded in stages:
-// the AABB (48 B), the OBB and its flag only if the AABB passes, the affine
-// frame only if the OBB passes.  (A lane-per-(point, entry) variant with a
-// segmented warp reduction measured 447 us: its lanes gather 32 different
-// records per load instead of broadcasting.)
-#ifndef FPX_PF_LANES
-#define FPX_PF_LANES 2
-#endif
-#ifndef FPX_PF_TRIP
-#define FPX_PF_TRIP 2
-#endif
-constexpr int kPfLanes = FPX_PF_LANES;
-constexpr int kPfTrip = FPX_PF_TRIP;  // list entries per loop trip (AABB loads in flight)
+// tests list entries j, j + kPfLanes, ..., kPfTrip of them per trip with
+// their AABB loads in flight; the lanes' (count, best) are combined with a
+// shuffle.  Consecutive points share one or two cells' lists, so the records
+// a warp reads at one time are few (L1 broadcast).  The record is loaded in
+// stages (frec_filter): the AABB (48 B), the OBB and its flag only if the
+// AABB passes, the affine frame only if the OBB passes.  The kernel is bound
+// by each lane's chain of dependent loads (order/cell -> list -> record):
+// measured variants (cfg-2, ncu, us): thread per point 330-343; lanes x trip
+// 1x2 ~310, 2x2 300-310 (kept), 2x4 ~310, 4x2 ~320; 48 or 64 resident warps
+// per SM (register caps, spills at 64) 300 / 360; lane per (point, entry)
+// with a segmented warp reduction 447 (32 different records per load);
+// element-major (warp per element over its hash-box cell rows, atomics per
+// point) 872 (3x the tests without the D5b cull).
+constexpr int kPfLanes = 2;  // lanes per point
+constexpr int kPfTrip = 2;   // list entries per loop trip (AABB loads in flight)
 
 template <int D>
 __global__ void __launch_bounds__(256)

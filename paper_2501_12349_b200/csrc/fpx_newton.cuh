@@ -1119,10 +1119,9 @@ __global__ void __launch_bounds__(128)
     const int L = qe - qs < FPX_LISTMAX ? qe - qs : FPX_LISTMAX;
     for (int q = lane; q < L; q += FPX_WARP) {
       const int e = m.elems[qs + q];
-      FRec R;
-      load_frec(m.frec, e, R);
-      const bool pass = frec_passes<D>(R, xs);
-      s_v[warp][q] = pass ? frec_bestfirst<D>(R, xs) : INFINITY;
+      double v = INFINITY;
+      const bool pass = frec_filter<D>(m.frec, e, xs, &v);
+      s_v[warp][q] = pass ? v : INFINITY;
       s_e[warp][q] = pass ? e : -1;
     }
     __syncwarp();
@@ -1149,11 +1148,8 @@ __global__ void __launch_bounds__(128)
     // more than FPX_RK passing: the rest kernel scans after the last listed
     // one; lists longer than FPX_LISTMAX: it scans everything after rank 0
     if (qe - qs > L) {  // list longer than the buffer: count the rest
-      for (int q = qs + L + lane; q < qe; q += FPX_WARP) {
-        FRec R;
-        load_frec(m.frec, m.elems[q], R);
-        np += __popc(__ballot_sync(__activemask(), frec_passes<D>(R, xs)));
-      }
+      for (int q = qs + L + lane; q < qe; q += FPX_WARP)
+        np += __popc(__ballot_sync(__activemask(), frec_filter<D>(m.frec, m.elems[q], xs, nullptr)));
       np = __shfl_sync(FPX_FULL, np, 0);
     }
     if (lane == 0) {
@@ -1424,18 +1420,21 @@ __global__ void __launch_bounds__(128, 2)
         const int nlist = cn < 0 ? -cn : cn;
         const bool all = cn == -1;
         const int te = all ? best[k] : clist[u * FPX_RK + nlist - 1];
-        FRec R;
-        load_frec(m.frec, te, R);
-        const double tv = frec_bestfirst<D>(R, xs);
+        double tv = 0.0;
+        {
+          double R[FPX_FREC];
+          frec_range<D, 3 * D + D * D, 4 * D + 2 * D * D>(m.frec, te, R);
+          tv = bestfirst_value(D, R + 3 * D + D * D, xs);
+        }
         int ax[3];
         const int64_t cell = cell_of(D, m.grid, m.ncell, xs, ax);
         int want = rank - nlist;
         for (int q = m.offsets[cell]; q < m.offsets[cell + 1]; ++q) {
           const int ee = m.elems[q];
           if (ee == best[k]) continue;  // round 1's candidate (rank 0)
-          load_frec(m.frec, ee, R);
-          if (!frec_passes<D>(R, xs)) continue;
-          if (!all && !bf_less(tv, te, frec_bestfirst<D>(R, xs), ee)) continue;
+          double ve = 0.0;
+          if (!frec_filter<D>(m.frec, ee, xs, &ve)) continue;
+          if (!all && !bf_less(tv, te, ve, ee)) continue;
           if (want-- == 0) {
             en = ee;
             break;
