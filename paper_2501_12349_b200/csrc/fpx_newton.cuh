@@ -252,15 +252,18 @@ __device__ __forceinline__ void eval_state_rt(const double* __restrict__ sX,
   constexpr int GNP = (LAY == 1 || LAY == 2) ? N : Lp::NP;
   double v0[N], g0[N], h0[N];
   lagrange<N, true>(z, scale, r[0], v0, g0, h0);
-#pragma unroll
+  // axes 1..dr-1 to the scratch: one rolled copy of the basis recursion
+  // (instruction footprint of the hot loop; r[a] by selects, not indexing)
+#pragma unroll 1
   for (int a = 1; a < DR; ++a) {
     double v[N], g[N], h[N];
-    lagrange<N, true>(z, scale, r[a], v, g, h);
+    lagrange<N, true>(z, scale, a == 1 ? r[1] : r[DR - 1], v, g, h);
+    double* sa = sb + (a - 1) * 3 * N * FPX_WARP;
 #pragma unroll
     for (int j = 0; j < N; ++j) {
-      sb[(((a - 1) * 3 + 0) * N + j) * FPX_WARP] = v[j];
-      sb[(((a - 1) * 3 + 1) * N + j) * FPX_WARP] = g[j];
-      sb[(((a - 1) * 3 + 2) * N + j) * FPX_WARP] = h[j];
+      sa[(0 * N + j) * FPX_WARP] = v[j];
+      sa[(1 * N + j) * FPX_WARP] = g[j];
+      sa[(2 * N + j) * FPX_WARP] = h[j];
     }
   }
 #define SB(a, kind, j) sb[((((a)-1) * 3 + (kind)) * N + (j)) * FPX_WARP]
@@ -390,50 +393,54 @@ __device__ __forceinline__ int symi(int a, int b) {
 template <int DR>
 __device__ __forceinline__ bool chol_solve(const double* A, const bool* act, const double* b,
                                            double* x) {
-  double L[3][3], y[3], iL[3];
+  // The active principal submatrix as the block-diagonal matrix with the
+  // held axes' rows and columns replaced by the identity (and zero right-
+  // hand side): the unconditional factorisation then computes exactly the
+  // masked one's values on the active axes (the identity block contributes
+  // exact zeros) and x = 0 on the held axes, without per-entry branches.
+  double Ap[6], bp[3], L[3][3], y[3], iL[3];
   double tr = 0.0;
 #pragma unroll
-  for (int k = 0; k < DR; ++k)
+  for (int k = 0; k < DR; ++k) {
     if (act[k]) tr += A[k];
+    Ap[k] = act[k] ? A[k] : 1.0;
+    bp[k] = act[k] ? b[k] : 0.0;
+  }
+#pragma unroll
+  for (int i = 1; i < DR; ++i)
+#pragma unroll
+    for (int k = 0; k < i; ++k) Ap[symi(i, k)] = act[i] && act[k] ? A[symi(i, k)] : 0.0;
   const double thr = 1e-14 * fabs(tr);
 #pragma unroll
   for (int k = 0; k < DR; ++k) {
-    if (!act[k]) continue;
-    double s = A[k];
+    double s = Ap[k];
 #pragma unroll
-    for (int m = 0; m < k; ++m)
-      if (act[m]) s -= L[k][m] * L[k][m];
-    if (!(s > thr)) return false;
+    for (int m = 0; m < k; ++m) s -= L[k][m] * L[k][m];
+    if (act[k] && !(s > thr)) return false;
     // 1/L[k][k] (L[k][k] itself is never used): one rsqrt instead of a
-    // sqrt and a division, ~100 fewer instructions in the Newton loop
-    // (round 1 654 -> 635 us); within 1 ulp of the oracle's 1/sqrt
+    // sqrt and a division (round 1 654 -> 635 us); within 1 ulp of the
+    // oracle's 1/sqrt
     iL[k] = rsqrt(s);
 #pragma unroll
     for (int i = k + 1; i < DR; ++i) {
-      if (!act[i]) continue;
-      double t = A[symi(i, k)];
+      double t = Ap[symi(i, k)];
 #pragma unroll
-      for (int m = 0; m < k; ++m)
-        if (act[m]) t -= L[i][m] * L[k][m];
+      for (int m = 0; m < k; ++m) t -= L[i][m] * L[k][m];
       L[i][k] = t * iL[k];
     }
   }
 #pragma unroll
   for (int k = 0; k < DR; ++k) {
-    if (!act[k]) continue;
-    double t = b[k];
+    double t = bp[k];
 #pragma unroll
-    for (int m = 0; m < k; ++m)
-      if (act[m]) t -= L[k][m] * y[m];
+    for (int m = 0; m < k; ++m) t -= L[k][m] * y[m];
     y[k] = t * iL[k];
   }
 #pragma unroll
   for (int k = DR - 1; k >= 0; --k) {
-    if (!act[k]) continue;
     double t = y[k];
 #pragma unroll
-    for (int m = k + 1; m < DR; ++m)
-      if (act[m]) t -= L[m][k] * x[m];
+    for (int m = k + 1; m < DR; ++m) t -= L[m][k] * x[m];
     x[k] = t * iL[k];
   }
   return true;
@@ -466,7 +473,8 @@ __device__ __forceinline__ bool constrained_step(const double* Hm, const double*
 #pragma unroll
     for (int a = 0; a < DR; ++a) {
       x[a] = freem[a] ? y[a] : 0.0;
-      if (freem[a] && ((r[a] == 1.0 && y[a] > 0.0) || (r[a] == -1.0 && y[a] < 0.0))) {
+      // on a face with the direction leaving it: |r| = 1 and r y > 0 (exact)
+      if (freem[a] && fabs(r[a]) == 1.0 && r[a] * y[a] > 0.0) {
         freem[a] = false;
         blocked = true;
       }
@@ -518,7 +526,7 @@ __device__ __forceinline__ void affine_seed(const double* fr, const double* xs, 
     double y = 0.0;
 #pragma unroll
     for (int b = 0; b < D; ++b) y = __dadd_rn(y, __dmul_rn(fr[D + a * D + b], dx[b]));
-    r0[a] = isfinite(y) ? fmin(1.0, fmax(-1.0, y)) : 0.0;
+    r0[a] = fabs(y) < INFINITY ? fmin(1.0, fmax(-1.0, y)) : 0.0;  // inf / NaN -> 0
   }
 }
 
@@ -526,7 +534,7 @@ template <int DR>
 __device__ __forceinline__ bool on_boundary(const double* r) {
   bool b = false;
 #pragma unroll
-  for (int a = 0; a < DR; ++a) b |= (r[a] == -1.0) | (r[a] == 1.0);
+  for (int a = 0; a < DR; ++a) b |= fabs(r[a]) == 1.0;
   return b;
 }
 
@@ -655,7 +663,7 @@ __device__ __forceinline__ NewtonOut newton_warp(const double* __restrict__ sX,
       bool freem[3] = {true, true, true};
 #pragma unroll
       for (int a = 0; a < DR; ++a)
-        if ((r[a] == 1.0 && st.J[a] < 0.0) || (r[a] == -1.0 && st.J[a] > 0.0)) freem[a] = false;
+        if (fabs(r[a]) == 1.0 && r[a] * st.J[a] < 0.0) freem[a] = false;  // descent leaves the face
       double Hm[6], s[3] = {0.0, 0.0, 0.0};
       int hit = 0;
       bool ok = false;
@@ -836,6 +844,34 @@ __device__ __forceinline__ double contract_flat(const double* __restrict__ U,
   }
 }
 
+// contract_flat for d_r = 3 with the outer (k) loop rolled: the axis-2
+// weights are read from the lane's shared scratch `w` (stride 32 doubles).
+// Runs once per located point inside the round-1 loop, whose instruction
+// footprint matters (the unrolled form is ~300 instructions at N = 5).
+template <int N>
+__device__ __forceinline__ double contract_flat_k(const double* __restrict__ U,
+                                                  const double* v0, const double* v1,
+                                                  const double* w) {
+  double q = 0.0;
+#pragma unroll 1
+  for (int k = 0; k < N; ++k) {
+    double t = 0.0;
+#pragma unroll
+    for (int j = 0; j < N; ++j) {
+      const double* row = U + N * (j + N * k);
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int i = 0; i < N; i += 2) {
+        s0 = fma(row[i], v0[i], s0);
+        if (i + 1 < N) s1 = fma(row[i + 1], v0[i + 1], s1);
+      }
+      t = fma(s0 + s1, v1[j], t);
+    }
+    q = fma(t, w[k * FPX_WARP], q);
+  }
+  return q;
+}
+
 // Same contraction from global memory (lexicographic, unpadded).
 template <int DR, int N>
 __device__ __forceinline__ double contract_gmem(const double* __restrict__ U,
@@ -967,7 +1003,7 @@ __device__ __forceinline__ bool propose_step(const NState& st, const double* r, 
   bool freem[3] = {true, true, true};
 #pragma unroll
   for (int a = 0; a < DR; ++a)
-    if ((r[a] == 1.0 && st.J[a] < 0.0) || (r[a] == -1.0 && st.J[a] > 0.0)) freem[a] = false;
+    if (fabs(r[a]) == 1.0 && r[a] * st.J[a] < 0.0) freem[a] = false;  // descent leaves the face
   double Hm[6], s[3] = {0.0, 0.0, 0.0};
   int hit = 0;
   bool ok = false;
@@ -1218,7 +1254,7 @@ template <int DR>
 __device__ __forceinline__ bool held_on_face(const double* r, const double* J) {
   bool held = false;
 #pragma unroll
-  for (int a = 0; a < DR; ++a) held |= (r[a] == 1.0 && J[a] < 0.0) || (r[a] == -1.0 && J[a] > 0.0);
+  for (int a = 0; a < DR; ++a) held |= fabs(r[a]) == 1.0 && r[a] * J[a] < 0.0;
   return held;
 }
 
@@ -1752,7 +1788,6 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
   double* z = smem;
   double* scale = smem + N;
   const int warp = threadIdx.x / FPX_WARP, lane = threadIdx.x % FPX_WARP;
-  const int wpb = blockDim.x / FPX_WARP;
   // slot (nslot <= S of them per warp): geometry [D][ROWS][NP] (= the
   // mesh.nodes_pad block) | frame (x_c, J_c^-1) | field [C][K] from the
   // 16-byte boundary below the element's block (when fstage)
@@ -1762,10 +1797,9 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
       smem + 2 * ((N + 1) & ~1) + (size_t)warp * (nslot * slot_stride + SCR * FPX_WARP);
   double* sb = slots + nslot * slot_stride + lane;
   double* stash = sb + Scratch<DR, N>::STASH * FPX_WARP;
-  StreamMeta<S>* meta =
-      reinterpret_cast<StreamMeta<S>*>(smem + 2 * ((N + 1) & ~1) +
-                                       (size_t)wpb * (nslot * slot_stride + SCR * FPX_WARP)) +
-      warp;
+  // ring metadata in static shared memory (shared-space loads, not generic)
+  __shared__ StreamMeta<S> s_meta[4];
+  StreamMeta<S>* meta = s_meta + warp;
   if (threadIdx.x < N) {
     z[threadIdx.x] = m.basis[FPX_BASIS_NODES(N, m.M) + threadIdx.x];
     scale[threadIdx.x] = m.basis[FPX_BASIS_SCALE(N, m.M) + threadIdx.x];
@@ -2081,12 +2115,33 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
       if (iters) iters[pt] = it;
       if (final) {
         if (field) {
-          double v[DR][N];
-          basis_values<DR, N>(z, scale, rc, v);
           const double* fu = fstage ? sX + field_off + meta->fsh[myslot]
                                     : field + (int64_t)e * C * K;
-          for (int c = 0; c < C; ++c)
-            values[(int64_t)pt * C + c] = contract_flat<DR, N>(fu + c * K, v);
+          if constexpr (DR == 3) {
+            // the lane's scratch is free once its solve is done: the three
+            // axes' basis values from one rolled copy of the recursion
+#pragma unroll 1
+            for (int a = 0; a < 3; ++a) {
+              double w[N], g[N], h[N];
+              lagrange<N, false>(z, scale, a == 0 ? rc[0] : (a == 1 ? rc[1] : rc[2]), w, g, h);
+#pragma unroll
+              for (int k = 0; k < N; ++k) sb[(a * N + k) * FPX_WARP] = w[k];
+            }
+            double v0[N], v1[N];
+#pragma unroll
+            for (int k = 0; k < N; ++k) {
+              v0[k] = sb[k * FPX_WARP];
+              v1[k] = sb[(N + k) * FPX_WARP];
+            }
+            for (int c = 0; c < C; ++c)
+              values[(int64_t)pt * C + c] =
+                  contract_flat_k<N>(fu + c * K, v0, v1, sb + 2 * N * FPX_WARP);
+          } else {
+            double v[DR][N];
+            basis_values<DR, N>(z, scale, rc, v);
+            for (int c = 0; c < C; ++c)
+              values[(int64_t)pt * C + c] = contract_flat<DR, N>(fu + c * K, v);
+          }
           ++s_evals;
         }
       } else {
@@ -2242,6 +2297,7 @@ struct Stream {
       sst = (sst + 13) / 16 * 16 + 2;  // slot stride = 16 bytes mod 128: distinct bank groups
       const size_t per_warp =
           (size_t)(ns * sst + Scratch<DR, N>::SLOTS * FPX_WARP) * 8 + sizeof(StreamMeta<S>);
+      // (+ the metadata, static shared memory: one StreamMeta per warp)
       for (int w = 4; w >= 1; --w) {  // warps per CTA
         const size_t sm = (size_t)(2 * ((N + 1) & ~1)) * 8 + (size_t)w * per_warp;
         if (sm > 227 * 1024) continue;
