@@ -754,7 +754,10 @@ __device__ __forceinline__ void write_not_found(int64_t k, int dr, int32_t* code
 // per SM (register caps, spills at 64) 300 / 360; lane per (point, entry)
 // with a segmented warp reduction 447 (32 different records per load);
 // element-major (warp per element over its hash-box cell rows, atomics per
-// point) 872 (3x the tests without the D5b cull).
+// point) 872 (3x the tests without the D5b cull); cell-major (warp per hash
+// cell, lanes = list entries holding their records, ballot + shuffle
+// reduction per point) 760 (cells hold ~1.1 points: the per-cell chain of
+// dependent loads is paid per point).
 constexpr int kPfLanes = 2;  // lanes per point
 constexpr int kPfTrip = 2;   // list entries per loop trip (AABB loads in flight)
 
