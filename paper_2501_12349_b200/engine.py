@@ -380,11 +380,11 @@ def _field_of(S: EngineSetup, field) -> Field:
 def find(S: EngineSetup, x, *, want_iters: bool = False) -> FindRecords:
     """Computational coordinates of every point."""
     xt = _prep_points(S, x)
+    if not S.group.single:
+        from .routing import find_routed
+        return find_routed(S, xt, None, want_iters)
     loc, stats = _find_local(S, xt, None, want_iters)
-    if S.group.single:
-        return _records_single(S, loc, stats)
-    from .routing import phase_b
-    return phase_b(S, xt, loc, stats, None)
+    return _records_single(S, loc, stats)
 
 
 def _records_single(S: EngineSetup, loc, stats, values_key=False) -> FindRecords:
@@ -688,13 +688,13 @@ def find_and_interpolate(S: EngineSetup, field, x, *, want_iters: bool = False):
     f = _field_of(S, field)
     xt = _prep_points(S, x)
     fused = f.order == S.order
-    loc, stats = _find_local(S, xt, f if fused else None, want_iters)
     if S.group.single:
+        loc, stats = _find_local(S, xt, f if fused else None, want_iters)
         rec = _records_single(S, loc, stats)
         vals = loc["values"] if fused else _eval_local(S, f, loc["code"], loc["elem"], loc["r"])
         return vals, rec
-    from .routing import phase_b
-    rec = phase_b(S, xt, loc, stats, f if fused else None)
+    from .routing import find_routed
+    rec = find_routed(S, xt, f if fused else None, want_iters)
     if fused:
         return rec.values, rec
     return interpolate(S, f, rec), rec

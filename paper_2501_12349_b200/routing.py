@@ -41,12 +41,42 @@ def global_cells(gmap, x: torch.Tensor) -> torch.Tensor:
     return torch.where(inside, cell, torch.full_like(cell, -1))
 
 
-def _candidate_masks(S, x: torch.Tensor) -> torch.Tensor:
+def _global_masks(S, x: torch.Tensor) -> torch.Tensor:
+    """Candidate-rank bitmask of every point (Psi_G lookup; 0 outside)."""
     cells = global_cells(S.global_map, x)
     mask = S.global_map.rank_mask.to(x.device)
-    m = torch.where(cells >= 0, mask[cells.clamp(min=0)].to(torch.int64),
-                    torch.zeros_like(cells))
-    return m & ~(1 << S.group.rank)
+    return torch.where(cells >= 0, mask[cells.clamp(min=0)].to(torch.int64),
+                       torch.zeros_like(cells))
+
+
+def _candidate_masks(S, x: torch.Tensor) -> torch.Tensor:
+    return _global_masks(S, x) & ~(1 << S.group.rank)
+
+
+def find_routed(S, x: torch.Tensor, field, want_iters: bool = False) -> "E.FindRecords":
+    """Multi-rank find: Phase A only on the points this rank can own (its
+    bit in the global map: a point outside every local hash box has no local
+    candidate, so its local record is NOT_FOUND without a search -- at N
+    ranks with uniform points that skips (N-1)/N of the local work), then
+    Phase B routing of the BORDER / NOT_FOUND records."""
+    n = x.shape[0]
+    dev = x.device
+    dr = S.ref_dim
+    mine = torch.nonzero((_global_masks(S, x) >> S.group.rank) & 1).flatten()
+    sub, stats = E._find_local(S, x[mine].contiguous(), field, want_iters)
+    nan = float("nan")
+    loc = dict(code=torch.full((n,), NOT_FOUND, dtype=torch.int32, device=dev),
+               elem=torch.full((n,), -1, dtype=torch.int32, device=dev),
+               r=torch.full((n, dr), nan, dtype=torch.float64, device=dev),
+               dist=torch.full((n,), nan, dtype=torch.float64, device=dev),
+               iters=torch.zeros(n, dtype=torch.int32, device=dev) if want_iters else None)
+    if field is not None:
+        loc["values"] = torch.full((n, field.components), nan, dtype=torch.float64, device=dev)
+    for k, v in sub.items():
+        if v is not None and loc.get(k) is not None:
+            loc[k][mine] = v
+    stats = {**stats, "local_points": int(mine.numel())}
+    return phase_b(S, x, loc, stats, field)
 
 
 def _pack_by_dest(masks: torch.Tensor, P: int):

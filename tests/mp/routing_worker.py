@@ -63,10 +63,8 @@ def main():
     engine._find_local = oracle_find_local
     engine._eval_local = oracle_eval_local
     x = toolkit.uniform_points(3000, 3, seed=100 + rank, lo=-0.02, hi=1.02)
-    loc, stats = oracle_find_local(S, torch.from_numpy(x),
-                                   engine.Field(torch.from_numpy(field[a:b]), 3))
-    rec = routing.phase_b(S, torch.from_numpy(x), loc, stats,
-                          engine.Field(torch.from_numpy(field[a:b]), 3))
+    # local search only where this rank can own the point, then Phase B
+    rec = routing.find_routed(S, torch.from_numpy(x), engine.Field(torch.from_numpy(field[a:b]), 3))
     vals = routing.interpolate_routed(S, engine.Field(torch.from_numpy(field[a:b]), 3), rec)
     np.savez(out_path, x=x, code=rec.code.numpy(), rank=rec.rank.numpy(), elem=rec.elem.numpy(),
              r=rec.r.numpy(), dist=rec.dist.numpy(), values=rec.values.numpy(),
