@@ -234,14 +234,15 @@ __device__ __forceinline__ void eval_state(const double* __restrict__ sX,
 // flag: one copy of the contraction in the streamed kernels, whose lone
 // warps at the end of a launch are bound by instruction fetch (the flag is
 // set in ~90% of their evaluations, so the predicated-off FMAs are rare).
-template <int D, int DR, int N, int LAY = 0>
+template <int D, int DR, int N, int LAY = 0, int W2C = -1>
 __device__ __forceinline__ void eval_state_rt(const double* __restrict__ sX,
                                            const double* __restrict__ z,
                                            const double* __restrict__ scale, const double* r,
                                            const double* xs, NState& S, double* sb, const bool W2) {
-  // the second-derivative terms are always accumulated (a select per FMA
-  // cost more issue slots than the ~10% evaluations that do not need them);
-  // W2 only gates their use in S.Q
+  // W2C = 1 / 0: second derivatives accumulated / not (compile time; round
+  // 1 picks the body per warp evaluation).  W2C = -1: accumulated always,
+  // the runtime flag W2 gates only their use in S.Q (the rest kernel: nearly
+  // all of its evaluations need them, and a select per FMA cost more)
   // LAY 0: geometry staged in shared memory, rows padded to NP;
   // LAY 1: read in place from global memory ([d][N^dr]);
   // LAY 2: a per-lane shared slot holding [d][N^dr] unpadded.
@@ -251,19 +252,19 @@ __device__ __forceinline__ void eval_state_rt(const double* __restrict__ sX,
   constexpr int GCS = (LAY == 1 || LAY == 2) ? Lp::K : Lp::CS;
   constexpr int GNP = (LAY == 1 || LAY == 2) ? N : Lp::NP;
   double v0[N], g0[N], h0[N];
-  lagrange<N, true>(z, scale, r[0], v0, g0, h0);
+  lagrange<N, W2C != 0>(z, scale, r[0], v0, g0, h0);
   // axes 1..dr-1 to the scratch: one rolled copy of the basis recursion
   // (instruction footprint of the hot loop; r[a] by selects, not indexing)
 #pragma unroll 1
   for (int a = 1; a < DR; ++a) {
     double v[N], g[N], h[N];
-    lagrange<N, true>(z, scale, a == 1 ? r[1] : r[DR - 1], v, g, h);
+    lagrange<N, W2C != 0>(z, scale, a == 1 ? r[1] : r[DR - 1], v, g, h);
     double* sa = sb + (a - 1) * 3 * N * FPX_WARP;
 #pragma unroll
     for (int j = 0; j < N; ++j) {
       sa[(0 * N + j) * FPX_WARP] = v[j];
       sa[(1 * N + j) * FPX_WARP] = g[j];
-      sa[(2 * N + j) * FPX_WARP] = h[j];
+      if (W2C != 0) sa[(2 * N + j) * FPX_WARP] = h[j];
     }
   }
 #define SB(a, kind, j) sb[((((a)-1) * 3 + (kind)) * N + (j)) * FPX_WARP]
@@ -297,18 +298,18 @@ __device__ __forceinline__ void eval_state_rt(const double* __restrict__ sX,
             else p = make_double2(row[i], 0.0);
             s0 = fma(p.x, v0[i], s0);
             s1 = fma(p.x, g0[i], s1);
-            s2 = fma(p.x, h0[i], s2);
+            if (W2C != 0) s2 = fma(p.x, h0[i], s2);
             if (i + 1 < N) {
               s0 = fma(p.y, v0[i + 1], s0);
               s1 = fma(p.y, g0[i + 1], s1);
-              s2 = fma(p.y, h0[i + 1], s2);
+              if (W2C != 0) s2 = fma(p.y, h0[i + 1], s2);
             }
           }
           const double vj = SB(1, 0, j), gj = SB(1, 1, j);
           t00 = fma(s0, vj, t00);
           t10 = fma(s1, vj, t10);
           t01 = fma(s0, gj, t01);
-          {
+          if (W2C != 0) {
             const double hj = SB(1, 2, j);
             t20 = fma(s2, vj, t20);
             t11 = fma(s1, gj, t11);
@@ -320,7 +321,7 @@ __device__ __forceinline__ void eval_state_rt(const double* __restrict__ sX,
         G[0] = fma(t10, vk, G[0]);
         G[1] = fma(t01, vk, G[1]);
         G[2] = fma(t00, gk, G[2]);
-        {
+        if (W2C != 0) {
           const double hk = SB(2, 2, k);
           H2[0] = fma(t20, vk, H2[0]);
           H2[1] = fma(t02, vk, H2[1]);
@@ -340,13 +341,13 @@ __device__ __forceinline__ void eval_state_rt(const double* __restrict__ sX,
           const double p = row[i];
           s0 = fma(p, v0[i], s0);
           s1 = fma(p, g0[i], s1);
-          s2 = fma(p, h0[i], s2);
+          if (W2C != 0) s2 = fma(p, h0[i], s2);
         }
         const double vj = SB(1, 0, j), gj = SB(1, 1, j);
         xv = fma(s0, vj, xv);
         G[0] = fma(s1, vj, G[0]);
         G[1] = fma(s0, gj, G[1]);
-        {
+        if (W2C != 0) {
           const double hj = SB(1, 2, j);
           H2[0] = fma(s2, vj, H2[0]);
           H2[1] = fma(s0, hj, H2[1]);
@@ -359,7 +360,7 @@ __device__ __forceinline__ void eval_state_rt(const double* __restrict__ sX,
         const double p = Xc[i];
         xv = fma(p, v0[i], xv);
         G[0] = fma(p, g0[i], G[0]);
-        H2[0] = fma(p, h0[i], H2[0]);
+        if (W2C != 0) H2[0] = fma(p, h0[i], H2[0]);
       }
     }
 #undef SB
@@ -377,7 +378,7 @@ __device__ __forceinline__ void eval_state_rt(const double* __restrict__ sX,
       S.H0[4] = fma(G[0], G[2], S.H0[4]);
       S.H0[5] = fma(G[1], G[2], S.H0[5]);
     }
-    if (W2) {
+    if (W2C == 1 || (W2C < 0 && W2)) {
 #pragma unroll
       for (int m = 0; m < 6; ++m) S.Q[m] = fma(dx, H2[m], S.Q[m]);
     }
@@ -2022,7 +2023,12 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
     ++nev;
     nev2 += w2 ? 1 : 0;
     nlev += phase == 2 ? 1 : 0;
-    eval_state_rt<D, DR, N, 0>(sX, z, scale, rn, xs, st, sb, w2);
+    // two compile-time bodies: without second derivatives when no lane of
+    // the warp is on a face (31% of the warp evaluations at cfg-2; the extra
+    // code cost more than it saved until the loop's footprint was trimmed:
+    // 0.711 vs 0.688 ms then, 0.578 vs 0.598 ms now)
+    if (w2) eval_state_rt<D, DR, N, 0, 1>(sX, z, scale, rn, xs, st, sb, true);
+    else eval_state_rt<D, DR, N, 0, 0>(sX, z, scale, rn, xs, st, sb, false);
     if (phase != 2) continue;
     // ---- this lane's trust-region Newton update (newton_warp, D8)
     bool done = false;
