@@ -517,12 +517,14 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
                                            (int)(nc + 2), st));
     }
     FPX_CK(cudaMemsetAsync(w.cell_cursor, 0, sizeof(int32_t) * (nc + 2), st));
-    // cell-ordered point copies for the prefilter: in buffers that are free
-    // until later phases (ux: round-1 stream records; perm: rest order)
+    // cell-ordered point copies and list ranges for the prefilter: in
+    // buffers that are free until later phases (ux: round-1 stream records;
+    // clist: rest lists)
     FPX_LAUNCH(fpx::launch_point_scatter(nn, a, M.d, xa, w.cellid + a, w.cell_off,
-                                         w.cell_cursor, w.order + a, w.ux + a * M.d,
-                                         w.perm + a, st));
-    FPX_LAUNCH(fpx::launch_prefilter(M, nn, w.ux + a * M.d, w.order + a, w.perm + a, w.best,
+                                         w.cell_cursor, w.order + a, w.ux + a * M.d, M.offsets,
+                                         nc, reinterpret_cast<int2*>(w.clist) + a, st));
+    FPX_LAUNCH(fpx::launch_prefilter(M, nn, w.ux + a * M.d, w.order + a,
+                                     reinterpret_cast<const int2*>(w.clist) + a, w.best,
                                      w.npass, code, elem, r, dist, iters,
                                      field ? values : nullptr, C, w.g1.count, stats, st));
   }

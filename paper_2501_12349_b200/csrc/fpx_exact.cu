@@ -708,13 +708,16 @@ __global__ void k_point_cells(fpx_mesh_t m, int64_t n, const double* __restrict_
 __global__ void k_point_scatter(int64_t n, int64_t base, int d, const double* __restrict__ x,
                                 const int32_t* __restrict__ cellid,
                                 const int32_t* __restrict__ cell_off, int32_t* cursor,
-                                int32_t* order, double* xo, int32_t* co) {
+                                int32_t* order, double* xo, const int32_t* __restrict__ offsets,
+                                int64_t nc, int2* lr) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * blockDim.x) {
     const int c = cellid[k];
     const int64_t pos = cell_off[c] + atomicAdd(&cursor[c], 1);
     order[pos] = (int32_t)(base + k);
-    co[pos] = c;
+    // the cell's hash-list range (empty outside the grid): one load in the
+    // prefilter's chain of dependent loads instead of cell -> offsets
+    lr[pos] = c < nc ? make_int2(offsets[c], offsets[c + 1]) : make_int2(0, 0);
     for (int a = 0; a < d; ++a) xo[pos * d + a] = x[k * d + a];
   }
 }
@@ -764,12 +767,10 @@ constexpr int kPfTrip = 2;   // list entries per loop trip (AABB loads in flight
 template <int D>
 __global__ void __launch_bounds__(256)
     k_prefilter_points(fpx_mesh_t m, int64_t n, const double* __restrict__ xo,
-                       const int32_t* __restrict__ order, const int32_t* __restrict__ co,
+                       const int32_t* __restrict__ order, const int2* __restrict__ lr,
                        int32_t* best, int32_t* npass, int32_t* code, int32_t* elem, double* r,
                        double* dist, int32_t* iters, double* values, int C, int32_t* elem_count,
                        int64_t* stats) {
-  int64_t nc = 1;
-  for (int c = 0; c < D; ++c) nc *= m.ncell;
   int64_t boxtests = 0;
   const int sub = threadIdx.x % kPfLanes;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x / kPfLanes;
@@ -779,14 +780,14 @@ __global__ void __launch_bounds__(256)
   for (int64_t it = 0; it < nround; ++it, t += stride) {
     const bool valid = t < n;
     const int64_t k = valid ? order[t] : 0;
-    const int64_t cell = valid ? co[t] : nc;
+    const int2 rng = valid ? lr[t] : make_int2(0, 0);
     double xx[D];
 #pragma unroll
     for (int c = 0; c < D; ++c) xx[c] = valid ? xo[t * D + c] : 0.0;
     int cnt = 0, bst = INT_MAX;
     double bval = INFINITY;
-    if (cell < nc) {
-      const int s = m.offsets[cell], e1 = m.offsets[cell + 1];
+    {
+      const int s = rng.x, e1 = rng.y;
       if (sub == 0) boxtests += e1 - s;
       // kPfTrip entries per trip (q, q + kPfLanes, ...): their AABB loads in flight
       for (int q = s + sub; q < e1; q += kPfTrip * kPfLanes) {
@@ -975,7 +976,7 @@ cudaError_t launch_cell_of(int d, const double* grid, int n, int64_t npts, const
   return cudaGetLastError();
 }
 cudaError_t launch_prefilter(const fpx_mesh_t& m, int64_t n, const double* xo,
-                             const int32_t* order, const int32_t* co, int32_t* best,
+                             const int32_t* order, const int2* co, int32_t* best,
                              int32_t* npass, int32_t* code, int32_t* elem, double* r,
                              double* dist, int32_t* iters, double* values, int C,
                              int32_t* elem_count, int64_t* stats, cudaStream_t st) {
@@ -991,9 +992,10 @@ cudaError_t launch_point_cells(const fpx_mesh_t& m, int64_t n, const double* x, 
 }
 cudaError_t launch_point_scatter(int64_t n, int64_t base, int d, const double* x,
                                  const int32_t* cellid, const int32_t* cell_off, int32_t* cursor,
-                                 int32_t* order, double* xo, int32_t* co, cudaStream_t st) {
+                                 int32_t* order, double* xo, const int32_t* offsets, int64_t nc,
+                                 int2* lr, cudaStream_t st) {
   k_point_scatter<<<grid_for(n, 256), 256, 0, st>>>(n, base, d, x, cellid, cell_off, cursor,
-                                                    order, xo, co);
+                                                    order, xo, offsets, nc, lr);
   return cudaGetLastError();
 }
 }  // namespace fpx

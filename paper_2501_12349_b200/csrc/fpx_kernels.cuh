@@ -46,7 +46,7 @@ cudaError_t launch_cell_of(int d, const double* grid, int n, int64_t npts, const
                            int64_t* cell, cudaStream_t st);
 // thread per point in hash-cell order (k_prefilter_points)
 cudaError_t launch_prefilter(const fpx_mesh_t& m, int64_t n, const double* xo,
-                             const int32_t* order, const int32_t* co, int32_t* best,
+                             const int32_t* order, const int2* co, int32_t* best,
                              int32_t* npass, int32_t* code, int32_t* elem, double* r,
                              double* dist, int32_t* iters, double* values, int C,
                              int32_t* elem_count, int64_t* stats, cudaStream_t st);
@@ -54,7 +54,8 @@ cudaError_t launch_point_cells(const fpx_mesh_t& m, int64_t n, const double* x, 
                                int32_t* cell_count, cudaStream_t st);
 cudaError_t launch_point_scatter(int64_t n, int64_t base, int d, const double* x,
                                  const int32_t* cellid, const int32_t* cell_off, int32_t* cursor,
-                                 int32_t* order, double* xo, int32_t* co, cudaStream_t st);
+                                 int32_t* order, double* xo, const int32_t* offsets, int64_t nc,
+                                 int2* lr, cudaStream_t st);
 // Element grouping (fpx_group.cu): count -> packed scan -> items + scatter.
 cudaError_t launch_make_items(int64_t E, const int32_t* count, const uint64_t* packed_off,
                               Item* items, int64_t* nitems_dev, cudaStream_t st);
