@@ -1765,6 +1765,17 @@ __device__ __forceinline__ void prefetch_chunk(const double* ux, const int4* ume
                   (size_t)len * sizeof(int4), lane);
 }
 
+// Round-1 per-lane scratch: the axis-1..d_r-1 basis values, plus the
+// Newton-state stash below order 7.  From N = 8 on (16.5 KB element slots)
+// a rejected step re-evaluates the current iterate instead, and the stash's
+// 4 KB per warp buys resident warps (rejections are rare: at N = 5 both
+// forms measured the same).
+template <int DR, int N>
+struct StreamScratch {
+  static constexpr bool LEAN = N >= 8;
+  static constexpr int SLOTS = (DR - 1) * 3 * N + (LEAN ? 0 : 16);
+};
+
 template <int S>
 struct StreamMeta {
   uint64_t mbar[S];
@@ -1783,7 +1794,8 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
                     int64_t* stats) {
   using L = Lay<D, DR, N>;
   constexpr int K = L::K;
-  constexpr int SCR = Scratch<DR, N>::SLOTS;
+  constexpr int SCR = StreamScratch<DR, N>::SLOTS;
+  constexpr bool LEAN = StreamScratch<DR, N>::LEAN;
   constexpr int FRAME = DR == D ? D + D * D : 0;  // affine frame doubles per slot
   extern __shared__ __align__(16) double smem[];
   double* z = smem;
@@ -1797,7 +1809,7 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
   double* slots =
       smem + 2 * ((N + 1) & ~1) + (size_t)warp * (nslot * slot_stride + SCR * FPX_WARP);
   double* sb = slots + nslot * slot_stride + lane;
-  double* stash = sb + Scratch<DR, N>::STASH * FPX_WARP;
+  double* stash = sb + Scratch<DR, N>::STASH * FPX_WARP;  // (unused when LEAN)
   // ring metadata in static shared memory (shared-space loads, not generic)
   __shared__ StreamMeta<S> s_meta[4];
   StreamMeta<S>* meta = s_meta + warp;
@@ -1832,6 +1844,7 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
   double alpha = 1.0, fcur = 0.0, pred = 0.0, smax = 0.0;
   NState st;
   int64_t s_newton = 0, s_iters = 0, s_evals = 0, nev = 0, nev2 = 0, s_chunks = 0, nlev = 0;
+  bool reeval = false;  // LEAN: this evaluation recomputes the state at rc
   // first chunk
   {
     int64_t c = 0;
@@ -2034,19 +2047,29 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
     bool done = false;
     if (first) {
       first = false;
+    } else if (LEAN && reeval) {
+      reeval = false;  // st is the state at rc again: on to the abort rule and the step
     } else {
       const double decr = fcur - st.f;
+      bool rejected = false;
       if (decr >= P.accept * pred) {
         if (decr >= P.keep * pred) alpha *= P.grow;
 #pragma unroll
         for (int a = 0; a < DR; ++a) rc[a] = rn[a];
       } else {
         alpha *= P.shrink;
-        unstash_state(stash, st);
+        if constexpr (!LEAN) unstash_state(stash, st);
         st.f = fcur;
+        rejected = true;
       }
       if (smax < P.tol) done = true;
       else if (it >= P.max_iters) done = true;
+      if (LEAN && rejected && !done) {  // the state at rc is re-evaluated next
+#pragma unroll
+        for (int a = 0; a < DR; ++a) rn[a] = rc[a];
+        reeval = true;
+        continue;
+      }
     }
     if (!done && redo && it >= 1) {
       // the abort rule of the rest kernel: held on a face for two
@@ -2084,7 +2107,7 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
 #pragma unroll
         for (int a = 0; a < DR; ++a) rc[a] = rn[a];
       } else {
-        stash_state(stash, st);
+        if constexpr (!LEAN) stash_state(stash, st);
       }
     }
     if (done) {
@@ -2302,7 +2325,7 @@ struct Stream {
       int sst = L::GEO + ((FRAME + 1) & ~1) + (fs ? C * L::K + 2 : 0);
       sst = (sst + 13) / 16 * 16 + 2;  // slot stride = 16 bytes mod 128: distinct bank groups
       const size_t per_warp =
-          (size_t)(ns * sst + Scratch<DR, N>::SLOTS * FPX_WARP) * 8 + sizeof(StreamMeta<S>);
+          (size_t)(ns * sst + StreamScratch<DR, N>::SLOTS * FPX_WARP) * 8 + sizeof(StreamMeta<S>);
       // (+ the metadata, static shared memory: one StreamMeta per warp)
       for (int w = 4; w >= 1; --w) {  // warps per CTA
         const size_t sm = (size_t)(2 * ((N + 1) & ~1)) * 8 + (size_t)w * per_warp;
