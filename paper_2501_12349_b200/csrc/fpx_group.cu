@@ -5,6 +5,8 @@
 // (items << 32 | count) words, then a scatter.  A work item is one element
 // and up to FPX_ITEM units; one warp processes one item.  Order within an
 // element is irrelevant: every unit's result depends only on its own inputs.
+#include <cub/device/device_scan.cuh>
+
 #include "fpx_common.cuh"
 #include "fpx_kernels.cuh"
 
@@ -62,30 +64,41 @@ __global__ void k_scatter_units(int64_t cap, const int64_t* __restrict__ n_dev,
   }
 }
 
-// Stream-ordered unit records of round 1 (k_newton_stream): for stream
-// position g, the point's coordinates ux[g] and umeta[g] = (point, element,
-// end of the element's group).  The round-1 loader and lane refill then read
-// one record each instead of the dependent sorted -> best -> packed_off chain.
-__global__ void k_stream_units(int64_t E, const uint64_t* __restrict__ packed_off,
-                               const int32_t* __restrict__ sorted, const int32_t* __restrict__ best,
-                               const int32_t* __restrict__ ecount, const double* __restrict__ x,
-                               int d, double* ux, int4* umeta) {
-  const int64_t nu = (int64_t)(packed_off[E] & 0xffffffffull);
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < nu;
-       g += (int64_t)gridDim.x * blockDim.x) {
-    const int pt = sorted[g];
-    const int e = best[pt];
-    const int64_t gend = (int64_t)(packed_off[e] & 0xffffffffull) + ecount[e];
-    for (int c = 0; c < d; ++c) ux[g * d + c] = x[(int64_t)pt * d + c];
-    umeta[g] = make_int4(pt, e, (int)gend, 0);
+// Stream-ordered unit records of round 1 (k_newton_stream), scattered
+// straight from the points: point k with best-first element e gets a slot
+// in e's group (packed_off = exclusive scan of the per-element counts) and
+// writes its coordinates ux[g] and umeta[g] = (point, element, end of the
+// element's group).  The round-1 loader and lane refill then read one
+// record each; no intermediate sorted-index array, no work items.
+__global__ void k_stream_scatter(int64_t n, const int32_t* __restrict__ best,
+                                 const uint64_t* __restrict__ packed_off,
+                                 const int32_t* __restrict__ ecount, const double* __restrict__ x,
+                                 int d, int32_t* cursor, double* ux, int4* umeta) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int e = best[k];
+    if (e < 0) continue;
+    const int64_t g0 = (int64_t)(packed_off[e] & 0xffffffffull);
+    const int64_t g = g0 + atomicAdd(&cursor[e], 1);
+    for (int c = 0; c < d; ++c) ux[g * d + c] = x[k * d + c];
+    umeta[g] = make_int4((int)k, e, (int)(g0 + ecount[e]), 0);
   }
 }
 
-cudaError_t launch_stream_units(int64_t n_cap, int64_t E, const uint64_t* packed_off,
-                                const int32_t* sorted, const int32_t* best, const int32_t* ecount,
-                                const double* x, int d, double* ux, int4* umeta, cudaStream_t st) {
-  k_stream_units<<<grid_of(n_cap, 256), 256, 0, st>>>(E, packed_off, sorted, best, ecount, x, d,
-                                                      ux, umeta);
+cudaError_t launch_stream_units(int64_t n, int64_t E, const int32_t* best, const int32_t* count,
+                                uint64_t* packed, uint64_t* packed_off, void* scan_temp,
+                                size_t scan_bytes, int32_t* cursor, const double* x, int d,
+                                double* ux, int4* umeta, cudaStream_t st) {
+  cudaError_t e;
+  k_pack_counts<<<grid_of(E, 256), 256, 0, st>>>(E, count, packed);
+  if ((e = cudaMemsetAsync(packed + E, 0, sizeof(uint64_t), st)) != cudaSuccess) return e;
+  size_t tb = scan_bytes;
+  if ((e = cub::DeviceScan::ExclusiveSum(scan_temp, tb, packed, packed_off, (int)(E + 1), st)) !=
+      cudaSuccess)
+    return e;
+  if ((e = cudaMemsetAsync(cursor, 0, sizeof(int32_t) * E, st)) != cudaSuccess) return e;
+  k_stream_scatter<<<grid_of(n, 256), 256, 0, st>>>(n, best, packed_off, count, x, d, cursor, ux,
+                                                    umeta);
   return cudaGetLastError();
 }
 

@@ -77,9 +77,10 @@ cudaError_t launch_scatter_units(int64_t nunits_cap, const int64_t* nunits_dev,
 // Newton / eval (fpx_newton.cu, FMA allowed).
 bool newton_supported(int d, int dr, int N);
 // Stream-ordered unit records (x and (point, element, group end)) of round 1.
-cudaError_t launch_stream_units(int64_t n_cap, int64_t E, const uint64_t* packed_off,
-                                const int32_t* sorted, const int32_t* best, const int32_t* ecount,
-                                const double* x, int d, double* ux, int4* umeta, cudaStream_t st);
+cudaError_t launch_stream_units(int64_t n, int64_t E, const int32_t* best, const int32_t* count,
+                                uint64_t* packed, uint64_t* packed_off, void* scan_temp,
+                                size_t scan_bytes, int32_t* cursor, const double* x, int d,
+                                double* ux, int4* umeta, cudaStream_t st);
 // Round 1 streamed (k_newton_stream): points in best-first element order as
 // stream records (ux / umeta from launch_stream_units; packed_off[E] = count).
 cudaError_t launch_newton_stream(const fpx_mesh_t& m, int64_t n, const double* ux,
