@@ -1145,7 +1145,10 @@ __global__ void __launch_bounds__(128)
   // each is the number of passing entries before it in (v, e) order
   __shared__ double s_v[4][FPX_LISTMAX];
   __shared__ int s_e[4][FPX_LISTMAX];
+  __shared__ int s_hist[FPX_HMAX];  // block histogram of the pass counts
   const int warp = threadIdx.x / FPX_WARP, lane = threadIdx.x % FPX_WARP;
+  for (int t = threadIdx.x; t < FPX_HMAX; t += blockDim.x) s_hist[t] = 0;
+  __syncthreads();
   const int64_t nun = *nun_dev;
   for (int64_t u = (int64_t)blockIdx.x * 4 + warp; u < nun; u += (int64_t)gridDim.x * 4) {
     const int64_t k = upts[u];
@@ -1194,10 +1197,13 @@ __global__ void __launch_bounds__(128)
     if (lane == 0) {
       cnum[u] = qe - qs > L ? -1 : (np > FPX_RK ? -FPX_RK : np);
       nps[u] = np;
-      atomicAdd(&hist[np < FPX_HMAX - 1 ? np : FPX_HMAX - 1], 1);
+      atomicAdd(&s_hist[np < FPX_HMAX - 1 ? np : FPX_HMAX - 1], 1);
     }
     __syncwarp();
   }
+  __syncthreads();
+  for (int t = threadIdx.x; t < FPX_HMAX; t += blockDim.x)
+    if (s_hist[t]) atomicAdd(&hist[t], s_hist[t]);
 }
 
 // Nearest-node seeds (D7: smallest physical distance, ties -> lowest
@@ -1323,7 +1329,16 @@ static __global__ void k_rest_scatter(const int64_t* __restrict__ nun_dev, const
   for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < nun;
        u += (int64_t)gridDim.x * blockDim.x) {
     const int v = nps[u] < FPX_HMAX - 1 ? nps[u] : FPX_HMAX - 1;
-    perm[bstart[v] + atomicAdd(&bcur[v], 1)] = (int32_t)u;
+    // warp-aggregated: one atomic per distinct bucket in the warp (a handful
+    // of buckets hold all the rest points; per-point atomics serialised)
+    const unsigned act = __activemask();
+    const unsigned peers = __match_any_sync(act, v);
+    const int lane = threadIdx.x % FPX_WARP;
+    const int leader = __ffs(peers) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(&bcur[v], __popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    perm[bstart[v] + base + __popc(peers & ((1u << lane) - 1u))] = (int32_t)u;
   }
 }
 
