@@ -130,6 +130,17 @@ int fpx_profile_round1(void* ev_start, void* ev_stop);
  * points (fpx_rest_patch_host) still change.  NULL clears it. */
 int fpx_set_round1_event(void* ev);
 
+/* (ABI 6) The next fpx_find calls on this thread start every point i on the
+ * element hint[i] (device int32 [n], local ids, all valid), e.g. a
+ * particle's element of the previous step: round 1 solves it there without
+ * the hash-list prefilter, keeps the result if it is INTERIOR (then it is
+ * the point's record: the unique zero of the injective element map), and
+ * otherwise searches the point's candidates in the rest phase as a find
+ * without hint would.  The records are those of fpx_find without hint
+ * (either owner on a shared face).  NULL clears it.
+ * Replaces: the per-step re-location of PAPER.md Algorithm 1 (Find). */
+int fpx_set_find_hint(const int32_t* elem);
+
 /* (ABI 6) The next fpx_find calls on this thread take their n points in k
  * contiguous chunks [n*c/k, n*(c+1)/k): chunk c may be read once events[c]
  * (cudaEvent_t) has completed.  The find waits on each event on its stream

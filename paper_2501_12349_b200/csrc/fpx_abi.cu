@@ -39,6 +39,8 @@ thread_local cudaEvent_t g_round1_done = nullptr;
 // fpx_set_upload_events: the points arrive in k chunks, chunk c ready at ev[c]
 constexpr int kMaxUpload = 16;
 thread_local int g_upload_k = 0;
+// fpx_set_find_hint: per point a hinted element for the next fpx_find
+thread_local const int32_t* g_hint = nullptr;
 thread_local cudaEvent_t g_upload_ev[kMaxUpload];
 
 // Layout of every find workspace at its last fpx_find (points, elements):
@@ -204,6 +206,20 @@ __global__ void k_find_totals(const int64_t* __restrict__ nun, const int64_t* __
 }
 
 
+// Hinted find: round 1 solves every point on its hinted element (best =
+// hint, npass = -1 marks the point as hinted), no prefilter.
+__global__ void k_hint_init(int64_t n, int64_t E, const int32_t* __restrict__ hint, int32_t* best,
+                            int32_t* npass, int32_t* count) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    const int e = hint[k];
+    const int eh = e >= 0 && e < E ? e : 0;  // (engine guarantees a valid hint)
+    best[k] = eh;
+    npass[k] = -1;
+    atomicAdd(&count[eh], 1);
+  }
+}
+
 __global__ void k_count_elems(int64_t n, const int32_t* __restrict__ elem, int32_t* count) {
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
        k += (int64_t)gridDim.x * blockDim.x)
@@ -264,6 +280,11 @@ int fpx_profile_round1(void* ev_start, void* ev_stop) {
 
 int fpx_set_round1_event(void* ev) {
   g_round1_done = reinterpret_cast<cudaEvent_t>(ev);
+  return FPX_OK;
+}
+
+int fpx_set_find_hint(const int32_t* elem) {
+  g_hint = elem;
   return FPX_OK;
 }
 
@@ -503,7 +524,13 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
   // filtered as soon as it has landed, under the next chunk's copy.
   const int64_t nc = w.ncells;
   FPX_CK(cudaMemsetAsync(w.g1.count, 0, sizeof(int32_t) * E, st));
-  const int nchunk = g_upload_k > 1 ? g_upload_k : 1;
+  const int nchunk = g_hint ? 0 : (g_upload_k > 1 ? g_upload_k : 1);
+  if (g_hint) {  // hinted find (particles): round 1 on the hinted elements, no prefilter
+    for (int ck = 0; ck < g_upload_k; ++ck) FPX_CK(cudaStreamWaitEvent(st, g_upload_ev[ck], 0));
+    g_launches += 1;
+    k_hint_init<<<grid1(n), 256, 0, st>>>(n, E, g_hint, w.best, w.npass, w.g1.count);
+    FPX_CK(cudaGetLastError());
+  }
   for (int ck = 0; ck < nchunk; ++ck) {
     const int64_t a = n * ck / nchunk, nn = n * (ck + 1) / nchunk - a;
     if (nchunk > 1) FPX_CK(cudaStreamWaitEvent(st, g_upload_ev[ck], 0));
@@ -540,16 +567,20 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
   FPX_CK(cudaMemsetAsync(w.chunk_ctr, 0, sizeof(int64_t), st));
   // candidates held on a face twice in a row stop early and are redone in
   // full only if their point ends without an INTERIOR (see k_rest_l1)
+  // (hinted: no abort rule / redo entries in round 1 -- the hinted element
+  // may not be a candidate; non-INTERIOR points go to the rest phase whole)
   FPX_LAUNCH(fpx::launch_newton_stream(M, n, w.ux, w.umeta, w.g1.packed_off, w.npass, code,
                                        elem, r, dist, iters, field, C, values, w.upts, w.nun,
-                                       w.chunk_ctr, w.redo, w.nredo, 2 * n + 1024, stats, st));
+                                       w.chunk_ctr, g_hint ? nullptr : w.redo, w.nredo,
+                                       2 * n + 1024, stats, st));
   if (g_prof_stop) FPX_CK(cudaEventRecord(g_prof_stop, st));
   // external record: also a real event node when captured into a CUDA graph
   if (g_round1_done) FPX_CK(cudaEventRecord(g_round1_done, st));
   // --- rest: remaining candidates of the unresolved points
   FPX_CK(cudaMemsetAsync(w.hist, 0, sizeof(int32_t) * 2 * FPX_HMAX, st));
   g_launches += 3;  // k_rest_lists, k_rest_order, k_rest_scatter, k_rest_pairlist
-  FPX_LAUNCH(fpx::launch_rest_lists(M, x, n, w.nun, w.upts, w.best, w.clist, w.cnum, w.nps,
+  FPX_LAUNCH(fpx::launch_rest_lists(M, x, n, w.nun, w.upts, w.best, w.npass, w.clist, w.cnum,
+                                    w.nps,
                                     w.hist,
                                     w.bstart, w.bcur, w.perm, w.cum, w.maxnp, w.pairs, w.npairs,
                                     st));

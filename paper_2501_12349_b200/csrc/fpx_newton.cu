@@ -63,12 +63,13 @@ struct RestLists {
 };
 
 cudaError_t launch_rest_lists(const fpx_mesh_t& m, const double* x, int64_t nun_cap,
-                              const int64_t* nun_dev, const int32_t* upts, const int32_t* best,
-                              int32_t* clist,
+                              const int64_t* nun_dev, const int32_t* upts, int32_t* best,
+                              const int32_t* npass, int32_t* clist,
                               int32_t* cnum, int32_t* nps, int32_t* hist, int32_t* bstart,
                               int32_t* bcur, int32_t* perm, int64_t* cum, int32_t* maxnp,
                               int4* pairs, int64_t* npairs, cudaStream_t st) {
-  return dispatch<RestLists>(m.d, m.dr, m.N, m, x, nun_cap, nun_dev, upts, best, clist, cnum,
+  return dispatch<RestLists>(m.d, m.dr, m.N, m, x, nun_cap, nun_dev, upts, best, npass, clist,
+                             cnum,
                              nps, hist,
                              bstart, bcur, perm, cum, maxnp, pairs, npairs, st);
 }

@@ -1138,7 +1138,7 @@ __device__ __forceinline__ double warp_min_nonneg(double d) {
 template <int D>
 __global__ void __launch_bounds__(128)
     k_rest_lists(fpx_mesh_t m, const double* __restrict__ x, const int64_t* __restrict__ nun_dev,
-                 const int32_t* __restrict__ upts, const int32_t* __restrict__ best,
+                 const int32_t* __restrict__ upts, int32_t* best, const int32_t* __restrict__ npass,
                  int32_t* clist, int32_t* cnum, int32_t* nps, int32_t* hist) {
   // warp per rest point: lanes test the hash-list entries (one filter record
   // each), (v, e) of the passing ones go to shared memory, and the rank of
@@ -1168,8 +1168,12 @@ __global__ void __launch_bounds__(128)
     }
     __syncwarp();
     // rank 0 is the candidate round 1 solved (the prefilter's choice);
-    // the others follow in (v, e) order
-    const int e0 = best[k];
+    // the others follow in (v, e) order.  A hinted point (npass < 0) has no
+    // rank-0 candidate: all of its passing candidates are ranked from 1.
+    const bool hinted = npass[k] < 0;
+    const int e0 = hinted ? -1 : best[k];
+    __syncwarp();
+    if (hinted && lane == 0) best[k] = -1;
     int np = 0;
     for (int q = lane; q < L; q += FPX_WARP) {
       const int e = s_e[warp][q];
@@ -1195,9 +1199,10 @@ __global__ void __launch_bounds__(128)
       np = __shfl_sync(FPX_FULL, np, 0);
     }
     if (lane == 0) {
-      cnum[u] = qe - qs > L ? -1 : (np > FPX_RK ? -FPX_RK : np);
-      nps[u] = np;
-      atomicAdd(&s_hist[np < FPX_HMAX - 1 ? np : FPX_HMAX - 1], 1);
+      const int npv = np + (hinted ? 1 : 0);  // ranks 0..npv-1 (rank 0 virtual when hinted)
+      cnum[u] = qe - qs > L ? -1 : (npv > FPX_RK ? -FPX_RK : npv);
+      nps[u] = npv;
+      atomicAdd(&s_hist[npv < FPX_HMAX - 1 ? npv : FPX_HMAX - 1], 1);
     }
     __syncwarp();
   }
@@ -1474,8 +1479,8 @@ __global__ void __launch_bounds__(128, 2)
         const int nlist = cn < 0 ? -cn : cn;
         const bool all = cn == -1;
         const int te = all ? best[k] : clist[u * FPX_RK + nlist - 1];
-        double tv = 0.0;
-        {
+        double tv = -INFINITY;  // te < 0: a hinted point, nothing listed before
+        if (te >= 0) {
           double R[FPX_FREC];
           frec_range<D, 3 * D + D * D, 4 * D + 2 * D * D>(m.frec, te, R);
           tv = bestfirst_value(D, R + 3 * D + D * D, xs);
@@ -1677,7 +1682,8 @@ __global__ void __launch_bounds__(128, 2)
       const double bd = *(volatile double*)&dist[k];
       bool take;
       if (cd == kInterior) take = bc != kInterior || e < be;
-      else take = bc != kInterior && (dd < bd || (dd == bd && e < be));
+      else  // (a hinted point's record starts as a NOT_FOUND placeholder)
+        take = bc == kNotFound || (bc != kInterior && (dd < bd || (dd == bd && e < be)));
       if (take) {
         code[k] = cd;
         elem[k] = e;
@@ -2150,12 +2156,18 @@ __global__ void __launch_bounds__(128, FPX_NEWTON_MINB)
         phase = 0;
         continue;
       }
-      const bool final = cd == kInterior || npass[pt] <= 1;
-      code[pt] = cd;
-      elem[pt] = e;
+      // npass < 0: a hinted find (fpx_set_find_hint) -- the hint is not
+      // known to be a candidate, so only an INTERIOR result (inside the
+      // element, hence passing its filter) is kept; otherwise the record is
+      // a NOT_FOUND placeholder and the rest phase searches all candidates
+      const int np = npass[pt];
+      const bool final = cd == kInterior || (np >= 0 && np <= 1);
+      const bool drop = !final && np < 0;
+      code[pt] = drop ? kNotFound : cd;
+      elem[pt] = drop ? -1 : e;
 #pragma unroll
-      for (int a = 0; a < DR; ++a) r[(int64_t)pt * DR + a] = rc[a];
-      dist[pt] = dd;
+      for (int a = 0; a < DR; ++a) r[(int64_t)pt * DR + a] = drop ? NAN : rc[a];
+      dist[pt] = drop ? NAN : dd;
       if (iters) iters[pt] = it;
       if (final) {
         if (field) {
@@ -2441,16 +2453,16 @@ struct Rest {
     return cudaGetLastError();
   }
   static cudaError_t lists(const fpx_mesh_t& m, const double* x, int64_t nun_cap,
-                           const int64_t* nun_dev, const int32_t* upts, const int32_t* best,
-                           int32_t* clist,
+                           const int64_t* nun_dev, const int32_t* upts, int32_t* best,
+                           const int32_t* npass, int32_t* clist,
                            int32_t* cnum, int32_t* nps, int32_t* hist, int32_t* bstart,
                            int32_t* bcur, int32_t* perm, int64_t* cum, int32_t* maxnp,
                            int4* pairs, int64_t* npairs, cudaStream_t st) {
     int64_t b = (nun_cap + 3) / 4;
     if (b > 148 * 16) b = 148 * 16;
     if (b < 1) b = 1;
-    k_rest_lists<D><<<(unsigned)b, 128, 0, st>>>(m, x, nun_dev, upts, best, clist, cnum, nps,
-                                                 hist);
+    k_rest_lists<D><<<(unsigned)b, 128, 0, st>>>(m, x, nun_dev, upts, best, npass, clist, cnum,
+                                                 nps, hist);
     k_rest_order<<<1, FPX_HMAX, 0, st>>>(hist, bstart, cum, maxnp, npairs);
     int64_t b2 = (nun_cap + 255) / 256;
     if (b2 > 148 * 8) b2 = 148 * 8;

@@ -315,7 +315,7 @@ class DeviceStats(Mapping):
 
 
 def _find_local(S: EngineSetup, x: torch.Tensor, field: Field | None = None,
-                want_iters: bool = False):
+                want_iters: bool = False, hint: torch.Tensor | None = None):
     """Phase A on this rank: the fpx_find kernel pipeline.  Returns a dict of
     device tensors (code, elem [local ids], r, dist, values?, iters?) and the
     kernel counters."""
@@ -335,11 +335,12 @@ def _find_local(S: EngineSetup, x: torch.Tensor, field: Field | None = None,
     if n == 0:
         return out, _stats_dict(np.zeros(_C.STATS_LEN, np.int64))
     x = x.contiguous()
-    return out, _find_into(S, x, out, field)
+    return out, _find_into(S, x, out, field, hint=hint)
 
 
 def _find_into(S: EngineSetup, x: torch.Tensor, out: dict, field: Field | None,
-               slot: int = 0, ws: torch.Tensor | None = None) -> DeviceStats:
+               slot: int = 0, ws: torch.Tensor | None = None,
+               hint: torch.Tensor | None = None) -> DeviceStats:
     """fpx_find on the current stream writing into caller-provided device
     slices (x contiguous); `slot` selects the shared workspace unless the
     caller owns one (`ws`, e.g. a captured graph's)."""
@@ -350,11 +351,21 @@ def _find_into(S: EngineSetup, x: torch.Tensor, out: dict, field: Field | None,
     blocks, C = (field.blocks, int(field.blocks.shape[1])) if field is not None else (None, 0)
     if ws is None:
         ws = _workspace(S, n, n, slot)
-    _C.check(_C.lib().fpx_find(
-        S.mesh_t, n, _C.ptr(x), _C.ptr(out["code"]), _C.ptr(out["elem"]), _C.ptr(out["r"]),
-        _C.ptr(out["dist"]), _C.ptr(out.get("iters")), _C.ptr(blocks), C,
-        _C.ptr(out.get("values")), _C.ptr(stats), n, _C.ptr(ws), ws.numel(),
-        _C.stream_handle()), "fpx_find")
+    L = _C.lib()
+    if hint is not None:
+        hint = hint.to(device=S.device, dtype=torch.int32).contiguous()
+        if hint.shape[0] != n:
+            raise ValueError(f"hint has {hint.shape[0]} entries for {n} points")
+        L.fpx_set_find_hint(_C.ptr(hint))
+    try:
+        _C.check(L.fpx_find(
+            S.mesh_t, n, _C.ptr(x), _C.ptr(out["code"]), _C.ptr(out["elem"]), _C.ptr(out["r"]),
+            _C.ptr(out["dist"]), _C.ptr(out.get("iters")), _C.ptr(blocks), C,
+            _C.ptr(out.get("values")), _C.ptr(stats), n, _C.ptr(ws), ws.numel(),
+            _C.stream_handle()), "fpx_find")
+    finally:
+        if hint is not None:
+            L.fpx_set_find_hint(None)
     return DeviceStats(stats)
 
 
@@ -377,13 +388,22 @@ def _field_of(S: EngineSetup, field) -> Field:
     return Field(b, f.order)
 
 
-def find(S: EngineSetup, x, *, want_iters: bool = False) -> FindRecords:
-    """Computational coordinates of every point."""
+def find(S: EngineSetup, x, *, want_iters: bool = False, hint=None) -> FindRecords:
+    """Computational coordinates of every point.
+
+    hint: optional element per point (global ids, e.g. the previous step's
+    records of moving particles, all found).  Each point is solved on its
+    hinted element first, without the hash-list prefilter; the records are
+    those of a find without hint (fpx_set_find_hint).  Single rank only
+    (ignored across ranks)."""
     xt = _prep_points(S, x)
     if not S.group.single:
         from .routing import find_routed
         return find_routed(S, xt, None, want_iters)
-    loc, stats = _find_local(S, xt, None, want_iters)
+    h = None
+    if hint is not None:  # (an invalid id is harmless: solved as element 0)
+        h = torch.as_tensor(hint).to(S.device).to(torch.int32) - S.elem_offset
+    loc, stats = _find_local(S, xt, None, want_iters, hint=h)
     return _records_single(S, loc, stats)
 
 

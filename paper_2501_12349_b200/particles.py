@@ -129,7 +129,10 @@ def advance(S: engine.EngineSetup, velocity, st: ParticleState, dt: float, box=N
                                      _C.stream_handle()), "fpx_particles_advance")
     ev["integrate"][1].record()
     ev["find"][0].record()
-    st.records = engine.find(S, st.x)
+    # re-location starts on each particle's previous element (hinted find:
+    # no prefilter; the records are those of a find without hint)
+    hint = st.records.elem if S.group.single and len(st) else None
+    st.records = engine.find(S, st.x, hint=hint)
     ev["find"][1].record()
     _drop_not_found(st)
     frac = nonlocal_fraction(S, st)

@@ -489,3 +489,33 @@ def test_invert_point_r0_and_idempotence():
     g = bounds.ElementGeometry(3, 3, 5, m.nodes[el[0]])
     res = invmap.invert_point(g, xs[0], r0=r1[0])
     assert res.iterations <= 1 and np.max(np.abs(res.r - r1[0])) < 1e-12
+
+
+@pytest.mark.parametrize("hint_kind", ["random", "previous", "true"])
+def test_hinted_find_matches_oracle(hint_kind):
+    # fpx_set_find_hint: each point solved first on a hinted element (no
+    # prefilter); the records must be those of a find without hint -- here
+    # against the oracle, for hints that are random (mostly wrong, some not
+    # even candidates), the elements of slightly displaced points (the
+    # particle case) and the owners themselves
+    m = toolkit.kershaw_mesh(6, 4)
+    S = engine.setup(m)
+    OS = oracle_for(S, m.nodes)
+    field = toolkit.analytic_field("smooth", m)
+    x = toolkit.uniform_points(6000, 3, seed=21, lo=-0.03, hi=1.03)
+    rng = np.random.default_rng(4)
+    base = engine.find(S, x)
+    found = base.code.cpu().numpy() != 2
+    x, base_elem = x[found], base.elem.cpu().numpy()[found]
+    if hint_kind == "random":
+        hint = rng.integers(0, m.num_elements, size=len(x))
+    elif hint_kind == "previous":
+        prev = engine.find(S, np.clip(x + rng.normal(scale=0.01, size=x.shape), 0, 1))
+        hint = np.where(prev.code.cpu().numpy() != 2, prev.elem.cpu().numpy(), 0)
+    else:
+        hint = base_elem
+    rec = engine.find(S, x, hint=torch.from_numpy(hint.astype(np.int32)))
+    check_records(OS, x, rec.code.cpu().numpy(), rec.elem.cpu().numpy(), rec.r.cpu().numpy(),
+                  rec.dist.cpu().numpy())
+    if hint_kind == "true":  # every point located in round 1: nothing left for the rest phase
+        assert rec.stats["rest_points"] <= int((rec.code.cpu().numpy() != 0).sum())
