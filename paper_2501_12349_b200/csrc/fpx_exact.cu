@@ -760,7 +760,10 @@ __device__ __forceinline__ void write_not_found(int64_t k, int dr, int32_t* code
 // point) 872 (3x the tests without the D5b cull); cell-major (warp per hash
 // cell, lanes = list entries holding their records, ballot + shuffle
 // reduction per point) 760 (cells hold ~1.1 points: the per-cell chain of
-// dependent loads is paid per point).
+// dependent loads is paid per point); a float hash box per list entry
+// (184 MB beside the lists) as a pre-test before the record 409 (six
+// scalar loads per entry and the extra DRAM traffic cost more than the
+// record loads they saved).
 constexpr int kPfLanes = 2;  // lanes per point
 constexpr int kPfTrip = 2;   // list entries per loop trip (AABB loads in flight)
 
