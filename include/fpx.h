@@ -145,7 +145,8 @@ int fpx_set_find_hint(const int32_t* elem);
  * contiguous chunks [n*c/k, n*(c+1)/k): chunk c may be read once events[c]
  * (cudaEvent_t) has completed.  The find waits on each event on its stream
  * just before sorting and filtering that chunk, so the host-to-device copy
- * of chunk c+1 overlaps the prefilter of chunk c.  k <= 1 or NULL clears. */
+ * of chunk c+1 overlaps the prefilter of chunk c (k = 1: the find waits on
+ * the one event before it starts).  k <= 0 or NULL clears. */
 int fpx_set_upload_events(int k, void* const* events);
 
 /* After a host-mode fpx_find (fpx_set_round1_event set; same stream, same

@@ -289,7 +289,7 @@ int fpx_set_find_hint(const int32_t* elem) {
 }
 
 int fpx_set_upload_events(int k, void* const* events) {
-  if (k <= 1 || !events) {
+  if (k <= 0 || !events) {
     g_upload_k = 0;
     return FPX_OK;
   }
@@ -533,7 +533,7 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
   }
   for (int ck = 0; ck < nchunk; ++ck) {
     const int64_t a = n * ck / nchunk, nn = n * (ck + 1) / nchunk - a;
-    if (nchunk > 1) FPX_CK(cudaStreamWaitEvent(st, g_upload_ev[ck], 0));
+    if (g_upload_k > 0) FPX_CK(cudaStreamWaitEvent(st, g_upload_ev[ck], 0));  // nchunk == k
     if (nn == 0) continue;
     const double* xa = x + a * M.d;
     FPX_CK(cudaMemsetAsync(w.cell_count, 0, sizeof(int32_t) * (nc + 2), st));

@@ -499,7 +499,8 @@ def _host_overlapped(S: EngineSetup, f: Field, x: torch.Tensor, out: dict, ws: d
     comp = torch.cuda.current_stream(S.device)
     up, dn = _streams(S, 2)
     n = int(x.shape[0])
-    if ws.get("events") is None:
+    if ws.get("events") is None or len(ws["events"]["up"]) != _UPLOAD_CHUNKS or \
+            len(ws["events"]["dn"]) != _DOWNLOAD_PIECES:
         evs = {k: [torch.cuda.Event() for _ in range(m)] for k, m in
                (("r1", 1), ("start", 1), ("up", _UPLOAD_CHUNKS), ("dn", _DOWNLOAD_PIECES),
                 ("rank", 1))}
@@ -507,7 +508,8 @@ def _host_overlapped(S: EngineSetup, f: Field, x: torch.Tensor, out: dict, ws: d
             for e in lst:
                 e.record(comp)
         ws["events"] = evs
-    gkey = (n, x.data_ptr(), f.blocks.data_ptr(), f.components) + \
+    gkey = (n, x.data_ptr(), f.blocks.data_ptr(), f.components, _UPLOAD_CHUNKS,
+            _DOWNLOAD_PIECES, _EARLY_PIECES) + \
         tuple(out[k].data_ptr() for k in _REC_KEYS) + \
         tuple(ws[k].data_ptr() for k in ("x", "values", "code", "elem", "r", "dist"))
     if S.options.graphs and ws.get("graph_key") != gkey:

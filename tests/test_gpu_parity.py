@@ -380,6 +380,27 @@ def test_host_pipeline_matches_device(chunks, kind):
     assert out["stats"]["points"] == x.shape[0]
 
 
+@pytest.mark.parametrize("upload,early", [(1, 4), (3, 0), (4, 8)])
+def test_host_pipeline_constants(monkeypatch, upload, early):
+    # the overlapped host path under other pipeline shapes: one upload chunk
+    # (its single event must still gate the find), no early download range
+    # (every range after the find), all ranges early (every record patched)
+    monkeypatch.setattr(engine, "_UPLOAD_CHUNKS", upload)
+    monkeypatch.setattr(engine, "_EARLY_PIECES", early)
+    mesh, pts = _host_case("hex")
+    S = engine.setup(mesh)
+    field = toolkit.analytic_field("smooth", mesh)
+    x = pts(7)
+    vals, rec = engine.find_and_interpolate(S, field, torch.from_numpy(x).cuda())
+    out = engine.find_and_interpolate_host(S, field, torch.from_numpy(x).pin_memory())
+    code = rec.code.cpu()
+    assert torch.equal(out["code"], code)
+    assert torch.equal(out["elem"], rec.elem.cpu())
+    found = code != 2
+    assert torch.allclose(out["r"][found], rec.r.cpu()[found], rtol=0, atol=1e-12)
+    assert torch.allclose(out["values"][found], vals.cpu()[found], rtol=1e-10, atol=1e-12)
+
+
 def test_spiral_newton_efficiency_gpu():
     # acceptance 6 on the device: the p=9 spiral element,
     # 10^4 interior points: every solve converges within 50 iterations, mean
