@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define FPX_ABI_VERSION 6
+#define FPX_ABI_VERSION 7
 
 /* error codes */
 #define FPX_OK 0
@@ -92,9 +92,22 @@ typedef struct fpx_mesh_t {
   /* (ABI 2) nodes with rows padded to an even length NP (N rounded up):
    * [E][d][N^(dr-1)][NP], 16-byte aligned rows (fpx_pad_nodes). */
   const double* nodes_pad;
+  /* (ABI 7) float pre-test records of the candidate filter
+   * (fpx_filter_records), two sections of E rows each:
+   *   box [E][FPX_FBOX]: aabb lo rounded down [d], hi rounded up [d], and at
+   *     index 6 the OBB mode (0 no OBB test, 1 float pre-test, 2 double only);
+   *   obb [E][FPX_FOBB] at fbox + FPX_FBOX*E: obb_c [d], obb_inv [d*d],
+   *     rounded to nearest (mode 1 only when every value is 0 or of
+   *     magnitude in [2^-100, 2^100]).
+   * Each pre-test decides pass / fail exactly where it can and leaves the
+   * rest (points within ~1e-7 relative of a face) to the double record, so
+   * the filter outcome is that of aabb_contains / obb_contains. */
+  const float* fbox;
 } fpx_mesh_t;
 
 #define FPX_FREC 32
+#define FPX_FBOX 8
+#define FPX_FOBB 12
 
 /* Diagnostic counters written by fpx_find (device int64[FPX_STATS_LEN]). */
 #define FPX_STAT_POINTS 0        /* points processed */
@@ -187,10 +200,12 @@ int fpx_setup_bounds(int d, int dr, int N, int M, int64_t E, const double* basis
  * bound_function_2d (dr=2, values [nf][N*N] with i fastest -> [nf][M][M]),
  * replacing bounds.py:155-171 and bounds.py:174-201. */
 /* Packs aabb/obb/frame/obb_ok into the per-element filter records (mesh.frec,
- * [E][FPX_FREC] doubles, 256-byte aligned rows) read by the find prefilter. */
+ * [E][FPX_FREC] doubles, 256-byte aligned rows) read by the find prefilter,
+ * and (ABI 7) their float pre-test records (mesh.fbox, (FPX_FBOX + FPX_FOBB)
+ * * E floats, 16-byte aligned). */
 int fpx_filter_records(int d, int64_t E, const double* aabb, const double* obb_c,
                        const double* obb_inv, const uint8_t* obb_ok, const double* frame,
-                       double* frec, void* stream);
+                       double* frec, float* fbox, void* stream);
 
 /* Copies nodes [E][d][N^dr] into the row-padded layout of mesh.nodes_pad. */
 int fpx_pad_nodes(int d, int dr, int N, int64_t E, const double* nodes, double* nodes_pad,

@@ -14,7 +14,7 @@ import torch
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("FPX_LIB") or os.path.join(HERE, "lib", "libfpx_sm100.so")
-ABI_VERSION = 6
+ABI_VERSION = 7
 
 INTERIOR, BORDER, NOT_FOUND = 0, 1, 2
 STAT_NAMES = ["points", "box_tests", "newton", "iters", "rest_points", "r1_warp_evals",
@@ -22,6 +22,7 @@ STAT_NAMES = ["points", "box_tests", "newton", "iters", "rest_points", "r1_warp_
               "rest_warp_evals", "rest_w2_evals", "rest_lane_evals", "redo", "r1_lane_evals"]
 STATS_LEN = len(STAT_NAMES)
 FREC = 32            # FPX_FREC: doubles per element filter record
+FBOX, FOBB = 8, 12   # FPX_FBOX / FPX_FOBB: floats per element pre-test record
 
 P = C.c_void_p
 
@@ -45,6 +46,7 @@ class MeshT(C.Structure):
         ("accept", C.c_double), ("shrink", C.c_double), ("alpha0", C.c_double),
         ("eps_d_abs", C.c_double), ("eps_d_rel", C.c_double),
         ("frec", P), ("nodes_pad", P),
+        ("fbox", P),
     ]
 
 
@@ -70,7 +72,7 @@ def lib():
         "fpx_profile_round1": ([P, P], i32),
         "fpx_probe_fp64": ([P, P], i32),
         "fpx_setup_bounds": ([i32, i32, i32, i32, i64, P, P, f64, P, P, P, P, P, P, P, P], i32),
-        "fpx_filter_records": ([i32, i64, P, P, P, P, P, P, P], i32),
+        "fpx_filter_records": ([i32, i64, P, P, P, P, P, P, P, P], i32),
         "fpx_pad_nodes": ([i32, i32, i32, i64, P, P, P], i32),
         "fpx_set_round1_event": ([P], i32),
         "fpx_rest_patch_host": ([i32, i32, i64, i64, i64, P, C.c_size_t, C.POINTER(MeshT), P, P,

@@ -382,11 +382,13 @@ int fpx_setup_bounds(int d, int dr, int N, int M, int64_t E, const double* basis
 
 int fpx_filter_records(int d, int64_t E, const double* aabb, const double* obb_c,
                        const double* obb_inv, const uint8_t* obb_ok, const double* frame,
-                       double* frec, void* stream) {
+                       double* frec, float* fbox, void* stream) {
   if (!(d == 2 || d == 3)) return fail(FPX_EINVAL, "filter records: bad d=%d", d);
   if (4 * d + 2 * d * d + 1 > FPX_FREC) return fail(FPX_EINVAL, "filter record too small");
   if (E <= 0) return FPX_OK;
-  FPX_LAUNCH(fpx::launch_filter_records(d, E, aabb, obb_c, obb_inv, obb_ok, frame, frec,
+  if (!fbox || (reinterpret_cast<uintptr_t>(fbox) & 15))
+    return fail(FPX_EINVAL, "filter records: fbox must be a 16-byte aligned array");
+  FPX_LAUNCH(fpx::launch_filter_records(d, E, aabb, obb_c, obb_inv, obb_ok, frame, frec, fbox,
                                         S(stream)));
   return FPX_OK;
 }
@@ -511,7 +513,8 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
   w.carve(cv, E, n);
   w.carve_cells(cv, n, cells_of(m));
   if (!cv.ok()) return fail(FPX_EINVAL, "find workspace too small (%zu < %zu)", ws_bytes, cv.off);
-  if (!m->frec) return fail(FPX_EINVAL, "mesh has no filter records (fpx_filter_records)");
+  if (!m->frec || !m->fbox)
+    return fail(FPX_EINVAL, "mesh has no filter records (fpx_filter_records)");
   if (!m->nodes_pad) return fail(FPX_EINVAL, "mesh has no padded nodes (fpx_pad_nodes)");
   {
     std::lock_guard<std::mutex> g(g_ws_mu);

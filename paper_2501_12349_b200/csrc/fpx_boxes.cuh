@@ -91,20 +91,111 @@ __device__ __forceinline__ void frec_range(const double* __restrict__ frec, int6
   }
 }
 
-// The candidate filter (D4) with the record loaded in stages: the AABB
-// (48 B), the OBB and its flag only if the AABB passes, the affine frame
-// only if the OBB passes (then *v = the best-first value).
+// ---- float pre-tests (include/fpx.h, mesh.fbox) -------------------------
+// Outcome 0 = the double test fails, 1 = it passes, 2 = undecided here (the
+// double record decides).  Either way the filter's outcome is the double
+// test's, bit for bit; the pre-tests only spare most candidates the double
+// record's loads (16 B + 8 B of box row instead of 48 B, 48 B of OBB row
+// instead of 104 B) -- the prefilter is bound by L1 wavefronts.
+constexpr int kFboxMode = 6;  // OBB mode slot of the box row
+
+// Box row: lo rounded down, hi rounded up.  xd = x rounded down, xu = up:
+// xu < lo' => x < lo; xd > lo' => xd >= nextup(lo') >= lo => x >= lo (same
+// for hi).  A failed test is exact whatever the magnitudes: x < lo' <= lo
+// leaves x - lo at least one float spacing away from 0, so the product in
+// aabb_in cannot underflow to -0.
 template <int D>
-__device__ __forceinline__ bool frec_filter(const double* __restrict__ frec, int64_t e,
-                                            const double* x, double* v) {
+__device__ __forceinline__ int fbox_aabb(const float* b, const double* x) {
+  int res = 1;
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    const float xd = __double2float_rd(x[c]), xu = __double2float_ru(x[c]);
+    if (xu < b[c] || xd > b[D + c]) return 0;
+    if (!(xd > b[c] && xu < b[D + c])) res = 2;
+  }
+  return res;
+}
+
+// OBB row (mode 1): cen', inv' = cen, inv rounded to nearest, every value 0
+// or normal with 24 bits kept.  y' = inv'(x - cen') differs from obb_in's y
+// by at most sum_b |inv_b - inv'_b||dx_b| + |inv'_b||cen_b - cen'_b| plus the
+// rounding of both sums, <= 2^-23 sum_b |inv'_b| (|dx'_b| + |cen'_b|); the
+// bound used is twice that (covering its own rounding).  NaN / inf -> 2.
+template <int D>
+__device__ __forceinline__ int fobb_in(const float* o, const double* x) {
+  double dx[D], ab[D];
+#pragma unroll
+  for (int b = 0; b < D; ++b) {
+    const double cb = (double)o[b];
+    dx[b] = x[b] - cb;
+    ab[b] = fabs(dx[b]) + fabs(cb);
+  }
+  int res = 1;
+#pragma unroll
+  for (int c = 0; c < D; ++c) {
+    double y = 0.0, bnd = 0.0;
+#pragma unroll
+    for (int b = 0; b < D; ++b) {
+      const double iv = (double)o[D + c * D + b];
+      y = fma(iv, dx[b], y);
+      bnd = fma(fabs(iv), ab[b], bnd);
+    }
+    bnd *= 0x1p-21;
+    const double ay = fabs(y);
+    if (ay - bnd > 1.0) return 0;
+    if (!(ay + bnd < 1.0)) res = 2;
+  }
+  return res;
+}
+
+template <int D>
+__device__ __forceinline__ void fbox_row(const float* __restrict__ fbox, int64_t e, float* b) {
+  const float4* p = reinterpret_cast<const float4*>(fbox + e * FPX_FBOX);
+  const float4 t0 = __ldg(p), t1 = __ldg(p + 1);
+  b[0] = t0.x, b[1] = t0.y, b[2] = t0.z, b[3] = t0.w;
+  b[4] = t1.x, b[5] = t1.y, b[6] = t1.z, b[7] = t1.w;
+}
+
+// OBB stage of the filter given the box row's mode (0, 1, 2).
+template <int D>
+__device__ __forceinline__ bool obb_stage(const fpx_mesh_t& m, int64_t e, float mode,
+                                          const double* x) {
+  if (mode == 0.0f) return true;
+  if (mode == 1.0f) {
+    const float4* p = reinterpret_cast<const float4*>(m.fbox + m.E * FPX_FBOX + e * FPX_FOBB);
+    float o[FPX_FOBB];
+#pragma unroll
+    for (int i = 0; i < (D + D * D + 3) / 4; ++i) {
+      const float4 t = __ldg(p + i);
+      o[4 * i] = t.x, o[4 * i + 1] = t.y, o[4 * i + 2] = t.z, o[4 * i + 3] = t.w;
+    }
+    const int r = fobb_in<D>(o, x);
+    if (r != 2) return r == 1;
+  }
   double R[FPX_FREC];
-  frec_range<D, 0, 2 * D>(frec, e, R);
-  if (!aabb_in(D, R, x)) return false;
-  frec_range<D, 2 * D, 3 * D + D * D>(frec, e, R);
-  frec_range<D, FPX_FREC - 1, FPX_FREC>(frec, e, R);
-  if (!(R[FPX_FREC - 1] == 0.0 || obb_in(D, R + 2 * D, R + 3 * D, x))) return false;
+  frec_range<D, 2 * D, 3 * D + D * D>(m.frec, e, R);
+  return obb_in(D, R + 2 * D, R + 3 * D, x);
+}
+
+// The candidate filter (D4) with the records loaded in stages: the float
+// box row, the OBB row only if the box passes, the affine frame only if the
+// OBB passes (then *v = the best-first value); the double rows only where
+// a float pre-test is undecided.
+template <int D>
+__device__ __forceinline__ bool frec_filter(const fpx_mesh_t& m, int64_t e, const double* x,
+                                            double* v) {
+  float b[FPX_FBOX];
+  fbox_row<D>(m.fbox, e, b);
+  int a = fbox_aabb<D>(b, x);
+  if (a == 2) {
+    double R[2 * D];
+    frec_range<D, 0, 2 * D>(m.frec, e, R);
+    a = aabb_in(D, R, x) ? 1 : 0;
+  }
+  if (a == 0 || !obb_stage<D>(m, e, b[kFboxMode], x)) return false;
   if (v) {
-    frec_range<D, 3 * D + D * D, 4 * D + 2 * D * D>(frec, e, R);
+    double R[FPX_FREC];
+    frec_range<D, 3 * D + D * D, 4 * D + 2 * D * D>(m.frec, e, R);
     *v = bestfirst_value(D, R + 3 * D + D * D, x);
   }
   return true;

@@ -749,8 +749,9 @@ __device__ __forceinline__ void write_not_found(int64_t k, int dr, int32_t* code
 // their AABB loads in flight; the lanes' (count, best) are combined with a
 // shuffle.  Consecutive points share one or two cells' lists, so the records
 // a warp reads at one time are few (L1 broadcast).  The record is loaded in
-// stages (frec_filter): the AABB (48 B), the OBB and its flag only if the
-// AABB passes, the affine frame only if the OBB passes.  The kernel is bound
+// stages (frec_filter): the float box row (32 B), the float OBB row only
+// if the box passes, the affine frame only if the OBB passes (double rows
+// only where a float pre-test is undecided).  The kernel is bound
 // by each lane's chain of dependent loads (order/cell -> list -> record):
 // measured variants (cfg-2, ncu, us): thread per point 330-343; lanes x trip
 // 1x2 ~310, 2x2 300-310 (kept), 2x4 ~310, 4x2 ~320; 48 or 64 resident warps
@@ -794,28 +795,29 @@ __global__ void __launch_bounds__(256)
       if (sub == 0) boxtests += e1 - s;
       // kPfTrip entries per trip (q, q + kPfLanes, ...): their AABB loads in flight
       for (int q = s + sub; q < e1; q += kPfTrip * kPfLanes) {
-        int ee[kPfTrip];
-        bool in[kPfTrip];
-        double R[kPfTrip][FPX_FREC];
+        int ee[kPfTrip], in[kPfTrip];
+        float B[kPfTrip][FPX_FBOX];
 #pragma unroll
         for (int h = 0; h < kPfTrip; ++h) {
           const bool ok = q + h * kPfLanes < e1;
           ee[h] = ok ? m.elems[q + h * kPfLanes] : -1;
         }
 #pragma unroll
-        for (int h = 0; h < kPfTrip; ++h)
-          frec_range<D, 0, 2 * D>(m.frec, ee[h] < 0 ? ee[0] : ee[h], R[h]);
+        for (int h = 0; h < kPfTrip; ++h) fbox_row<D>(m.fbox, ee[h] < 0 ? ee[0] : ee[h], B[h]);
 #pragma unroll
-        for (int h = 0; h < kPfTrip; ++h) in[h] = ee[h] >= 0 && aabb_in(D, R[h], xx);
+        for (int h = 0; h < kPfTrip; ++h) in[h] = ee[h] >= 0 ? fbox_aabb<D>(B[h], xx) : 0;
 #pragma unroll
         for (int h = 0; h < kPfTrip; ++h) {  // list order
-          if (!in[h]) continue;
-          frec_range<D, 2 * D, 3 * D + D * D>(m.frec, ee[h], R[h]);
-          frec_range<D, FPX_FREC - 1, FPX_FREC>(m.frec, ee[h], R[h]);
-          if (!(R[h][FPX_FREC - 1] == 0.0 || obb_in(D, R[h] + 2 * D, R[h] + 3 * D, xx))) continue;
-          frec_range<D, 3 * D + D * D, 4 * D + 2 * D * D>(m.frec, ee[h], R[h]);
+          if (in[h] == 0) continue;
+          double R[FPX_FREC];
+          if (in[h] == 2) {  // undecided in float: the double box
+            frec_range<D, 0, 2 * D>(m.frec, ee[h], R);
+            if (!aabb_in(D, R, xx)) continue;
+          }
+          if (!obb_stage<D>(m, ee[h], B[h][kFboxMode], xx)) continue;
+          frec_range<D, 3 * D + D * D, 4 * D + 2 * D * D>(m.frec, ee[h], R);
           ++cnt;
-          const double v = bestfirst_value(D, R[h] + 3 * D + D * D, xx);
+          const double v = bestfirst_value(D, R + 3 * D + D * D, xx);
           if (v < bval) {  // strict: ties keep the lower (earlier) id
             bval = v;
             bst = ee[h];
@@ -852,11 +854,19 @@ __global__ void __launch_bounds__(256)
 
 // Packed candidate-filter records (include/fpx.h, FPX_FREC): one 256-byte
 // row per element so the prefilter fetches a candidate in one round trip.
+// Also the float pre-test rows (include/fpx.h, fbox): the box rounded
+// outwards, the OBB rounded to nearest where float keeps 24 bits of every
+// value (fpx_boxes.cuh, fbox_aabb / fobb_in).
+__device__ __forceinline__ bool float_exact_range(double v) {
+  const double a = fabs(v);
+  return a == 0.0 || (a >= 0x1p-100 && a <= 0x1p100);
+}
+
 __global__ void k_filter_records(int d, int64_t E, const double* __restrict__ aabb,
                                  const double* __restrict__ obb_c,
                                  const double* __restrict__ obb_inv,
                                  const uint8_t* __restrict__ obb_ok,
-                                 const double* __restrict__ frame, double* frec) {
+                                 const double* __restrict__ frame, double* frec, float* fbox) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E;
        e += (int64_t)gridDim.x * blockDim.x) {
     double* R = frec + e * FPX_FREC;
@@ -867,6 +877,24 @@ __global__ void k_filter_records(int d, int64_t E, const double* __restrict__ aa
     for (int t = 0; t < d + d * d; ++t) R[o++] = frame[e * (d + d * d) + t];
     while (o < FPX_FREC - 1) R[o++] = 0.0;
     R[FPX_FREC - 1] = obb_ok[e] ? 1.0 : 0.0;
+    float* B = fbox + e * FPX_FBOX;
+    float* O = fbox + E * FPX_FBOX + e * FPX_FOBB;
+    for (int t = 0; t < FPX_FBOX; ++t) B[t] = 0.0f;
+    for (int t = 0; t < FPX_FOBB; ++t) O[t] = 0.0f;
+    for (int c = 0; c < d; ++c) {
+      B[c] = __double2float_rd(aabb[e * 2 * d + c]);
+      B[d + c] = __double2float_ru(aabb[e * 2 * d + d + c]);
+    }
+    bool fl = true;
+    for (int t = 0; t < d; ++t) {
+      O[t] = __double2float_rn(obb_c[e * d + t]);
+      fl = fl && float_exact_range(obb_c[e * d + t]);
+    }
+    for (int t = 0; t < d * d; ++t) {
+      O[d + t] = __double2float_rn(obb_inv[e * d * d + t]);
+      fl = fl && float_exact_range(obb_inv[e * d * d + t]);
+    }
+    B[kFboxMode] = !obb_ok[e] ? 0.0f : (fl ? 1.0f : 2.0f);
   }
 }
 
@@ -943,9 +971,10 @@ cudaError_t launch_pad_nodes(int d, int dr, int N, int64_t E, const double* node
 }
 cudaError_t launch_filter_records(int d, int64_t E, const double* aabb, const double* obb_c,
                                   const double* obb_inv, const uint8_t* obb_ok,
-                                  const double* frame, double* frec, cudaStream_t st) {
+                                  const double* frame, double* frec, float* fbox,
+                                  cudaStream_t st) {
   k_filter_records<<<grid_for(E, 256), 256, 0, st>>>(d, E, aabb, obb_c, obb_inv, obb_ok, frame,
-                                                     frec);
+                                                     frec, fbox);
   return cudaGetLastError();
 }
 cudaError_t launch_hash_grid(int d, int64_t E, const double* box, int ncell, double* grid,

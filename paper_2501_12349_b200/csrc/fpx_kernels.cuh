@@ -30,7 +30,8 @@ cudaError_t launch_pad_nodes(int d, int dr, int N, int64_t E, const double* node
                              cudaStream_t st);
 cudaError_t launch_filter_records(int d, int64_t E, const double* aabb, const double* obb_c,
                                   const double* obb_inv, const uint8_t* obb_ok,
-                                  const double* frame, double* frec, cudaStream_t st);
+                                  const double* frame, double* frec, float* fbox,
+                                  cudaStream_t st);
 cudaError_t launch_hash_grid(int d, int64_t E, const double* box, int ncell, double* grid,
                              cudaStream_t st);
 cudaError_t launch_hash_count(int d, int64_t E, const double* box, const double* obb_c,

@@ -1162,7 +1162,7 @@ __global__ void __launch_bounds__(128)
     for (int q = lane; q < L; q += FPX_WARP) {
       const int e = m.elems[qs + q];
       double v = INFINITY;
-      const bool pass = frec_filter<D>(m.frec, e, xs, &v);
+      const bool pass = frec_filter<D>(m, e, xs, &v);
       s_v[warp][q] = pass ? v : INFINITY;
       s_e[warp][q] = pass ? e : -1;
     }
@@ -1195,7 +1195,7 @@ __global__ void __launch_bounds__(128)
     // one; lists longer than FPX_LISTMAX: it scans everything after rank 0
     if (qe - qs > L) {  // list longer than the buffer: count the rest
       for (int q = qs + L + lane; q < qe; q += FPX_WARP)
-        np += __popc(__ballot_sync(__activemask(), frec_filter<D>(m.frec, m.elems[q], xs, nullptr)));
+        np += __popc(__ballot_sync(__activemask(), frec_filter<D>(m, m.elems[q], xs, nullptr)));
       np = __shfl_sync(FPX_FULL, np, 0);
     }
     if (lane == 0) {
@@ -1492,7 +1492,7 @@ __global__ void __launch_bounds__(128, 2)
           const int ee = m.elems[q];
           if (ee == best[k]) continue;  // round 1's candidate (rank 0)
           double ve = 0.0;
-          if (!frec_filter<D>(m.frec, ee, xs, &ve)) continue;
+          if (!frec_filter<D>(m, ee, xs, &ve)) continue;
           if (!all && !bf_less(tv, te, ve, ee)) continue;
           if (want-- == 0) {
             en = ee;

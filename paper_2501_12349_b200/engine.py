@@ -136,11 +136,14 @@ def _assemble(S: EngineSetup) -> None:
     m.eps_d_abs = -1.0 if opt.eps_d is None else float(opt.eps_d)
     m.eps_d_rel = float(opt.eps_d_rel)
     # packed candidate-filter records (one 256-byte row per element)
+    # and their float pre-test records (box section, then OBB section)
     S.frec = torch.empty((E, _C.FREC), dtype=torch.float64, device=dev)
+    S.fbox = torch.empty((_C.FBOX + _C.FOBB) * max(E, 1), dtype=torch.float32, device=dev)
     _C.check(_C.lib().fpx_filter_records(
         d, E, _C.ptr(S.aabb), _C.ptr(S.obb_c), _C.ptr(S.obb_inv), _C.ptr(S.obb_ok),
-        _C.ptr(S.frame), _C.ptr(S.frec), _C.stream_handle()), "fpx_filter_records")
-    m.frec = S.frec.data_ptr()
+        _C.ptr(S.frame), _C.ptr(S.frec), _C.ptr(S.fbox), _C.stream_handle()),
+        "fpx_filter_records")
+    m.frec, m.fbox = S.frec.data_ptr(), S.fbox.data_ptr()
     # rows padded to even length: 16-byte vector loads of the geometry
     NP = N + (N % 2)
     S.nodes_pad = torch.empty((E, d, (N ** dr) // N, NP), dtype=torch.float64, device=dev)

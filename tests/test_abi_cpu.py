@@ -42,5 +42,5 @@ def test_no_cpu_fallback():
 
 def test_mesh_struct_layout():
     # fpx_mesh_t: 4 int32, int64, 8 pointers, 2 int32, 2 pointers, int32 + pad,
-    # 6 doubles, 2 doubles, (ABI 2) frec + nodes_pad pointers
-    assert ctypes.sizeof(_C.MeshT) == 16 + 8 + 8 * 8 + 8 + 16 + 8 + 48 + 16 + 16
+    # 6 doubles, 2 doubles, (ABI 2) frec + nodes_pad pointers, (ABI 7) fbox
+    assert ctypes.sizeof(_C.MeshT) == 16 + 8 + 8 * 8 + 8 + 16 + 8 + 48 + 16 + 16 + 8

@@ -401,6 +401,55 @@ def test_host_pipeline_constants(monkeypatch, upload, early):
     assert torch.allclose(out["values"][found], vals.cpu()[found], rtol=1e-10, atol=1e-12)
 
 
+def _filter_boundary_points(S, rng, nel=60):
+    """Points on and next to the candidate filter's decision surfaces: the
+    AABB faces (exactly, one ulp either side, 1e-9 out) and the OBB faces
+    (y_c = +-(1 + delta), delta down to 1e-12) of random elements -- the
+    float pre-tests' undecided band and both sides of it."""
+    d = S.phys_dim
+    aabb = S.aabb.cpu().numpy().reshape(-1, 2, d)
+    oc = S.obb_c.cpu().numpy().reshape(-1, d)
+    oi = S.obb_inv.cpu().numpy().reshape(-1, d, d)
+    ok = S.obb_ok.cpu().numpy().astype(bool)
+    E = aabb.shape[0]
+    pts = []
+    for e in rng.choice(E, size=min(nel, E), replace=False):
+        lo, hi = aabb[e]
+        mid = 0.5 * (lo + hi)
+        for c in range(d):
+            for v in (lo[c], hi[c]):
+                for w in (v, np.nextafter(v, -np.inf), np.nextafter(v, np.inf), v - 1e-9, v + 1e-9):
+                    q = mid.copy()
+                    q[c] = w
+                    pts.append(q)
+        if ok[e]:
+            A = np.linalg.inv(oi[e])
+            for c in range(d):
+                for sgn in (-1.0, 1.0):
+                    for dl in (-1e-9, -1e-12, 0.0, 1e-12, 1e-9, 1e-7):
+                        y = rng.uniform(-0.9, 0.9, d)
+                        y[c] = sgn * (1.0 + dl)
+                        pts.append(oc[e] + A @ y)
+    return np.array(pts)
+
+
+@pytest.mark.parametrize("kind", ["hex", "quad"])
+def test_filter_pretests_on_decision_surfaces(kind):
+    # the float pre-tests of the candidate filter (include/fpx.h, fbox) leave
+    # the filter's outcome that of the double tests: points on the AABB / OBB
+    # faces of boundary elements are NOT_FOUND or BORDER by that outcome alone
+    if kind == "hex":
+        m = toolkit.kershaw_mesh(6, 3)
+    else:
+        m = toolkit.box_mesh(2, 10, 4)
+    S = engine.setup(m)
+    OS = oracle_for(S, m.nodes)
+    x = _filter_boundary_points(S, np.random.default_rng(17))
+    rec, orec = assert_find_parity(S, OS, x, toolkit.analytic_field("smooth", m))
+    codes = set(orec["code"].tolist())
+    assert {1, 2} <= codes, codes  # both outcomes on the faces of exterior elements
+
+
 def test_spiral_newton_efficiency_gpu():
     # acceptance 6 (SPEC.md:510) on the device: the p=9 spiral element,
     # 10^4 interior points: every solve converges within 50 iterations, mean
