@@ -764,12 +764,16 @@ __device__ __forceinline__ void write_not_found(int64_t k, int dr, int32_t* code
 // dependent loads is paid per point); a float hash box per list entry
 // (184 MB beside the lists) as a pre-test before the record 409 (six
 // scalar loads per entry and the extra DRAM traffic cost more than the
-// record loads they saved).
+// record loads they saved).  With the float pre-test rows (ABI 7: 299 ->
+// 232 us, L1 wavefronts 82% -> 58% of peak) the kernel turns latency bound
+// and occupancy matters: lanes x trip re-measured 1x2 263, 1x4 301, 2x1 243,
+// 2x2 233, 2x3 268, 2x4 286, 4x1 235, 4x2 232, 8x1 266; registers capped at
+// 48 (5 blocks/SM) 208 (kept), at 40 (6 blocks, spills) 225.
 constexpr int kPfLanes = 2;  // lanes per point
 constexpr int kPfTrip = 2;   // list entries per loop trip (AABB loads in flight)
 
 template <int D>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 5)  // 48 registers: 40 warps per SM (64 registers, 32 warps: +12%)
     k_prefilter_points(fpx_mesh_t m, int64_t n, const double* __restrict__ xo,
                        const int32_t* __restrict__ order, const int2* __restrict__ lr,
                        int32_t* best, int32_t* npass, int32_t* code, int32_t* elem, double* r,
