@@ -92,22 +92,19 @@ typedef struct fpx_mesh_t {
   /* (ABI 2) nodes with rows padded to an even length NP (N rounded up):
    * [E][d][N^(dr-1)][NP], 16-byte aligned rows (fpx_pad_nodes). */
   const double* nodes_pad;
-  /* (ABI 7) float pre-test records of the candidate filter
-   * (fpx_filter_records), two sections of E rows each:
-   *   box [E][FPX_FBOX]: aabb lo rounded down [d], hi rounded up [d], and at
-   *     index 6 the OBB mode (0 no OBB test, 1 float pre-test, 2 double only);
-   *   obb [E][FPX_FOBB] at fbox + FPX_FBOX*E: obb_c [d], obb_inv [d*d],
-   *     rounded to nearest (mode 1 only when every value is 0 or of
-   *     magnitude in [2^-100, 2^100]).
-   * Each pre-test decides pass / fail exactly where it can and leaves the
-   * rest (points within ~1e-7 relative of a face) to the double record, so
-   * the filter outcome is that of aabb_contains / obb_contains. */
+  /* (ABI 7) float pre-test rows of the candidate filter (fpx_filter_records),
+   * [E][FPX_FROW] floats: aabb lo rounded down [d] at 0, hi rounded up [d] at
+   * d, the OBB mode at 6 (0 no OBB test, 1 float pre-test, 2 double only),
+   * obb_c [d] at 8 and obb_inv [d*d] at 8+d rounded to nearest (mode 1 only
+   * when every value is 0 or of magnitude in [2^-100, 2^100]).  Each
+   * pre-test decides pass / fail exactly where it can and leaves the rest
+   * (points within ~1e-7 relative of a face) to the double record, so the
+   * filter outcome is that of aabb_contains / obb_contains. */
   const float* fbox;
 } fpx_mesh_t;
 
 #define FPX_FREC 32
-#define FPX_FBOX 8
-#define FPX_FOBB 12
+#define FPX_FROW 20
 
 /* Diagnostic counters written by fpx_find (device int64[FPX_STATS_LEN]). */
 #define FPX_STAT_POINTS 0        /* points processed */
@@ -201,8 +198,8 @@ int fpx_setup_bounds(int d, int dr, int N, int M, int64_t E, const double* basis
  * replacing bounds.py:155-171 and bounds.py:174-201. */
 /* Packs aabb/obb/frame/obb_ok into the per-element filter records (mesh.frec,
  * [E][FPX_FREC] doubles, 256-byte aligned rows) read by the find prefilter,
- * and (ABI 7) their float pre-test records (mesh.fbox, (FPX_FBOX + FPX_FOBB)
- * * E floats, 16-byte aligned). */
+ * and (ABI 7) their float pre-test rows (mesh.fbox, [E][FPX_FROW] floats,
+ * 16-byte aligned). */
 int fpx_filter_records(int d, int64_t E, const double* aabb, const double* obb_c,
                        const double* obb_inv, const uint8_t* obb_ok, const double* frame,
                        double* frec, float* fbox, void* stream);

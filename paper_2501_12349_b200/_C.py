@@ -22,7 +22,7 @@ STAT_NAMES = ["points", "box_tests", "newton", "iters", "rest_points", "r1_warp_
               "rest_warp_evals", "rest_w2_evals", "rest_lane_evals", "redo", "r1_lane_evals"]
 STATS_LEN = len(STAT_NAMES)
 FREC = 32            # FPX_FREC: doubles per element filter record
-FBOX, FOBB = 8, 12   # FPX_FBOX / FPX_FOBB: floats per element pre-test record
+FROW = 20            # FPX_FROW: floats per element pre-test row
 
 P = C.c_void_p
 

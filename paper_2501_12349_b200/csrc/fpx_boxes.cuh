@@ -95,11 +95,14 @@ __device__ __forceinline__ void frec_range(const double* __restrict__ frec, int6
 // Outcome 0 = the double test fails, 1 = it passes, 2 = undecided here (the
 // double record decides).  Either way the filter's outcome is the double
 // test's, bit for bit; the pre-tests only spare most candidates the double
-// record's loads (16 B + 8 B of box row instead of 48 B, 48 B of OBB row
-// instead of 104 B) -- the prefilter is bound by L1 wavefronts.
-constexpr int kFboxMode = 6;  // OBB mode slot of the box row
+// record's loads: one 80-byte row (box and OBB in one round trip: at cfg-2
+// 99% of listed candidates pass the AABB and 30% the OBB, so the OBB half
+// is always wanted) instead of 152 bytes in two dependent steps -- the
+// prefilter is bound by L1 wavefronts and load latency.
+constexpr int kFboxMode = 6;  // OBB mode slot of the row
+constexpr int kFrowObb = 8;   // obb_c, obb_inv
 
-// Box row: lo rounded down, hi rounded up.  xd = x rounded down, xu = up:
+// Box: lo rounded down, hi rounded up.  xd = x rounded down, xu = up:
 // xu < lo' => x < lo; xd > lo' => xd >= nextup(lo') >= lo => x >= lo (same
 // for hi).  A failed test is exact whatever the magnitudes: x < lo' <= lo
 // leaves x - lo at least one float spacing away from 0, so the product in
@@ -116,83 +119,82 @@ __device__ __forceinline__ int fbox_aabb(const float* b, const double* x) {
   return res;
 }
 
-// OBB row (mode 1): cen', inv' = cen, inv rounded to nearest, every value 0
-// or normal with 24 bits kept.  y' = inv'(x - cen') differs from obb_in's y
-// by at most sum_b |inv_b - inv'_b||dx_b| + |inv'_b||cen_b - cen'_b| plus the
-// rounding of both sums, <= 2^-23 sum_b |inv'_b| (|dx'_b| + |cen'_b|); the
-// bound used is twice that (covering its own rounding).  NaN / inf -> 2.
+// OBB (mode 1) in float arithmetic: cen', inv' = cen, inv rounded to
+// nearest (every value 0 or normal: 24 bits kept), x' = x rounded to
+// nearest.  y' = fl(inv'(x' - cen')) differs from obb_in's y by at most
+//   sum_b |inv_b - inv'_b||x_b - cen_b| + |inv'_b|(|x_b - x'_b| + |cen_b - cen'_b|)
+//   + the float rounding of dx' and of the three-term sum
+//   <= 6 * 2^-24 sum_b |inv'_b| (|dx'_b| + |x'_b| + |cen'_b|),
+// plus 2^-149 |inv'| where x' is subnormal; the bound used is 2^-19 times
+// the sum (5x slack, covering its own rounding and that of the compares)
+// plus 2^-40.  NaN / inf (x beyond float range) -> 2.
 template <int D>
 __device__ __forceinline__ int fobb_in(const float* o, const double* x) {
-  double dx[D], ab[D];
+  float dx[D], ab[D];
 #pragma unroll
   for (int b = 0; b < D; ++b) {
-    const double cb = (double)o[b];
-    dx[b] = x[b] - cb;
-    ab[b] = fabs(dx[b]) + fabs(cb);
+    const float xf = __double2float_rn(x[b]);
+    dx[b] = __fsub_rn(xf, o[b]);
+    ab[b] = fabsf(dx[b]) + fabsf(xf) + fabsf(o[b]);
   }
   int res = 1;
 #pragma unroll
   for (int c = 0; c < D; ++c) {
-    double y = 0.0, bnd = 0.0;
+    float y = 0.0f, bnd = 0.0f;
 #pragma unroll
     for (int b = 0; b < D; ++b) {
-      const double iv = (double)o[D + c * D + b];
-      y = fma(iv, dx[b], y);
-      bnd = fma(fabs(iv), ab[b], bnd);
+      const float iv = o[D + c * D + b];
+      y = fmaf(iv, dx[b], y);
+      bnd = fmaf(fabsf(iv), ab[b], bnd);
     }
-    bnd *= 0x1p-21;
-    const double ay = fabs(y);
-    if (ay - bnd > 1.0) return 0;
-    if (!(ay + bnd < 1.0)) res = 2;
+    bnd = fmaf(bnd, 0x1p-19f, 0x1p-40f);
+    const float ay = fabsf(y);
+    if (ay - bnd > 1.0f) return 0;
+    if (!(ay + bnd < 1.0f)) res = 2;
   }
   return res;
 }
 
+// The row's floats the D-dimensional tests read (16-byte loads).
 template <int D>
-__device__ __forceinline__ void fbox_row(const float* __restrict__ fbox, int64_t e, float* b) {
-  const float4* p = reinterpret_cast<const float4*>(fbox + e * FPX_FBOX);
-  const float4 t0 = __ldg(p), t1 = __ldg(p + 1);
-  b[0] = t0.x, b[1] = t0.y, b[2] = t0.z, b[3] = t0.w;
-  b[4] = t1.x, b[5] = t1.y, b[6] = t1.z, b[7] = t1.w;
-}
-
-// OBB stage of the filter given the box row's mode (0, 1, 2).
-template <int D>
-__device__ __forceinline__ bool obb_stage(const fpx_mesh_t& m, int64_t e, float mode,
-                                          const double* x) {
-  if (mode == 0.0f) return true;
-  if (mode == 1.0f) {
-    const float4* p = reinterpret_cast<const float4*>(m.fbox + m.E * FPX_FBOX + e * FPX_FOBB);
-    float o[FPX_FOBB];
+__device__ __forceinline__ void frow_load(const float* __restrict__ fbox, int64_t e, float* b) {
+  const float4* p = reinterpret_cast<const float4*>(fbox + e * FPX_FROW);
 #pragma unroll
-    for (int i = 0; i < (D + D * D + 3) / 4; ++i) {
-      const float4 t = __ldg(p + i);
-      o[4 * i] = t.x, o[4 * i + 1] = t.y, o[4 * i + 2] = t.z, o[4 * i + 3] = t.w;
-    }
-    const int r = fobb_in<D>(o, x);
-    if (r != 2) return r == 1;
+  for (int i = 0; i < (kFrowObb + D + D * D + 3) / 4; ++i) {
+    const float4 t = __ldg(p + i);
+    b[4 * i] = t.x, b[4 * i + 1] = t.y, b[4 * i + 2] = t.z, b[4 * i + 3] = t.w;
   }
-  double R[FPX_FREC];
-  frec_range<D, 2 * D, 3 * D + D * D>(m.frec, e, R);
-  return obb_in(D, R + 2 * D, R + 3 * D, x);
 }
 
-// The candidate filter (D4) with the records loaded in stages: the float
-// box row, the OBB row only if the box passes, the affine frame only if the
-// OBB passes (then *v = the best-first value); the double rows only where
-// a float pre-test is undecided.
+// AABB and OBB tests of candidate e from its loaded row (the double record
+// only where a pre-test is undecided).
+template <int D>
+__device__ __forceinline__ bool frow_passes(const fpx_mesh_t& m, int64_t e, const float* b,
+                                            const double* x) {
+  const float mode = b[kFboxMode];
+  const int a = fbox_aabb<D>(b, x);
+  const int o = mode == 0.0f ? 1 : (mode == 1.0f ? fobb_in<D>(b + kFrowObb, x) : 2);
+  if (a == 0 || o == 0) return false;
+  double R[FPX_FREC];
+  if (a == 2) {
+    frec_range<D, 0, 2 * D>(m.frec, e, R);
+    if (!aabb_in(D, R, x)) return false;
+  }
+  if (o == 2) {
+    frec_range<D, 2 * D, 3 * D + D * D>(m.frec, e, R);
+    if (!obb_in(D, R + 2 * D, R + 3 * D, x)) return false;
+  }
+  return true;
+}
+
+// The candidate filter (D4): the float row, then the affine frame only if
+// the candidate passes (then *v = the best-first value).
 template <int D>
 __device__ __forceinline__ bool frec_filter(const fpx_mesh_t& m, int64_t e, const double* x,
                                             double* v) {
-  float b[FPX_FBOX];
-  fbox_row<D>(m.fbox, e, b);
-  int a = fbox_aabb<D>(b, x);
-  if (a == 2) {
-    double R[2 * D];
-    frec_range<D, 0, 2 * D>(m.frec, e, R);
-    a = aabb_in(D, R, x) ? 1 : 0;
-  }
-  if (a == 0 || !obb_stage<D>(m, e, b[kFboxMode], x)) return false;
+  float b[FPX_FROW];
+  frow_load<D>(m.fbox, e, b);
+  if (!frow_passes<D>(m, e, b, x)) return false;
   if (v) {
     double R[FPX_FREC];
     frec_range<D, 3 * D + D * D, 4 * D + 2 * D * D>(m.frec, e, R);

@@ -745,18 +745,18 @@ __device__ __forceinline__ void write_not_found(int64_t k, int dr, int32_t* code
 
 //
 // kPfLanes lanes per point, points in hash-cell order: lane j of a point
-// tests list entries j, j + kPfLanes, ..., kPfTrip of them per trip with
-// their AABB loads in flight; the lanes' (count, best) are combined with a
-// shuffle.  Consecutive points share one or two cells' lists, so the records
-// a warp reads at one time are few (L1 broadcast).  The record is loaded in
-// stages (frec_filter): the float box row (32 B), the float OBB row only
-// if the box passes, the affine frame only if the OBB passes (double rows
-// only where a float pre-test is undecided).  The kernel is bound
-// by each lane's chain of dependent loads (order/cell -> list -> record):
-// measured variants (cfg-2, ncu, us): thread per point 330-343; lanes x trip
-// 1x2 ~310, 2x2 300-310 (kept), 2x4 ~310, 4x2 ~320; 48 or 64 resident warps
-// per SM (register caps, spills at 64) 300 / 360; lane per (point, entry)
-// with a segmented warp reduction 447 (32 different records per load);
+// tests list entries j, j + kPfLanes, ...; the lanes' (count, best) are
+// combined with a shuffle.  Consecutive points share one or two cells'
+// lists, so the records a warp reads at one time are few (L1 broadcast).
+// Per entry: the element's 80-byte float row (box + OBB pre-tests, one
+// round trip; the double record only in the ~1e-7 undecided band), then
+// the double affine frame only if it passes (best-first value).  At cfg-2
+// 99% of listed candidates pass the AABB and 30% the OBB.
+// Measured variants (cfg-2, ncu, us).  Double records, 256-byte rows:
+// thread per point 330-343; lanes x trip (entries in flight per lane) 1x2
+// ~310, 2x2 300-310, 2x4 ~310, 4x2 ~320; 48 or 64 resident warps per SM
+// (register caps, spills at 64) 300 / 360; lane per (point, entry) with a
+// segmented warp reduction 447 (32 different records per load);
 // element-major (warp per element over its hash-box cell rows, atomics per
 // point) 872 (3x the tests without the D5b cull); cell-major (warp per hash
 // cell, lanes = list entries holding their records, ballot + shuffle
@@ -764,16 +764,17 @@ __device__ __forceinline__ void write_not_found(int64_t k, int dr, int32_t* code
 // dependent loads is paid per point); a float hash box per list entry
 // (184 MB beside the lists) as a pre-test before the record 409 (six
 // scalar loads per entry and the extra DRAM traffic cost more than the
-// record loads they saved).  With the float pre-test rows (ABI 7: 299 ->
-// 232 us, L1 wavefronts 82% -> 58% of peak) the kernel turns latency bound
-// and occupancy matters: lanes x trip re-measured 1x2 263, 1x4 301, 2x1 243,
-// 2x2 233, 2x3 268, 2x4 286, 4x1 235, 4x2 232, 8x1 266; registers capped at
-// 48 (5 blocks/SM) 208 (kept), at 40 (6 blocks, spills) 225.
+// record loads they saved).  Float pre-tests (ABI 7): separate box and OBB
+// rows, double OBB arithmetic 232 (L1 wavefronts 82% -> 58% of peak; the
+// kernel turns latency bound); + registers capped at 48 (5 blocks/SM) 208
+// (64: 232, 40 with spills: 225); one 80-byte row 195 (2x2 lanes x trip:
+// 243, 4x1 216, 1x1 231); float OBB arithmetic 187; next entry's id loaded
+// ahead 181; warp-uniform loop bounds (spills 40 -> 8 bytes) 174 (kept;
+// register caps 62: 181, 40: 200, 32: 246).
 constexpr int kPfLanes = 2;  // lanes per point
-constexpr int kPfTrip = 2;   // list entries per loop trip (AABB loads in flight)
 
 template <int D>
-__global__ void __launch_bounds__(256, 5)  // 48 registers: 40 warps per SM (64 registers, 32 warps: +12%)
+__global__ void __launch_bounds__(256, 5)  // 48 registers: 40 warps per SM
     k_prefilter_points(fpx_mesh_t m, int64_t n, const double* __restrict__ xo,
                        const int32_t* __restrict__ order, const int2* __restrict__ lr,
                        int32_t* best, int32_t* npass, int32_t* code, int32_t* elem, double* r,
@@ -782,10 +783,12 @@ __global__ void __launch_bounds__(256, 5)  // 48 registers: 40 warps per SM (64 
   int64_t boxtests = 0;
   const int sub = threadIdx.x % kPfLanes;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x / kPfLanes;
-  // whole warps iterate together (the shuffles below need every lane)
-  const int64_t nround = (n + stride - 1) / stride;
-  int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kPfLanes;
-  for (int64_t it = 0; it < nround; ++it, t += stride) {
+  // whole warps iterate together (the shuffles below need every lane): the
+  // loop runs on the warp's first point, the same in all its lanes
+  const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31)) / kPfLanes;
+  const int lp = (threadIdx.x & 31) / kPfLanes;
+  for (int64_t tw = w0; tw < n; tw += stride) {
+    const int64_t t = tw + lp;
     const bool valid = t < n;
     const int64_t k = valid ? order[t] : 0;
     const int2 rng = valid ? lr[t] : make_int2(0, 0);
@@ -797,35 +800,22 @@ __global__ void __launch_bounds__(256, 5)  // 48 registers: 40 warps per SM (64 
     {
       const int s = rng.x, e1 = rng.y;
       if (sub == 0) boxtests += e1 - s;
-      // kPfTrip entries per trip (q, q + kPfLanes, ...): their AABB loads in flight
-      for (int q = s + sub; q < e1; q += kPfTrip * kPfLanes) {
-        int ee[kPfTrip], in[kPfTrip];
-        float B[kPfTrip][FPX_FBOX];
-#pragma unroll
-        for (int h = 0; h < kPfTrip; ++h) {
-          const bool ok = q + h * kPfLanes < e1;
-          ee[h] = ok ? m.elems[q + h * kPfLanes] : -1;
-        }
-#pragma unroll
-        for (int h = 0; h < kPfTrip; ++h) fbox_row<D>(m.fbox, ee[h] < 0 ? ee[0] : ee[h], B[h]);
-#pragma unroll
-        for (int h = 0; h < kPfTrip; ++h) in[h] = ee[h] >= 0 ? fbox_aabb<D>(B[h], xx) : 0;
-#pragma unroll
-        for (int h = 0; h < kPfTrip; ++h) {  // list order
-          if (in[h] == 0) continue;
-          double R[FPX_FREC];
-          if (in[h] == 2) {  // undecided in float: the double box
-            frec_range<D, 0, 2 * D>(m.frec, ee[h], R);
-            if (!aabb_in(D, R, xx)) continue;
-          }
-          if (!obb_stage<D>(m, ee[h], B[h][kFboxMode], xx)) continue;
-          frec_range<D, 3 * D + D * D, 4 * D + 2 * D * D>(m.frec, ee[h], R);
-          ++cnt;
-          const double v = bestfirst_value(D, R + 3 * D + D * D, xx);
-          if (v < bval) {  // strict: ties keep the lower (earlier) id
-            bval = v;
-            bst = ee[h];
-          }
+      // entries q, q + kPfLanes, ...; the next entry's id is loaded before
+      // this one's row, so the list -> row chain overlaps across entries
+      int en = s + sub < e1 ? m.elems[s + sub] : -1;
+      for (int q = s + sub; q < e1; q += kPfLanes) {
+        const int e = en;
+        en = q + kPfLanes < e1 ? m.elems[q + kPfLanes] : -1;
+        float B[FPX_FROW];
+        frow_load<D>(m.fbox, e, B);
+        if (!frow_passes<D>(m, e, B, xx)) continue;
+        double R[FPX_FREC];
+        frec_range<D, 3 * D + D * D, 4 * D + 2 * D * D>(m.frec, e, R);
+        ++cnt;
+        const double v = bestfirst_value(D, R + 3 * D + D * D, xx);
+        if (v < bval) {  // strict: ties keep the lower (earlier) id
+          bval = v;
+          bst = e;
         }
       }
     }
@@ -881,10 +871,9 @@ __global__ void k_filter_records(int d, int64_t E, const double* __restrict__ aa
     for (int t = 0; t < d + d * d; ++t) R[o++] = frame[e * (d + d * d) + t];
     while (o < FPX_FREC - 1) R[o++] = 0.0;
     R[FPX_FREC - 1] = obb_ok[e] ? 1.0 : 0.0;
-    float* B = fbox + e * FPX_FBOX;
-    float* O = fbox + E * FPX_FBOX + e * FPX_FOBB;
-    for (int t = 0; t < FPX_FBOX; ++t) B[t] = 0.0f;
-    for (int t = 0; t < FPX_FOBB; ++t) O[t] = 0.0f;
+    float* B = fbox + e * FPX_FROW;
+    float* O = B + kFrowObb;
+    for (int t = 0; t < FPX_FROW; ++t) B[t] = 0.0f;
     for (int c = 0; c < d; ++c) {
       B[c] = __double2float_rd(aabb[e * 2 * d + c]);
       B[d + c] = __double2float_ru(aabb[e * 2 * d + d + c]);

@@ -136,9 +136,9 @@ def _assemble(S: EngineSetup) -> None:
     m.eps_d_abs = -1.0 if opt.eps_d is None else float(opt.eps_d)
     m.eps_d_rel = float(opt.eps_d_rel)
     # packed candidate-filter records (one 256-byte row per element)
-    # and their float pre-test records (box section, then OBB section)
+    # and their float pre-test rows
     S.frec = torch.empty((E, _C.FREC), dtype=torch.float64, device=dev)
-    S.fbox = torch.empty((_C.FBOX + _C.FOBB) * max(E, 1), dtype=torch.float32, device=dev)
+    S.fbox = torch.empty((max(E, 1), _C.FROW), dtype=torch.float32, device=dev)
     _C.check(_C.lib().fpx_filter_records(
         d, E, _C.ptr(S.aabb), _C.ptr(S.obb_c), _C.ptr(S.obb_inv), _C.ptr(S.obb_ok),
         _C.ptr(S.frame), _C.ptr(S.frec), _C.ptr(S.fbox), _C.stream_handle()),
