@@ -476,9 +476,10 @@ class _SummedStats(Mapping):
         return _C.STATS_LEN
 
 
-_UPLOAD_CHUNKS = 2     # host path: points uploaded in chunks, each filtered as it lands
-_DOWNLOAD_PIECES = 8   # host path: records downloaded in point ranges ...
-_EARLY_PIECES = 4      # ... the first ones under the rest kernels (then patched)
+# host path (tools/e2e_knobs.py, profiles/e2e_knobs_r3.txt)
+_UPLOAD_CHUNKS = 4     # points uploaded in chunks, each filtered as it lands
+_DOWNLOAD_PIECES = 4   # records downloaded in point ranges ...
+_EARLY_PIECES = 2      # ... the first ones under the rest kernels (then patched)
 
 
 def _host_overlapped(S: EngineSetup, f: Field, x: torch.Tensor, out: dict, ws: dict,
@@ -573,7 +574,7 @@ def _host_device_part(S: EngineSetup, f: Field, x: torch.Tensor, out: dict, ws: 
     # early ranges on `dn` (copies only: a kernel there would wait for an SM
     # behind the persistent rest kernels) while the rest runs, the late ones
     # (and the rank column) once the find is complete
-    Pn, Pe = _DOWNLOAD_PIECES, _EARLY_PIECES
+    Pn, Pe = _DOWNLOAD_PIECES, min(_EARLY_PIECES, _DOWNLOAD_PIECES)
     rng = [(n * j // Pn, n * (j + 1) // Pn) for j in range(Pn)]
     dn.wait_event(ev["r1"][0])
     with torch.cuda.stream(dn):

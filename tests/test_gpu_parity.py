@@ -380,12 +380,13 @@ def test_host_pipeline_matches_device(chunks, kind):
     assert out["stats"]["points"] == x.shape[0]
 
 
-@pytest.mark.parametrize("upload,early", [(1, 4), (3, 0), (4, 8)])
-def test_host_pipeline_constants(monkeypatch, upload, early):
+@pytest.mark.parametrize("upload,pieces,early", [(1, 4, 2), (3, 8, 0), (4, 8, 8), (2, 1, 1)])
+def test_host_pipeline_constants(monkeypatch, upload, pieces, early):
     # the overlapped host path under other pipeline shapes: one upload chunk
     # (its single event must still gate the find), no early download range
     # (every range after the find), all ranges early (every record patched)
     monkeypatch.setattr(engine, "_UPLOAD_CHUNKS", upload)
+    monkeypatch.setattr(engine, "_DOWNLOAD_PIECES", pieces)
     monkeypatch.setattr(engine, "_EARLY_PIECES", early)
     mesh, pts = _host_case("hex")
     S = engine.setup(mesh)

@@ -25,10 +25,11 @@ def main():
                r=torch.empty((n, 3), dtype=torch.float64, **pin),
                dist=torch.empty(n, dtype=torch.float64, **pin))
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
-    for up in (1, 2, 4):
-        for early in (3, 4, 5, 6):
+    for up, pieces, early in ((4, 8, 4), (4, 4, 2), (4, 2, 1), (3, 4, 2), (4, 6, 3), (4, 4, 3),
+                              (4, 3, 2), (4, 4, 2)):
+        if True:
             engine._UPLOAD_CHUNKS, engine._EARLY_PIECES = up, early
-            S.__dict__.pop("_host_pipe", None)
+            engine._DOWNLOAD_PIECES = pieces
             ts = []
             for k in range(13):
                 flush.fill_(k)
@@ -37,7 +38,7 @@ def main():
                 engine.find_and_interpolate_host(S, F, x, out=out, sync=True)
                 ts.append((time.perf_counter() - t0) * 1e3)
             ts = sorted(ts[3:])
-            print(f"upload_chunks {up} early_pieces {early}: median {ts[len(ts) // 2]:.3f} ms "
+            print(f"upload_chunks {up} pieces {pieces} early {early}: median {ts[len(ts) // 2]:.3f} ms "
                   f"min {ts[0]:.3f}", flush=True)
 
 
