@@ -770,7 +770,8 @@ __device__ __forceinline__ void write_not_found(int64_t k, int dr, int32_t* code
 // (64: 232, 40 with spills: 225); one 80-byte row 195 (2x2 lanes x trip:
 // 243, 4x1 216, 1x1 231); float OBB arithmetic 187; next entry's id loaded
 // ahead 181; warp-uniform loop bounds (spills 40 -> 8 bytes) 174 (kept;
-// register caps 62: 181, 40: 200, 32: 246).
+// register caps 62: 181, 40: 200, 32: 246).  Points in input order (no
+// cell sort, uniform points): prefilter 256 + scatter 18 against 177 + 55.
 constexpr int kPfLanes = 2;  // lanes per point
 
 template <int D>
