@@ -563,9 +563,10 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
   FPX_CK(cudaMemsetAsync(w.nredo, 0, sizeof(int64_t), st));
   // --- round 1: group by best-first element, Newton, fused eval
   g_launches += 1;  // k_pack_counts (k_stream_scatter counted by FPX_LAUNCH)
+  // in the prefilter's hash-cell order (no sort in hinted mode)
   FPX_LAUNCH(fpx::launch_stream_units(n, E, w.best, w.g1.count, w.g1.packed, w.g1.packed_off,
-                                      w.g1.temp, w.g1.temp_bytes, w.g1.cursor, x, M.d, w.ux,
-                                      w.umeta, st));
+                                      w.g1.temp, w.g1.temp_bytes, w.g1.cursor, x, M.d,
+                                      g_hint ? nullptr : w.order, w.ux, w.umeta, st));
   if (g_prof_start) FPX_CK(cudaEventRecord(g_prof_start, st));
   FPX_CK(cudaMemsetAsync(w.chunk_ctr, 0, sizeof(int64_t), st));
   // candidates held on a face twice in a row stop early and are redone in

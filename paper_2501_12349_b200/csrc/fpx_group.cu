@@ -73,13 +73,24 @@ __global__ void k_scatter_units(int64_t cap, const int64_t* __restrict__ n_dev,
 __global__ void k_stream_scatter(int64_t n, const int32_t* __restrict__ best,
                                  const uint64_t* __restrict__ packed_off,
                                  const int32_t* __restrict__ ecount, const double* __restrict__ x,
-                                 int d, int32_t* cursor, double* ux, int4* umeta) {
-  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
-       k += (int64_t)gridDim.x * blockDim.x) {
+                                 int d, const int32_t* __restrict__ order, int32_t* cursor,
+                                 double* ux, int4* umeta) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    // points in hash-cell order (the prefilter's): neighbouring lanes mostly
+    // share a best element, so their records land in consecutive slots
+    const int64_t k = order ? order[t] : t;
     const int e = best[k];
     if (e < 0) continue;
+    const unsigned act = __activemask();
+    const unsigned peers = __match_any_sync(act, e);
+    const int lane = threadIdx.x % 32;
+    const int leader = __ffs(peers) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(&cursor[e], __popc(peers));
+    base = __shfl_sync(peers, base, leader);
     const int64_t g0 = (int64_t)(packed_off[e] & 0xffffffffull);
-    const int64_t g = g0 + atomicAdd(&cursor[e], 1);
+    const int64_t g = g0 + base + __popc(peers & ((1u << lane) - 1u));
     for (int c = 0; c < d; ++c) ux[g * d + c] = x[k * d + c];
     umeta[g] = make_int4((int)k, e, (int)(g0 + ecount[e]), 0);
   }
@@ -88,7 +99,7 @@ __global__ void k_stream_scatter(int64_t n, const int32_t* __restrict__ best,
 cudaError_t launch_stream_units(int64_t n, int64_t E, const int32_t* best, const int32_t* count,
                                 uint64_t* packed, uint64_t* packed_off, void* scan_temp,
                                 size_t scan_bytes, int32_t* cursor, const double* x, int d,
-                                double* ux, int4* umeta, cudaStream_t st) {
+                                const int32_t* order, double* ux, int4* umeta, cudaStream_t st) {
   cudaError_t e;
   k_pack_counts<<<grid_of(E, 256), 256, 0, st>>>(E, count, packed);
   if ((e = cudaMemsetAsync(packed + E, 0, sizeof(uint64_t), st)) != cudaSuccess) return e;
@@ -97,8 +108,8 @@ cudaError_t launch_stream_units(int64_t n, int64_t E, const int32_t* best, const
       cudaSuccess)
     return e;
   if ((e = cudaMemsetAsync(cursor, 0, sizeof(int32_t) * E, st)) != cudaSuccess) return e;
-  k_stream_scatter<<<grid_of(n, 256), 256, 0, st>>>(n, best, packed_off, count, x, d, cursor, ux,
-                                                    umeta);
+  k_stream_scatter<<<grid_of(n, 256), 256, 0, st>>>(n, best, packed_off, count, x, d, order,
+                                                    cursor, ux, umeta);
   return cudaGetLastError();
 }
 

@@ -81,7 +81,7 @@ bool newton_supported(int d, int dr, int N);
 cudaError_t launch_stream_units(int64_t n, int64_t E, const int32_t* best, const int32_t* count,
                                 uint64_t* packed, uint64_t* packed_off, void* scan_temp,
                                 size_t scan_bytes, int32_t* cursor, const double* x, int d,
-                                double* ux, int4* umeta, cudaStream_t st);
+                                const int32_t* order, double* ux, int4* umeta, cudaStream_t st);
 // Round 1 streamed (k_newton_stream): points in best-first element order as
 // stream records (ux / umeta from launch_stream_units; packed_off[E] = count).
 cudaError_t launch_newton_stream(const fpx_mesh_t& m, int64_t n, const double* ux,
