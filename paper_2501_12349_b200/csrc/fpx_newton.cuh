@@ -1134,73 +1134,83 @@ __device__ __forceinline__ double warp_min_nonneg(double d) {
 // Best-first ranked candidate lists of the rest points: the passing
 // entries of the hash list sorted by (v, e), FPX_RK per point
 // kept; beyond that the rest kernel scans the list itself.
-#define FPX_LISTMAX 256
+#define FPX_LISTMAX 128
+constexpr int kRlLanes = 16;                   // lanes per rest point (lists hold ~9 entries)
+constexpr int kRlGroups = 128 / kRlLanes;      // points per 128-thread block at a time
 template <int D>
 __global__ void __launch_bounds__(128)
     k_rest_lists(fpx_mesh_t m, const double* __restrict__ x, const int64_t* __restrict__ nun_dev,
                  const int32_t* __restrict__ upts, int32_t* best, const int32_t* __restrict__ npass,
                  int32_t* clist, int32_t* cnum, int32_t* nps, int32_t* hist) {
-  // warp per rest point: lanes test the hash-list entries (one filter record
-  // each), (v, e) of the passing ones go to shared memory, and the rank of
-  // each is the number of passing entries before it in (v, e) order
-  __shared__ double s_v[4][FPX_LISTMAX];
-  __shared__ int s_e[4][FPX_LISTMAX];
+  // kRlLanes lanes per rest point: they test the hash-list entries (one
+  // float row each), (v, e) of the passing ones go to shared memory, and the
+  // rank of each is the number of passing entries before it in (v, e) order
+  __shared__ double s_v[kRlGroups][FPX_LISTMAX];
+  __shared__ int s_e[kRlGroups][FPX_LISTMAX];
   __shared__ int s_hist[FPX_HMAX];  // block histogram of the pass counts
-  const int warp = threadIdx.x / FPX_WARP, lane = threadIdx.x % FPX_WARP;
+  const int grp = threadIdx.x / kRlLanes, gl = threadIdx.x % kRlLanes;
   for (int t = threadIdx.x; t < FPX_HMAX; t += blockDim.x) s_hist[t] = 0;
   __syncthreads();
   const int64_t nun = *nun_dev;
-  for (int64_t u = (int64_t)blockIdx.x * 4 + warp; u < nun; u += (int64_t)gridDim.x * 4) {
-    const int64_t k = upts[u];
+  // the loop runs on the block's first point (uniform), so the groups of a
+  // warp stay together for the shuffles; a group past the end idles
+  for (int64_t u0 = (int64_t)blockIdx.x * kRlGroups; u0 < nun;
+       u0 += (int64_t)gridDim.x * kRlGroups) {
+    const int64_t u = u0 + grp;
+    const bool valid = u < nun;
+    const int64_t k = valid ? upts[u] : 0;
     double xs[D];
 #pragma unroll
-    for (int c = 0; c < D; ++c) xs[c] = x[k * D + c];
+    for (int c = 0; c < D; ++c) xs[c] = valid ? x[k * D + c] : 0.0;
     int ax[3];
-    const int64_t cell = cell_of(D, m.grid, m.ncell, xs, ax);
+    const int64_t cell = valid ? cell_of(D, m.grid, m.ncell, xs, ax) : -1;
     const int qs = cell >= 0 ? m.offsets[cell] : 0, qe = cell >= 0 ? m.offsets[cell + 1] : 0;
     const int L = qe - qs < FPX_LISTMAX ? qe - qs : FPX_LISTMAX;
-    for (int q = lane; q < L; q += FPX_WARP) {
+    for (int q = gl; q < L; q += kRlLanes) {
       const int e = m.elems[qs + q];
       double v = INFINITY;
       const bool pass = frec_filter<D>(m, e, xs, &v);
-      s_v[warp][q] = pass ? v : INFINITY;
-      s_e[warp][q] = pass ? e : -1;
+      s_v[grp][q] = pass ? v : INFINITY;
+      s_e[grp][q] = pass ? e : -1;
     }
     __syncwarp();
     // rank 0 is the candidate round 1 solved (the prefilter's choice);
     // the others follow in (v, e) order.  A hinted point (npass < 0) has no
     // rank-0 candidate: all of its passing candidates are ranked from 1.
-    const bool hinted = npass[k] < 0;
-    const int e0 = hinted ? -1 : best[k];
+    const bool hinted = valid && npass[k] < 0;
+    const int e0 = hinted || !valid ? -1 : best[k];
     __syncwarp();
-    if (hinted && lane == 0) best[k] = -1;
+    if (hinted && gl == 0) best[k] = -1;
     int np = 0;
-    for (int q = lane; q < L; q += FPX_WARP) {
-      const int e = s_e[warp][q];
+    for (int q = gl; q < L; q += kRlLanes) {
+      const int e = s_e[grp][q];
       if (e < 0) continue;
       ++np;
-      const double v = s_v[warp][q];
+      const double v = s_v[grp][q];
       int rank = 0;
       if (e != e0) {
         rank = 1;
         for (int j = 0; j < L; ++j) {
-          const int ej = s_e[warp][j];
-          rank += (ej >= 0 && ej != e0 && bf_less(s_v[warp][j], ej, v, e)) ? 1 : 0;
+          const int ej = s_e[grp][j];
+          rank += (ej >= 0 && ej != e0 && bf_less(s_v[grp][j], ej, v, e)) ? 1 : 0;
         }
       }
       if (rank < FPX_RK) clist[u * FPX_RK + rank] = e;
     }
-    for (int o = 16; o > 0; o >>= 1) np += __shfl_xor_sync(FPX_FULL, np, o);
+    for (int o = kRlLanes / 2; o > 0; o >>= 1) np += __shfl_xor_sync(FPX_FULL, np, o);
     // more than FPX_RK passing: the rest kernel scans after the last listed
     // one; lists longer than FPX_LISTMAX: it scans everything after rank 0
-    if (qe - qs > L) {  // list longer than the buffer: count the rest
-      for (int q = qs + L + lane; q < qe; q += FPX_WARP)
-        np += __popc(__ballot_sync(__activemask(), frec_filter<D>(m, m.elems[q], xs, nullptr)));
-      np = __shfl_sync(FPX_FULL, np, 0);
+    const bool over = qe - qs > L;  // list longer than the buffer: count the rest
+    if (__any_sync(FPX_FULL, over)) {
+      int extra = 0;
+      for (int q = qs + L + gl; q < qe; q += kRlLanes)
+        extra += frec_filter<D>(m, m.elems[q], xs, nullptr) ? 1 : 0;
+      for (int o = kRlLanes / 2; o > 0; o >>= 1) extra += __shfl_xor_sync(FPX_FULL, extra, o);
+      np += extra;
     }
-    if (lane == 0) {
+    if (valid && gl == 0) {
       const int npv = np + (hinted ? 1 : 0);  // ranks 0..npv-1 (rank 0 virtual when hinted)
-      cnum[u] = qe - qs > L ? -1 : (npv > FPX_RK ? -FPX_RK : npv);
+      cnum[u] = over ? -1 : (npv > FPX_RK ? -FPX_RK : npv);
       nps[u] = npv;
       atomicAdd(&s_hist[npv < FPX_HMAX - 1 ? npv : FPX_HMAX - 1], 1);
     }
@@ -2458,7 +2468,7 @@ struct Rest {
                            int32_t* cnum, int32_t* nps, int32_t* hist, int32_t* bstart,
                            int32_t* bcur, int32_t* perm, int64_t* cum, int32_t* maxnp,
                            int4* pairs, int64_t* npairs, cudaStream_t st) {
-    int64_t b = (nun_cap + 3) / 4;
+    int64_t b = (nun_cap + kRlGroups - 1) / kRlGroups;
     if (b > 148 * 16) b = 148 * 16;
     if (b < 1) b = 1;
     k_rest_lists<D><<<(unsigned)b, 128, 0, st>>>(m, x, nun_dev, upts, best, npass, clist, cnum,

@@ -451,6 +451,21 @@ def test_filter_pretests_on_decision_surfaces(kind):
     assert {1, 2} <= codes, codes  # both outcomes on the faces of exterior elements
 
 
+@pytest.mark.parametrize("cells", [1, 2])
+def test_long_hash_lists_match_oracle(cells):
+    # a coarse local map: every list holds more entries than the ranking
+    # buffers (FPX_LISTMAX, FPX_RK), so the rest phase takes its overflow
+    # paths (counting past the buffer, scanning the list after the last
+    # ranked candidate); the records must not change
+    m = toolkit.kershaw_mesh(8, 3)   # 512 elements
+    S = engine.setup(m, options=engine.EngineOptions(cells_local=cells))
+    assert S.max_list > (128 if cells == 1 else 16), S.max_list
+    OS = oracle_for(S, m.nodes)
+    x = toolkit.uniform_points(4000, 3, seed=23, lo=-0.05, hi=1.05)
+    rec, _ = assert_find_parity(S, OS, x, toolkit.analytic_field("smooth", m))
+    assert rec.stats["rest_points"] > 0
+
+
 def test_spiral_newton_efficiency_gpu():
     # acceptance 6 on the device: the p=9 spiral element,
     # 10^4 interior points: every solve converges within 50 iterations, mean
