@@ -772,6 +772,8 @@ __device__ __forceinline__ void write_not_found(int64_t k, int dr, int32_t* code
 // ahead 181; warp-uniform loop bounds (spills 40 -> 8 bytes) 174 (kept;
 // register caps 62: 181, 40: 200, 32: 246).  Points in input order (no
 // cell sort, uniform points): prefilter 256 + scatter 18 against 177 + 55.
+// 256-bit loads (LDG.E.ENL2.256) of 96-byte rows and a 32-byte aligned
+// frame: 176 against 176 (the load instruction count is not the bound).
 constexpr int kPfLanes = 2;  // lanes per point
 
 template <int D>
