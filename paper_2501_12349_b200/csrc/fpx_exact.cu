@@ -774,6 +774,9 @@ __device__ __forceinline__ void write_not_found(int64_t k, int dr, int32_t* code
 // cell sort, uniform points): prefilter 256 + scatter 18 against 177 + 55.
 // 256-bit loads (LDG.E.ENL2.256) of 96-byte rows and a 32-byte aligned
 // frame: 176 against 176 (the load instruction count is not the bound).
+// Both lanes of a point on the same entry, each reading half of every row
+// and frame (3 + 3 loads instead of 5 + 6, outcomes exchanged by a
+// pair-masked shuffle): 375 (the per-point chain of entries doubles).
 constexpr int kPfLanes = 2;  // lanes per point
 
 template <int D>
