@@ -492,8 +492,9 @@ def _host_overlapped(S: EngineSetup, f: Field, x: torch.Tensor, out: dict, ws: d
       * after round 1 every record except the ~5% the rest phase revisits
         is final, so the first _EARLY_PIECES of _DOWNLOAD_PIECES point ranges
         of the records go down on a second copy stream under the rest
-        kernels (about what the link moves in that time), the other ranges
-        once the find is complete;
+        kernels (about what the link moves in that time), then the rank
+        column (final after round 1 as well), the other ranges once the find
+        is complete;
       * the early ranges' revisited records are written straight into the
         (pinned, mapped) host arrays by a zero-copy kernel
         (fpx_rest_patch_host) while the late ranges download.
@@ -501,13 +502,13 @@ def _host_overlapped(S: EngineSetup, f: Field, x: torch.Tensor, out: dict, ws: d
     their lines in the CPU caches, and the next call's download into them
     then snoops (measured +2 ms per call)."""
     comp = torch.cuda.current_stream(S.device)
-    up, dn = _streams(S, 2)
+    up, dn, rk = _streams(S, 3)
     n = int(x.shape[0])
     if ws.get("events") is None or len(ws["events"]["up"]) != _UPLOAD_CHUNKS or \
-            len(ws["events"]["dn"]) != _DOWNLOAD_PIECES:
+            len(ws["events"]["dn"]) != _DOWNLOAD_PIECES or "done" not in ws["events"]:
         evs = {k: [torch.cuda.Event() for _ in range(m)] for k, m in
                (("r1", 1), ("start", 1), ("up", _UPLOAD_CHUNKS), ("dn", _DOWNLOAD_PIECES),
-                ("rank", 1))}
+                ("rank", 1), ("done", 1))}
         for lst in evs.values():  # torch creates the CUDA event on first record
             for e in lst:
                 e.record(comp)
@@ -517,18 +518,18 @@ def _host_overlapped(S: EngineSetup, f: Field, x: torch.Tensor, out: dict, ws: d
         tuple(out[k].data_ptr() for k in _REC_KEYS) + \
         tuple(ws[k].data_ptr() for k in ("x", "values", "code", "elem", "r", "dist"))
     if S.options.graphs and ws.get("graph_key") != gkey:
-        _host_device_part(S, f, x, out, ws, up, dn)  # warm-up outside capture
+        _host_device_part(S, f, x, out, ws, up, dn, rk)  # warm-up outside capture
         comp.synchronize()
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g):
-            st = _host_device_part(S, f, x, out, ws, up, dn)
+            st = _host_device_part(S, f, x, out, ws, up, dn, rk)
         ws.update(graph=g, graph_key=gkey, graph_stats=st)
     if S.options.graphs:
         ws["graph"].replay()
         # a snapshot per call: the graph rewrites its counter buffer each replay
         st = DeviceStats(ws["graph_stats"]._t.clone())
     else:
-        st = _host_device_part(S, f, x, out, ws, up, dn)
+        st = _host_device_part(S, f, x, out, ws, up, dn, rk)
     if not sync:
         raise ValueError("the overlapped host path completes on the host (sync=True)")
     comp.synchronize()
@@ -539,7 +540,8 @@ def _host_overlapped(S: EngineSetup, f: Field, x: torch.Tensor, out: dict, ws: d
 _REC_KEYS = ("values", "code", "elem", "r", "dist", "rank")
 
 
-def _host_device_part(S: EngineSetup, f: Field, x: torch.Tensor, out: dict, ws: dict, up, dn):
+def _host_device_part(S: EngineSetup, f: Field, x: torch.Tensor, out: dict, ws: dict, up, dn,
+                      rk):
     """Device work of _host_overlapped (capturable; see there)."""
     L = _C.lib()
     comp = torch.cuda.current_stream(S.device)
@@ -576,6 +578,15 @@ def _host_device_part(S: EngineSetup, f: Field, x: torch.Tensor, out: dict, ws: 
     # (and the rank column) once the find is complete
     Pn, Pe = _DOWNLOAD_PIECES, min(_EARLY_PIECES, _DOWNLOAD_PIECES)
     rng = [(n * j // Pn, n * (j + 1) // Pn) for j in range(Pn)]
+    # the rank column is final after round 1 too: a find without hint only
+    # turns BORDER records into other found records after it, and NOT_FOUND
+    # is the prefilter's (no candidate); its small kernel runs beside the
+    # rest kernels and the column goes down behind the early ranges
+    rk.wait_event(ev["r1"][0])
+    with torch.cuda.stream(rk):
+        torch.where(ws["code"] != NOT_FOUND, torch.zeros_like(ws["elem"]),
+                    torch.full_like(ws["elem"], -1), out=ws["rank"])
+        ev["rank"][0].record(rk)
     dn.wait_event(ev["r1"][0])
     with torch.cuda.stream(dn):
         for j in range(Pe):
@@ -583,16 +594,16 @@ def _host_device_part(S: EngineSetup, f: Field, x: torch.Tensor, out: dict, ws: 
             for k in ("values", "code", "elem", "r", "dist"):
                 out[k][a:b].copy_(ws[k][a:b], non_blocking=True)
             ev["dn"][j].record(dn)
-    torch.where(loc["code"] != NOT_FOUND, torch.zeros_like(loc["elem"]),
-                torch.full_like(loc["elem"], -1), out=ws["rank"])
-    ev["rank"][0].record(comp)
     dn.wait_event(ev["rank"][0])
+    with torch.cuda.stream(dn):
+        out["rank"].copy_(ws["rank"], non_blocking=True)
+    ev["done"][0].record(comp)
+    dn.wait_event(ev["done"][0])
     with torch.cuda.stream(dn):
         for j in range(Pe, Pn):
             a, b = rng[j]
             for k in ("values", "code", "elem", "r", "dist"):
                 out[k][a:b].copy_(ws[k][a:b], non_blocking=True)
-        out["rank"].copy_(ws["rank"], non_blocking=True)
     # the early ranges' rest records, each as soon as its download has landed
     for j in range(Pe):
         a, b = rng[j]

@@ -34,7 +34,7 @@ def main():
     comp = torch.cuda.current_stream()
     mk = lambda m: [torch.cuda.Event(enable_timing=True) for _ in range(m)]  # noqa: E731
     evs = {"r1": mk(1), "start": mk(1), "up": mk(engine._UPLOAD_CHUNKS),
-           "dn": mk(engine._DOWNLOAD_PIECES), "rank": mk(1)}
+           "dn": mk(engine._DOWNLOAD_PIECES), "rank": mk(1), "done": mk(1)}
     for lst in evs.values():
         for e in lst:
             e.record(comp)
@@ -53,6 +53,7 @@ def main():
         row.append(f"r1={s.elapsed_time(evs['r1'][0]):.3f}")
         row += [f"dn{j}={s.elapsed_time(e):.3f}" for j, e in enumerate(evs["dn"][:engine._EARLY_PIECES])]
         row.append(f"rank={s.elapsed_time(evs['rank'][0]):.3f}")
+        row.append(f"done={s.elapsed_time(evs['done'][0]):.3f}")
         row.append(f"end={s.elapsed_time(end):.3f}")
         print(f"wall {wall:.3f} ms | " + " ".join(row), flush=True)
 
