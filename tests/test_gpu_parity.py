@@ -451,6 +451,29 @@ def test_filter_pretests_on_decision_surfaces(kind):
     assert {1, 2} <= codes, codes  # both outcomes on the faces of exterior elements
 
 
+@pytest.mark.parametrize("shift,scale", [(1.0e6, 1.0), (0.0, 1.0e-30), (-3.0e3, 1.0e5)])
+def test_far_and_scaled_meshes_match_oracle(shift, scale):
+    # the float pre-test rows lose their resolution far from the origin or
+    # at extreme scales (every test undecided, the double record decides;
+    # at 1e-30 the float values are subnormal: double only) -- same records
+    from paper_2501_12349_b200.toolkit import MeshData
+    base = toolkit.kershaw_mesh(4, 3)
+    m = MeshData(np.ascontiguousarray(base.nodes * scale + shift), 3, 3, 3)
+    S = engine.setup(m)
+    OS = oracle_for(S, m.nodes)
+    x = toolkit.uniform_points(3000, 3, seed=29, lo=-0.05, hi=1.05) * scale + shift
+    rec = engine.find(S, x)
+    orec = OS.find(x)
+    code, elem = rec.code.cpu().numpy(), rec.elem.cpu().numpy()
+    # the filter decides the candidate sets: codes identical, and the owner
+    # of every point away from a face (the absolute r*/d* tolerances of
+    # check_records assume O(1) coordinates)
+    assert np.array_equal(code, orec["code"])
+    inner = (code == 0) & np.all(np.abs(orec["r"]) < 1.0 - 1e-6, axis=1)
+    assert inner.sum() > 1000
+    assert np.array_equal(elem[inner], orec["elem"][inner])
+
+
 @pytest.mark.parametrize("cells", [1, 2])
 def test_long_hash_lists_match_oracle(cells):
     # a coarse local map: every list holds more entries than the ranking
