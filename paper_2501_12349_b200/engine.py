@@ -581,7 +581,9 @@ def _host_device_part(S: EngineSetup, f: Field, x: torch.Tensor, out: dict, ws: 
     # the rank column is final after round 1 too: a find without hint only
     # turns BORDER records into other found records after it, and NOT_FOUND
     # is the prefilter's (no candidate); its small kernel runs beside the
-    # rest kernels and the column goes down behind the early ranges
+    # rest kernels (which may rewrite a rest point's code meanwhile: from one
+    # found code to another, the same rank either way) and the column goes
+    # down behind the early ranges
     rk.wait_event(ev["r1"][0])
     with torch.cuda.stream(rk):
         torch.where(ws["code"] != NOT_FOUND, torch.zeros_like(ws["elem"]),
