@@ -257,10 +257,13 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    local = local % max(torch.cuda.device_count(), 1) if args.backend == "gloo" else local
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     group = None
-    if world > 1:
+    if world > 1 and args.backend == "gloo":
+        dist.init_process_group("gloo")
+    elif world > 1:
         dist.init_process_group("nccl", device_id=dev)
         group = transport.RankGroup.from_torch()
     mesh, field, x_host = build_inputs(rank)
@@ -288,7 +291,7 @@ def run_ours(args):
     def max_over_ranks(v):
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        t = torch.tensor([v], dtype=torch.float64, device=dev if args.backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t)
 
@@ -419,6 +422,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-sample", type=int, default=50000)
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process group for N > 1 (gloo: several ranks sharing one GPU, "
+                         "a check of the multi-rank path, not a measurement)")
     ap.add_argument("--workload", default="cfg2", choices=sorted(WORKLOADS),
                     help="cfg2 = the BASELINE headline (default); cfg3 / cfg4 = the other "
                          "BASELINE configs that fit one GPU")
