@@ -777,7 +777,8 @@ __device__ __forceinline__ void write_not_found(int64_t k, int dr, int32_t* code
 // Both lanes of a point on the same entry, each reading half of every row
 // and frame (3 + 3 loads instead of 5 + 6, outcomes exchanged by a
 // pair-masked shuffle): 375 (the per-point chain of entries doubles).
-// The next point's header loaded ahead: 190 (spills at 48 registers).
+// The next point's header loaded ahead: 190 (spills at 48 registers); the
+// next entry's row loaded ahead: 290 (48 registers) / 225 (64).
 constexpr int kPfLanes = 2;  // lanes per point
 
 template <int D>
