@@ -1145,6 +1145,7 @@ __global__ void __launch_bounds__(128)
   // kRlLanes lanes per rest point: they test the hash-list entries (one
   // float row each), (v, e) of the passing ones go to shared memory, and the
   // rank of each is the number of passing entries before it in (v, e) order
+  // (v: rest_rank_value, fpx_boxes.cuh)
   __shared__ double s_v[kRlGroups][FPX_LISTMAX];
   __shared__ int s_e[kRlGroups][FPX_LISTMAX];
   __shared__ int s_hist[FPX_HMAX];  // block histogram of the pass counts
@@ -1169,14 +1170,15 @@ __global__ void __launch_bounds__(128)
     for (int q = gl; q < L; q += kRlLanes) {
       const int e = m.elems[qs + q];
       double v = INFINITY;
-      const bool pass = frec_filter<D>(m, e, xs, &v);
+      const bool pass = frec_filter_rest<D>(m, e, xs, &v);
       s_v[grp][q] = pass ? v : INFINITY;
       s_e[grp][q] = pass ? e : -1;
     }
     __syncwarp();
     // rank 0 is the candidate round 1 solved (the prefilter's choice);
-    // the others follow in (v, e) order.  A hinted point (npass < 0) has no
-    // rank-0 candidate: all of its passing candidates are ranked from 1.
+    // the others follow in (v, e) order of the rest rank value.  A hinted
+    // point (npass < 0) has no rank-0 candidate: all of its passing
+    // candidates are ranked from 1.
     const bool hinted = valid && npass[k] < 0;
     const int e0 = hinted || !valid ? -1 : best[k];
     __syncwarp();
@@ -1490,11 +1492,7 @@ __global__ void __launch_bounds__(128, 2)
         const bool all = cn == -1;
         const int te = all ? best[k] : clist[u * FPX_RK + nlist - 1];
         double tv = -INFINITY;  // te < 0: a hinted point, nothing listed before
-        if (te >= 0) {
-          double R[FPX_FREC];
-          frec_range<D, 3 * D + D * D, 4 * D + 2 * D * D>(m.frec, te, R);
-          tv = bestfirst_value(D, R + 3 * D + D * D, xs);
-        }
+        if (te >= 0) tv = rest_rank_of<D>(m, te, xs);
         int ax[3];
         const int64_t cell = cell_of(D, m.grid, m.ncell, xs, ax);
         int want = rank - nlist;
@@ -1502,7 +1500,7 @@ __global__ void __launch_bounds__(128, 2)
           const int ee = m.elems[q];
           if (ee == best[k]) continue;  // round 1's candidate (rank 0)
           double ve = 0.0;
-          if (!frec_filter<D>(m, ee, xs, &ve)) continue;
+          if (!frec_filter_rest<D>(m, ee, xs, &ve)) continue;
           if (!all && !bf_less(tv, te, ve, ee)) continue;
           if (want-- == 0) {
             en = ee;
