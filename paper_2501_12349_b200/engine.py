@@ -479,7 +479,7 @@ class _SummedStats(Mapping):
 # host path (tools/e2e_knobs.py, profiles/e2e_knobs_r3.txt)
 _UPLOAD_CHUNKS = 4     # points uploaded in chunks, each filtered as it lands
 _DOWNLOAD_PIECES = 4   # records downloaded in point ranges ...
-_EARLY_PIECES = 2      # ... the first ones under the rest kernels (then patched)
+_EARLY_PIECES = 1      # ... the first ones under the rest kernels (then patched)
 
 
 def _host_overlapped(S: EngineSetup, f: Field, x: torch.Tensor, out: dict, ws: dict,
