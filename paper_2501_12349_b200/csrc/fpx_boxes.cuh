@@ -91,6 +91,21 @@ __device__ __forceinline__ void frec_range(const double* __restrict__ frec, int6
   }
 }
 
+// |inv (x - cen)|_inf with the OBB test's terms (rest ranking, prefilter).
+__device__ __forceinline__ double obb_norm(int d, const double* __restrict__ cen,
+                                           const double* __restrict__ inv, const double* x) {
+  double dx[3];
+  for (int c = 0; c < d; ++c) dx[c] = __dsub_rn(x[c], cen[c]);
+  double v = 0.0;
+  for (int c = 0; c < d; ++c) {
+    double y = 0.0;
+    for (int b = 0; b < d; ++b) y = __dadd_rn(y, __dmul_rn(inv[c * d + b], dx[b]));
+    v = fabs(y) > v ? fabs(y) : v;
+  }
+  return v;
+}
+
+
 // ---- float pre-tests (include/fpx.h, mesh.fbox) -------------------------
 // Outcome 0 = the double test fails, 1 = it passes, 2 = undecided here (the
 // double record decides).  Either way the filter's outcome is the double
@@ -129,8 +144,8 @@ __device__ __forceinline__ int fbox_aabb(const float* b, const double* x) {
 // the sum (5x slack, covering its own rounding and that of the compares)
 // plus 2^-40.  NaN / inf (x beyond float range) -> 2.
 template <int D>
-__device__ __forceinline__ int fobb_in(const float* o, const double* x) {
-  float dx[D], ab[D];
+__device__ __forceinline__ int fobb_in(const float* o, const double* x, float* ymax = nullptr) {
+  float dx[D], ab[D], ym = 0.0f;
 #pragma unroll
   for (int b = 0; b < D; ++b) {
     const float xf = __double2float_rn(x[b]);
@@ -151,7 +166,9 @@ __device__ __forceinline__ int fobb_in(const float* o, const double* x) {
     const float ay = fabsf(y);
     if (ay - bnd > 1.0f) return 0;
     if (!(ay + bnd < 1.0f)) res = 2;
+    ym = ay > ym ? ay : ym;
   }
+  if (ymax) *ymax = ym;
   return res;
 }
 
@@ -167,13 +184,17 @@ __device__ __forceinline__ void frow_load(const float* __restrict__ fbox, int64_
 }
 
 // AABB and OBB tests of candidate e from its loaded row (the double record
-// only where a pre-test is undecided).
+// only where a pre-test is undecided).  yn (optional): the OBB norm
+// |obb_inv (x - obb_c)|_inf of a passing candidate, from the float
+// pre-test (mode 1) or the double record (mode 2), 0 without an OBB
+// (mode 0): a term of the prefilter's ranking (k_prefilter_points).
 template <int D>
 __device__ __forceinline__ bool frow_passes(const fpx_mesh_t& m, int64_t e, const float* b,
-                                            const double* x) {
+                                            const double* x, float* yn = nullptr) {
   const float mode = b[kFboxMode];
   const int a = fbox_aabb<D>(b, x);
-  const int o = mode == 0.0f ? 1 : (mode == 1.0f ? fobb_in<D>(b + kFrowObb, x) : 2);
+  float ym = 0.0f;
+  const int o = mode == 0.0f ? 1 : (mode == 1.0f ? fobb_in<D>(b + kFrowObb, x, &ym) : 2);
   if (a == 0 || o == 0) return false;
   double R[FPX_FREC];
   if (a == 2) {
@@ -183,7 +204,9 @@ __device__ __forceinline__ bool frow_passes(const fpx_mesh_t& m, int64_t e, cons
   if (o == 2) {
     frec_range<D, 2 * D, 3 * D + D * D>(m.frec, e, R);
     if (!obb_in(D, R + 2 * D, R + 3 * D, x)) return false;
+    if (mode != 1.0f) ym = (float)obb_norm(D, R + 2 * D, R + 3 * D, x);
   }
+  if (yn) *yn = ym;
   return true;
 }
 
@@ -212,19 +235,6 @@ __device__ __forceinline__ bool frec_filter(const fpx_mesh_t& m, int64_t e, cons
 // record is found: a point is INTERIOR in at most one element of a
 // conforming mesh, and a BORDER point's record is the D6 minimum over all
 // of its candidates.
-__device__ __forceinline__ double obb_norm(int d, const double* __restrict__ cen,
-                                           const double* __restrict__ inv, const double* x) {
-  double dx[3];
-  for (int c = 0; c < d; ++c) dx[c] = __dsub_rn(x[c], cen[c]);
-  double v = 0.0;
-  for (int c = 0; c < d; ++c) {
-    double y = 0.0;
-    for (int b = 0; b < d; ++b) y = __dadd_rn(y, __dmul_rn(inv[c * d + b], dx[b]));
-    v = fabs(y) > v ? fabs(y) : v;
-  }
-  return v;
-}
-
 template <int D>
 __device__ __forceinline__ double rest_rank_value(const fpx_mesh_t& m, int64_t e, float mode,
                                                   const double* x) {

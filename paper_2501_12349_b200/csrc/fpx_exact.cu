@@ -789,6 +789,7 @@ __global__ void __launch_bounds__(256, 5)  // 48 registers: 40 warps per SM
                        double* dist, int32_t* iters, double* values, int C, int32_t* elem_count,
                        int64_t* stats) {
   int64_t boxtests = 0;
+  const bool vol = m.dr == D;
   const int sub = threadIdx.x % kPfLanes;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x / kPfLanes;
   // whole warps iterate together (the shuffles below need every lane): the
@@ -816,11 +817,15 @@ __global__ void __launch_bounds__(256, 5)  // 48 registers: 40 warps per SM
         en = q + kPfLanes < e1 ? m.elems[q + kPfLanes] : -1;
         float B[FPX_FROW];
         frow_load<D>(m.fbox, e, B);
-        if (!frow_passes<D>(m, e, B, xx)) continue;
+        float yn = 0.0f;
+        if (!frow_passes<D>(m, e, B, xx, &yn)) continue;
         double R[FPX_FREC];
         frec_range<D, 3 * D + D * D, 4 * D + 2 * D * D>(m.frec, e, R);
         ++cnt;
-        const double v = bestfirst_value(D, R + 3 * D + D * D, xx);
+        // round 1's candidate: the smallest affine best-first value plus, for
+        // volume meshes, the OBB norm (cfg-2 sample: 4.3% of the points
+        // left for the rest phase against 5.1% with the affine value alone)
+        const double v = bestfirst_value(D, R + 3 * D + D * D, xx) + (vol ? (double)yn : 0.0);
         if (v < bval) {  // strict: ties keep the lower (earlier) id
           bval = v;
           bst = e;
