@@ -159,6 +159,16 @@ int fpx_set_find_hint(const int32_t* elem);
  * the one event before it starts).  k <= 0 or NULL clears. */
 int fpx_set_upload_events(int k, void* const* events);
 
+/* (ABI 7) With upload events for k chunks set, the next fpx_find calls on
+ * this thread also group and solve round 1 per chunk, right after the
+ * chunk is filtered, and record events[c] (cudaEvent_t) on their stream when
+ * chunk c's round 1 is done: from then on the records of points
+ * [n*c/k, n*(c+1)/k) are final except those of the rest points (revisited
+ * after the last chunk; fpx_rest_patch_host).  k must equal the upload
+ * chunk count to take effect; k <= 0 or NULL clears.  The records are
+ * those of a find without it. */
+int fpx_set_round1_events(int k, void* const* events);
+
 /* After a host-mode fpx_find (fpx_set_round1_event set; same stream, same
  * workspace, same n): writes the records of the points in [k0, k1) that the
  * rest phase settled straight into host record arrays (pinned, mapped;

@@ -78,6 +78,7 @@ def lib():
         "fpx_rest_patch_host": ([i32, i32, i64, i64, i64, P, C.c_size_t, C.POINTER(MeshT), P, P,
                                  P, P, P, P, P, P, P, P, P], i32),
         "fpx_set_upload_events": ([i32, P], i32),
+        "fpx_set_round1_events": ([i32, P], i32),
         "fpx_set_find_hint": ([P], i32),
         "fpx_particles_advance": ([i32, i64, P, P, P, P, P, f64, f64, i32, P, i32, P], i32),
         "fpx_bound_function": ([i32, i32, i32, i64, P, P, P, P, P], i32),
@@ -106,6 +107,7 @@ def exported_symbols():
     return ["fpx_abi_version", "fpx_last_error", "fpx_launch_count", "fpx_profile_round1",
             "fpx_probe_fp64", "fpx_supported", "fpx_setup_bounds", "fpx_filter_records", "fpx_pad_nodes",
             "fpx_particles_advance", "fpx_set_round1_event", "fpx_rest_patch_host", "fpx_set_upload_events",
+            "fpx_set_round1_events",
             "fpx_set_find_hint",
             "fpx_bound_function", "fpx_hash_workspace_bytes", "fpx_hash_build", "fpx_cell_of",
             "fpx_find_workspace_bytes", "fpx_find", "fpx_eval_workspace_bytes",

@@ -39,9 +39,12 @@ thread_local cudaEvent_t g_round1_done = nullptr;
 // fpx_set_upload_events: the points arrive in k chunks, chunk c ready at ev[c]
 constexpr int kMaxUpload = 16;
 thread_local int g_upload_k = 0;
+// fpx_set_round1_events: round 1 per upload chunk, chunk c's done at ev[c]
+thread_local int g_r1_k = 0;
 // fpx_set_find_hint: per point a hinted element for the next fpx_find
 thread_local const int32_t* g_hint = nullptr;
 thread_local cudaEvent_t g_upload_ev[kMaxUpload];
+thread_local cudaEvent_t g_r1_ev[kMaxUpload];
 
 // Layout of every find workspace at its last fpx_find (points, elements):
 // fpx_rest_patch_host re-carves the workspace and must see the same layout.
@@ -280,6 +283,17 @@ int fpx_profile_round1(void* ev_start, void* ev_stop) {
 
 int fpx_set_round1_event(void* ev) {
   g_round1_done = reinterpret_cast<cudaEvent_t>(ev);
+  return FPX_OK;
+}
+
+int fpx_set_round1_events(int k, void* const* events) {
+  if (k <= 0 || !events) {
+    g_r1_k = 0;
+    return FPX_OK;
+  }
+  if (k > kMaxUpload) return fail(FPX_EINVAL, "round-1 events: k=%d > %d", k, kMaxUpload);
+  for (int c = 0; c < k; ++c) g_r1_ev[c] = reinterpret_cast<cudaEvent_t>(events[c]);
+  g_r1_k = k;
   return FPX_OK;
 }
 
@@ -528,6 +542,13 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
   const int64_t nc = w.ncells;
   FPX_CK(cudaMemsetAsync(w.g1.count, 0, sizeof(int32_t) * E, st));
   const int nchunk = g_hint ? 0 : (g_upload_k > 1 ? g_upload_k : 1);
+  // round 1 per chunk (host mode, fpx_set_round1_events): each chunk is
+  // grouped and solved as soon as it is filtered, so its records can go
+  // down while the next chunks are uploaded and solved; one rest phase
+  const bool r1_chunks = !g_hint && g_r1_k > 0 && g_r1_k == nchunk;
+  FPX_CK(cudaMemsetAsync(w.nun, 0, sizeof(int64_t), st));
+  FPX_CK(cudaMemsetAsync(w.counter, 0, 2 * sizeof(int64_t), st));
+  FPX_CK(cudaMemsetAsync(w.nredo, 0, sizeof(int64_t), st));
   if (g_hint) {  // hinted find (particles): round 1 on the hinted elements, no prefilter
     for (int ck = 0; ck < g_upload_k; ++ck) FPX_CK(cudaStreamWaitEvent(st, g_upload_ev[ck], 0));
     g_launches += 1;
@@ -539,6 +560,7 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
     if (g_upload_k > 0) FPX_CK(cudaStreamWaitEvent(st, g_upload_ev[ck], 0));  // nchunk == k
     if (nn == 0) continue;
     const double* xa = x + a * M.d;
+    if (r1_chunks && ck > 0) FPX_CK(cudaMemsetAsync(w.g1.count, 0, sizeof(int32_t) * E, st));
     FPX_CK(cudaMemsetAsync(w.cell_count, 0, sizeof(int32_t) * (nc + 2), st));
     FPX_LAUNCH(fpx::launch_point_cells(M, nn, xa, w.cellid + a, w.cell_count, st));
     {
@@ -557,27 +579,39 @@ int fpx_find(const fpx_mesh_t* m, int64_t n, const double* x, int32_t* code, int
                                      reinterpret_cast<const int2*>(w.clist) + a, w.best,
                                      w.npass, code, elem, r, dist, iters,
                                      field ? values : nullptr, C, w.g1.count, stats, st));
+    if (r1_chunks) {  // the chunk's round 1: its stream records in its own range
+      g_launches += 1;
+      FPX_LAUNCH(fpx::launch_stream_units(nn, E, w.best, w.g1.count, w.g1.packed,
+                                          w.g1.packed_off, w.g1.temp, w.g1.temp_bytes,
+                                          w.g1.cursor, x, M.d, w.order + a, w.ux + a * M.d,
+                                          w.umeta + a, st));
+      FPX_CK(cudaMemsetAsync(w.chunk_ctr, 0, sizeof(int64_t), st));
+      FPX_LAUNCH(fpx::launch_newton_stream(M, nn, w.ux + a * M.d, w.umeta + a, w.g1.packed_off,
+                                           w.npass, code, elem, r, dist, iters, field, C, values,
+                                           w.upts, w.nun, w.chunk_ctr, w.redo, w.nredo,
+                                           2 * n + 1024, stats, st));
+      FPX_CK(cudaEventRecord(g_r1_ev[ck], st));
+    }
   }
-  FPX_CK(cudaMemsetAsync(w.nun, 0, sizeof(int64_t), st));
-  FPX_CK(cudaMemsetAsync(w.counter, 0, 2 * sizeof(int64_t), st));
-  FPX_CK(cudaMemsetAsync(w.nredo, 0, sizeof(int64_t), st));
-  // --- round 1: group by best-first element, Newton, fused eval
-  g_launches += 1;  // k_pack_counts (k_stream_scatter counted by FPX_LAUNCH)
-  // in the prefilter's hash-cell order (no sort in hinted mode)
-  FPX_LAUNCH(fpx::launch_stream_units(n, E, w.best, w.g1.count, w.g1.packed, w.g1.packed_off,
-                                      w.g1.temp, w.g1.temp_bytes, w.g1.cursor, x, M.d,
-                                      g_hint ? nullptr : w.order, w.ux, w.umeta, st));
-  if (g_prof_start) FPX_CK(cudaEventRecord(g_prof_start, st));
-  FPX_CK(cudaMemsetAsync(w.chunk_ctr, 0, sizeof(int64_t), st));
-  // candidates held on a face twice in a row stop early and are redone in
-  // full only if their point ends without an INTERIOR (see k_rest_l1)
-  // (hinted: no abort rule / redo entries in round 1 -- the hinted element
-  // may not be a candidate; non-INTERIOR points go to the rest phase whole)
-  FPX_LAUNCH(fpx::launch_newton_stream(M, n, w.ux, w.umeta, w.g1.packed_off, w.npass, code,
-                                       elem, r, dist, iters, field, C, values, w.upts, w.nun,
-                                       w.chunk_ctr, g_hint ? nullptr : w.redo, w.nredo,
-                                       2 * n + 1024, stats, st));
-  if (g_prof_stop) FPX_CK(cudaEventRecord(g_prof_stop, st));
+  if (!r1_chunks) {
+    // --- round 1: group by best-first element, Newton, fused eval
+    g_launches += 1;  // k_pack_counts (k_stream_scatter counted by FPX_LAUNCH)
+    // in the prefilter's hash-cell order (no sort in hinted mode)
+    FPX_LAUNCH(fpx::launch_stream_units(n, E, w.best, w.g1.count, w.g1.packed, w.g1.packed_off,
+                                        w.g1.temp, w.g1.temp_bytes, w.g1.cursor, x, M.d,
+                                        g_hint ? nullptr : w.order, w.ux, w.umeta, st));
+    if (g_prof_start) FPX_CK(cudaEventRecord(g_prof_start, st));
+    FPX_CK(cudaMemsetAsync(w.chunk_ctr, 0, sizeof(int64_t), st));
+    // candidates held on a face twice in a row stop early and are redone in
+    // full only if their point ends without an INTERIOR (see k_rest_l1)
+    // (hinted: no abort rule / redo entries in round 1 -- the hinted element
+    // may not be a candidate; non-INTERIOR points go to the rest phase whole)
+    FPX_LAUNCH(fpx::launch_newton_stream(M, n, w.ux, w.umeta, w.g1.packed_off, w.npass, code,
+                                         elem, r, dist, iters, field, C, values, w.upts, w.nun,
+                                         w.chunk_ctr, g_hint ? nullptr : w.redo, w.nredo,
+                                         2 * n + 1024, stats, st));
+    if (g_prof_stop) FPX_CK(cudaEventRecord(g_prof_stop, st));
+  }
   // external record: also a real event node when captured into a CUDA graph
   if (g_round1_done) FPX_CK(cudaEventRecord(g_round1_done, st));
   // --- rest: remaining candidates of the unresolved points

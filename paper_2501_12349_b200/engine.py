@@ -480,6 +480,10 @@ class _SummedStats(Mapping):
 _UPLOAD_CHUNKS = 4     # points uploaded in chunks, each filtered as it lands
 _DOWNLOAD_PIECES = 4   # records downloaded in point ranges ...
 _EARLY_PIECES = 1      # ... the first ones under the rest kernels (then patched)
+_R1_PER_CHUNK = False  # round 1 per upload chunk (fpx_set_round1_events): each
+                       # chunk's records go down as soon as it is solved; off:
+                       # a round 1 on a quarter of the points takes 0.33 ms
+                       # against 0.59 for all of them (e2e 2.4-3.0 ms against 2.36)
 
 
 def _host_overlapped(S: EngineSetup, f: Field, x: torch.Tensor, out: dict, ws: dict,
@@ -504,17 +508,18 @@ def _host_overlapped(S: EngineSetup, f: Field, x: torch.Tensor, out: dict, ws: d
     comp = torch.cuda.current_stream(S.device)
     up, dn, rk = _streams(S, 3)
     n = int(x.shape[0])
+    npieces = _UPLOAD_CHUNKS if _R1_PER_CHUNK else _DOWNLOAD_PIECES
     if ws.get("events") is None or len(ws["events"]["up"]) != _UPLOAD_CHUNKS or \
-            len(ws["events"]["dn"]) != _DOWNLOAD_PIECES or "done" not in ws["events"]:
+            len(ws["events"]["dn"]) != npieces or "r1c" not in ws["events"]:
         evs = {k: [torch.cuda.Event() for _ in range(m)] for k, m in
-               (("r1", 1), ("start", 1), ("up", _UPLOAD_CHUNKS), ("dn", _DOWNLOAD_PIECES),
-                ("rank", 1), ("done", 1))}
+               (("r1", 1), ("start", 1), ("up", _UPLOAD_CHUNKS), ("dn", npieces),
+                ("rank", 1), ("done", 1), ("r1c", _UPLOAD_CHUNKS))}
         for lst in evs.values():  # torch creates the CUDA event on first record
             for e in lst:
                 e.record(comp)
         ws["events"] = evs
     gkey = (n, x.data_ptr(), f.blocks.data_ptr(), f.components, _UPLOAD_CHUNKS,
-            _DOWNLOAD_PIECES, _EARLY_PIECES) + \
+            _DOWNLOAD_PIECES, _EARLY_PIECES, _R1_PER_CHUNK) + \
         tuple(out[k].data_ptr() for k in _REC_KEYS) + \
         tuple(ws[k].data_ptr() for k in ("x", "values", "code", "elem", "r", "dist"))
     if S.options.graphs and ws.get("graph_key") != gkey:
@@ -566,12 +571,19 @@ def _host_device_part(S: EngineSetup, f: Field, x: torch.Tensor, out: dict, ws: 
             ev["up"][c].record(up)
     handles = (ctypes.c_void_p * K)(*[e.cuda_event for e in ev["up"]])
     L.fpx_set_upload_events(K, ctypes.cast(handles, ctypes.c_void_p))
+    if _R1_PER_CHUNK:
+        r1h = (ctypes.c_void_p * K)(*[e.cuda_event for e in ev["r1c"]])
+        L.fpx_set_round1_events(K, ctypes.cast(r1h, ctypes.c_void_p))
     L.fpx_set_round1_event(ev["r1"][0].cuda_event)
     try:
         st = _find_into(S, ws["x"], loc, f, ws=wsf)
     finally:
         L.fpx_set_round1_event(None)
+        L.fpx_set_round1_events(0, None)
         L.fpx_set_upload_events(0, None)
+    if _R1_PER_CHUNK:
+        _host_downloads_per_chunk(S, f, out, ws, wsf, n, K, comp, dn, rk)
+        return st
     # after round 1 every record but the rest points' is final: download the
     # early ranges on `dn` (copies only: a kernel there would wait for an SM
     # behind the persistent rest kernels) while the rest runs, the late ones
@@ -619,6 +631,44 @@ def _host_device_part(S: EngineSetup, f: Field, x: torch.Tensor, out: dict, ws: 
                  "fpx_rest_patch_host")
     comp.wait_stream(dn)
     return st
+
+
+def _host_downloads_per_chunk(S, f, out, ws, wsf, n, K, comp, dn, rk):
+    """Downloads of the per-chunk pipeline (_R1_PER_CHUNK): chunk c's point
+    range goes down as soon as its round 1 is done (under the next chunks'
+    work), the rank column once every round 1 is, and each range's rest
+    records are patched in (fpx_rest_patch_host) after the rest phase."""
+    L = _C.lib()
+    ev = ws["events"]
+    dr, C = S.ref_dim, f.components
+    rng = [(n * c // K, n * (c + 1) // K) for c in range(K)]
+    for c in range(K):
+        a, b = rng[c]
+        dn.wait_event(ev["r1c"][c])
+        with torch.cuda.stream(dn):
+            for k in ("values", "code", "elem", "r", "dist"):
+                out[k][a:b].copy_(ws[k][a:b], non_blocking=True)
+            ev["dn"][c].record(dn)
+    # the rank column is final after round 1 (see _host_device_part)
+    rk.wait_event(ev["r1"][0])
+    with torch.cuda.stream(rk):
+        torch.where(ws["code"] != NOT_FOUND, torch.zeros_like(ws["elem"]),
+                    torch.full_like(ws["elem"], -1), out=ws["rank"])
+        ev["rank"][0].record(rk)
+    dn.wait_event(ev["rank"][0])
+    with torch.cuda.stream(dn):
+        out["rank"].copy_(ws["rank"], non_blocking=True)
+    for c in range(K):
+        a, b = rng[c]
+        comp.wait_event(ev["dn"][c])
+        _C.check(L.fpx_rest_patch_host(dr, C, n, a, b, _C.ptr(wsf), wsf.numel(), S.mesh_t,
+                                       _C.ptr(ws["code"]), _C.ptr(ws["elem"]), _C.ptr(ws["r"]),
+                                       _C.ptr(ws["dist"]), _C.ptr(ws["values"]),
+                                       out["code"].data_ptr(), out["elem"].data_ptr(),
+                                       out["r"].data_ptr(), out["dist"].data_ptr(),
+                                       out["values"].data_ptr(), _C.stream_handle()),
+                 "fpx_rest_patch_host")
+    comp.wait_stream(dn)
 
 
 def _streams(S: EngineSetup, k: int) -> list:

@@ -380,11 +380,16 @@ def test_host_pipeline_matches_device(chunks, kind):
     assert out["stats"]["points"] == x.shape[0]
 
 
-@pytest.mark.parametrize("upload,pieces,early", [(1, 4, 2), (3, 8, 0), (4, 8, 8), (2, 1, 1)])
-def test_host_pipeline_constants(monkeypatch, upload, pieces, early):
+@pytest.mark.parametrize("upload,pieces,early,r1c", [
+    (1, 4, 2, False), (3, 8, 0, False), (4, 8, 8, False), (2, 1, 1, False),
+    (1, 4, 1, True), (3, 4, 1, True), (5, 4, 1, True)])
+def test_host_pipeline_constants(monkeypatch, upload, pieces, early, r1c):
     # the overlapped host path under other pipeline shapes: one upload chunk
     # (its single event must still gate the find), no early download range
-    # (every range after the find), all ranges early (every record patched)
+    # (every range after the find), all ranges early (every record patched);
+    # and round 1 per upload chunk with the chunk's records downloaded as
+    # soon as it is solved (r1c)
+    monkeypatch.setattr(engine, "_R1_PER_CHUNK", r1c)
     monkeypatch.setattr(engine, "_UPLOAD_CHUNKS", upload)
     monkeypatch.setattr(engine, "_DOWNLOAD_PIECES", pieces)
     monkeypatch.setattr(engine, "_EARLY_PIECES", early)
