@@ -231,10 +231,10 @@ __device__ __forceinline__ bool frec_filter(const fpx_mesh_t& m, int64_t e, cons
 // element has an OBB (row mode != 0), else its best-first value.  Measured
 // on cfg-2, the point's owner is the first of its remaining candidates in
 // this order for 87% of the rest points (53% in best-first order; mean rank
-// 1.18 against 2.46; tools/rank_study.py).  The order decides only how soon a point's INTERIOR
-// record is found: a point is INTERIOR in at most one element of a
-// conforming mesh, and a BORDER point's record is the D6 minimum over all
-// of its candidates.
+// 1.18 against 2.46; tests/rank_study.py).  The order decides only how
+// soon a point's INTERIOR record is found: a point is INTERIOR in at most
+// one element of a conforming mesh, and a BORDER point's record is the D6
+// minimum over all of its candidates.
 template <int D>
 __device__ __forceinline__ double rest_rank_value(const fpx_mesh_t& m, int64_t e, float mode,
                                                   const double* x) {

@@ -825,7 +825,7 @@ __global__ void __launch_bounds__(256, 5)  // 48 registers: 40 warps per SM
         // round 1's candidate: the smallest affine best-first value plus, for
         // volume meshes, the OBB norm (cfg-2 sample: 4.3% of the points
         // left for the rest phase against 5.1% with the affine value alone;
-        // tools/rank_study.py)
+        // tests/rank_study.py)
         const double v = bestfirst_value(D, R + 3 * D + D * D, xx) + (vol ? (double)yn : 0.0);
         if (v < bval) {  // strict: ties keep the lower (earlier) id
           bval = v;

@@ -3,7 +3,10 @@ map): how often each ranking puts a point's owner first -- for round 1's
 pick among all passing candidates, and for the rest phase's order among the
 remaining ones.  Records do not depend on either order.
 
-    python tools/rank_study.py [npoints] > profiles/rank_study_r3.txt"""
+    python tests/rank_study.py [npoints] > profiles/rank_study_r3.txt
+
+Test infrastructure (it runs the oracle); test_rank_study.py checks the
+same facts on a smaller sample."""
 import os
 import sys
 
@@ -14,9 +17,8 @@ from oracle import oracle as O  # noqa: E402  (test infrastructure: the checker'
 from paper_2501_12349_b200 import toolkit  # noqa: E402
 
 
-def main():
-    npts = int(sys.argv[1]) if len(sys.argv) > 1 else 30000
-    m = toolkit.kershaw_mesh(32, 4)
+def study(npts=30000, n=32, p=4):
+    m = toolkit.kershaw_mesh(n, p)
     OS = O.OracleSetup(m.nodes, 3, 3, 4)
     bx = OS.boxes
     x = toolkit.uniform_points(npts, 3, seed=1001)
@@ -53,11 +55,16 @@ def main():
         for name, v in (("affine", va[keep]), ("obb", vo[keep])):
             cc = c[keep][np.lexsort((c[keep], v))]
             rest[name].append(int(np.nonzero(cc == owner)[0][0]) + 1)
+    return total, {k: v / total for k, v in picks.items()}, {k: np.array(v) for k, v in rest.items()}
+
+
+def main():
+    npts = int(sys.argv[1]) if len(sys.argv) > 1 else 30000
+    total, picks, rest = study(npts)
     print(f"# cfg-2 sample: {total} INTERIOR points with their owner among the candidates")
-    for name, miss in picks.items():
-        print(f"round-1 pick by {name:11s}: points left for the rest phase {miss / total:.4f}")
+    for name, frac in picks.items():
+        print(f"round-1 pick by {name:11s}: points left for the rest phase {frac:.4f}")
     for name, r in rest.items():
-        r = np.array(r)
         print(f"rest order by {name:7s}: owner first {np.mean(r == 1):.3f}, mean owner rank {r.mean():.3f}"
               f" ({r.size} rest points)")
 
